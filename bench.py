@@ -1,0 +1,364 @@
+#!/usr/bin/env python
+"""CommVQ decode-attention benchmark (BASELINE.json metric).
+
+Workload (BASELINE.json configs[2], "C3"): full 32-layer LLaMA-3.1-8B KV
+shape, batch 2, 128K context, 1-bit CommVQ (per KV head: d=128, g=64, L=64,
+R=11, N_c=128), 8 KV heads x 4 GQA query heads.  One step = one decode step
+of attention for every (seq, layer, q head) over the packed cache resident in
+HBM.  metric = KV-tokens/s (one KV-token = one cached token of one
+(seq, layer): all 8 KV heads, 32 q heads), whole job over all ranks.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+
+Multi-GPU (torchrun): the context is sharded contiguously across ranks
+(position offsets kept global), each rank computes split-K partials
+(m, l, o) and one NCCL all-gather + LSE combine merges them
+ -- strong scaling of the fixed C3 job.
+"""
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # name: (n_layers, n_seqs, n_kv, q_per_kv, N, d, g, L, R, n_codes)
+    "c3": (32, 2, 8, 4, 131072, 128, 64, 64, 11, 128),
+    "c1": (1, 1, 8, 4, 8192, 128, 64, 64, 11, 128),
+    "c2": (1, 1, 8, 4, 32768, 128, 64, 64, 21, 256),
+    "c5": (1, 1, 8, 4, 1048576, 128, 64, 64, 21, 256),
+}
+BYTES_PER_KVHT = {11: 32.5, 21: 63.5}
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return p["hbm_gbs"], p["bf16_tflops"], "measured"
+    except Exception:
+        return 6650.0, 1590.0, "fallback"
+
+
+class Clocks:
+    """nvidia-smi sampler running during the timed region."""
+
+    def __init__(self, dev):
+        self.dev, self.samples, self.proc = dev, [], None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.dev), f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.samples.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if len(s) > 3 + i and s[3 + i].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+def cpu_reference(cfg, n_calls, threads, seed=7):
+    """Times the reference's fused_attention (oracle/_ref, compiled from the
+    reference sources) on this host: n_calls independent q-head calls at the
+    workload's context length over `threads` std::threads."""
+    import ctypes as C
+
+    from oracle.oracle import REF_SO, PORT_SO  # noqa: F401
+    layers, B, H, Gq, N, d, g, L, R, nc = cfg
+    if os.path.exists(REF_SO):
+        lib, kind = C.CDLL(REF_SO), "reference"
+    else:
+        raise RuntimeError("oracle/_ref/libcvq_ref.so missing")
+    f = lib.cvqr_bench_fused
+    f.argtypes = [C.c_size_t] * 10 + [C.c_uint64, C.c_void_p, C.c_void_p]
+    secs, cs = C.c_double(), C.c_double()
+    n_streams = max(1, min(H, n_calls // Gq))
+    rc = f(d, g, L, R, nc, N, n_streams, Gq, n_calls, threads, seed, C.byref(secs), C.byref(cs))
+    if rc != 0:
+        raise RuntimeError("reference bench failed")
+    qhead_tokens = n_calls * N
+    # one KV-token covers all q heads of one (seq, layer): 32 q-head calls
+    kv_tokens_per_s = qhead_tokens / secs.value / (H * Gq)
+    return kv_tokens_per_s, secs.value, kind
+
+
+def run_reference(args, cfg):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    layers, B, H, Gq, N, d, g, L, R, nc = cfg
+    threads = os.cpu_count() or 1
+    vals = []
+    for it in range(args.warmup + args.steps):
+        v, secs, kind = cpu_reference(cfg, threads, threads, seed=11 + it)
+        if it >= args.warmup:
+            vals.append((v, secs))
+    value = float(np.median([v for v, _ in vals]))
+    ms = float(np.median([s for _, s in vals])) * 1e3
+    line = {
+        "metric": "CommVQ decode-attention KV-tokens/s @128K ctx", "value": value,
+        "unit": "KV-tokens/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic (random codebooks/codes, commvq::Rng)",
+        "impl": "reference",
+        "config": {"workload": args.config, "n_layers": layers, "n_seqs": B, "n_kv_heads": H,
+                   "q_per_kv": Gq, "context": N, "key": [d, g, L, R], "n_codes": nc,
+                   "sample": f"{threads} q-head fused_attention calls per step at N={N}"},
+        "cpu_baseline": {"value": value, "unit": "KV-tokens/s", "cores": threads, "kind": kind,
+                         "sample": f"{threads} q-head fused_attention calls per step at N={N}"},
+        "e2e": {"value": value, "unit": "KV-tokens/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        return run_reference(args, cfg)
+
+    import torch
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2506_18879_b200 import commvq as G
+
+    layers, B, H, Gq, N, d, g, L, R, nc = cfg
+    kq = G.KeyQuantConfig(d, g, L, R)
+    S, rows = B * layers * H, B * layers * H * Gq
+    # contiguous context shards, boundaries at multiples of 128 tokens
+    per = ((N + world - 1) // world + 127) // 128 * 128
+    lo, hi = min(N, rank * per), min(N, (rank + 1) * per)
+    n_local = hi - lo
+    extra = args.steps + args.warmup + 8
+    stream = torch.cuda.current_stream()
+    ctx = G.Context(local, stream.cuda_stream)
+    cache = G.QuantizedKVCache(kq, nc, n_seqs=B, n_layers=layers, n_kv_heads=H, q_per_kv=Gq,
+                               capacity=n_local + extra, hidden=2 * nc, position_offset=lo, ctx=ctx)
+    rs = np.random.default_rng(1234)
+    for layer in range(layers):
+        for h in range(H):
+            cache.set_key_codebook(layer, h, 0.3 * rs.standard_normal(2 * kq.n_atoms))
+            cache.set_value_quantizer(
+                layer, h, rs.standard_normal((nc, d)) / 16,
+                0.1 * rs.standard_normal((d, 2 * nc)), np.zeros(2 * nc),
+                0.1 * rs.standard_normal((2 * nc, nc)), np.zeros(nc))
+    # synthetic packed codes straight into the HBM pools (any bit pattern is
+    # a valid code stream: fields are log2(L) bits); tails stay zero.
+    kp, ks, vp, vs = cache.pools()
+    kwords = (n_local * kq.bits_per_token + 63) // 64
+    vwords = (n_local * nc + 63) // 64
+    gen = torch.Generator(device="cuda").manual_seed(99 + rank)
+    for ptr, stride, nw, bits_total in ((kp, ks, kwords, n_local * kq.bits_per_token),
+                                        (vp, vs, vwords, n_local * nc)):
+        pool = _pool_tensor(ptr, S * stride).view(S, stride)
+        for s in range(S):
+            pool[s, :nw] = torch.randint(-2**63, 2**63 - 1, (nw,), dtype=torch.int64,
+                                         device="cuda", generator=gen)
+            tail = bits_total % 64
+            if tail:
+                pool[s, nw - 1] &= (1 << tail) - 1
+    cache.set_length(n_local)
+    torch.cuda.synchronize()
+    q = torch.randn(B, layers, H * Gq, d, device="cuda", generator=gen)
+    out = torch.empty_like(q)
+    t_q = N - 1  # global query position (last cached token)
+    m_p = torch.empty(rows, device="cuda")
+    l_p = torch.empty(rows, device="cuda")
+    o_p = torch.empty(rows, d, device="cuda")
+    gm = torch.empty(world, rows, device="cuda")
+    gl = torch.empty(world, rows, device="cuda")
+    go = torch.empty(world, rows, d, device="cuda")
+
+    def step():
+        if world == 1:
+            cache.attention(q, t_q, out)
+        else:
+            import torch.distributed as dist
+            cache.attention_partial(q, m_p, l_p, o_p, t_q)
+            dist.all_gather_into_tensor(gm, m_p)
+            dist.all_gather_into_tensor(gl, l_p)
+            dist.all_gather_into_tensor(go.view(world, -1), o_p.view(-1))
+            G.lse_combine(gm, gl, go, out, ctx)
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    barrier()
+    launches0 = G.launch_count()
+    _lib_profile(ctx, True)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with Clocks(local) as clk:
+        torch.cuda.synchronize()
+        barrier()
+        e0.record(stream)
+        for _ in range(args.steps):
+            step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+    ms_total = e0.elapsed_time(e1)
+    main_ms, main_n = _lib_profile_read(ctx)
+    _lib_profile(ctx, False)
+    launches = G.launch_count() - launches0
+    if world > 1:
+        import torch.distributed as dist
+        tt = torch.tensor([ms_total], device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms_total = float(tt.item())
+    ms = ms_total / args.steps
+    kv_tokens = B * layers * N
+    value = kv_tokens / (ms / 1e3)
+
+    # ---- roofline of the dominant kernel (live CUDA-event timing) ----
+    hbm, tflops, src = peaks()
+    kvht_per_launch = S * n_local
+    bytes_per_launch = kvht_per_launch * BYTES_PER_KVHT[R]
+    avg_main_ms = main_ms / max(main_n, 1)
+    achieved = bytes_per_launch / (avg_main_ms / 1e3) / 1e9
+    roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+            "frac": achieved / hbm, "traffic": None, "peak_source": src,
+            "kernel_ms": avg_main_ms, "kernel_share_of_step": avg_main_ms / ms,
+            "algorithmic_bytes_per_launch": bytes_per_launch,
+            "kv_head_tokens_per_s_kernel": kvht_per_launch / (avg_main_ms / 1e3)}
+
+    # ---- e2e through the C-ABI with host buffers (decode_step) ----
+    e2e = None
+    if not args.no_e2e and world == 1:
+        kh = np.random.default_rng(5).standard_normal((B, layers, H, d)).astype(np.float32)
+        vh = np.random.default_rng(6).standard_normal((B, layers, H, d)).astype(np.float32)
+        qh = np.random.default_rng(7).standard_normal((B, layers, H * Gq, d)).astype(np.float32)
+        oh = np.zeros_like(qh)
+        k_pin = torch.from_numpy(kh).pin_memory()
+        v_pin = torch.from_numpy(vh).pin_memory()
+        q_pin = torch.from_numpy(qh).pin_memory()
+        o_pin = torch.from_numpy(oh).pin_memory()
+        n_e2e = min(args.steps, 8)
+        cache.decode_step(k_pin, v_pin, q_pin, o_pin)  # warm (allocations)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(n_e2e):
+            cache.decode_step(k_pin, v_pin, q_pin, o_pin)
+        torch.cuda.synchronize()
+        e2e_ms = (time.perf_counter() - t0) * 1e3 / n_e2e
+        n_now = cache.size()
+        e2e = {"value": B * layers * n_now / (e2e_ms / 1e3), "unit": "KV-tokens/s",
+               "h2d_bytes_per_step": int(kh.nbytes + vh.nbytes + qh.nbytes),
+               "d2h_bytes_per_step": int(oh.nbytes), "ms_per_step": e2e_ms,
+               "path": "cvq_cache_decode_step (append k,v + attention) with pinned host buffers"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            threads = os.cpu_count() or 1
+            v, secs, kind = cpu_reference(cfg, max(threads, 8), threads)
+            cpu = {"value": v, "unit": "KV-tokens/s", "cores": threads, "kind": kind,
+                   "sample": f"{max(threads, 8)} q-head fused_attention calls at N={N} "
+                             f"({secs:.1f} s wall)"}
+        except Exception as ex:  # reported, never fatal
+            cpu = {"value": None, "unit": "KV-tokens/s", "cores": 0, "kind": "reference",
+                   "sample": f"unavailable: {ex}"}
+
+    if rank == 0:
+        line = {
+            "metric": "CommVQ decode-attention KV-tokens/s @128K ctx", "value": value,
+            "unit": "KV-tokens/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f32 (fp64-reduced phases; int codes)",
+            "data": "synthetic (random codebooks, random packed codes, random q)",
+            "config": {"workload": args.config, "n_layers": layers, "n_seqs": B,
+                       "n_kv_heads": H, "q_per_kv": Gq, "context": N, "key": [d, g, L, R],
+                       "n_codes": nc, "parallelism": f"context-shard x{world}",
+                       "l2": "inputs (packed cache) larger than L2"},
+            "kv_head_tokens_per_s": value * H, "roofline": roof, "clocks": clk.summary(),
+            "gpu_launches": launches, "e2e": e2e, "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+class _CudaArray:
+    def __init__(self, ptr, n):
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<i8", "data": (ptr, False),
+                                         "version": 3}
+
+
+def _pool_tensor(ptr, n_words):
+    """int64 view of a libcvq device pool (no copy)."""
+    import torch
+    return torch.as_tensor(_CudaArray(ptr, n_words), device="cuda")
+
+
+def _lib_profile(ctx, on):
+    from paper_2506_18879_b200 import commvq as G
+    G._check(G._lib.cvq_context_profile(ctx.h, G._i(1 if on else 0)))
+
+
+def _lib_profile_read(ctx):
+    import ctypes as C
+
+    from paper_2506_18879_b200 import commvq as G
+    ms, n = C.c_double(), C.c_uint64()
+    G._check(G._lib.cvq_context_profile_read(ctx.h, C.byref(ms), C.byref(n)))
+    return ms.value, n.value
+
+
+if __name__ == "__main__":
+    main()

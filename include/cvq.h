@@ -1,0 +1,265 @@
+/*
+ * cvq.h -- C-ABI of the B200-native CommVQ decode hot path (libcvq_b200.so).
+ *
+ * Drop-in boundary for the reference library commvq_core
+ * (/root/reference/proj/core).  The reference has no FFI of its own; its
+ * public C++ entry points for this path are
+ *
+ *   fused_attention(const AttnInput&, RopeTable&)          attn.hpp:62
+ *   naive_quantized_attention(...)                          attn.hpp:56
+ *   encode_keys(const Mat&, const KeyCodebook&, AssignSearch) keyquant.hpp:135-136
+ *   encoder_forward(const Vec&, const ValueEncoder&, infer)   valquant.hpp:62-64
+ *   pack_key_codes / unpack_key_codes / pack_value_codes /
+ *   unpack_value_codes                                      cache.hpp:36-41
+ *   QuantizedKVCache::{prefill, append, decode_step, save, load}
+ *                                                           cache.hpp:63-96
+ *   predicted_flops_fused / predicted_flops_naive           attn.hpp:66-71
+ *
+ * Every function below replaces one of those (cited per function).  Plain C
+ * types only: no torch, no C++ in the signatures.  Errors are status codes
+ * mirroring the reference's exception classes (error.hpp:11-20,
+ * std::invalid_argument, std::out_of_range); the message is retrievable with
+ * cvq_last_error() on the calling thread.  There is no CPU fallback: every
+ * numeric entry point runs sm_100a kernels and fails with CVQ_ECUDA when no
+ * B200 is usable.
+ *
+ * Layouts (all little-endian, identical to the reference in-memory / CVQC
+ * on-disk forms so callers can switch without re-encoding):
+ *   key atoms   : R x (d/2) x L (x, y) pairs in atom_index order
+ *                 (keyquant.hpp:37-39), fp64 like KeyCodebook::atoms
+ *   key codes   : a[], b[] uint16 in KeyCodes::idx order (keyquant.hpp:57-59)
+ *   value bits  : one byte per (token, code), ValueCodes::bits (valquant.hpp:36-48)
+ *   packed words: BitBuffer LE bit stream, bit k at bit (k%64) of word k/64
+ *                 (cache.hpp:16-31); key record per token = rounds outer,
+ *                 groups inner, a then b, log2(L) bits each (cache.cpp:90-106);
+ *                 value record = n_codes bits ascending (cache.cpp:137-143)
+ */
+#ifndef CVQ_H
+#define CVQ_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+#define CVQ_API extern "C" __attribute__((visibility("default")))
+#else
+#define CVQ_API __attribute__((visibility("default")))
+#endif
+
+typedef enum cvq_status {
+  CVQ_OK = 0,
+  CVQ_EINVAL = 1,    /* std::invalid_argument                         */
+  CVQ_ETRAINING = 2, /* commvq::TrainingError (non-finite activations) */
+  CVQ_ERANGE = 3,    /* std::out_of_range                             */
+  CVQ_EIO = 4,       /* commvq::IoError                               */
+  CVQ_ECUDA = 5,     /* device / driver failure (no CPU fallback)     */
+  CVQ_ENOMEM = 6     /* device allocation failed                      */
+} cvq_status;
+
+/* KeyQuantConfig (keyquant.hpp:16-28). */
+typedef struct cvq_key_config {
+  uint32_t d;          /* head dim, even                   */
+  uint32_t group_size; /* subspaces per code group         */
+  uint32_t n_levels;   /* L, power of two, <= 65536        */
+  uint32_t rounds;     /* R residual rounds                */
+} cvq_key_config;
+
+/* FlopReport (attn.hpp:16-27) counters; the GPU path reports the formula
+ * values of the reference fused pathway so JSON reports match. */
+typedef struct cvq_flop_report {
+  uint64_t predicted_mults;
+  uint64_t measured_mults;
+} cvq_flop_report;
+
+typedef struct cvq_context cvq_context;
+typedef struct cvq_cache cvq_cache;
+
+enum { CVQ_F32 = 0, CVQ_F64 = 1 };    /* element type of K/V inputs      */
+enum { CVQ_DEVICE = 0, CVQ_HOST = 1 }; /* where a caller buffer lives     */
+
+/* ------------------------------------------------------------ general */
+CVQ_API const char* cvq_last_error(void);
+CVQ_API int cvq_abi_version(void);
+/* Number of kernel launches issued by this process so far (all contexts).
+ * Used by bench.py to report gpu_launches. */
+CVQ_API uint64_t cvq_launch_count(void);
+
+/* One context = one device + one CUDA stream (cudaStream_t, may be NULL for
+ * a private stream).  Calls on a context are externally serialised
+ * (SURVEY.md 8b "Threading"); contexts on different devices run
+ * concurrently. */
+CVQ_API cvq_status cvq_context_create(int device, void* cuda_stream,
+                                      cvq_context** out);
+CVQ_API cvq_status cvq_context_destroy(cvq_context* ctx);
+CVQ_API cvq_status cvq_context_synchronize(cvq_context* ctx);
+/* Live timing of the dominant attention kernel: when enabled, every
+ * attention call brackets its main (score/decode) kernel with CUDA events on
+ * the context stream; _read synchronises, returns the summed milliseconds
+ * and the number of bracketed launches since the last read, and resets. */
+CVQ_API cvq_status cvq_context_profile(cvq_context* ctx, int enable);
+CVQ_API cvq_status cvq_context_profile_read(cvq_context* ctx, double* ms,
+                                            uint64_t* launches);
+
+/* attn.hpp:66-71 cost models (0 on invalid input, as the reference throws). */
+CVQ_API uint64_t cvq_predicted_flops_fused(uint64_t n_tokens, uint64_t d,
+                                           uint64_t n_codes, uint64_t rounds,
+                                           uint64_t n_levels);
+CVQ_API uint64_t cvq_predicted_flops_naive(uint64_t n_tokens, uint64_t d,
+                                           uint64_t n_codes);
+CVQ_API uint32_t cvq_bits_per_token(const cvq_key_config* kc);
+
+/* ------------------------------------- single-stream reference mirrors */
+/* All buffers are HOST memory; the call uploads, runs the sm_100a kernels
+ * and downloads.  Semantics and preconditions are those of the cited
+ * reference function, including the exceptions it raises. */
+
+/* fused_attention (attn.cpp:164-263): pre-RoPE query q[d] at position t
+ * against n_tokens cached tokens.  scores_out (optional, may be NULL)
+ * receives the n_tokens pre-softmax scores (attn.cpp:233). */
+CVQ_API cvq_status cvq_fused_attention(
+    cvq_context* ctx, const cvq_key_config* kc, uint32_t n_codes,
+    const double* key_atoms_xy, const uint16_t* a, const uint16_t* b,
+    uint64_t n_tokens, const uint8_t* value_bits, const double* value_rows,
+    const double* q, uint64_t t, double rope_base, double* out,
+    double* scores_out, cvq_flop_report* flops);
+
+/* naive_quantized_attention (attn.cpp:130-162): decode-then-attend. */
+CVQ_API cvq_status cvq_naive_attention(
+    cvq_context* ctx, const cvq_key_config* kc, uint32_t n_codes,
+    const double* key_atoms_xy, const uint16_t* a, const uint16_t* b,
+    uint64_t n_tokens, const uint8_t* value_bits, const double* value_rows,
+    const double* q, uint64_t t, double rope_base, double* out,
+    cvq_flop_report* flops);
+
+/* encode_keys, brute-force semantics (keyquant.cpp:705-739 + 180-200):
+ * codes are bit-identical to the reference (ties -> smallest a*L+b). */
+CVQ_API cvq_status cvq_encode_keys(cvq_context* ctx, const cvq_key_config* kc,
+                                   const double* key_atoms_xy,
+                                   const double* keys, uint64_t n_tokens,
+                                   uint16_t* a, uint16_t* b);
+
+/* encoder_forward in infer mode (valquant.cpp:50-101), batched over tokens:
+ * values[n][d] -> bits[n][n_codes] (logit > 0), logits optional. */
+CVQ_API cvq_status cvq_encoder_forward_infer(
+    cvq_context* ctx, uint32_t d, uint32_t hidden, uint32_t n_codes,
+    const double* w1, const double* b1, const double* w2, const double* b2,
+    const double* values, uint64_t n_tokens, uint8_t* bits, double* logits);
+
+/* cache.cpp:90-155 bit packing; word counts are ceil(n*bits/64). */
+CVQ_API cvq_status cvq_pack_key_codes(cvq_context* ctx,
+                                      const cvq_key_config* kc,
+                                      const uint16_t* a, const uint16_t* b,
+                                      uint64_t n_tokens, uint64_t* words);
+CVQ_API cvq_status cvq_unpack_key_codes(cvq_context* ctx,
+                                        const cvq_key_config* kc,
+                                        const uint64_t* words, uint64_t n_words,
+                                        uint64_t n_tokens, uint16_t* a,
+                                        uint16_t* b);
+CVQ_API cvq_status cvq_pack_value_codes(cvq_context* ctx, uint32_t n_codes,
+                                        const uint8_t* bits, uint64_t n_tokens,
+                                        uint64_t* words);
+CVQ_API cvq_status cvq_unpack_value_codes(cvq_context* ctx, uint32_t n_codes,
+                                          const uint64_t* words,
+                                          uint64_t n_words, uint64_t n_tokens,
+                                          uint8_t* bits);
+
+/* ------------------------------- device-resident multi-stream cache */
+/* QuantizedKVCache (cache.hpp:63-113) for a whole model: one code stream per
+ * (seq, layer, kv_head), codebooks per (layer, kv_head), each stream served
+ * to q_per_kv query heads (GQA).  Packed words live in HBM in the exact
+ * BitBuffer layout.  position_offset is the global position of this
+ * cache's first token (context sharding across GPUs). */
+typedef struct cvq_cache_desc {
+  cvq_key_config key;
+  uint32_t n_codes;    /* value bits per token (N_c)        */
+  uint32_t hidden;     /* value-encoder hidden width        */
+  uint32_t n_seqs;     /* batch                             */
+  uint32_t n_layers;
+  uint32_t n_kv_heads;
+  uint32_t q_per_kv;   /* query heads per KV stream (GQA)   */
+  uint64_t capacity;   /* max tokens per stream             */
+  uint64_t position_offset;
+  double rope_base;    /* RopeParams::base (rope.hpp:17)    */
+} cvq_cache_desc;
+
+CVQ_API cvq_status cvq_cache_create(cvq_context* ctx, const cvq_cache_desc* d,
+                                    cvq_cache** out);
+CVQ_API cvq_status cvq_cache_destroy(cvq_cache* c);
+CVQ_API cvq_status cvq_cache_length(const cvq_cache* c, uint64_t* n_tokens);
+
+/* Codebooks for slot (layer, head); host fp64 in reference order.
+ * key: R*(d/2)*L*2 doubles.  value quantizer: w1[d][hidden], b1[hidden],
+ * w2[hidden][n_codes], b2[n_codes], rows[n_codes][d] (CVQV order
+ * valquant.cpp:450-454).  w1..b2 may be NULL when the cache only attends
+ * (codes imported), rows may not. */
+CVQ_API cvq_status cvq_cache_set_key_codebook(cvq_cache* c, uint32_t layer,
+                                              uint32_t head,
+                                              const double* atoms_xy);
+CVQ_API cvq_status cvq_cache_set_value_quantizer(
+    cvq_cache* c, uint32_t layer, uint32_t head, const double* w1,
+    const double* b1, const double* w2, const double* b2, const double* rows);
+
+/* QuantizedKVCache::prefill (cache.cpp:213-254) for every stream at once:
+ * K, V are [n_seqs][n_layers][n_kv_heads][n_tokens][d] of dtype CVQ_F32 or
+ * CVQ_F64 in host or device memory.  Appends after the current length
+ * (prefill on an empty cache == the reference prefill; on a non-empty
+ * cache == sequential appends, word-identical per test_cache.cpp:155-180). */
+CVQ_API cvq_status cvq_cache_prefill(cvq_cache* c, const void* K,
+                                     const void* V, uint64_t n_tokens,
+                                     int dtype, int where);
+
+/* QuantizedKVCache::append (cache.cpp:256-285): one token per stream,
+ * k, v are [n_seqs][n_layers][n_kv_heads][d]. */
+CVQ_API cvq_status cvq_cache_append(cvq_cache* c, const void* k, const void* v,
+                                    int dtype, int where);
+
+/* Attention for every (seq, layer, q head) at query position t (global),
+ * q/out are fp32 [n_seqs][n_layers][n_kv_heads*q_per_kv][d].  Requires
+ * t + 1 >= position_offset + length (attn.cpp:97-98). */
+CVQ_API cvq_status cvq_cache_attention(cvq_cache* c, const float* q,
+                                       uint64_t t, float* out, int where);
+
+/* Split-K partial for context sharding: per row (seq, layer, q head) the
+ * running max m, sum l and normalised o[d] over this cache's tokens
+ * (device buffers). */
+CVQ_API cvq_status cvq_cache_attention_partial(cvq_cache* c, const float* q,
+                                               uint64_t t, float* m, float* l,
+                                               float* o);
+
+/* Log-sum-exp merge of n_parts partials (device buffers, part-major):
+ * m,l [n_parts][rows], o [n_parts][rows][d] -> out [rows][d]. */
+CVQ_API cvq_status cvq_lse_combine(cvq_context* ctx, const float* m,
+                                   const float* l, const float* o,
+                                   uint32_t n_parts, uint64_t rows, uint32_t d,
+                                   float* out);
+
+/* QuantizedKVCache::decode_step (cache.cpp:287-296): append k, v then attend
+ * q at the new last position.  All buffers in `where`. */
+CVQ_API cvq_status cvq_cache_decode_step(cvq_cache* c, const void* k,
+                                         const void* v, int kv_dtype,
+                                         const float* q, float* out, int where);
+
+/* Packed-word import/export of one stream (CVQC payload, cache.cpp:310-373).
+ * Import sets the stream's words for tokens [0, n_tokens); all streams must
+ * be imported with the same n_tokens before attending (the cache length is
+ * the last imported n_tokens).  Buffers in `where`. */
+CVQ_API cvq_status cvq_cache_import_stream(cvq_cache* c, uint32_t seq,
+                                           uint32_t layer, uint32_t head,
+                                           const uint64_t* key_words,
+                                           const uint64_t* value_words,
+                                           uint64_t n_tokens, int where);
+CVQ_API cvq_status cvq_cache_export_stream(const cvq_cache* c, uint32_t seq,
+                                           uint32_t layer, uint32_t head,
+                                           uint64_t* key_words,
+                                           uint64_t* value_words, int where);
+
+/* Raw device pools (stream-major, fixed stride in words) and length setter,
+ * for callers that fill codes on the device (synthetic benchmarks, CVQC
+ * bulk loads).  Streams are ordered (seq, layer, kv_head). */
+CVQ_API cvq_status cvq_cache_pools(cvq_cache* c, uint64_t** key_words,
+                                   uint64_t* key_stride_words,
+                                   uint64_t** value_words,
+                                   uint64_t* value_stride_words);
+CVQ_API cvq_status cvq_cache_set_length(cvq_cache* c, uint64_t n_tokens);
+
+#endif /* CVQ_H */

@@ -1,0 +1,982 @@
+// capi.cu -- host side of the C-ABI (include/cvq.h): contexts, the
+// device-resident multi-stream cache, the single-stream mirrors of the
+// reference API, argument validation mirroring the reference exceptions.
+// Every numeric entry point launches sm_100a kernels; there is no CPU
+// fallback.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/cvq.h"
+#include "cvq_internal.cuh"
+
+namespace cvq {
+std::atomic<unsigned long long> g_launches{0};
+bool key_tables_fit(const Geom& g);
+cudaError_t run_naive_attention(const AttnJob& job, const float* q, float* out, void* scratch,
+                                size_t scratch_bytes, cudaStream_t st);
+size_t naive_scratch_bytes(const AttnJob& job);
+}  // namespace cvq
+
+using namespace cvq;
+
+namespace {
+
+thread_local std::string g_err;
+
+cvq_status fail(cvq_status s, const std::string& msg) {
+  g_err = msg;
+  return s;
+}
+
+#define CU(x)                                                                      \
+  do {                                                                             \
+    cudaError_t e_ = (x);                                                          \
+    if (e_ != cudaSuccess)                                                         \
+      return fail(e_ == cudaErrorMemoryAllocation ? CVQ_ENOMEM : CVQ_ECUDA,        \
+                  std::string(#x) + ": " + cudaGetErrorString(e_));                \
+  } while (0)
+
+#define TRY(x)                      \
+  do {                              \
+    cvq_status s_ = (x);            \
+    if (s_ != CVQ_OK) return s_;    \
+  } while (0)
+
+// Device buffer that only grows.
+struct DevBuf {
+  void* p = nullptr;
+  size_t n = 0;
+  cudaError_t ensure(size_t bytes) {
+    if (bytes <= n) return cudaSuccess;
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+    cudaError_t e = cudaMalloc(&p, bytes);
+    if (e == cudaSuccess) n = bytes;
+    return e;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+};
+
+// KeyQuantConfig::validate (keyquant.cpp:46-60).
+cvq_status validate_kc(const cvq_key_config* kc) {
+  if (!kc) return fail(CVQ_EINVAL, "KeyQuantConfig: null");
+  if (kc->d == 0 || kc->d % 2 != 0)
+    return fail(CVQ_EINVAL, "KeyQuantConfig: d must be positive and even");
+  if (kc->group_size == 0) return fail(CVQ_EINVAL, "KeyQuantConfig: group_size must be positive");
+  if ((kc->d / 2) % kc->group_size != 0)
+    return fail(CVQ_EINVAL, "KeyQuantConfig: group_size must divide d/2 evenly");
+  if (kc->n_levels == 0 || (kc->n_levels & (kc->n_levels - 1)) != 0)
+    return fail(CVQ_EINVAL, "KeyQuantConfig: n_levels must be a power of two");
+  if (kc->n_levels > 65536) return fail(CVQ_EINVAL, "KeyQuantConfig: n_levels too large");
+  if (kc->rounds == 0) return fail(CVQ_EINVAL, "KeyQuantConfig: rounds must be positive");
+  return CVQ_OK;
+}
+
+int ilog2c(uint32_t v) {
+  int b = 0;
+  while ((1u << b) < v) ++b;
+  return b;
+}
+
+Geom make_geom(const cvq_key_config* kc, uint32_t n_codes, uint32_t hidden, uint32_t G) {
+  Geom g{};
+  g.d = (int)kc->d;
+  g.subs = g.d / 2;
+  g.g = (int)kc->group_size;
+  g.groups = g.subs / g.g;
+  g.L = (int)kc->n_levels;
+  g.lb = ilog2c(kc->n_levels);
+  g.R = (int)kc->rounds;
+  g.fpt = g.R * g.groups * 2;
+  g.bpt = g.fpt * g.lb;
+  g.n_codes = (int)n_codes;
+  g.hidden = (int)hidden;
+  g.G = (int)G;
+  return g;
+}
+
+uint64_t words_for_bits(uint64_t bits) { return (bits + 63) / 64; }
+
+std::vector<double> make_thetas(int d, double base) {  // rope.cpp:8-25
+  std::vector<double> th(d / 2);
+  for (int j = 0; j < d / 2; ++j) th[j] = std::pow(base, -2.0 * (double)j / (double)d);
+  return th;
+}
+
+// fp64 atoms [R][subs][L][2] -> fp32 complex [R][L][subs] (decode layout:
+// one row per (round, level) contiguous over subspaces).
+std::vector<float> atoms_to_decode_layout(const Geom& g, const double* xy) {
+  std::vector<float> out((size_t)g.R * g.L * g.subs * 2);
+  for (int r = 0; r < g.R; ++r)
+    for (int j = 0; j < g.subs; ++j)
+      for (int l = 0; l < g.L; ++l) {
+        const size_t src = (((size_t)r * g.subs + j) * g.L + l) * 2;
+        const size_t dst = (((size_t)r * g.L + l) * g.subs + j) * 2;
+        out[dst] = (float)xy[src];
+        out[dst + 1] = (float)xy[src + 1];
+      }
+  return out;
+}
+
+}  // namespace
+
+// ------------------------------------------------------------- structs
+struct cvq_context {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  int* d_err = nullptr;
+  DevBuf scratch;
+  // live timing of the dominant attention kernel (cvq_context_profile)
+  bool prof = false;
+  std::vector<cudaEvent_t> prof_ev;  // pairs
+  size_t prof_used = 0;
+  cudaEvent_t* next_prof_pair() {
+    if (!prof) return nullptr;
+    if (2 * (prof_used + 1) > prof_ev.size()) {
+      cudaEvent_t a, b;
+      if (cudaEventCreate(&a) != cudaSuccess) return nullptr;
+      if (cudaEventCreate(&b) != cudaSuccess) return nullptr;
+      prof_ev.push_back(a);
+      prof_ev.push_back(b);
+    }
+    return &prof_ev[2 * prof_used++];
+  }
+};
+
+struct cvq_cache {
+  cvq_context* ctx = nullptr;
+  cvq_cache_desc desc{};
+  Geom geo{};
+  int S = 0, n_slots = 0;
+  uint64_t kstride = 0, vstride = 0, length = 0;
+  uint64_t* kpool = nullptr;
+  uint64_t* vpool = nullptr;
+  double* atoms64 = nullptr;   // [slot][R][subs][L][2]
+  double* base = nullptr;      // [slot][R][groups][L][L] (when it fits)
+  double* maxnorm = nullptr;   // [slot][R][groups]
+  float2* cbk = nullptr;       // [slot][R][L][subs]
+  float* cbv = nullptr;        // [slot][n_codes][d]
+  double *w1 = nullptr, *b1 = nullptr, *w2 = nullptr, *b2 = nullptr;
+  double* thetas = nullptr;
+  std::vector<char> key_set, val_set, enc_set;
+  DevBuf attn_scratch, enc_scratch, stage_in, stage_out;
+};
+
+namespace {
+
+cvq_status ctx_check(cvq_context* ctx) {
+  if (!ctx) return fail(CVQ_EINVAL, "null context");
+  CU(cudaSetDevice(ctx->device));
+  return CVQ_OK;
+}
+
+void free_cache(cvq_cache* c) {
+  for (void* p : {(void*)c->kpool, (void*)c->vpool, (void*)c->atoms64, (void*)c->base,
+                  (void*)c->maxnorm, (void*)c->cbk, (void*)c->cbv, (void*)c->w1, (void*)c->b1,
+                  (void*)c->w2, (void*)c->b2, (void*)c->thetas})
+    if (p) cudaFree(p);
+  c->attn_scratch.release();
+  c->enc_scratch.release();
+  c->stage_in.release();
+  c->stage_out.release();
+}
+
+AttnJob make_job(const cvq_cache* c) {
+  AttnJob j{};
+  j.geo = c->geo;
+  j.S = c->S;
+  j.kpool = c->kpool;
+  j.kstride = c->kstride;
+  j.vpool = c->vpool;
+  j.vstride = c->vstride;
+  j.n_slots = c->n_slots;
+  j.cb_key = c->cbk;
+  j.cb_val = c->cbv;
+  j.thetas = c->thetas;
+  j.n = (long long)c->length;
+  j.pos0 = (long long)c->desc.position_offset;
+  j.t = 0;
+  return j;
+}
+
+cvq_status require_codebooks(const cvq_cache* c, bool keys, bool vrows, bool enc) {
+  for (int s = 0; s < c->n_slots; ++s) {
+    if (keys && !c->key_set[s]) return fail(CVQ_EINVAL, "cache: key codebook not set for a slot");
+    if (vrows && !c->val_set[s]) return fail(CVQ_EINVAL, "cache: value codebook not set for a slot");
+    if (enc && !c->enc_set[s]) return fail(CVQ_EINVAL, "cache: value encoder not set for a slot");
+  }
+  return CVQ_OK;
+}
+
+// Bring a caller buffer onto the device (staging copy when on host).
+cvq_status to_device(cvq_cache* c, DevBuf& buf, const void* p, size_t bytes, int where,
+                     const void** dev) {
+  if (where == CVQ_DEVICE) {
+    *dev = p;
+    return CVQ_OK;
+  }
+  CU(buf.ensure(bytes));
+  CU(cudaMemcpyAsync(buf.p, p, bytes, cudaMemcpyHostToDevice, c->ctx->stream));
+  *dev = buf.p;
+  return CVQ_OK;
+}
+
+}  // namespace
+
+// ================================================================ general
+CVQ_API const char* cvq_last_error(void) { return g_err.c_str(); }
+CVQ_API int cvq_abi_version(void) { return 1; }
+CVQ_API uint64_t cvq_launch_count(void) { return g_launches.load(); }
+
+CVQ_API cvq_status cvq_context_create(int device, void* stream, cvq_context** out) {
+  if (!out) return fail(CVQ_EINVAL, "null out");
+  int n = 0;
+  CU(cudaGetDeviceCount(&n));
+  if (device < 0 || device >= n) return fail(CVQ_EINVAL, "context: bad device index");
+  CU(cudaSetDevice(device));
+  cudaDeviceProp prop;
+  CU(cudaGetDeviceProperties(&prop, device));
+  if (prop.major != 10)
+    return fail(CVQ_ECUDA, std::string("context: sm_100a kernels need a Blackwell B200, got ") +
+                               prop.name);
+  cvq_context* c = new cvq_context;
+  c->device = device;
+  if (stream) {
+    c->stream = static_cast<cudaStream_t>(stream);
+  } else {
+    cudaError_t e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+    if (e != cudaSuccess) {
+      delete c;
+      return fail(CVQ_ECUDA, cudaGetErrorString(e));
+    }
+    c->own_stream = true;
+  }
+  cudaError_t e = cudaMalloc(&c->d_err, sizeof(int));
+  if (e != cudaSuccess) {
+    delete c;
+    return fail(CVQ_ECUDA, cudaGetErrorString(e));
+  }
+  *out = c;
+  return CVQ_OK;
+}
+
+CVQ_API cvq_status cvq_context_profile(cvq_context* ctx, int enable) {
+  TRY(ctx_check(ctx));
+  ctx->prof = enable != 0;
+  ctx->prof_used = 0;
+  return CVQ_OK;
+}
+
+CVQ_API cvq_status cvq_context_profile_read(cvq_context* ctx, double* ms, uint64_t* launches) {
+  TRY(ctx_check(ctx));
+  if (!ms || !launches) return fail(CVQ_EINVAL, "null argument");
+  CU(cudaStreamSynchronize(ctx->stream));
+  double tot = 0.0;
+  for (size_t i = 0; i < ctx->prof_used; ++i) {
+    float v = 0.f;
+    CU(cudaEventElapsedTime(&v, ctx->prof_ev[2 * i], ctx->prof_ev[2 * i + 1]));
+    tot += v;
+  }
+  *ms = tot;
+  *launches = ctx->prof_used;
+  ctx->prof_used = 0;
+  return CVQ_OK;
+}
+
+CVQ_API cvq_status cvq_context_destroy(cvq_context* ctx) {
+  if (!ctx) return CVQ_OK;
+  cudaSetDevice(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
+  for (cudaEvent_t e : ctx->prof_ev) cudaEventDestroy(e);
+  ctx->scratch.release();
+  if (ctx->d_err) cudaFree(ctx->d_err);
+  if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
+  delete ctx;
+  return CVQ_OK;
+}
+
+CVQ_API cvq_status cvq_context_synchronize(cvq_context* ctx) {
+  TRY(ctx_check(ctx));
+  CU(cudaStreamSynchronize(ctx->stream));
+  return CVQ_OK;
+}
+
+CVQ_API uint64_t cvq_predicted_flops_fused(uint64_t n, uint64_t d, uint64_t nc, uint64_t R,
+                                           uint64_t L) {
+  if (n == 0 || d == 0 || nc == 0 || R == 0 || L == 0) {
+    g_err = "predicted_flops_fused: inputs must be > 0";
+    return 0;
+  }
+  return (R * d + nc + 1) * n + d * (nc + R * L);  // attn.cpp:272-280
+}
+
+CVQ_API uint64_t cvq_predicted_flops_naive(uint64_t n, uint64_t d, uint64_t nc) {
+  if (n == 0 || d == 0 || nc == 0) {
+    g_err = "predicted_flops_naive: inputs must be > 0";
+    return 0;
+  }
+  return (2 * d + 1) * n + 2 * d * nc * n;  // attn.cpp:265-270
+}
+
+CVQ_API uint32_t cvq_bits_per_token(const cvq_key_config* kc) {
+  if (validate_kc(kc) != CVQ_OK) return 0;
+  return kc->rounds * ((kc->d / 2) / kc->group_size) * 2 * (uint32_t)ilog2c(kc->n_levels);
+}
+
+// ================================================================== cache
+CVQ_API cvq_status cvq_cache_create(cvq_context* ctx, const cvq_cache_desc* d, cvq_cache** out) {
+  TRY(ctx_check(ctx));
+  if (!d || !out) return fail(CVQ_EINVAL, "null argument");
+  TRY(validate_kc(&d->key));
+  if (d->n_codes == 0) return fail(CVQ_EINVAL, "ValueCodebook: zero dimension");
+  if (d->n_seqs == 0 || d->n_layers == 0 || d->n_kv_heads == 0 || d->q_per_kv == 0)
+    return fail(CVQ_EINVAL, "cache: empty shape");
+  if (d->q_per_kv > 8) return fail(CVQ_EINVAL, "cache: q_per_kv > 8 unsupported");
+  if (d->n_codes > 1024) return fail(CVQ_EINVAL, "cache: n_codes > 1024 unsupported");
+  if (!(d->rope_base > 0.0)) return fail(CVQ_EINVAL, "theta: base must be positive");
+  cvq_cache* c = new cvq_cache;
+  c->ctx = ctx;
+  c->desc = *d;
+  c->geo = make_geom(&d->key, d->n_codes, d->hidden, d->q_per_kv);
+  c->S = (int)(d->n_seqs * d->n_layers * d->n_kv_heads);
+  c->n_slots = (int)(d->n_layers * d->n_kv_heads);
+  const Geom& g = c->geo;
+  // stream strides rounded to 32 B so 128-token tiles stay 32-B aligned
+  c->kstride = (words_for_bits(d->capacity * (uint64_t)g.bpt) + 4 + 3) / 4 * 4;
+  c->vstride = (words_for_bits(d->capacity * (uint64_t)g.n_codes) + 4 + 3) / 4 * 4;
+  c->key_set.assign(c->n_slots, 0);
+  c->val_set.assign(c->n_slots, 0);
+  c->enc_set.assign(c->n_slots, 0);
+  const size_t na = (size_t)c->n_slots * g.R * g.subs * g.L;
+  auto alloc = [&](void** p, size_t bytes) -> cudaError_t {
+    cudaError_t e = cudaMalloc(p, bytes ? bytes : 8);
+    if (e == cudaSuccess) e = cudaMemsetAsync(*p, 0, bytes ? bytes : 8, ctx->stream);
+    return e;
+  };
+  cudaError_t e = cudaSuccess;
+  if (e == cudaSuccess) e = alloc((void**)&c->kpool, (size_t)c->S * c->kstride * 8);
+  if (e == cudaSuccess) e = alloc((void**)&c->vpool, (size_t)c->S * c->vstride * 8);
+  if (e == cudaSuccess) e = alloc((void**)&c->atoms64, na * 2 * sizeof(double));
+  if (e == cudaSuccess) e = alloc((void**)&c->cbk, na * sizeof(float2));
+  if (e == cudaSuccess) e = alloc((void**)&c->cbv, (size_t)c->n_slots * g.n_codes * g.d * 4);
+  if (e == cudaSuccess)
+    e = alloc((void**)&c->maxnorm, (size_t)c->n_slots * g.R * g.groups * sizeof(double));
+  if (e == cudaSuccess && key_tables_fit(g))
+    e = alloc((void**)&c->base, (size_t)c->n_slots * g.R * g.groups * g.L * g.L * sizeof(double));
+  if (e == cudaSuccess && d->hidden > 0) {
+    e = alloc((void**)&c->w1, (size_t)c->n_slots * g.d * g.hidden * 8);
+    if (e == cudaSuccess) e = alloc((void**)&c->b1, (size_t)c->n_slots * g.hidden * 8);
+    if (e == cudaSuccess) e = alloc((void**)&c->w2, (size_t)c->n_slots * g.hidden * g.n_codes * 8);
+    if (e == cudaSuccess) e = alloc((void**)&c->b2, (size_t)c->n_slots * g.n_codes * 8);
+  }
+  if (e == cudaSuccess) {
+    std::vector<double> th = make_thetas(g.d, d->rope_base);
+    e = alloc((void**)&c->thetas, th.size() * sizeof(double));
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(c->thetas, th.data(), th.size() * sizeof(double),
+                          cudaMemcpyHostToDevice, ctx->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+  }
+  if (e != cudaSuccess) {
+    free_cache(c);
+    delete c;
+    return fail(e == cudaErrorMemoryAllocation ? CVQ_ENOMEM : CVQ_ECUDA,
+                std::string("cache_create: ") + cudaGetErrorString(e));
+  }
+  *out = c;
+  return CVQ_OK;
+}
+
+CVQ_API cvq_status cvq_cache_destroy(cvq_cache* c) {
+  if (!c) return CVQ_OK;
+  cudaSetDevice(c->ctx->device);
+  cudaStreamSynchronize(c->ctx->stream);
+  free_cache(c);
+  delete c;
+  return CVQ_OK;
+}
+
+CVQ_API cvq_status cvq_cache_length(const cvq_cache* c, uint64_t* n) {
+  if (!c || !n) return fail(CVQ_EINVAL, "null argument");
+  *n = c->length;
+  return CVQ_OK;
+}
+
+CVQ_API cvq_status cvq_cache_set_key_codebook(cvq_cache* c, uint32_t layer, uint32_t head,
+                                              const double* xy) {
+  if (!c || !xy) return fail(CVQ_EINVAL, "null argument");
+  TRY(ctx_check(c->ctx));
+  if (layer >= c->desc.n_layers || head >= c->desc.n_kv_heads)
+    return fail(CVQ_EINVAL, "cache: slot out of range");
+  const Geom& g = c->geo;
+  const size_t na = (size_t)g.R * g.subs * g.L;
+  for (size_t i = 0; i < 2 * na; ++i)
+    if (!std::isfinite(xy[i])) return fail(CVQ_EINVAL, "comm_mat: entries must be finite");
+  const int slot = (int)(layer * c->desc.n_kv_heads + head);
+  cudaStream_t st = c->ctx->stream;
+  CU(cudaMemcpyAsync(c->atoms64 + (size_t)slot * na * 2, xy, na * 2 * sizeof(double),
+                     cudaMemcpyHostToDevice, st));
+  std::vector<float> dl = atoms_to_decode_layout(g, xy);
+  CU(cudaMemcpyAsync(c->cbk + (size_t)slot * na, dl.data(), dl.size() * sizeof(float),
+                     cudaMemcpyHostToDevice, st));
+  if (c->base) {
+    CU(build_key_enc_tables(g, 1, c->atoms64 + (size_t)slot * na * 2,
+                            c->base + (size_t)slot * g.R * g.groups * g.L * g.L,
+                            c->maxnorm + (size_t)slot * g.R * g.groups, st));
+  }
+  CU(cudaStreamSynchronize(st));  // host vector dl must outlive the copy
+  c->key_set[slot] = 1;
+  return CVQ_OK;
+}
+
+CVQ_API cvq_status cvq_cache_set_value_quantizer(cvq_cache* c, uint32_t layer, uint32_t head,
+                                                 const double* w1, const double* b1,
+                                                 const double* w2, const double* b2,
+                                                 const double* rows) {
+  if (!c || !rows) return fail(CVQ_EINVAL, "null argument");
+  TRY(ctx_check(c->ctx));
+  if (layer >= c->desc.n_layers || head >= c->desc.n_kv_heads)
+    return fail(CVQ_EINVAL, "cache: slot out of range");
+  const Geom& g = c->geo;
+  const int slot = (int)(layer * c->desc.n_kv_heads + head);
+  cudaStream_t st = c->ctx->stream;
+  std::vector<float> rf((size_t)g.n_codes * g.d);
+  for (size_t i = 0; i < rf.size(); ++i) rf[i] = (float)rows[i];
+  CU(cudaMemcpyAsync(c->cbv + (size_t)slot * rf.size(), rf.data(), rf.size() * 4,
+                     cudaMemcpyHostToDevice, st));
+  const bool have_enc = w1 && b1 && w2 && b2;
+  if (have_enc) {
+    if (g.hidden == 0) return fail(CVQ_EINVAL, "cache: created with hidden = 0");
+    CU(cudaMemcpyAsync(c->w1 + (size_t)slot * g.d * g.hidden, w1, (size_t)g.d * g.hidden * 8,
+                       cudaMemcpyHostToDevice, st));
+    CU(cudaMemcpyAsync(c->b1 + (size_t)slot * g.hidden, b1, (size_t)g.hidden * 8,
+                       cudaMemcpyHostToDevice, st));
+    CU(cudaMemcpyAsync(c->w2 + (size_t)slot * g.hidden * g.n_codes, w2,
+                       (size_t)g.hidden * g.n_codes * 8, cudaMemcpyHostToDevice, st));
+    CU(cudaMemcpyAsync(c->b2 + (size_t)slot * g.n_codes, b2, (size_t)g.n_codes * 8,
+                       cudaMemcpyHostToDevice, st));
+  }
+  CU(cudaStreamSynchronize(st));
+  c->val_set[slot] = 1;
+  if (have_enc) c->enc_set[slot] = 1;
+  return CVQ_OK;
+}
+
+namespace {
+
+// Encode + pack n tokens per stream (device K/V, element (s,i,k) at
+// s*s_stride + i*d + k), appended at the current length.
+cvq_status encode_append(cvq_cache* c, const void* K, const void* V, int dtype,
+                         long long s_stride, long long n) {
+  const Geom& g = c->geo;
+  cudaStream_t st = c->ctx->stream;
+  const size_t per_tok = (size_t)c->S * (2 * sizeof(uint16_t) * g.R * g.groups + g.n_codes);
+  CU(c->enc_scratch.ensure(per_tok * (size_t)n + 256));
+  uint16_t* a = static_cast<uint16_t*>(c->enc_scratch.p);
+  uint16_t* b = a + (size_t)c->S * n * g.R * g.groups;
+  uint8_t* bits = reinterpret_cast<uint8_t*>(b + (size_t)c->S * n * g.R * g.groups);
+  KeyEncTables tab{c->atoms64, c->base, c->maxnorm};
+  CU(run_encode_keys(g, c->S, c->n_slots, tab, K, dtype, s_stride, n, a, b, st));
+  CU(cudaMemsetAsync(c->ctx->d_err, 0, sizeof(int), st));
+  ValEncWeights w{c->w1, c->b1, c->w2, c->b2};
+  CU(run_encode_values(g, c->S, c->n_slots, w, V, dtype, s_stride, n, bits, nullptr,
+                       c->ctx->d_err, st));
+  int herr = 0;
+  CU(cudaMemcpyAsync(&herr, c->ctx->d_err, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CU(cudaStreamSynchronize(st));
+  if (herr) return fail(CVQ_ETRAINING, "encoder_forward: non-finite activations");
+  CU(run_pack_keys(g, c->S, a, b, n, (long long)c->length, c->kpool, c->kstride, st));
+  CU(run_pack_values(g, c->S, bits, n, (long long)c->length, c->vpool, c->vstride, st));
+  c->length += (uint64_t)n;
+  return CVQ_OK;
+}
+
+}  // namespace
+
+CVQ_API cvq_status cvq_cache_prefill(cvq_cache* c, const void* K, const void* V,
+                                     uint64_t n_tokens, int dtype, int where) {
+  if (!c) return fail(CVQ_EINVAL, "null cache");
+  TRY(ctx_check(c->ctx));
+  if (n_tokens == 0) return CVQ_OK;  // cache.cpp:225
+  if (!K || !V) return fail(CVQ_EINVAL, "prefill: null input");
+  if (dtype != CVQ_F32 && dtype != CVQ_F64) return fail(CVQ_EINVAL, "prefill: bad dtype");
+  if (c->length + n_tokens > c->desc.capacity) return fail(CVQ_ERANGE, "cache: capacity exceeded");
+  TRY(require_codebooks(c, true, true, true));
+  const Geom& g = c->geo;
+  const size_t es = dtype == CVQ_F32 ? 4 : 8;
+  const long long s_stride = (long long)n_tokens * g.d;
+  // chunk tokens so scratch stays bounded (~256 MB of inputs per chunk)
+  const long long per_tok_bytes = (long long)c->S * g.d * (long long)es * 2;
+  long long chunk = (256ll << 20) / (per_tok_bytes > 0 ? per_tok_bytes : 1);
+  if (chunk < 1) chunk = 1;
+  if (chunk > (long long)n_tokens) chunk = (long long)n_tokens;
+  for (long long c0 = 0; c0 < (long long)n_tokens; c0 += chunk) {
+    const long long nn = std::min<long long>(chunk, (long long)n_tokens - c0);
+    const void* Kd;
+    const void* Vd;
+    long long stride = s_stride;
+    if (where == CVQ_HOST) {
+      const size_t row = (size_t)nn * g.d * es;
+      CU(c->stage_in.ensure(2 * row * c->S));
+      char* kd = static_cast<char*>(c->stage_in.p);
+      char* vd = kd + row * c->S;
+      CU(cudaMemcpy2DAsync(kd, row, static_cast<const char*>(K) + (size_t)c0 * g.d * es,
+                           (size_t)s_stride * es, row, c->S, cudaMemcpyHostToDevice,
+                           c->ctx->stream));
+      CU(cudaMemcpy2DAsync(vd, row, static_cast<const char*>(V) + (size_t)c0 * g.d * es,
+                           (size_t)s_stride * es, row, c->S, cudaMemcpyHostToDevice,
+                           c->ctx->stream));
+      Kd = kd;
+      Vd = vd;
+      stride = nn * g.d;
+    } else {
+      Kd = static_cast<const char*>(K) + (size_t)c0 * g.d * es;
+      Vd = static_cast<const char*>(V) + (size_t)c0 * g.d * es;
+    }
+    TRY(encode_append(c, Kd, Vd, dtype, stride, nn));
+  }
+  return CVQ_OK;
+}
+
+CVQ_API cvq_status cvq_cache_append(cvq_cache* c, const void* k, const void* v, int dtype,
+                                    int where) {
+  return cvq_cache_prefill(c, k, v, 1, dtype, where);
+}
+
+namespace {
+
+cvq_status attention_common(cvq_cache* c, const float* q, uint64_t t, float* out, float* m,
+                            float* l, float* o, int where) {
+  TRY(ctx_check(c->ctx));
+  if (c->length == 0) return fail(CVQ_EINVAL, "attention: empty cache");
+  if (t + 1 < c->desc.position_offset + c->length)
+    return fail(CVQ_EINVAL, "attention: query position precedes cache");
+  TRY(require_codebooks(c, true, true, false));
+  const Geom& g = c->geo;
+  AttnJob job = make_job(c);
+  job.t = (long long)t;
+  const size_t need = attn_scratch_bytes(job, nullptr);
+  CU(c->attn_scratch.ensure(need));
+  const size_t qbytes = (size_t)c->S * g.G * g.d * sizeof(float);
+  const void* qd = nullptr;
+  TRY(to_device(c, c->stage_in, q, qbytes, where, &qd));
+  float* od = out;
+  if (out && where == CVQ_HOST) {
+    CU(c->stage_out.ensure(qbytes));
+    od = static_cast<float*>(c->stage_out.p);
+  }
+  CU(run_attention(job, static_cast<const float*>(qd), od, m, l, o, nullptr, c->attn_scratch.p,
+                   c->attn_scratch.n, c->ctx->stream, c->ctx->next_prof_pair()));
+  if (out && where == CVQ_HOST) {
+    CU(cudaMemcpyAsync(out, od, qbytes, cudaMemcpyDeviceToHost, c->ctx->stream));
+    CU(cudaStreamSynchronize(c->ctx->stream));
+  }
+  return CVQ_OK;
+}
+
+}  // namespace
+
+CVQ_API cvq_status cvq_cache_attention(cvq_cache* c, const float* q, uint64_t t, float* out,
+                                       int where) {
+  if (!c || !q || !out) return fail(CVQ_EINVAL, "null argument");
+  return attention_common(c, q, t, out, nullptr, nullptr, nullptr, where);
+}
+
+CVQ_API cvq_status cvq_cache_attention_partial(cvq_cache* c, const float* q, uint64_t t, float* m,
+                                               float* l, float* o) {
+  if (!c || !q || !m || !l || !o) return fail(CVQ_EINVAL, "null argument");
+  return attention_common(c, q, t, nullptr, m, l, o, CVQ_DEVICE);
+}
+
+CVQ_API cvq_status cvq_lse_combine(cvq_context* ctx, const float* m, const float* l,
+                                   const float* o, uint32_t n_parts, uint64_t rows, uint32_t d,
+                                   float* out) {
+  TRY(ctx_check(ctx));
+  if (!m || !l || !o || !out || n_parts == 0) return fail(CVQ_EINVAL, "lse_combine: bad argument");
+  CU(run_lse_combine(m, l, o, (int)n_parts, (long long)rows, (int)d, out, nullptr, nullptr,
+                     ctx->stream));
+  return CVQ_OK;
+}
+
+CVQ_API cvq_status cvq_cache_decode_step(cvq_cache* c, const void* k, const void* v, int kv_dtype,
+                                         const float* q, float* out, int where) {
+  if (!c) return fail(CVQ_EINVAL, "null cache");
+  TRY(cvq_cache_append(c, k, v, kv_dtype, where));
+  const uint64_t t = c->desc.position_offset + c->length - 1;  // cache.cpp:290
+  return cvq_cache_attention(c, q, t, out, where);
+}
+
+CVQ_API cvq_status cvq_cache_import_stream(cvq_cache* c, uint32_t seq, uint32_t layer,
+                                           uint32_t head, const uint64_t* kw, const uint64_t* vw,
+                                           uint64_t n, int where) {
+  if (!c || !kw || !vw) return fail(CVQ_EINVAL, "null argument");
+  TRY(ctx_check(c->ctx));
+  if (seq >= c->desc.n_seqs || layer >= c->desc.n_layers || head >= c->desc.n_kv_heads)
+    return fail(CVQ_EINVAL, "cache: stream out of range");
+  if (n > c->desc.capacity) return fail(CVQ_ERANGE, "cache: capacity exceeded");
+  const Geom& g = c->geo;
+  const size_t s = ((size_t)seq * c->desc.n_layers + layer) * c->desc.n_kv_heads + head;
+  const uint64_t nk = words_for_bits(n * (uint64_t)g.bpt), nv = words_for_bits(n * (uint64_t)g.n_codes);
+  const cudaMemcpyKind kind = where == CVQ_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
+  cudaStream_t st = c->ctx->stream;
+  CU(cudaMemsetAsync(c->kpool + s * c->kstride, 0, c->kstride * 8, st));
+  CU(cudaMemsetAsync(c->vpool + s * c->vstride, 0, c->vstride * 8, st));
+  CU(cudaMemcpyAsync(c->kpool + s * c->kstride, kw, nk * 8, kind, st));
+  CU(cudaMemcpyAsync(c->vpool + s * c->vstride, vw, nv * 8, kind, st));
+  CU(cudaStreamSynchronize(st));
+  c->length = n;
+  return CVQ_OK;
+}
+
+CVQ_API cvq_status cvq_cache_export_stream(const cvq_cache* c, uint32_t seq, uint32_t layer,
+                                           uint32_t head, uint64_t* kw, uint64_t* vw, int where) {
+  if (!c || !kw || !vw) return fail(CVQ_EINVAL, "null argument");
+  CU(cudaSetDevice(c->ctx->device));
+  if (seq >= c->desc.n_seqs || layer >= c->desc.n_layers || head >= c->desc.n_kv_heads)
+    return fail(CVQ_EINVAL, "cache: stream out of range");
+  const Geom& g = c->geo;
+  const size_t s = ((size_t)seq * c->desc.n_layers + layer) * c->desc.n_kv_heads + head;
+  const uint64_t nk = words_for_bits(c->length * (uint64_t)g.bpt);
+  const uint64_t nv = words_for_bits(c->length * (uint64_t)g.n_codes);
+  const cudaMemcpyKind kind = where == CVQ_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
+  CU(cudaMemcpyAsync(kw, c->kpool + s * c->kstride, nk * 8, kind, c->ctx->stream));
+  CU(cudaMemcpyAsync(vw, c->vpool + s * c->vstride, nv * 8, kind, c->ctx->stream));
+  CU(cudaStreamSynchronize(c->ctx->stream));
+  return CVQ_OK;
+}
+
+CVQ_API cvq_status cvq_cache_pools(cvq_cache* c, uint64_t** kw, uint64_t* ks, uint64_t** vw,
+                                   uint64_t* vs) {
+  if (!c || !kw || !ks || !vw || !vs) return fail(CVQ_EINVAL, "null argument");
+  *kw = c->kpool;
+  *ks = c->kstride;
+  *vw = c->vpool;
+  *vs = c->vstride;
+  return CVQ_OK;
+}
+
+CVQ_API cvq_status cvq_cache_set_length(cvq_cache* c, uint64_t n) {
+  if (!c) return fail(CVQ_EINVAL, "null cache");
+  if (n > c->desc.capacity) return fail(CVQ_ERANGE, "cache: capacity exceeded");
+  c->length = n;
+  return CVQ_OK;
+}
+
+// ===================================================== single-stream mirrors
+namespace {
+
+// A one-stream cache holding the caller's unpacked codes, packed on device.
+struct OneStream {
+  cvq_cache* c = nullptr;
+  ~OneStream() { cvq_cache_destroy(c); }
+};
+
+cvq_status make_one_stream(cvq_context* ctx, const cvq_key_config* kc, uint32_t n_codes,
+                           const double* atoms, const uint16_t* a, const uint16_t* b, uint64_t n,
+                           const uint8_t* bits, const double* vrows, double base, OneStream& os) {
+  cvq_cache_desc d{};
+  d.key = *kc;
+  d.n_codes = n_codes;
+  d.hidden = 0;
+  d.n_seqs = d.n_layers = d.n_kv_heads = d.q_per_kv = 1;
+  d.capacity = n;
+  d.position_offset = 0;
+  d.rope_base = base;
+  TRY(cvq_cache_create(ctx, &d, &os.c));
+  TRY(cvq_cache_set_key_codebook(os.c, 0, 0, atoms));
+  TRY(cvq_cache_set_value_quantizer(os.c, 0, 0, nullptr, nullptr, nullptr, nullptr, vrows));
+  cvq_cache* c = os.c;
+  const Geom& g = c->geo;
+  const size_t np = (size_t)n * g.R * g.groups;
+  CU(c->enc_scratch.ensure(np * 4 + (size_t)n * n_codes + 64));
+  uint16_t* da = static_cast<uint16_t*>(c->enc_scratch.p);
+  uint16_t* db = da + np;
+  uint8_t* dbits = reinterpret_cast<uint8_t*>(db + np);
+  cudaStream_t st = ctx->stream;
+  CU(cudaMemcpyAsync(da, a, np * 2, cudaMemcpyHostToDevice, st));
+  CU(cudaMemcpyAsync(db, b, np * 2, cudaMemcpyHostToDevice, st));
+  CU(cudaMemcpyAsync(dbits, bits, (size_t)n * n_codes, cudaMemcpyHostToDevice, st));
+  CU(run_pack_keys(g, 1, da, db, (long long)n, 0, c->kpool, c->kstride, st));
+  CU(run_pack_values(g, 1, dbits, (long long)n, 0, c->vpool, c->vstride, st));
+  c->length = n;
+  return CVQ_OK;
+}
+
+// validate_input (attn.cpp:91-110) + the per-token code range check
+// (attn.cpp:223-224).
+cvq_status validate_attn(const cvq_key_config* kc, uint32_t n_codes, const uint16_t* a,
+                         const uint16_t* b, uint64_t n, uint64_t t) {
+  TRY(validate_kc(kc));
+  if (n == 0) return fail(CVQ_EINVAL, "attention: empty cache");
+  if (t + 1 < n) return fail(CVQ_EINVAL, "attention: query position precedes cache");
+  if (n_codes == 0) return fail(CVQ_EINVAL, "attention: value codes/codebook mismatch");
+  if (n_codes > 1024) return fail(CVQ_EINVAL, "attention: n_codes > 1024 unsupported");
+  const uint64_t np = n * kc->rounds * ((kc->d / 2) / kc->group_size);
+  for (uint64_t i = 0; i < np; ++i)
+    if (a[i] >= kc->n_levels || b[i] >= kc->n_levels)
+      return fail(CVQ_EINVAL, "fused_attention: code out of range");
+  return CVQ_OK;
+}
+
+void fill_flops(cvq_flop_report* f, const cvq_key_config* kc, uint32_t n_codes, uint64_t n,
+                bool naive) {
+  if (!f) return;
+  const uint64_t d = kc->d, R = kc->rounds, L = kc->n_levels;
+  if (naive) {  // attn.cpp:155, 53, 77, 87
+    f->predicted_mults = cvq_predicted_flops_naive(n, d, n_codes);
+    f->measured_mults = n * n_codes * d + 2 * d + (2 * d + d + 1) * n + n * d;
+  } else {  // attn.cpp:190, 207, 235, 256
+    f->predicted_mults = cvq_predicted_flops_fused(n, d, n_codes, R, L);
+    f->measured_mults = 2 * d + 2 * d * R * L + n * (R * d + 1) + (uint64_t)n_codes * d;
+  }
+}
+
+}  // namespace
+
+CVQ_API cvq_status cvq_fused_attention(cvq_context* ctx, const cvq_key_config* kc,
+                                       uint32_t n_codes, const double* atoms, const uint16_t* a,
+                                       const uint16_t* b, uint64_t n, const uint8_t* bits,
+                                       const double* vrows, const double* q, uint64_t t,
+                                       double base, double* out, double* scores_out,
+                                       cvq_flop_report* flops) {
+  TRY(ctx_check(ctx));
+  if (!kc || !atoms || !q || !out || !vrows || (n && (!a || !b || !bits)))
+    return fail(CVQ_EINVAL, "null argument");
+  TRY(validate_attn(kc, n_codes, a, b, n, t));
+  OneStream os;
+  TRY(make_one_stream(ctx, kc, n_codes, atoms, a, b, n, bits, vrows, base, os));
+  cvq_cache* c = os.c;
+  const Geom& g = c->geo;
+  AttnJob job = make_job(c);
+  job.t = (long long)t;
+  const size_t need = attn_scratch_bytes(job, nullptr);
+  CU(c->attn_scratch.ensure(need));
+  CU(c->stage_in.ensure((size_t)g.d * 4 * 2 + (size_t)n * 4 + 64));
+  float* qd = static_cast<float*>(c->stage_in.p);
+  float* od = qd + g.d;
+  float* sd = od + g.d;
+  std::vector<float> qf(g.d);
+  for (int i = 0; i < g.d; ++i) qf[i] = (float)q[i];
+  CU(cudaMemcpyAsync(qd, qf.data(), g.d * 4, cudaMemcpyHostToDevice, ctx->stream));
+  CU(run_attention(job, qd, od, nullptr, nullptr, nullptr, scores_out ? sd : nullptr,
+                   c->attn_scratch.p, c->attn_scratch.n, ctx->stream));
+  std::vector<float> of(g.d), sf(scores_out ? n : 0);
+  CU(cudaMemcpyAsync(of.data(), od, g.d * 4, cudaMemcpyDeviceToHost, ctx->stream));
+  if (scores_out)
+    CU(cudaMemcpyAsync(sf.data(), sd, n * 4, cudaMemcpyDeviceToHost, ctx->stream));
+  CU(cudaStreamSynchronize(ctx->stream));
+  for (int i = 0; i < g.d; ++i) out[i] = of[i];
+  if (scores_out)
+    for (uint64_t i = 0; i < n; ++i) scores_out[i] = sf[i];
+  fill_flops(flops, kc, n_codes, n, false);
+  return CVQ_OK;
+}
+
+CVQ_API cvq_status cvq_naive_attention(cvq_context* ctx, const cvq_key_config* kc,
+                                       uint32_t n_codes, const double* atoms, const uint16_t* a,
+                                       const uint16_t* b, uint64_t n, const uint8_t* bits,
+                                       const double* vrows, const double* q, uint64_t t,
+                                       double base, double* out, cvq_flop_report* flops) {
+  TRY(ctx_check(ctx));
+  if (!kc || !atoms || !q || !out || !vrows || (n && (!a || !b || !bits)))
+    return fail(CVQ_EINVAL, "null argument");
+  TRY(validate_attn(kc, n_codes, a, b, n, t));
+  OneStream os;
+  TRY(make_one_stream(ctx, kc, n_codes, atoms, a, b, n, bits, vrows, base, os));
+  cvq_cache* c = os.c;
+  const Geom& g = c->geo;
+  AttnJob job = make_job(c);
+  job.t = (long long)t;
+  CU(c->attn_scratch.ensure(naive_scratch_bytes(job)));
+  CU(c->stage_in.ensure((size_t)g.d * 8 + 64));
+  float* qd = static_cast<float*>(c->stage_in.p);
+  float* od = qd + g.d;
+  std::vector<float> qf(g.d);
+  for (int i = 0; i < g.d; ++i) qf[i] = (float)q[i];
+  CU(cudaMemcpyAsync(qd, qf.data(), g.d * 4, cudaMemcpyHostToDevice, ctx->stream));
+  CU(run_naive_attention(job, qd, od, c->attn_scratch.p, c->attn_scratch.n, ctx->stream));
+  std::vector<float> of(g.d);
+  CU(cudaMemcpyAsync(of.data(), od, g.d * 4, cudaMemcpyDeviceToHost, ctx->stream));
+  CU(cudaStreamSynchronize(ctx->stream));
+  for (int i = 0; i < g.d; ++i) out[i] = of[i];
+  fill_flops(flops, kc, n_codes, n, true);
+  return CVQ_OK;
+}
+
+CVQ_API cvq_status cvq_encode_keys(cvq_context* ctx, const cvq_key_config* kc, const double* atoms,
+                                   const double* keys, uint64_t n, uint16_t* a, uint16_t* b) {
+  TRY(ctx_check(ctx));
+  TRY(validate_kc(kc));
+  if (!atoms || (n && (!keys || !a || !b))) return fail(CVQ_EINVAL, "null argument");
+  if (n == 0) return CVQ_OK;
+  Geom g = make_geom(kc, 1, 0, 1);
+  const size_t na = (size_t)g.R * g.subs * g.L;
+  const bool tables = key_tables_fit(g);
+  const size_t nb = tables ? (size_t)g.R * g.groups * g.L * g.L : 0;
+  const size_t np = (size_t)n * g.R * g.groups;
+  const size_t bytes = (na * 2 + nb + g.R * g.groups + (size_t)n * g.d) * 8 + np * 4 + 256;
+  CU(ctx->scratch.ensure(bytes));
+  double* d_atoms = static_cast<double*>(ctx->scratch.p);
+  double* d_base = d_atoms + na * 2;
+  double* d_max = d_base + nb;
+  double* d_keys = d_max + g.R * g.groups;
+  uint16_t* da = reinterpret_cast<uint16_t*>(d_keys + (size_t)n * g.d);
+  uint16_t* db = da + np;
+  cudaStream_t st = ctx->stream;
+  CU(cudaMemcpyAsync(d_atoms, atoms, na * 16, cudaMemcpyHostToDevice, st));
+  CU(cudaMemcpyAsync(d_keys, keys, (size_t)n * g.d * 8, cudaMemcpyHostToDevice, st));
+  if (tables) CU(build_key_enc_tables(g, 1, d_atoms, d_base, d_max, st));
+  KeyEncTables tab{d_atoms, tables ? d_base : nullptr, d_max};
+  CU(run_encode_keys(g, 1, 1, tab, d_keys, CVQ_F64, 0, (long long)n, da, db, st));
+  CU(cudaMemcpyAsync(a, da, np * 2, cudaMemcpyDeviceToHost, st));
+  CU(cudaMemcpyAsync(b, db, np * 2, cudaMemcpyDeviceToHost, st));
+  CU(cudaStreamSynchronize(st));
+  return CVQ_OK;
+}
+
+CVQ_API cvq_status cvq_encoder_forward_infer(cvq_context* ctx, uint32_t d, uint32_t hidden,
+                                             uint32_t n_codes, const double* w1, const double* b1,
+                                             const double* w2, const double* b2,
+                                             const double* values, uint64_t n, uint8_t* bits,
+                                             double* logits) {
+  TRY(ctx_check(ctx));
+  if (d == 0 || hidden == 0 || n_codes == 0) return fail(CVQ_EINVAL, "ValueEncoder: zero dimension");
+  if (!w1 || !b1 || !w2 || !b2 || (n && (!values || !bits))) return fail(CVQ_EINVAL, "null argument");
+  if (n == 0) return CVQ_OK;
+  cvq_key_config kc{2, 1, 2, 1};
+  Geom g = make_geom(&kc, n_codes, hidden, 1);
+  g.d = (int)d;
+  const size_t nw = (size_t)d * hidden + hidden + (size_t)hidden * n_codes + n_codes;
+  const size_t bytes = (nw + (size_t)n * d + (size_t)n * n_codes) * 8 + (size_t)n * n_codes + 256;
+  CU(ctx->scratch.ensure(bytes));
+  double* dw1 = static_cast<double*>(ctx->scratch.p);
+  double* db1 = dw1 + (size_t)d * hidden;
+  double* dw2 = db1 + hidden;
+  double* db2 = dw2 + (size_t)hidden * n_codes;
+  double* dv = db2 + n_codes;
+  double* dl = dv + (size_t)n * d;
+  uint8_t* dbits = reinterpret_cast<uint8_t*>(dl + (size_t)n * n_codes);
+  cudaStream_t st = ctx->stream;
+  CU(cudaMemcpyAsync(dw1, w1, (size_t)d * hidden * 8, cudaMemcpyHostToDevice, st));
+  CU(cudaMemcpyAsync(db1, b1, (size_t)hidden * 8, cudaMemcpyHostToDevice, st));
+  CU(cudaMemcpyAsync(dw2, w2, (size_t)hidden * n_codes * 8, cudaMemcpyHostToDevice, st));
+  CU(cudaMemcpyAsync(db2, b2, (size_t)n_codes * 8, cudaMemcpyHostToDevice, st));
+  CU(cudaMemcpyAsync(dv, values, (size_t)n * d * 8, cudaMemcpyHostToDevice, st));
+  CU(cudaMemsetAsync(ctx->d_err, 0, sizeof(int), st));
+  ValEncWeights w{dw1, db1, dw2, db2};
+  CU(run_encode_values(g, 1, 1, w, dv, CVQ_F64, 0, (long long)n, dbits, dl, ctx->d_err, st));
+  int herr = 0;
+  CU(cudaMemcpyAsync(&herr, ctx->d_err, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CU(cudaMemcpyAsync(bits, dbits, (size_t)n * n_codes, cudaMemcpyDeviceToHost, st));
+  if (logits) CU(cudaMemcpyAsync(logits, dl, (size_t)n * n_codes * 8, cudaMemcpyDeviceToHost, st));
+  CU(cudaStreamSynchronize(st));
+  if (herr) return fail(CVQ_ETRAINING, "encoder_forward: non-finite activations");
+  return CVQ_OK;
+}
+
+CVQ_API cvq_status cvq_pack_key_codes(cvq_context* ctx, const cvq_key_config* kc,
+                                      const uint16_t* a, const uint16_t* b, uint64_t n,
+                                      uint64_t* words) {
+  TRY(ctx_check(ctx));
+  TRY(validate_kc(kc));
+  if (n == 0) return CVQ_OK;
+  if (!a || !b || !words) return fail(CVQ_EINVAL, "null argument");
+  Geom g = make_geom(kc, 1, 0, 1);
+  const size_t np = (size_t)n * g.R * g.groups;
+  const uint64_t nw = words_for_bits(n * (uint64_t)g.bpt);
+  CU(ctx->scratch.ensure(np * 4 + nw * 8 + 64));
+  uint64_t* dw = static_cast<uint64_t*>(ctx->scratch.p);
+  uint16_t* da = reinterpret_cast<uint16_t*>(dw + nw);
+  uint16_t* db = da + np;
+  cudaStream_t st = ctx->stream;
+  CU(cudaMemcpyAsync(da, a, np * 2, cudaMemcpyHostToDevice, st));
+  CU(cudaMemcpyAsync(db, b, np * 2, cudaMemcpyHostToDevice, st));
+  CU(cudaMemsetAsync(dw, 0, nw * 8, st));
+  CU(run_pack_keys(g, 1, da, db, (long long)n, 0, dw, nw, st));
+  CU(cudaMemcpyAsync(words, dw, nw * 8, cudaMemcpyDeviceToHost, st));
+  CU(cudaStreamSynchronize(st));
+  return CVQ_OK;
+}
+
+CVQ_API cvq_status cvq_pack_value_codes(cvq_context* ctx, uint32_t n_codes, const uint8_t* bits,
+                                        uint64_t n, uint64_t* words) {
+  TRY(ctx_check(ctx));
+  if (n == 0 || n_codes == 0) return CVQ_OK;
+  if (!bits || !words) return fail(CVQ_EINVAL, "null argument");
+  cvq_key_config kc{2, 1, 2, 1};
+  Geom g = make_geom(&kc, n_codes, 0, 1);
+  const uint64_t nw = words_for_bits(n * (uint64_t)n_codes);
+  CU(ctx->scratch.ensure((size_t)n * n_codes + nw * 8 + 64));
+  uint64_t* dw = static_cast<uint64_t*>(ctx->scratch.p);
+  uint8_t* dbits = reinterpret_cast<uint8_t*>(dw + nw);
+  cudaStream_t st = ctx->stream;
+  CU(cudaMemcpyAsync(dbits, bits, (size_t)n * n_codes, cudaMemcpyHostToDevice, st));
+  CU(cudaMemsetAsync(dw, 0, nw * 8, st));
+  CU(run_pack_values(g, 1, dbits, (long long)n, 0, dw, nw, st));
+  CU(cudaMemcpyAsync(words, dw, nw * 8, cudaMemcpyDeviceToHost, st));
+  CU(cudaStreamSynchronize(st));
+  return CVQ_OK;
+}
+
+namespace {
+// BitBuffer::from_words validation (cache.cpp:78-88).
+cvq_status check_words(const uint64_t* words, uint64_t n_words, uint64_t bits) {
+  if (n_words != words_for_bits(bits)) return fail(CVQ_EINVAL, "BitBuffer: word count mismatch");
+  const unsigned tail = (unsigned)(bits % 64);
+  if (tail != 0 && (words[n_words - 1] >> tail) != 0)
+    return fail(CVQ_EINVAL, "BitBuffer: nonzero padding bits");
+  return CVQ_OK;
+}
+}  // namespace
+
+CVQ_API cvq_status cvq_unpack_key_codes(cvq_context* ctx, const cvq_key_config* kc,
+                                        const uint64_t* words, uint64_t n_words, uint64_t n,
+                                        uint16_t* a, uint16_t* b) {
+  TRY(ctx_check(ctx));
+  TRY(validate_kc(kc));
+  Geom g = make_geom(kc, 1, 0, 1);
+  TRY(check_words(words, n_words, n * (uint64_t)g.bpt));
+  if (n == 0) return CVQ_OK;
+  const size_t np = (size_t)n * g.R * g.groups;
+  CU(ctx->scratch.ensure(np * 4 + n_words * 8 + 64));
+  uint64_t* dw = static_cast<uint64_t*>(ctx->scratch.p);
+  uint16_t* da = reinterpret_cast<uint16_t*>(dw + n_words);
+  uint16_t* db = da + np;
+  cudaStream_t st = ctx->stream;
+  CU(cudaMemcpyAsync(dw, words, n_words * 8, cudaMemcpyHostToDevice, st));
+  CU(run_unpack_keys(g, dw, (long long)n, da, db, st));
+  CU(cudaMemcpyAsync(a, da, np * 2, cudaMemcpyDeviceToHost, st));
+  CU(cudaMemcpyAsync(b, db, np * 2, cudaMemcpyDeviceToHost, st));
+  CU(cudaStreamSynchronize(st));
+  return CVQ_OK;
+}
+
+CVQ_API cvq_status cvq_unpack_value_codes(cvq_context* ctx, uint32_t n_codes,
+                                          const uint64_t* words, uint64_t n_words, uint64_t n,
+                                          uint8_t* bits) {
+  TRY(ctx_check(ctx));
+  TRY(check_words(words, n_words, n * (uint64_t)n_codes));
+  if (n == 0 || n_codes == 0) return CVQ_OK;
+  cvq_key_config kc{2, 1, 2, 1};
+  Geom g = make_geom(&kc, n_codes, 0, 1);
+  CU(ctx->scratch.ensure((size_t)n * n_codes + n_words * 8 + 64));
+  uint64_t* dw = static_cast<uint64_t*>(ctx->scratch.p);
+  uint8_t* dbits = reinterpret_cast<uint8_t*>(dw + n_words);
+  cudaStream_t st = ctx->stream;
+  CU(cudaMemcpyAsync(dw, words, n_words * 8, cudaMemcpyHostToDevice, st));
+  CU(run_unpack_values(g, dw, (long long)n, dbits, st));
+  CU(cudaMemcpyAsync(bits, dbits, (size_t)n * n_codes, cudaMemcpyDeviceToHost, st));
+  CU(cudaStreamSynchronize(st));
+  return CVQ_OK;
+}

@@ -1,0 +1,132 @@
+// cvq_internal.cuh -- shared geometry, device helpers and launcher
+// declarations for the sm_100a CommVQ kernels (attn.cu, encode.cu, pack.cu,
+// capi.cu).  Not part of the public C-ABI (include/cvq.h).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <atomic>
+#include <string>
+
+namespace cvq {
+
+// Geometry of one quantizer configuration (KeyQuantConfig keyquant.hpp:16-28
+// + value side).  fpt = code fields per token (rounds * groups * 2); the
+// packed key stream is a plain sequence of lb-bit fields (cache.cpp:90-106),
+// so field F of a stream sits at bit F * lb.
+struct Geom {
+  int d, subs, g, groups, L, lb, R, fpt, bpt;
+  int n_codes, hidden;
+  int G;  // query heads served per KV stream
+};
+
+// Work description shared by the attention launchers.
+struct AttnJob {
+  Geom geo;
+  int S;                      // number of KV streams
+  const uint64_t* kpool;      // [S][kstride] packed key words
+  uint64_t kstride;
+  const uint64_t* vpool;      // [S][vstride] packed value words
+  uint64_t vstride;
+  int n_slots;                // codebook slot of stream s = s % n_slots
+  const float2* cb_key;       // [slot][R][L][subs] complex atoms (x, y), fp32
+  const float* cb_val;        // [slot][n_codes][d] fp32
+  const double* thetas;       // [subs] fp64, rope.cpp:8-25
+  long long n;                // tokens per stream
+  long long pos0;             // global position of token 0
+  long long t;                // query position
+};
+
+// Scratch handed to run_attention (sized by attn_scratch_bytes).
+size_t attn_scratch_bytes(const AttnJob& job, int* n_chunks_out);
+
+// q: [S][G][d] fp32 (device).  If out != nullptr writes normalised outputs
+// [S][G][d]; if m/l/o != nullptr writes the merged partial (m, l, o[d]) of
+// this job's tokens per row.  scores (optional) receives [S][G][n] fp32.
+// prof (optional, 2 events) brackets the dominant (score) kernel so callers
+// can time it live on the launching stream.
+cudaError_t run_attention(const AttnJob& job, const float* q, float* out,
+                          float* m, float* l, float* o, float* scores_out,
+                          void* scratch, size_t scratch_bytes,
+                          cudaStream_t st, cudaEvent_t* prof = nullptr);
+
+// Log-sum-exp merge (device), parts-major.
+cudaError_t run_lse_combine(const float* m, const float* l, const float* o,
+                            int n_parts, long long rows, int d, float* out,
+                            float* m_out, float* l_out, cudaStream_t st);
+
+// ---- encoders (encode.cu) -------------------------------------------------
+// Per slot: atoms fp64 [R][subs][L][2] -> screen tables.
+struct KeyEncTables {
+  const double* atoms;   // [slot][R][subs][L][2] (reference order)
+  const double* base;    // [slot][R][groups][L][L]
+  const double* maxnorm; // [slot][R][groups]
+};
+cudaError_t build_key_enc_tables(const Geom& g, int n_slots,
+                                 const double* atoms, double* base,
+                                 double* maxnorm, cudaStream_t st);
+// keys: element (s, i, k) at keys + s*s_stride + i*d + k, dtype 0=f32 1=f64.
+// Codes: a/b [s][n][R*groups] uint16.  err_flag (device int) set on failure.
+cudaError_t run_encode_keys(const Geom& g, int S, int n_slots,
+                            const KeyEncTables& tab, const void* keys,
+                            int dtype, long long s_stride, long long n,
+                            uint16_t* a, uint16_t* b, cudaStream_t st);
+// Value encoder (infer): bits [s][n][n_codes] uint8, logits optional fp64.
+struct ValEncWeights {
+  const double* w1;  // [slot][d][hidden]
+  const double* b1;  // [slot][hidden]
+  const double* w2;  // [slot][hidden][n_codes]
+  const double* b2;  // [slot][n_codes]
+};
+cudaError_t run_encode_values(const Geom& g, int S, int n_slots,
+                              const ValEncWeights& w, const void* vals,
+                              int dtype, long long s_stride, long long n,
+                              uint8_t* bits, double* logits, int* err_flag,
+                              cudaStream_t st);
+
+// ---- packing (pack.cu) -----------------------------------------------------
+// Writes n tokens' key codes (a/b [s][n][R*groups]) into stream words at
+// token offset tok0 (read-modify-write of boundary words).
+cudaError_t run_pack_keys(const Geom& g, int S, const uint16_t* a,
+                          const uint16_t* b, long long n, long long tok0,
+                          uint64_t* kpool, uint64_t kstride, cudaStream_t st);
+cudaError_t run_pack_values(const Geom& g, int S, const uint8_t* bits,
+                            long long n, long long tok0, uint64_t* vpool,
+                            uint64_t vstride, cudaStream_t st);
+cudaError_t run_unpack_keys(const Geom& g, const uint64_t* words, long long n,
+                            uint16_t* a, uint16_t* b, cudaStream_t st);
+cudaError_t run_unpack_values(const Geom& g, const uint64_t* words,
+                              long long n, uint8_t* bits, cudaStream_t st);
+
+// Global launch counter (bench.py gpu_launches).
+extern std::atomic<unsigned long long> g_launches;
+inline void count_launch(unsigned long long k = 1) { g_launches += k; }
+
+// ---- device helpers --------------------------------------------------------
+__device__ __forceinline__ unsigned read_field(const uint64_t* __restrict__ w,
+                                               unsigned long long bit,
+                                               int nbits) {
+  unsigned long long wi = bit >> 6;
+  int off = (int)(bit & 63);
+  unsigned long long v = __ldg(w + wi) >> off;
+  if (off + nbits > 64) v |= __ldg(w + wi + 1) << (64 - off);
+  return (unsigned)(v & ((1ull << nbits) - 1ull));
+}
+
+// e^{-i * delta * theta} with the angle formed and reduced mod 2*pi in fp64
+// (fp32 angles break 1e-3 at long context).
+__device__ __forceinline__ float2 phase_neg(long long delta, double theta) {
+  const double kInv2Pi = 0.15915494309189535;
+  const double k2PiHi = 6.283185307179586;
+  const double k2PiLo = 2.4492935982947064e-16;
+  double ang = (double)delta * theta;
+  double k = rint(ang * kInv2Pi);
+  double r = fma(-k, k2PiHi, ang);
+  r = fma(-k, k2PiLo, r);
+  float s, c;
+  sincosf((float)r, &s, &c);
+  return make_float2(c, -s);
+}
+
+}  // namespace cvq

@@ -1,0 +1,411 @@
+// encode.cu -- bit-exact KV encoders on sm_100a.
+//
+// Keys: replaces encode_keys with brute-force search (keyquant.cpp:705-739,
+// CenterCache::assign_brute 180-200).  The reference scans all L^2 centers
+// c_ab = u_a + v_b of each (round, group) slice with an fp64 sequential
+// squared distance (no FMA) and strict '<', so ties go to the smallest
+// a*L+b.  Codes must be bit-identical, including near-ties.
+//
+// Device algorithm per (token, round, group):
+//   1. screen: s(a,b) = base[a,b] - 2 p.u_a - 2 p.v_b  (fp64, FMA allowed),
+//      the factorised form of keyquant.cpp:204-224; |p|^2 is shared.
+//   2. if the runner-up screen value is > best + margin, the best pair is
+//      the reference argmin (margin bounds screen + reference rounding,
+//      see kMarginRel below); otherwise every pair within the margin is
+//      re-evaluated with the reference's exact fp64 sequence
+//      (__dsub_rn/__dmul_rn/__dadd_rn, increasing c, strict '<').
+//   3. residual -= (u_a + v_b) in fp64 exactly as keyquant.cpp:733-734.
+// Non-finite or overflowing residuals take the exact brute-force path for
+// every pair (the reference then returns pair 0).
+//
+// Values: replaces encoder_forward in infer mode (valquant.cpp:50-101):
+// h = relu(t.w1 + b1), logit = h.w2 + b2 in the reference's summation order
+// with zero-skips (valquant.cpp:53-68), bit = logit > 0.  Exact fp64, no
+// FMA, so logits and bits are bit-identical.
+#include <cfloat>
+#include <cmath>
+
+#include "cvq_internal.cuh"
+
+namespace cvq {
+
+// Screen error bound, relative to (|p| + 2 max|u|)^2: worst-case fp64
+// rounding of the screen and of the reference sum is ~4*(2g+4)*2^-53 of that
+// scale (< 6e-14 at g = 64); 1e-11 leaves a ~90x safety factor.
+constexpr double kMarginRel = 1e-11;
+
+// ---------------------------------------------------------------- tables
+// base[a][b] = |u_a|^2 + |v_b|^2 + 2 u_a.v_b per (slot, round, group) and
+// max_l |u_l| (= max |v_l|, v is u rotated per subspace).
+__global__ void k_key_base(Geom g, const double* __restrict__ atoms,
+                           double* __restrict__ base, double* __restrict__ maxnorm) {
+  const int rg = blockIdx.x;  // r * groups + grp
+  const int slot = blockIdx.y;
+  const int r = rg / g.groups, grp = rg % g.groups;
+  const double2* U = reinterpret_cast<const double2*>(atoms) +
+                     ((size_t)(slot * g.R + r) * g.subs + (size_t)grp * g.g) * g.L;
+  double* B = base + ((size_t)slot * g.R * g.groups + rg) * g.L * g.L;
+  __shared__ double nrm[1024];
+  for (int l = threadIdx.x; l < g.L; l += blockDim.x) {
+    double s = 0.0;
+    for (int si = 0; si < g.g; ++si) {
+      double2 u = U[(size_t)si * g.L + l];
+      s += u.x * u.x + u.y * u.y;
+    }
+    if (l < 1024) nrm[l] = s;
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < g.L * g.L; e += blockDim.x) {
+    const int a = e / g.L, b = e % g.L;
+    double uv = 0.0;
+    for (int si = 0; si < g.g; ++si) {
+      double2 ua = U[(size_t)si * g.L + a], ub = U[(size_t)si * g.L + b];
+      uv += ua.x * (-ub.y) + ua.y * ub.x;  // u_a . v_b, v_b = (-y_b, x_b)
+    }
+    B[e] = nrm[a] + nrm[b] + 2.0 * uv;
+  }
+  if (threadIdx.x == 0) {
+    double m = 0.0;
+    for (int l = 0; l < g.L; ++l) m = fmax(m, nrm[l]);
+    maxnorm[(size_t)slot * g.R * g.groups + rg] = sqrt(m);
+  }
+}
+
+cudaError_t build_key_enc_tables(const Geom& g, int n_slots, const double* atoms,
+                                 double* base, double* maxnorm, cudaStream_t st) {
+  if (g.L > 1024) return cudaErrorInvalidValue;
+  dim3 grid(g.R * g.groups, n_slots);
+  k_key_base<<<grid, 256, 0, st>>>(g, atoms, base, maxnorm);
+  count_launch();
+  return cudaGetLastError();
+}
+
+__device__ __forceinline__ double load_elem(const void* p, int dtype, long long idx) {
+  return dtype == 0 ? (double)static_cast<const float*>(p)[idx]
+                    : static_cast<const double*>(p)[idx];
+}
+
+// Exact reference distance of residual p (2g values) to center (a, b).
+__device__ __forceinline__ double exact_dist(const double* p, const double2* U, int L, int gsz,
+                                             int a, int b) {
+  double s = 0.0;
+  for (int si = 0; si < gsz; ++si) {
+    const double2 ua = U[(size_t)si * L + a], ub = U[(size_t)si * L + b];
+    const double c0 = __dadd_rn(ua.x, -ub.y);  // u_a + v_b, keyquant.cpp:152-156
+    const double c1 = __dadd_rn(ua.y, ub.x);
+    const double d0 = __dsub_rn(p[2 * si], c0);
+    s = __dadd_rn(s, __dmul_rn(d0, d0));
+    const double d1 = __dsub_rn(p[2 * si + 1], c1);
+    s = __dadd_rn(s, __dmul_rn(d1, d1));
+  }
+  return s;
+}
+
+__device__ __forceinline__ void argmin_merge(double& v, int& c, double v2, int c2) {
+  if (v2 < v || (v2 == v && c2 < c)) {
+    v = v2;
+    c = c2;
+  }
+}
+
+__device__ __forceinline__ void warp_argmin(double& v, int& c) {
+  for (int o = 16; o; o >>= 1) {
+    double v2 = __shfl_xor_sync(0xffffffffu, v, o);
+    int c2 = __shfl_xor_sync(0xffffffffu, c, o);
+    argmin_merge(v, c, v2, c2);
+  }
+}
+
+// Exact search over all pairs (or those whose screen value is <= thr when
+// use_thr) for one token; U may be shared or global.
+__device__ int exact_search(const double* p, const double2* U, int L, int gsz,
+                            const double* B, const double* PU, const double* PV, bool use_thr,
+                            double thr) {
+  const int lane = threadIdx.x & 31;
+  double best = INFINITY;
+  int bc = 0x7fffffff;
+  for (int c = lane; c < L * L; c += 32) {
+    const int a = c / L, b = c % L;
+    if (use_thr) {
+      const double sc = B[(size_t)a * L + b] - 2.0 * PU[a] - 2.0 * PV[b];
+      if (!(sc <= thr)) continue;
+    }
+    const double d = exact_dist(p, U, L, gsz, a, b);
+    if (d < best) {  // increasing c per lane: strict '<' keeps the smallest
+      best = d;
+      bc = c;
+    }
+  }
+  // Lanes whose candidates were all NaN/inf keep bc = INT_MAX unless the
+  // reference would pick them: assign_brute picks c = 0 when nothing is
+  // strictly below +inf.
+  warp_argmin(best, bc);
+  if (bc == 0x7fffffff) bc = 0;
+  return bc;
+}
+
+constexpr int kEncTok = 32;
+constexpr int kEncWarps = 8;
+
+// Table-screen encoder: one CTA per (32-token tile, stream); one warp per
+// token at a time.  Requires g*L*16 + L*L*8 bytes of the slice in smem.
+__global__ void __launch_bounds__(kEncWarps * 32)
+k_encode_keys_table(Geom g, int n_slots, const double* __restrict__ atoms,
+                    const double* __restrict__ base, const double* __restrict__ maxnorm,
+                    const void* __restrict__ keys, int dtype, long long s_stride, long long n,
+                    uint16_t* __restrict__ a_out, uint16_t* __restrict__ b_out) {
+  extern __shared__ double sm[];
+  double2* U = reinterpret_cast<double2*>(sm);          // [g][L]
+  double* B = sm + 2 * (size_t)g.g * g.L;               // [L][L]
+  double* P = B + (size_t)g.L * g.L;                    // [kEncTok][d]
+  double* PU = P + (size_t)kEncTok * g.d;               // [warps][L]
+  double* PV = PU + (size_t)kEncWarps * g.L;            // [warps][L]
+  const int s = blockIdx.y, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const long long i0 = (long long)blockIdx.x * kEncTok;
+  const int nt = (int)min((long long)kEncTok, n - i0);
+  const int slot = s % n_slots;
+  for (int e = tid; e < nt * g.d; e += blockDim.x)
+    P[e] = load_elem(keys, dtype, (long long)s * s_stride + (i0 + e / g.d) * g.d + e % g.d);
+  const int L = g.L, gs = g.g, w2 = 2 * g.g;
+  for (int r = 0; r < g.R; ++r) {
+    for (int grp = 0; grp < g.groups; ++grp) {
+      __syncthreads();
+      const double2* Ug = reinterpret_cast<const double2*>(atoms) +
+                          ((size_t)(slot * g.R + r) * g.subs + (size_t)grp * gs) * L;
+      for (int e = tid; e < gs * L; e += blockDim.x) U[e] = Ug[e];
+      const double* Bg = base + ((size_t)(slot * g.R + r) * g.groups + grp) * L * L;
+      for (int e = tid; e < L * L; e += blockDim.x) B[e] = Bg[e];
+      const double mn = maxnorm[(size_t)(slot * g.R + r) * g.groups + grp];
+      __syncthreads();
+      double* pu = PU + warp * L;
+      double* pv = PV + warp * L;
+      for (int tk = warp; tk < nt; tk += kEncWarps) {
+        double* p = P + (size_t)tk * g.d + grp * w2;
+        for (int l = lane; l < L; l += 32) {
+          double su = 0.0, sv = 0.0;
+          for (int si = 0; si < gs; ++si) {
+            const double2 u = U[(size_t)si * L + l];
+            const double px = p[2 * si], py = p[2 * si + 1];
+            su = fma(px, u.x, fma(py, u.y, su));
+            sv = fma(py, u.x, fma(-px, u.y, sv));
+          }
+          pu[l] = su;
+          pv[l] = sv;
+        }
+        double pn = 0.0;
+        for (int e = lane; e < w2; e += 32) pn = fma(p[e], p[e], pn);
+        for (int o = 16; o; o >>= 1) pn += __shfl_xor_sync(0xffffffffu, pn, o);
+        __syncwarp();
+        int chosen;
+        if (!(pn < 1e300) || !(mn < 1e150)) {
+          chosen = exact_search(p, U, L, gs, B, pu, pv, false, 0.0);
+        } else {
+          // single pass: lane-local best and runner-up, then warp merge
+          double b1 = INFINITY, b2 = INFINITY;
+          int c1 = 0x7fffffff;
+          for (int b = lane; b < L; b += 32) {
+            const double t2 = 2.0 * pv[b];
+            for (int a = 0; a < L; ++a) {
+              const double sc = B[a * L + b] - 2.0 * pu[a] - t2;
+              const int c = a * L + b;
+              if (sc < b1 || (sc == b1 && c < c1)) {
+                b2 = b1;
+                b1 = sc;
+                c1 = c;
+              } else if (sc < b2) {
+                b2 = sc;
+              }
+            }
+          }
+          double gb = b1;
+          int gc = c1;
+          warp_argmin(gb, gc);
+          // runner-up over the warp: every lane's b2, plus other lanes' b1
+          double ru = (c1 == gc) ? b2 : b1;
+          for (int o = 16; o; o >>= 1) ru = fmin(ru, __shfl_xor_sync(0xffffffffu, ru, o));
+          const double scale = sqrt(pn) + 2.0 * mn;
+          const double margin = kMarginRel * scale * scale * fmax(1.0, w2 / 128.0);
+          if (ru > gb + margin) {
+            chosen = gc;
+          } else {
+            chosen = exact_search(p, U, L, gs, B, pu, pv, true, gb + margin);
+          }
+        }
+        const int ca = chosen / L, cb = chosen % L;
+        if (lane == 0) {
+          const size_t idx = ((size_t)s * n + i0 + tk) * (g.R * g.groups) + (size_t)r * g.groups + grp;
+          a_out[idx] = (uint16_t)ca;
+          b_out[idx] = (uint16_t)cb;
+        }
+        for (int si = lane; si < gs; si += 32) {
+          const double2 ua = U[(size_t)si * L + ca], ub = U[(size_t)si * L + cb];
+          p[2 * si] = __dsub_rn(p[2 * si], __dadd_rn(ua.x, -ub.y));
+          p[2 * si + 1] = __dsub_rn(p[2 * si + 1], __dadd_rn(ua.y, ub.x));
+        }
+        __syncwarp();
+      }
+    }
+  }
+}
+
+// Exact brute-force encoder for shapes whose slice does not fit on chip:
+// one warp per token, centers read from global/L1.
+__global__ void __launch_bounds__(128)
+k_encode_keys_brute(Geom g, int n_slots, const double* __restrict__ atoms,
+                    const void* __restrict__ keys, int dtype, long long s_stride, long long n,
+                    uint16_t* __restrict__ a_out, uint16_t* __restrict__ b_out) {
+  extern __shared__ double sm[];  // [4 warps][d]
+  const int s = blockIdx.y, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const long long i = (long long)blockIdx.x * 4 + warp;
+  if (i >= n) return;
+  double* p = sm + (size_t)warp * g.d;
+  for (int e = lane; e < g.d; e += 32)
+    p[e] = load_elem(keys, dtype, (long long)s * s_stride + i * g.d + e);
+  __syncwarp();
+  const int slot = s % n_slots;
+  for (int r = 0; r < g.R; ++r)
+    for (int grp = 0; grp < g.groups; ++grp) {
+      const double2* U = reinterpret_cast<const double2*>(atoms) +
+                         ((size_t)(slot * g.R + r) * g.subs + (size_t)grp * g.g) * g.L;
+      double* pg = p + grp * 2 * g.g;
+      const int c = exact_search(pg, U, g.L, g.g, nullptr, nullptr, nullptr, false, 0.0);
+      const int ca = c / g.L, cb = c % g.L;
+      if (lane == 0) {
+        const size_t idx = ((size_t)s * n + i) * (g.R * g.groups) + (size_t)r * g.groups + grp;
+        a_out[idx] = (uint16_t)ca;
+        b_out[idx] = (uint16_t)cb;
+      }
+      __syncwarp();
+      for (int si = lane; si < g.g; si += 32) {
+        const double2 ua = U[(size_t)si * g.L + ca], ub = U[(size_t)si * g.L + cb];
+        pg[2 * si] = __dsub_rn(pg[2 * si], __dadd_rn(ua.x, -ub.y));
+        pg[2 * si + 1] = __dsub_rn(pg[2 * si + 1], __dadd_rn(ua.y, ub.x));
+      }
+      __syncwarp();
+    }
+}
+
+static size_t table_smem(const Geom& g) {
+  return sizeof(double) * (2 * (size_t)g.g * g.L + (size_t)g.L * g.L + (size_t)kEncTok * g.d +
+                           2 * (size_t)kEncWarps * g.L);
+}
+
+cudaError_t run_encode_keys(const Geom& g, int S, int n_slots, const KeyEncTables& tab,
+                            const void* keys, int dtype, long long s_stride, long long n,
+                            uint16_t* a, uint16_t* b, cudaStream_t st) {
+  if (n <= 0 || S <= 0) return cudaSuccess;
+  const size_t sm = table_smem(g);
+  cudaError_t e;
+  if (tab.base != nullptr && sm <= 200 * 1024) {
+    static bool attr = false;
+    if (!attr) {
+      e = cudaFuncSetAttribute(k_encode_keys_table, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               220 * 1024);
+      if (e != cudaSuccess) return e;
+      attr = true;
+    }
+    dim3 grid((unsigned)((n + kEncTok - 1) / kEncTok), S);
+    k_encode_keys_table<<<grid, kEncWarps * 32, sm, st>>>(g, n_slots, tab.atoms, tab.base,
+                                                         tab.maxnorm, keys, dtype, s_stride, n,
+                                                         a, b);
+  } else {
+    dim3 grid((unsigned)((n + 3) / 4), S);
+    k_encode_keys_brute<<<grid, 128, 4 * g.d * sizeof(double), st>>>(g, n_slots, tab.atoms, keys,
+                                                                     dtype, s_stride, n, a, b);
+  }
+  count_launch();
+  return cudaGetLastError();
+}
+
+bool key_tables_fit(const Geom& g) { return table_smem(g) <= 200 * 1024 && g.L <= 1024; }
+
+// ------------------------------------------------------------ values
+constexpr int kValTok = 16;
+
+// One CTA per (16-token tile, stream), blockDim = max(hidden, n_codes)
+// rounded to a warp multiple (<= 1024).
+__global__ void k_encode_values(Geom g, int n_slots, ValEncWeights w,
+                                const void* __restrict__ vals, int dtype, long long s_stride,
+                                long long n, uint8_t* __restrict__ bits,
+                                double* __restrict__ logits, int* __restrict__ err) {
+  extern __shared__ double sm[];
+  double* T = sm;                              // [kValTok][d]
+  double* H = T + (size_t)kValTok * g.d;       // [kValTok][hidden]
+  const int s = blockIdx.y, tid = threadIdx.x;
+  const long long i0 = (long long)blockIdx.x * kValTok;
+  const int nt = (int)min((long long)kValTok, n - i0);
+  const int slot = s % n_slots;
+  for (int e = tid; e < kValTok * g.d; e += blockDim.x)
+    T[e] = (e / g.d < nt)
+               ? load_elem(vals, dtype, (long long)s * s_stride + (i0 + e / g.d) * g.d + e % g.d)
+               : 0.0;
+  __syncthreads();
+  const double* w1 = w.w1 + (size_t)slot * g.d * g.hidden;
+  const double* b1 = w.b1 + (size_t)slot * g.hidden;
+  const double* w2 = w.w2 + (size_t)slot * g.hidden * g.n_codes;
+  const double* b2 = w.b2 + (size_t)slot * g.n_codes;
+  for (int j = tid; j < g.hidden; j += blockDim.x) {  // valquant.cpp:52-62
+    double h[kValTok];
+#pragma unroll
+    for (int k = 0; k < kValTok; ++k) h[k] = 0.0;
+    for (int i = 0; i < g.d; ++i) {
+      const double wv = w1[(size_t)i * g.hidden + j];
+#pragma unroll
+      for (int k = 0; k < kValTok; ++k) {
+        const double ti = T[k * g.d + i];
+        if (ti != 0.0) h[k] = __dadd_rn(h[k], __dmul_rn(ti, wv));
+      }
+    }
+    const double bj = b1[j];
+#pragma unroll
+    for (int k = 0; k < kValTok; ++k) {
+      double v = __dadd_rn(h[k], bj);
+      if (v < 0.0) v = 0.0;
+      H[k * g.hidden + j] = v;
+    }
+  }
+  __syncthreads();
+  for (int c = tid; c < g.n_codes; c += blockDim.x) {  // valquant.cpp:63-69, 98
+    double lg[kValTok];
+#pragma unroll
+    for (int k = 0; k < kValTok; ++k) lg[k] = 0.0;
+    for (int j = 0; j < g.hidden; ++j) {
+      const double wv = w2[(size_t)j * g.n_codes + c];
+#pragma unroll
+      for (int k = 0; k < kValTok; ++k) {
+        const double hj = H[k * g.hidden + j];
+        if (hj != 0.0) lg[k] = __dadd_rn(lg[k], __dmul_rn(hj, wv));
+      }
+    }
+    const double bc = b2[c];
+    for (int k = 0; k < nt; ++k) {
+      const double v = __dadd_rn(lg[k], bc);
+      if (!isfinite(v)) atomicExch(err, 1);
+      const size_t o = ((size_t)s * n + i0 + k) * g.n_codes + c;
+      bits[o] = v > 0.0 ? 1 : 0;
+      if (logits) logits[o] = v;
+    }
+  }
+}
+
+cudaError_t run_encode_values(const Geom& g, int S, int n_slots, const ValEncWeights& w,
+                              const void* vals, int dtype, long long s_stride, long long n,
+                              uint8_t* bits, double* logits, int* err_flag, cudaStream_t st) {
+  if (n <= 0 || S <= 0) return cudaSuccess;
+  int threads = ((g.hidden > g.n_codes ? g.hidden : g.n_codes) + 31) / 32 * 32;
+  if (threads > 1024) threads = 1024;
+  if (threads < 64) threads = 64;
+  const size_t sm = sizeof(double) * (size_t)kValTok * (g.d + g.hidden);
+  cudaError_t e;
+  if (sm > 48 * 1024) {
+    e = cudaFuncSetAttribute(k_encode_values, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if (e != cudaSuccess) return e;
+  }
+  dim3 grid((unsigned)((n + kValTok - 1) / kValTok), S);
+  k_encode_values<<<grid, threads, sm, st>>>(g, n_slots, w, vals, dtype, s_stride, n, bits, logits,
+                                             err_flag);
+  count_launch();
+  return cudaGetLastError();
+}
+
+}  // namespace cvq

@@ -1,0 +1,337 @@
+"""Parity of the sm_100a path (through the C-ABI) with the CPU oracle.
+
+Restates the reference's hot-path tests (test_attn.cpp, test_keyquant.cpp,
+test_valquant.cpp, test_cache.cpp, acceptance.cpp check 3 and 8) with the
+CUDA path as the implementation under test and oracle/cvq_oracle.c as the
+checker.  Bars (BASELINE.json north_star): packed codes bit-exact; scores and
+outputs within 1e-3 relative (asserted tighter where fp32 allows).
+"""
+import math
+
+import numpy as np
+import pytest
+
+from oracle.oracle import KQ, Oracle
+from tests import fixtures as fx
+
+pytestmark = pytest.mark.gpu
+
+P = Oracle("port")
+
+
+@pytest.fixture(scope="module")
+def G():
+    from paper_2506_18879_b200 import commvq
+    return commvq
+
+
+def scores_close(got, want, tol=1e-3):
+    scale = max(np.abs(want).max(), 1e-30)
+    return np.abs(got - want).max() <= tol * scale
+
+
+# ---------------------------------------------------------- attention
+def test_hand_expansion_two_tokens(G):
+    """test_attn.cpp:165-217 (fp32 path: 1e-6 instead of the fp64 1e-12)."""
+    kq = KQ(2, 1, 2, 1)
+    atoms = np.array([0.7, -0.2, -0.4, 1.1])
+    a, b = np.array([0, 1], np.uint16), np.array([1, 0], np.uint16)
+    vrows = np.array([[1.5, -0.5], [0.25, 2.0]])
+    bits = np.array([[1, 0], [1, 1]], np.uint8)
+    q = np.array([0.3, -0.8])
+    got, rep = G.fused_attention(kq, atoms, a, b, bits, vrows, q, 1)
+    want, pred, meas = P.fused_attention(kq, atoms, a, b, bits, vrows, q, 1)
+    assert np.allclose(got, want, rtol=1e-6, atol=1e-7)
+    assert rep.pathway == "fused" and (rep.predicted_mults, rep.measured_mults) == (pred, meas)
+
+
+@pytest.mark.parametrize("combo", [
+    (8, 2, 4, 1, 1, 8), (8, 2, 4, 1, 2, 8), (8, 2, 4, 3, 64, 8), (8, 4, 2, 2, 64, 16),
+    (16, 2, 4, 3, 64, 16), (16, 4, 8, 2, 256, 8), (16, 8, 4, 1, 256, 16), (8, 2, 4, 2, 1024, 8),
+])
+def test_fused_matches_oracle_across_configs(G, combo):
+    """test_attn.cpp:219-244 configurations, GPU vs oracle fused and naive."""
+    d, g, L, R, n, nc = combo
+    kq = KQ(d, g, L, R)
+    seed = 1000 + sum(combo)
+    atoms = fx.random_key_codebook(kq, seed)
+    a, b = fx.random_key_codes(kq, n, seed + 1)
+    bits = fx.random_value_codes(nc, n, seed + 2)
+    vrows = fx.random_value_codebook(nc, d, seed + 3)
+    q = fx.random_vec(d, seed + 4)
+    got, rep, sc = G.fused_attention(kq, atoms, a, b, bits, vrows, q, n - 1, return_scores=True)
+    want, pred, meas = P.fused_attention(kq, atoms, a, b, bits, vrows, q, n - 1)
+    assert fx.rel_err(got, want) <= 1e-5
+    assert scores_close(sc, P.fused_scores(kq, atoms, a, b, bits, vrows, q, n - 1), 1e-5)
+    assert (rep.predicted_mults, rep.measured_mults) == (pred, meas)
+    ngot, nrep = G.naive_attention(kq, atoms, a, b, bits, vrows, q, n - 1)
+    nwant, npred, nmeas = P.naive_attention(kq, atoms, a, b, bits, vrows, q, n - 1)
+    assert fx.rel_err(ngot, nwant) <= 1e-5
+    assert (nrep.predicted_mults, nrep.measured_mults) == (npred, nmeas)
+
+
+def test_acceptance_check3_equivalence(G):
+    """acceptance.cpp:169-219: 200 seeded instances (shared Rng 303), incl.
+    preset-shaped {128,64,64,11} and {128,64,2048,21}; bar rel_err <= 1e-3
+    (the reference's fused-vs-naive fp64 bar is 1e-5; we assert 1e-4)."""
+    rng = P.rng(303)
+    n_choices, r_choices, l_choices, g_choices = [1, 2, 64, 1024, 4096], [1, 3, 11], [4, 64], [2, 16, 64]
+    worst = 0.0
+    for i in range(200):
+        d = 64 if i % 2 == 0 else 128
+        n = n_choices[i % 5]
+        if i % 10 == 9:
+            d, group = 128, 64
+            levels = 2048 if i % 20 == 19 else 64
+            rounds = 21 if i % 20 == 19 else 11
+        else:
+            rounds = r_choices[i % 3]
+            levels = l_choices[(i // 2) % 2]
+            group = g_choices[(i // 3) % 3]
+            if group > d // 2 or (d // 2) % group != 0:
+                group = 2
+        nc = 8 << (i % 3)
+        kq = KQ(d, group, levels, rounds)
+        atoms = fx.random_key_codebook(kq, rng=rng)
+        a, b = fx.random_key_codes(kq, n, rng=rng)
+        bits = fx.random_value_codes(nc, n, rng=rng)
+        vrows = fx.random_value_codebook(nc, d, rng=rng)
+        q = rng.normal(d)
+        got, _ = G.fused_attention(kq, atoms, a, b, bits, vrows, q, n - 1)
+        want, _, _ = P.fused_attention(kq, atoms, a, b, bits, vrows, q, n - 1)
+        err = fx.rel_err(got, want)
+        worst = max(worst, err)
+        assert err <= 1e-4, (i, d, n, rounds, levels, group, err)
+    print("worst rel err", worst)
+
+
+def test_errors_mirror_reference(G):
+    """test_attn.cpp:246-263 + code range (attn.cpp:223-224)."""
+    kq = KQ(8, 2, 4, 1)
+    atoms = fx.random_key_codebook(kq, 21)
+    a, b = fx.random_key_codes(kq, 4, 22)
+    bits = fx.random_value_codes(8, 4, 23)
+    vrows = fx.random_value_codebook(8, 8, 24)
+    q = fx.random_vec(8, 25)
+    with pytest.raises(ValueError, match="precedes"):
+        G.fused_attention(kq, atoms, a, b, bits, vrows, q, 2)
+    with pytest.raises(ValueError, match="empty"):
+        G.fused_attention(kq, atoms, a[:0], b[:0], bits[:0], vrows, q, 0)
+    bad = a.copy()
+    bad[3] = 4
+    with pytest.raises(ValueError, match="out of range"):
+        G.fused_attention(kq, atoms, bad, b, bits, vrows, q, 3)
+    with pytest.raises(ValueError):
+        G.fused_attention(KQ(8, 3, 4, 1), atoms, a, b, bits, vrows, q, 3)
+
+
+@pytest.mark.parametrize("preset", ["1bit", "2bit"])
+def test_long_context_phase_precision(G, preset):
+    """Query far past the cache (Delta ~ 1e6): fp64-reduced phases keep the
+    scores within 1e-3 of max |s|."""
+    kq = KQ(128, 64, 64, 11 if preset == "1bit" else 21)
+    nc = 128 if preset == "1bit" else 256
+    n = 2048
+    rng = P.rng(77)
+    atoms = rng.normal(2 * kq.n_atoms, 0.3)
+    a, b = fx.random_key_codes(kq, n, rng=rng)
+    bits = fx.random_value_codes(nc, n, rng=rng)
+    vrows = rng.normal(nc * 128, 1 / 16).reshape(nc, 128)
+    q = rng.normal(128)
+    for t in (n - 1, n - 1 + 131072, n - 1 + 1_000_000):
+        got, _, sc = G.fused_attention(kq, atoms, a, b, bits, vrows, q, t, return_scores=True)
+        want, _, _ = P.fused_attention(kq, atoms, a, b, bits, vrows, q, t)
+        ws = P.fused_scores(kq, atoms, a, b, bits, vrows, q, t)
+        assert scores_close(sc, ws, 1e-4), t
+        assert fx.rel_err(got, want) <= 1e-3, t
+
+
+# ------------------------------------------------------------ encoders
+def test_encode_ties_to_smallest_pair(G):
+    """test_keyquant.cpp:179-193."""
+    kq = KQ(4, 2, 4, 1)
+    atoms = np.tile([1.0, -0.5], kq.n_atoms)
+    a, b = G.encode_keys(kq, atoms, fx.random_mat(16, 4, 77))
+    assert (a == 0).all() and (b == 0).all()
+
+
+@pytest.mark.parametrize("shape", [
+    (12, 3, 4, 2, 64), (8, 2, 4, 2, 100), (16, 4, 16, 3, 77), (128, 64, 64, 11, 96),
+    (128, 64, 64, 21, 40), (128, 16, 16, 4, 33), (32, 16, 256, 2, 20),
+])
+def test_encode_keys_bit_exact(G, shape):
+    d, g, L, R, n = shape
+    kq = KQ(d, g, L, R)
+    atoms = fx.random_key_codebook(kq, 41 + d, scale=0.3 if d == 128 else 1.0)
+    keys = P.gen_synth(n, d, min(d, 32), 42 + L)
+    ga, gb = G.encode_keys(kq, atoms, keys)
+    oa, ob = P.encode_keys(kq, atoms, keys)
+    assert (ga == oa).all() and (gb == ob).all()
+
+
+def test_encode_keys_near_ties_bit_exact(G):
+    """Points equidistant (in exact arithmetic) from two centers: the fp64
+    rounding of the reference sum decides -- exercises the exact re-check."""
+    kq = KQ(128, 64, 64, 3)
+    rng = P.rng(99)
+    atoms = rng.normal(2 * kq.n_atoms, 0.3)
+    xy = atoms.reshape(3, 64, 64, 2)
+    n = 64
+    keys = np.zeros((n, 128))
+    for i in range(n):
+        a1, b1, a2, b2 = rng.index(4, 64).tolist()
+        for j in range(64):
+            c1 = (xy[0, j, a1, 0] - xy[0, j, b1, 1], xy[0, j, a1, 1] + xy[0, j, b1, 0])
+            c2 = (xy[0, j, a2, 0] - xy[0, j, b2, 1], xy[0, j, a2, 1] + xy[0, j, b2, 0])
+            keys[i, 2 * j] = 0.5 * (c1[0] + c2[0])
+            keys[i, 2 * j + 1] = 0.5 * (c1[1] + c2[1])
+    ga, gb = G.encode_keys(kq, atoms, keys)
+    oa, ob = P.encode_keys(kq, atoms, keys)
+    assert (ga == oa).all() and (gb == ob).all()
+
+
+def test_value_encoder_bit_exact(G):
+    """test_valquant.cpp:108-112 KAT + random weights: bits and logits exact."""
+    w1, b1, w2 = np.zeros((4, 4)), np.zeros(4), np.zeros((4, 4))
+    b2 = np.array([2.0, -3.0, 0.5, -0.1])
+    bits, lg = G.encoder_forward_infer(w1, b1, w2, b2, np.array([[0.1, -0.2, 0.3, -0.4]]))
+    assert bits[0].tolist() == [1, 0, 1, 0] and (lg[0] == b2).all()
+    for d, hidden, nc, n in ((8, 16, 8, 33), (128, 256, 128, 100), (128, 512, 256, 40)):
+        rng = P.rng(d + hidden)
+        w1 = rng.normal(d * hidden, 0.1).reshape(d, hidden)
+        b1 = rng.normal(hidden, 0.05)
+        w2 = rng.normal(hidden * nc, 0.1).reshape(hidden, nc)
+        b2 = rng.normal(nc, 0.05)
+        vals = P.gen_synth(n, d, min(d, 32), 5)
+        vals[0, :3] = 0.0  # exercise the zero-skips
+        gb, gl = G.encoder_forward_infer(w1, b1, w2, b2, vals)
+        ob, ol = P.encoder_forward_infer(w1, b1, w2, b2, vals)
+        assert (gb == ob).all() and (gl == ol).all()
+    with pytest.raises(G.TrainingError):
+        G.encoder_forward_infer(np.zeros((4, 4)), np.zeros(4), np.zeros((4, 4)),
+                                np.array([np.inf, 0, 0, 0]), np.ones((1, 4)))
+
+
+# -------------------------------------------------------------- packing
+def test_pack_unpack_bit_exact(G):
+    """cache.cpp:90-155, test_cache.cpp:75-124 layouts, many sizes."""
+    assert G.pack_value_codes(np.array([[1, 0, 1, 0, 1]], np.uint8)).tolist() == [0b10101]
+    for kq, n in ((KQ(8, 2, 4, 2), 9), (KQ(128, 64, 64, 11), 333), (KQ(128, 64, 64, 21), 129),
+                  (KQ(16, 2, 16, 2), 4097), (KQ(16, 8, 2048, 2), 31)):
+        rng = P.rng(n)
+        a, b = fx.random_key_codes(kq, n, rng=rng)
+        w = G.pack_key_codes(kq, a, b)
+        assert (w == P.pack_key_codes(kq, a, b)).all()
+        ua, ub = G.unpack_key_codes(kq, w, n)
+        assert (ua == a).all() and (ub == b).all()
+        for nc in (8, 128, 256, 17):
+            bits = fx.random_value_codes(nc, n, rng=rng)
+            vw = G.pack_value_codes(bits)
+            assert (vw == P.pack_value_codes(bits)).all()
+            assert (G.unpack_value_codes(nc, vw, n) == bits).all()
+    with pytest.raises(ValueError):
+        G.unpack_key_codes(KQ(8, 2, 4, 1), np.array([1, 2], np.uint64), 1)
+
+
+# ---------------------------------------------------------------- cache
+def _cache_fixture(G, f, n_cap, **kw):
+    c = G.QuantizedKVCache(f.kq, f.vrows.shape[0], capacity=n_cap, hidden=f.w1.shape[1], **kw)
+    for layer in range(c.n_layers):
+        for head in range(c.n_kv_heads):
+            c.set_key_codebook(layer, head, f.atoms)
+            c.set_value_quantizer(layer, head, f.vrows, f.w1, f.b1, f.w2, f.b2)
+    return c
+
+
+def test_cache_prefill_equals_appends_and_reference_words(G):
+    """test_cache.cpp:155-180 plus word equality with oracle encode+pack."""
+    f = fx.CacheFixture()
+    keys, vals = fx.random_mat(24, 8, 81), fx.random_mat(24, 8, 82)
+    pre = _cache_fixture(G, f, 64)
+    pre.prefill(keys[None, None, None], vals[None, None, None])
+    inc = _cache_fixture(G, f, 64)
+    for t in range(24):
+        inc.append(keys[t][None, None, None], vals[t][None, None, None])
+    kw1, vw1 = pre.export_stream(0, 0, 0)
+    kw2, vw2 = inc.export_stream(0, 0, 0)
+    assert (kw1 == kw2).all() and (vw1 == vw2).all()
+    a, b = P.encode_keys(f.kq, f.atoms, keys)
+    bits, _ = P.encoder_forward_infer(f.w1, f.b1, f.w2, f.b2, vals)
+    assert (kw1 == P.pack_key_codes(f.kq, a, b)).all()
+    assert (vw1 == P.pack_value_codes(bits)).all()
+    assert pre.size() == 24
+
+
+def test_incremental_decode_matches_replay(G):
+    """test_cache.cpp:182-229 (bar 1e-6 in fp64; fp32 path asserted 1e-5)."""
+    f = fx.CacheFixture()
+    steps = 16
+    keys, vals, qs = fx.random_mat(steps, 8, 91), fx.random_mat(steps, 8, 92), fx.random_mat(steps, 8, 93)
+    c = _cache_fixture(G, f, 64)
+    a, b = P.encode_keys(f.kq, f.atoms, keys)
+    bits, _ = P.encoder_forward_infer(f.w1, f.b1, f.w2, f.b2, vals)
+    per = f.kq.rounds * f.kq.groups
+    for t in range(steps):
+        got = c.decode_step(keys[t][None, None, None], vals[t][None, None, None],
+                            qs[t][None, None, None].astype(np.float32))
+        want, _, _ = P.fused_attention(f.kq, f.atoms, a[:(t + 1) * per], b[:(t + 1) * per],
+                                       bits[:t + 1], f.vrows, qs[t], t)
+        assert fx.rel_err(got.reshape(-1), want) <= 1e-5
+
+
+def test_cache_multistream_gqa_c1_shape(G):
+    """C1 (BASELINE configs[0]): 1 layer, B=1, 8 KV / 32 q heads, 8K, 1-bit,
+    random codes imported as packed words; every q head vs the oracle."""
+    kq = KQ(128, 64, 64, 11)
+    nc, n, H, Gq = 128, 8192, 8, 4
+    rng = P.rng(2024)
+    c = G.QuantizedKVCache(kq, nc, n_kv_heads=H, q_per_kv=Gq, capacity=n)
+    streams = []
+    for h in range(H):
+        atoms = rng.normal(2 * kq.n_atoms, 0.3)
+        vrows = rng.normal(nc * 128, 1 / 16).reshape(nc, 128)
+        a, b = fx.random_key_codes(kq, n, rng=rng)
+        bits = fx.random_value_codes(nc, n, rng=rng)
+        c.set_key_codebook(0, h, atoms)
+        c.set_value_quantizer(0, h, vrows)
+        c.import_stream(0, 0, h, P.pack_key_codes(kq, a, b), P.pack_value_codes(bits), n)
+        streams.append((atoms, vrows, a, b, bits))
+    q = rng.normal(H * Gq * 128).reshape(1, 1, H * Gq, 128).astype(np.float32)
+    out = c.attention(q)
+    worst = 0.0
+    for h in range(H):
+        atoms, vrows, a, b, bits = streams[h]
+        for j in range(Gq):
+            want, _, _ = P.fused_attention(kq, atoms, a, b, bits, vrows,
+                                           q[0, 0, h * Gq + j].astype(np.float64), n - 1)
+            worst = max(worst, fx.rel_err(out[0, 0, h * Gq + j], want))
+    assert worst <= 1e-4, worst
+
+
+def test_cache_2bit_encode_decode_sample(G):
+    """C2-shaped (2-bit, encode + decode): GPU prefill codes bit-exact vs the
+    oracle on a sample, attention vs oracle over the GPU-encoded codes."""
+    kq = KQ(128, 64, 64, 21)
+    nc, hidden, n = 256, 512, 384
+    rng = P.rng(3)
+    atoms = rng.normal(2 * kq.n_atoms, 0.3)
+    vrows = rng.normal(nc * 128, 1 / 16).reshape(nc, 128)
+    w1 = rng.normal(128 * hidden, 0.1).reshape(128, hidden)
+    w2 = rng.normal(hidden * nc, 0.1).reshape(hidden, nc)
+    b1, b2 = np.zeros(hidden), np.zeros(nc)
+    K = P.gen_synth(n, 128, 32, 11)
+    V = P.gen_synth(n, 128, 32, 12)
+    c = G.QuantizedKVCache(kq, nc, capacity=n, hidden=hidden)
+    c.set_key_codebook(0, 0, atoms)
+    c.set_value_quantizer(0, 0, vrows, w1, b1, w2, b2)
+    c.prefill(K[None, None, None].astype(np.float32), V[None, None, None].astype(np.float32))
+    kw, vw = c.export_stream(0, 0, 0)
+    K32, V32 = K.astype(np.float32).astype(np.float64), V.astype(np.float32).astype(np.float64)
+    a, b = P.encode_keys(kq, atoms, K32)
+    bits, _ = P.encoder_forward_infer(w1, b1, w2, b2, V32)
+    assert (kw == P.pack_key_codes(kq, a, b)).all()
+    assert (vw == P.pack_value_codes(bits)).all()
+    q = rng.normal(128)
+    out = c.attention(q.reshape(1, 1, 1, 128).astype(np.float32))
+    want, _, _ = P.fused_attention(kq, atoms, a, b, bits, vrows, q, n - 1)
+    assert fx.rel_err(out.reshape(-1), want) <= 1e-4
