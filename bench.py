@@ -181,7 +181,10 @@ def main():
     lo, hi = min(N, rank * per), min(N, (rank + 1) * per)
     n_local = hi - lo
     extra = args.steps + args.warmup + 8
-    stream = torch.cuda.current_stream()
+    # a real (non-default) stream shared by torch and libcvq, so the CUDA
+    # events below see the library's kernels
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
     ctx = G.Context(local, stream.cuda_stream)
     cache = G.QuantizedKVCache(kq, nc, n_seqs=B, n_layers=layers, n_kv_heads=H, q_per_kv=Gq,
                                capacity=n_local + extra, hidden=2 * nc, position_offset=lo, ctx=ctx)

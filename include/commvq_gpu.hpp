@@ -1,0 +1,401 @@
+// commvq_gpu.hpp -- C++ drop-in adapter over libcvq_b200.so (include/cvq.h).
+//
+// Callers of the reference library commvq_core switch by namespace:
+//
+//   commvq::fused_attention(in, table)       ->  commvq::gpu::fused_attention(in, table)
+//   commvq::naive_quantized_attention(...)   ->  commvq::gpu::naive_quantized_attention(...)
+//   commvq::encode_keys(keys, cb)            ->  commvq::gpu::encode_keys(keys, cb)
+//   commvq::encoder_forward(t, enc, infer,.) ->  commvq::gpu::encoder_forward(...)
+//   commvq::pack_key_codes(...) & friends    ->  commvq::gpu::pack_key_codes(...)
+//   commvq::QuantizedKVCache                 ->  commvq::gpu::QuantizedKVCache
+//
+// Types are the reference's own public types (attn.hpp, keyquant.hpp,
+// valquant.hpp, cache.hpp), so this header is compiled with the reference's
+// include directory on the path; it adds no symbols to commvq_core and the
+// two can be linked into one binary (tests/cpp/parity.cpp does exactly that).
+// Preconditions and exception types mirror the reference functions cited
+// below; numerics run on the B200 (no CPU fallback).
+#pragma once
+
+#include <cmath>
+#include <cstdint>
+#include <cstdio>
+#include <fstream>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "commvq/attn.hpp"
+#include "commvq/cache.hpp"
+#include "commvq/error.hpp"
+#include "commvq/keyquant.hpp"
+#include "commvq/valquant.hpp"
+#include "cvq.h"
+
+namespace commvq {
+namespace gpu {
+
+inline void check(cvq_status s) {
+  if (s == CVQ_OK) return;
+  const std::string msg = cvq_last_error();
+  switch (s) {
+    case CVQ_EINVAL: throw std::invalid_argument(msg);
+    case CVQ_ETRAINING: throw TrainingError(msg);
+    case CVQ_ERANGE: throw std::out_of_range(msg);
+    case CVQ_EIO: throw IoError(msg);
+    default: throw std::runtime_error("libcvq_b200: " + msg);
+  }
+}
+
+// One context per thread on device 0 (calls on a context are serialised).
+inline cvq_context* context() {
+  struct Holder {
+    cvq_context* c = nullptr;
+    ~Holder() { cvq_context_destroy(c); }
+  };
+  thread_local Holder h;
+  if (!h.c) check(cvq_context_create(0, nullptr, &h.c));
+  return h.c;
+}
+
+inline cvq_key_config key_config(const KeyQuantConfig& c) {
+  return cvq_key_config{static_cast<uint32_t>(c.d), static_cast<uint32_t>(c.group_size),
+                        static_cast<uint32_t>(c.n_levels), static_cast<uint32_t>(c.rounds)};
+}
+
+inline std::vector<double> atoms_xy(const KeyCodebook& cb) {
+  std::vector<double> xy(2 * cb.atoms.size());
+  for (size_t i = 0; i < cb.atoms.size(); ++i) {
+    xy[2 * i] = cb.atoms[i].x;
+    xy[2 * i + 1] = cb.atoms[i].y;
+  }
+  return xy;
+}
+
+// validate_input (attn.cpp:91-110), including the RopeTable check.
+inline void validate(const AttnInput& in, const RopeTable& table) {
+  const KeyQuantConfig& kc = in.key_codebook.config;
+  const size_t n = in.key_codes.tokens;
+  if (n == 0) throw std::invalid_argument("attention: empty cache");
+  if (in.value_codes.tokens != n)
+    throw std::invalid_argument("attention: key/value token counts differ");
+  if (in.t + 1 < n) throw std::invalid_argument("attention: query position precedes cache");
+  if (in.q.size() != kc.d || in.value_codebook.d != kc.d || in.rope.d != kc.d)
+    throw std::invalid_argument("attention: dimension mismatch");
+  if (in.value_codes.n_codes != in.value_codebook.n_codes)
+    throw std::invalid_argument("attention: value codes/codebook mismatch");
+  if (in.key_codes.rounds != kc.rounds || in.key_codes.groups != kc.groups() ||
+      in.key_codes.n_levels != kc.n_levels)
+    throw std::invalid_argument("attention: key codes/codebook mismatch");
+  if (table.params().d != kc.d)
+    throw std::invalid_argument("attention: rope table dimension mismatch");
+}
+
+inline AttnResult attend(const AttnInput& in, RopeTable& table, bool naive) {
+  validate(in, table);
+  const KeyQuantConfig& kc = in.key_codebook.config;
+  const cvq_key_config ck = key_config(kc);
+  const std::vector<double> xy = atoms_xy(in.key_codebook);
+  AttnResult r;
+  r.out.assign(kc.d, 0.0);
+  cvq_flop_report fl{};
+  const uint32_t nc = static_cast<uint32_t>(in.value_codebook.n_codes);
+  if (naive)
+    check(cvq_naive_attention(context(), &ck, nc, xy.data(), in.key_codes.a.data(),
+                              in.key_codes.b.data(), in.key_codes.tokens,
+                              in.value_codes.bits.data(), in.value_codebook.rows.data.data(),
+                              in.q.data(), in.t, in.rope.base, r.out.data(), &fl));
+  else
+    check(cvq_fused_attention(context(), &ck, nc, xy.data(), in.key_codes.a.data(),
+                              in.key_codes.b.data(), in.key_codes.tokens,
+                              in.value_codes.bits.data(), in.value_codebook.rows.data.data(),
+                              in.q.data(), in.t, in.rope.base, r.out.data(), nullptr, &fl));
+  r.flops.pathway = naive ? "naive" : "fused";
+  r.flops.tokens = in.key_codes.tokens;
+  r.flops.d = kc.d;
+  r.flops.n_codes = in.value_codebook.n_codes;
+  r.flops.rounds = kc.rounds;
+  r.flops.n_levels = kc.n_levels;
+  r.flops.predicted_mults = fl.predicted_mults;
+  r.flops.measured_mults = fl.measured_mults;
+  return r;
+}
+
+// attn.hpp:62 / attn.cpp:164-263.  The RopeTable is not read (phases are
+// formed on the device from fp64-reduced angles) but its dimension is
+// checked as the reference does.
+inline AttnResult fused_attention(const AttnInput& in, RopeTable& table) {
+  return attend(in, table, false);
+}
+
+// attn.hpp:56 / attn.cpp:130-162.
+inline AttnResult naive_quantized_attention(const AttnInput& in, RopeTable& table) {
+  return attend(in, table, true);
+}
+
+// keyquant.hpp:135-136 / keyquant.cpp:705-739.  Codes are those of the
+// reference brute-force search for either AssignSearch value (the
+// reference's two searches agree, test_keyquant.cpp:159-177).
+inline KeyCodes encode_keys(const Mat& keys, const KeyCodebook& cb,
+                            AssignSearch = AssignSearch::brute_force) {
+  cb.config.validate();
+  if (keys.cols != cb.config.d) throw std::invalid_argument("encode_keys: keys width != d");
+  KeyCodes codes = KeyCodes::empty(cb.config, keys.rows);
+  if (keys.rows == 0) return codes;
+  const cvq_key_config ck = key_config(cb.config);
+  const std::vector<double> xy = atoms_xy(cb);
+  check(cvq_encode_keys(context(), &ck, xy.data(), keys.data.data(), keys.rows,
+                        codes.a.data(), codes.b.data()));
+  return codes;
+}
+
+// valquant.hpp:62-64, infer mode on the device (train mode draws Gumbel
+// noise from the caller's CPU Rng and is calibration, not the decode path).
+inline EncoderOut encoder_forward(const Vec& t, const ValueEncoder& enc, EncoderMode mode,
+                                  double temperature, Rng* = nullptr) {
+  if (t.size() != enc.d) throw std::invalid_argument("encoder_forward: input size != d");
+  if (!(temperature > 0.0)) throw std::invalid_argument("encoder_forward: temperature must be > 0");
+  if (mode != EncoderMode::infer)
+    throw std::invalid_argument("gpu::encoder_forward: only infer mode runs on the device");
+  EncoderOut out;
+  out.bits.resize(enc.n_codes);
+  out.logits.resize(enc.n_codes);
+  out.soft.resize(enc.n_codes);
+  check(cvq_encoder_forward_infer(context(), static_cast<uint32_t>(enc.d),
+                                  static_cast<uint32_t>(enc.hidden),
+                                  static_cast<uint32_t>(enc.n_codes), enc.w1.data.data(),
+                                  enc.b1.data(), enc.w2.data.data(), enc.b2.data(), t.data(), 1,
+                                  out.bits.data(), out.logits.data()));
+  for (size_t k = 0; k < enc.n_codes; ++k)  // valquant.cpp:96 (sigmoid of the raw logit)
+    out.soft[k] = 1.0 / (1.0 + std::exp(-(out.logits[k] / temperature)));
+  return out;
+}
+
+// cache.hpp:36-41.
+inline std::vector<uint64_t> pack_key_codes(const KeyCodes& codes) {
+  KeyQuantConfig c;
+  c.d = codes.groups ? 2 * codes.groups : 2;
+  c.group_size = 1;
+  c.n_levels = codes.n_levels;
+  c.rounds = codes.rounds;
+  const cvq_key_config ck = key_config(c);
+  const uint32_t bpt = cvq_bits_per_token(&ck);
+  if (bpt == 0) throw std::invalid_argument("pack_key_codes: n_levels not a power of two");
+  std::vector<uint64_t> w((codes.tokens * bpt + 63) / 64);
+  if (codes.tokens)
+    check(cvq_pack_key_codes(context(), &ck, codes.a.data(), codes.b.data(), codes.tokens,
+                             w.data()));
+  return w;
+}
+
+inline KeyCodes unpack_key_codes(const std::vector<uint64_t>& words, size_t tokens,
+                                 const KeyQuantConfig& config) {
+  config.validate();
+  KeyCodes codes = KeyCodes::empty(config, tokens);
+  const cvq_key_config ck = key_config(config);
+  check(cvq_unpack_key_codes(context(), &ck, words.data(), words.size(), tokens,
+                             codes.a.data(), codes.b.data()));
+  return codes;
+}
+
+inline std::vector<uint64_t> pack_value_codes(const ValueCodes& codes) {
+  std::vector<uint64_t> w((codes.tokens * codes.n_codes + 63) / 64);
+  if (codes.tokens)
+    check(cvq_pack_value_codes(context(), static_cast<uint32_t>(codes.n_codes),
+                               codes.bits.data(), codes.tokens, w.data()));
+  return w;
+}
+
+inline ValueCodes unpack_value_codes(const std::vector<uint64_t>& words, size_t tokens,
+                                     size_t n_codes) {
+  ValueCodes codes = ValueCodes::empty(n_codes, tokens);
+  check(cvq_unpack_value_codes(context(), static_cast<uint32_t>(n_codes), words.data(),
+                               words.size(), tokens, codes.bits.data()));
+  return codes;
+}
+
+// QuantizedKVCache (cache.hpp:63-113), single stream like the reference,
+// with the packed words resident in HBM.  save/load write and read the CVQC
+// format of cache.cpp:310-373, so caches move freely between the two.
+class QuantizedKVCache {
+ public:
+  QuantizedKVCache(std::shared_ptr<const KeyCodebook> key_codebook,
+                   std::shared_ptr<const ValueCodebook> value_codebook,
+                   std::shared_ptr<const ValueEncoder> encoder, size_t capacity = 1 << 16)
+      : kcb_(std::move(key_codebook)), vcb_(std::move(value_codebook)), enc_(std::move(encoder)) {
+    if (!kcb_) throw std::invalid_argument("cache: key codebook is null");
+    if (!vcb_) throw std::invalid_argument("cache: value codebook is null");
+    if (!enc_) throw std::invalid_argument("cache: encoder is null");
+    kcb_->config.validate();
+    if (vcb_->d != kcb_->config.d) throw std::invalid_argument("cache: key/value dimension mismatch");
+    if (enc_->d != kcb_->config.d || enc_->n_codes != vcb_->n_codes)
+      throw std::invalid_argument("cache: encoder does not match value codebook");
+    cvq_cache_desc d{};
+    d.key = key_config(kcb_->config);
+    d.n_codes = static_cast<uint32_t>(vcb_->n_codes);
+    d.hidden = static_cast<uint32_t>(enc_->hidden);
+    d.n_seqs = d.n_layers = d.n_kv_heads = d.q_per_kv = 1;
+    d.capacity = capacity;
+    d.rope_base = 10000.0;  // cache.cpp:47-50 uses the default base
+    check(cvq_cache_create(context(), &d, &c_));
+    const std::vector<double> xy = atoms_xy(*kcb_);
+    check(cvq_cache_set_key_codebook(c_, 0, 0, xy.data()));
+    check(cvq_cache_set_value_quantizer(c_, 0, 0, enc_->w1.data.data(), enc_->b1.data(),
+                                        enc_->w2.data.data(), enc_->b2.data(),
+                                        vcb_->rows.data.data()));
+  }
+  ~QuantizedKVCache() { cvq_cache_destroy(c_); }
+  QuantizedKVCache(const QuantizedKVCache&) = delete;
+  QuantizedKVCache& operator=(const QuantizedKVCache&) = delete;
+
+  static std::unique_ptr<QuantizedKVCache> prefill(
+      const Mat& keys, const Mat& values, std::shared_ptr<const KeyCodebook> kcb,
+      std::shared_ptr<const ValueCodebook> vcb, std::shared_ptr<const ValueEncoder> enc,
+      size_t capacity = 0) {
+    if (keys.rows != values.rows)
+      throw std::invalid_argument("prefill: key/value token count mismatch");
+    auto c = std::make_unique<QuantizedKVCache>(kcb, vcb, enc,
+                                                capacity ? capacity : keys.rows + 4096);
+    const size_t d = c->kcb_->config.d;
+    if (keys.rows > 0 && (keys.cols != d || values.cols != d))
+      throw std::invalid_argument("prefill: wrong dimension");
+    if (keys.rows)
+      check(cvq_cache_prefill(c->c_, keys.data.data(), values.data.data(), keys.rows, CVQ_F64,
+                              CVQ_HOST));
+    return c;
+  }
+
+  size_t size() const {
+    uint64_t n = 0;
+    check(cvq_cache_length(c_, &n));
+    return n;
+  }
+
+  void append(const Vec& key, const Vec& value) {
+    const size_t d = kcb_->config.d;
+    if (key.size() != d || value.size() != d) throw std::invalid_argument("append: wrong dimension");
+    check(cvq_cache_append(c_, key.data(), value.data(), CVQ_F64, CVQ_HOST));
+  }
+
+  Vec decode_step(const Vec& key, const Vec& value, const Vec& q, FlopReport* flops = nullptr) {
+    const size_t d = kcb_->config.d;
+    if (q.size() != d) throw std::invalid_argument("attention: dimension mismatch");
+    append(key, value);
+    std::vector<float> qf(q.begin(), q.end()), of(d);
+    check(cvq_cache_attention(c_, qf.data(), size() - 1, of.data(), CVQ_HOST));
+    if (flops) {
+      const KeyQuantConfig& kc = kcb_->config;
+      flops->pathway = "fused";
+      flops->tokens = size();
+      flops->d = d;
+      flops->n_codes = vcb_->n_codes;
+      flops->rounds = kc.rounds;
+      flops->n_levels = kc.n_levels;
+      flops->predicted_mults = predicted_flops_fused(size(), d, vcb_->n_codes, kc.rounds, kc.n_levels);
+      flops->measured_mults = 2 * d + 2 * d * kc.rounds * kc.n_levels +
+                              size() * (kc.rounds * d + 1) + vcb_->n_codes * d;
+    }
+    return Vec(of.begin(), of.end());
+  }
+
+  std::vector<uint64_t> packed_key_words() const { return export_words().first; }
+  std::vector<uint64_t> packed_value_words() const { return export_words().second; }
+
+  // CVQC v1 (cache.cpp:310-327): magic, version, d, g, L, R, N_c, tokens,
+  // key words, value words, all little-endian.
+  void save(const std::string& path) const {
+    auto [kw, vw] = export_words();
+    std::ofstream os(path, std::ios::binary | std::ios::trunc);
+    if (!os) throw IoError("cannot open for write: " + path);
+    const KeyQuantConfig& c = kcb_->config;
+    put32(os, 0x43515643u);
+    put32(os, 1);
+    put32(os, static_cast<uint32_t>(c.d));
+    put32(os, static_cast<uint32_t>(c.group_size));
+    put32(os, static_cast<uint32_t>(c.n_levels));
+    put32(os, static_cast<uint32_t>(c.rounds));
+    put32(os, static_cast<uint32_t>(vcb_->n_codes));
+    put64(os, size());
+    put64(os, kw.size());
+    for (uint64_t w : kw) put64(os, w);
+    put64(os, vw.size());
+    for (uint64_t w : vw) put64(os, w);
+    if (!os) throw IoError("write failed: " + path);
+  }
+
+  // cache.cpp:329-373.
+  static std::unique_ptr<QuantizedKVCache> load(const std::string& path,
+                                                std::shared_ptr<const KeyCodebook> kcb,
+                                                std::shared_ptr<const ValueCodebook> vcb,
+                                                std::shared_ptr<const ValueEncoder> enc,
+                                                size_t extra_capacity = 4096) {
+    std::ifstream is(path, std::ios::binary);
+    if (!is) throw IoError("cannot open: " + path);
+    if (get32(is) != 0x43515643u) throw IoError("not a cache file: " + path);
+    if (get32(is) != 1) throw IoError("unsupported cache version: " + path);
+    const uint32_t d = get32(is), g = get32(is), L = get32(is), r = get32(is), nc = get32(is);
+    if (!kcb || !vcb) throw std::invalid_argument("cache: codebook is null");
+    const KeyQuantConfig& cfg = kcb->config;
+    if (d != cfg.d || g != cfg.group_size || L != cfg.n_levels || r != cfg.rounds ||
+        nc != vcb->n_codes)
+      throw IoError("cache config does not match provided codebooks: " + path);
+    const uint64_t tokens = get64(is);
+    const uint64_t nkw = get64(is);
+    if (nkw != (tokens * cfg.bits_per_token() + 63) / 64)
+      throw IoError("cache key payload size mismatch: " + path);
+    std::vector<uint64_t> kw(nkw);
+    for (auto& w : kw) w = get64(is);
+    const uint64_t nvw = get64(is);
+    if (nvw != (tokens * nc + 63) / 64) throw IoError("cache value payload size mismatch: " + path);
+    std::vector<uint64_t> vw(nvw);
+    for (auto& w : vw) w = get64(is);
+    is.peek();
+    if (!is.eof()) throw IoError("trailing bytes in cache file: " + path);
+    try {  // BitBuffer::from_words padding check (cache.cpp:78-88)
+      gpu::unpack_key_codes(kw, tokens, cfg);
+      gpu::unpack_value_codes(vw, tokens, nc);
+    } catch (const std::invalid_argument& e) {
+      throw IoError(std::string("corrupt cache payload: ") + e.what());
+    }
+    auto c = std::make_unique<QuantizedKVCache>(kcb, vcb, enc, tokens + extra_capacity);
+    check(cvq_cache_import_stream(c->c_, 0, 0, 0, kw.data(), vw.data(), tokens, CVQ_HOST));
+    return c;
+  }
+
+ private:
+  std::pair<std::vector<uint64_t>, std::vector<uint64_t>> export_words() const {
+    const size_t n = size();
+    std::vector<uint64_t> kw((n * kcb_->config.bits_per_token() + 63) / 64);
+    std::vector<uint64_t> vw((n * vcb_->n_codes + 63) / 64);
+    if (n) check(cvq_cache_export_stream(c_, 0, 0, 0, kw.data(), vw.data(), CVQ_HOST));
+    return {std::move(kw), std::move(vw)};
+  }
+  static void put32(std::ostream& os, uint32_t v) {
+    unsigned char b[4] = {static_cast<unsigned char>(v), static_cast<unsigned char>(v >> 8),
+                          static_cast<unsigned char>(v >> 16), static_cast<unsigned char>(v >> 24)};
+    os.write(reinterpret_cast<const char*>(b), 4);
+  }
+  static void put64(std::ostream& os, uint64_t v) {
+    put32(os, static_cast<uint32_t>(v));
+    put32(os, static_cast<uint32_t>(v >> 32));
+  }
+  static uint32_t get32(std::istream& is) {
+    unsigned char b[4];
+    is.read(reinterpret_cast<char*>(b), 4);
+    if (!is) throw IoError("cache file: truncated read");
+    return uint32_t(b[0]) | uint32_t(b[1]) << 8 | uint32_t(b[2]) << 16 | uint32_t(b[3]) << 24;
+  }
+  static uint64_t get64(std::istream& is) {
+    const uint64_t lo = get32(is);
+    return lo | (uint64_t(get32(is)) << 32);
+  }
+
+  std::shared_ptr<const KeyCodebook> kcb_;
+  std::shared_ptr<const ValueCodebook> vcb_;
+  std::shared_ptr<const ValueEncoder> enc_;
+  cvq_cache* c_ = nullptr;
+};
+
+}  // namespace gpu
+}  // namespace commvq

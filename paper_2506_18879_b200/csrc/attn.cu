@@ -316,7 +316,7 @@ bool fast_path_applies(const AttnJob& job);
 size_t fast_scratch_bytes(const AttnJob& job, int* n_chunks);
 cudaError_t run_attention_fast(const AttnJob& job, const float* q, float* pm,
                                float* pl, float* po, int n_chunks, void* scratch,
-                               cudaStream_t st, cudaEvent_t* prof);
+                               cudaStream_t st, cudaEvent_t* prof, float* scores_out);
 
 static int generic_chunk(const AttnJob& job) {
   long long want = (job.n * (long long)job.S + 591) / 592;  // >= ~4 CTAs/SM
@@ -351,7 +351,7 @@ cudaError_t run_attention(const AttnJob& job, const float* q, float* out,
   const size_t need = attn_scratch_bytes(job, &nc);
   if (scratch_bytes < need || g.G > kMaxG) return cudaErrorInvalidValue;
   char* p = static_cast<char*>(scratch);
-  const bool fast = fast_path_applies(job) && scores_out == nullptr;
+  const bool fast = fast_path_applies(job);
   float* pm;
   float* pl;
   float* po;
@@ -361,7 +361,7 @@ cudaError_t run_attention(const AttnJob& job, const float* q, float* out,
     pm = reinterpret_cast<float*>(p + extra);
     pl = pm + (size_t)nc * rows;
     po = pl + (size_t)nc * rows;
-    e = run_attention_fast(job, q, pm, pl, po, nc, p, st, prof);
+    e = run_attention_fast(job, q, pm, pl, po, nc, p, st, prof, scores_out);
     if (e != cudaSuccess) return e;
   } else {
     const int CH = generic_chunk(job);

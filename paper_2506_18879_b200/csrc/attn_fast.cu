@@ -1,16 +1,482 @@
-// attn_fast.cu -- specialised decode-attention path (filled in below).
+// attn_fast.cu -- specialised CommVQ decode attention for the LLaMA-shaped
+// head presets (d = 128, one 64-subspace group per round, L = 64 levels,
+// R rounds, N_c value codes, G query heads per KV stream), sm_100a.
+//
+// Split of the work:
+//  F1 k_fast_score  grid (context chunks, stream x subspace-split).  Each CTA
+//     keeps its slice of the fp32 key codebook -- R x 64 levels x JC
+//     subspaces, 176 KiB at R=11/JC=32 and 168 KiB at R=21/JC=16 -- resident
+//     in shared memory, streams the packed key words of 128-token tiles with
+//     cp.async (double-buffered), unpacks the 6-bit fields once per tile and
+//     decodes K_j = sum_r U[r,a_r,j] + i U[r,b_r,j] with one lane per
+//     subspace (conflict-free 256-B row reads), applies the per-position
+//     RoPE phase (fp64-reduced base per 8-token run, fp32 recurrence inside),
+//     and reduces the G query-head dot products across lanes with a
+//     butterfly reduce-scatter.  Writes partial scores [S][JS][n][G].
+//  F2 k_fast_value  grid (context chunks, stream).  Sums the JS partial
+//     scores, softmax statistics of the chunk, z[k][h] += p_h(i) bit_k(i)
+//     from cp.async-staged value words (attn.cpp:239-247), then
+//     o = z . C_V / l (attn.cpp:249-255).  Writes the chunk partial (m, l, o)
+//     merged by k_combine (attn.cu).
+#include <cfloat>
+
 #include "cvq_internal.cuh"
 
 namespace cvq {
 
-bool fast_path_applies(const AttnJob&) { return false; }
-size_t fast_scratch_bytes(const AttnJob&, int* n_chunks) {
-  *n_chunks = 0;
-  return 0;
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kTile = 128;
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
 }
-cudaError_t run_attention_fast(const AttnJob&, const float*, float*, float*, float*, int, void*,
-                               cudaStream_t, cudaEvent_t*) {
-  return cudaErrorNotSupported;
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+struct FastArgs {
+  const uint64_t* kpool;
+  uint64_t kstride;
+  const uint64_t* vpool;
+  uint64_t vstride;
+  const float2* cb;   // [slot][R][64][64]
+  const float* cbv;   // [slot][NC][128]
+  int n_slots;
+  const float* q;     // [S][G][128]
+  const double* thetas;
+  long long t, pos0, n;
+  int chunk;          // F1 tokens per CTA (multiple of 128)
+  int chunk2;         // F2 tokens per CTA (multiple of 128)
+  int S;
+  float* ps;          // [S][JS][n][G] partial scores
+  float* scores_out;  // optional [S][G][n]
+  float *pm, *pl, *po;
+};
+
+// Butterfly reduce-scatter of NV values across the JC lanes of a group:
+// afterwards lane keeps max(NV/JC, 1) sums starting at value index `base`.
+// When NV < JC the last levels are plain butterfly sums; only lanes whose
+// bits at those levels are zero report (`writer`).
+template <int NV, int JC>
+__device__ __forceinline__ int reduce_scatter(float (&v)[NV], int lane, bool& writer) {
+  int base = 0;
+  int cnt = NV;
+  writer = true;
+#pragma unroll
+  for (int o = JC / 2; o >= 1; o >>= 1) {
+    const bool up = (lane & o) != 0;
+    if (cnt > 1) {
+      const int half = cnt / 2;
+#pragma unroll
+      for (int i = 0; i < NV / 2; ++i) {
+        if (i < half) {
+          const float send = up ? v[i] : v[i + half];
+          const float keep = up ? v[i + half] : v[i];
+          v[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+        }
+      }
+      if (up) base += half;
+      cnt = half;
+    } else {
+      v[0] += __shfl_xor_sync(0xffffffffu, v[0], o);
+      if (up) writer = false;
+    }
+  }
+  return base;
+}
+
+// packed fp32x2 add (FADD2 on sm_100a)
+__device__ __forceinline__ void add2(float2& acc, const float2 v) {
+  asm("{.reg .b64 a, b;\n\tmov.b64 a, {%0, %1};\n\tmov.b64 b, {%2, %3};\n\t"
+      "add.rn.f32x2 a, a, b;\n\tmov.b64 {%0, %1}, a;}"
+      : "+f"(acc.x), "+f"(acc.y)
+      : "f"(v.x), "f"(v.y));
+}
+
+constexpr int kF1Threads = 512;  // 16 warps: one 8-token run each per 128-token tile
+
+template <int R, int JC, int G>
+__global__ void __launch_bounds__(kF1Threads, 1) k_fast_score(FastArgs a) {
+  constexpr int JS = 64 / JC;
+  constexpr int TP = 32 / JC;                  // tokens per warp step
+  constexpr int NSTEP = 8 / TP;                // steps per run (8 tokens per warp)
+  constexpr int CW = ((2 * R + 15) / 16) * 16; // code bytes per token
+  constexpr int WPT = 24 * R;                  // words per 128-token tile (12R bits/token)
+  constexpr int NV = NSTEP * G;                // values per lane before reduction
+  static_assert(kF1Threads / 32 * 8 == kTile, "one pass per tile");
+  extern __shared__ __align__(16) unsigned char smem[];
+  float2* cbs = reinterpret_cast<float2*>(smem);                          // [R][64][JC]
+  uint64_t* wbuf = reinterpret_cast<uint64_t*>(smem + (size_t)R * 64 * JC * 8);  // [2][WPT]
+  uint8_t* codes = reinterpret_cast<uint8_t*>(wbuf + 2 * WPT);           // [kTile][CW]
+
+  const int s = blockIdx.y / JS, js = blockIdx.y % JS;
+  const long long i0 = (long long)blockIdx.x * a.chunk;
+  const long long i1 = min(a.n, i0 + a.chunk);
+  if (i0 >= i1) return;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int slot = s % a.n_slots;
+
+  const float2* cbg = a.cb + (size_t)slot * R * 64 * 64 + js * JC;
+  for (int e = tid; e < R * 64 * (JC / 2); e += kF1Threads) {
+    const int row = e / (JC / 2), c2 = e % (JC / 2);
+    cp_async16(cbs + row * JC + 2 * c2, cbg + (size_t)row * 64 + 2 * c2);
+  }
+  cp_async_commit();
+  const uint64_t* kw = a.kpool + (size_t)s * a.kstride + (size_t)(i0 / kTile) * WPT;
+  const int ntiles = (int)((i1 - i0 + kTile - 1) / kTile);
+  auto load_tile = [&](int k, int buf) {
+    const uint64_t* src = kw + (size_t)k * WPT;
+    for (int e = tid; e < WPT / 2; e += kF1Threads) cp_async16(wbuf + buf * WPT + 2 * e, src + 2 * e);
+    cp_async_commit();
+  };
+  load_tile(0, 0);
+
+  // per-lane constants: subspace j, query heads' conj(q_j)/sqrt(d), phase step
+  const int tg = lane / JC, jc = lane % JC;
+  const int j = js * JC + jc;
+  const double theta = a.thetas[j];
+  float2 w[G];
+#pragma unroll
+  for (int h = 0; h < G; ++h) {
+    const float* qr = a.q + ((size_t)s * G + h) * 128;
+    w[h] = make_float2(qr[2 * j] * 0.08838834764831845f, -qr[2 * j + 1] * 0.08838834764831845f);
+  }
+  float2 stepm;  // e^{+i TP theta}
+  {
+    double sn, cs;
+    sincos((double)TP * theta, &sn, &cs);
+    stepm = make_float2((float)cs, (float)sn);
+  }
+  float* ps = a.ps + ((size_t)(s * JS + js) * a.n) * G;
+
+  for (int k = 0; k < ntiles; ++k) {
+    if (k + 1 < ntiles) {
+      load_tile(k + 1, (k + 1) & 1);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    // unpack the tile's 6-bit fields (2R per token) into bytes
+    const uint64_t* wt = wbuf + (k & 1) * WPT;
+    for (int e = tid; e < kTile * 2 * R; e += kF1Threads) {
+      const int tok = e / (2 * R), f = e % (2 * R);
+      const unsigned bit = (unsigned)e * 6u;
+      const unsigned wi = bit >> 6, off = bit & 63u;
+      unsigned long long v = wt[wi] >> off;
+      if (off > 58u) v |= wt[wi + 1] << (64u - off);
+      codes[tok * CW + f] = (uint8_t)(v & 63u);
+    }
+    __syncthreads();
+    const long long ti = i0 + (long long)k * kTile;
+    const int valid = (int)min((long long)kTile, i1 - ti);
+    {
+      const int tok0 = warp * 8;
+      if (tok0 < valid) {
+      float2 ph = phase_neg(a.t - (a.pos0 + ti + tok0 + tg), theta);
+      float acc[NV];
+#pragma unroll
+      for (int st = 0; st < NSTEP; ++st) {
+        const int dlt = tok0 + st * TP + tg;
+        const uint4* cd = reinterpret_cast<const uint4*>(codes + dlt * CW);
+        uint4 cv[CW / 16];
+#pragma unroll
+        for (int c = 0; c < CW / 16; ++c) cv[c] = cd[c];
+        const uint32_t* cw = reinterpret_cast<const uint32_t*>(cv);
+        float2 ka = make_float2(0.f, 0.f), kb = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const uint32_t word = cw[(2 * r) >> 2];
+          const unsigned ca = __byte_perm(word, 0, 0x4440 | ((2 * r) & 3));
+          const unsigned cbb = __byte_perm(word, 0, 0x4440 | ((2 * r + 1) & 3));
+          add2(ka, cbs[(r * 64 + ca) * JC + jc]);
+          add2(kb, cbs[(r * 64 + cbb) * JC + jc]);
+        }
+        const float kx = ka.x - kb.y, ky = ka.y + kb.x;  // K = sum u_a + i sum u_b
+        const float rx = ph.x * kx - ph.y * ky;
+        const float ry = ph.x * ky + ph.y * kx;
+#pragma unroll
+        for (int h = 0; h < G; ++h) acc[st * G + h] = w[h].x * rx - w[h].y * ry;
+        const float nx = ph.x * stepm.x - ph.y * stepm.y;
+        ph.y = ph.x * stepm.y + ph.y * stepm.x;
+        ph.x = nx;
+      }
+      bool writer;
+      const int base = reduce_scatter<NV, JC>(acc, lane, writer);
+      constexpr int VPL = NV / JC > 0 ? NV / JC : 1;
+#pragma unroll
+      for (int m = 0; m < VPL; ++m) {
+        const int vi = base + m;
+        const int st = vi / G, h = vi % G;
+        const int dlt = tok0 + st * TP + tg;
+        if (writer && dlt < valid) ps[(ti + dlt) * G + h] = acc[m];
+      }
+      }
+    }
+    __syncthreads();
+  }
+}
+
+template <int NC, int G, int JS>
+__global__ void __launch_bounds__(kThreads) k_fast_value(FastArgs a) {
+  constexpr int CPL = NC / 32;       // codes per lane
+  constexpr int WPTOK = NC / 64;     // value words per token
+  extern __shared__ __align__(16) unsigned char smem[];
+  float* sc = reinterpret_cast<float*>(smem);                                 // [chunk2][G]
+  uint64_t* vw = reinterpret_cast<uint64_t*>(sc + (size_t)a.chunk2 * G);     // [chunk2][WPTOK]
+  float* zr = reinterpret_cast<float*>(vw + (size_t)a.chunk2 * WPTOK);       // [8][NC][G]
+  __shared__ float red[8][G];
+  __shared__ float mh[G], lh[G];
+  const int s = blockIdx.y;
+  const long long i0 = (long long)blockIdx.x * a.chunk2;
+  const long long i1 = min(a.n, i0 + a.chunk2);
+  const int cnt = (int)(i1 - i0);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+
+  // stage the chunk's value words (token-aligned, 16-B aligned)
+  const uint64_t* vsrc = a.vpool + (size_t)s * a.vstride + (size_t)i0 * WPTOK;
+  const int nw = ((cnt * WPTOK + 1) / 2) * 2;
+  for (int e = tid; e < nw / 2; e += kThreads) cp_async16(vw + 2 * e, vsrc + 2 * e);
+  cp_async_commit();
+
+  // full scores = sum of the JS partials; chunk max per head
+  float mx[G];
+#pragma unroll
+  for (int h = 0; h < G; ++h) mx[h] = -FLT_MAX;
+  for (int e = tid; e < cnt; e += kThreads) {
+    float v[G];
+#pragma unroll
+    for (int h = 0; h < G; ++h) v[h] = 0.f;
+#pragma unroll
+    for (int js = 0; js < JS; ++js) {
+      const float* p = a.ps + (((size_t)(s * JS + js) * a.n) + i0 + e) * G;
+#pragma unroll
+      for (int h = 0; h < G; ++h) v[h] += p[h];
+    }
+#pragma unroll
+    for (int h = 0; h < G; ++h) {
+      sc[e * G + h] = v[h];
+      mx[h] = fmaxf(mx[h], v[h]);
+      if (a.scores_out) a.scores_out[((size_t)s * G + h) * a.n + i0 + e] = v[h];
+    }
+  }
+#pragma unroll
+  for (int h = 0; h < G; ++h) {
+    float v = mx[h];
+    for (int o = 16; o; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+    if (lane == 0) red[warp][h] = v;
+  }
+  __syncthreads();
+  if (tid < G) {
+    float v = red[0][tid];
+    for (int w = 1; w < kThreads / 32; ++w) v = fmaxf(v, red[w][tid]);
+    mh[tid] = v;
+  }
+  __syncthreads();
+  float ls[G];
+#pragma unroll
+  for (int h = 0; h < G; ++h) ls[h] = 0.f;
+  for (int e = tid; e < cnt; e += kThreads) {
+#pragma unroll
+    for (int h = 0; h < G; ++h) {
+      const float p = __expf(sc[e * G + h] - mh[h]);
+      sc[e * G + h] = p;
+      ls[h] += p;
+    }
+  }
+#pragma unroll
+  for (int h = 0; h < G; ++h) {
+    float v = ls[h];
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) red[warp][h] = v;
+  }
+  cp_async_wait<0>();
+  __syncthreads();
+  if (tid < G) {
+    float v = 0.f;
+    for (int w = 0; w < kThreads / 32; ++w) v += red[w][tid];
+    lh[tid] = v;
+  }
+  // z[c][h] += p_h(i) * bit_c(i); lane owns codes [CPL*lane, CPL*lane+CPL)
+  float z[CPL][G];
+#pragma unroll
+  for (int c = 0; c < CPL; ++c)
+#pragma unroll
+    for (int h = 0; h < G; ++h) z[c][h] = 0.f;
+  const int wsel = (CPL * lane) >> 6, sh = (CPL * lane) & 63;
+#pragma unroll 4
+  for (int e = warp; e < cnt; e += kThreads / 32) {
+    const unsigned bits = (unsigned)(vw[(size_t)e * WPTOK + wsel] >> sh);
+    float p[G];
+#pragma unroll
+    for (int h = 0; h < G; ++h) p[h] = sc[e * G + h];
+#pragma unroll
+    for (int c = 0; c < CPL; ++c)
+      if (bits & (1u << c)) {
+#pragma unroll
+        for (int h = 0; h < G; ++h) z[c][h] += p[h];
+      }
+  }
+#pragma unroll
+  for (int c = 0; c < CPL; ++c)
+#pragma unroll
+    for (int h = 0; h < G; ++h) zr[((size_t)warp * NC + CPL * lane + c) * G + h] = z[c][h];
+  __syncthreads();
+  for (int e = tid; e < NC * G; e += kThreads) {
+    float v = 0.f;
+    for (int w = 0; w < kThreads / 32; ++w) v += zr[(size_t)w * NC * G + e];
+    zr[e] = v;  // warp-0 slot reused for the total
+  }
+  __syncthreads();
+  const float* cb = a.cbv + (size_t)(s % a.n_slots) * NC * 128;
+  const long long rows = (long long)a.S * G;
+  for (int e = tid; e < G * 128; e += kThreads) {
+    const int h = e / 128, jd = e % 128;
+    float acc = 0.f;
+#pragma unroll 8
+    for (int k = 0; k < NC; ++k) acc += zr[k * G + h] * __ldg(cb + (size_t)k * 128 + jd);
+    const long long row = (long long)s * G + h;
+    a.po[((long long)blockIdx.x * rows + row) * 128 + jd] = acc / lh[h];
+  }
+  if (tid < G) {
+    const long long row = (long long)s * G + tid;
+    a.pm[(long long)blockIdx.x * rows + row] = mh[tid];
+    a.pl[(long long)blockIdx.x * rows + row] = lh[tid];
+  }
+}
+
+int jc_for(int R) { return R <= 12 ? 32 : 16; }
+
+size_t f1_smem(int R, int JC) {
+  return (size_t)R * 64 * JC * 8 + 2 * 24 * R * 8 + (size_t)kTile * (((2 * R + 15) / 16) * 16);
+}
+
+int f1_chunk(const AttnJob& job) {
+  const int JS = 64 / jc_for(job.geo.R);
+  long long want = (job.n * (long long)job.S * JS + 2 * 148 - 1) / (2 * 148);
+  long long ch = (want + kTile - 1) / kTile * kTile;
+  if (ch < 512) ch = 512;
+  if (ch > 8192) ch = 8192;
+  return (int)ch;
+}
+
+int f2_chunk(const AttnJob& job) {
+  long long want = (job.n * (long long)job.S + 2 * 148 - 1) / (2 * 148);
+  long long ch = (want + kTile - 1) / kTile * kTile;
+  if (ch < 256) ch = 256;
+  if (ch > 2048) ch = 2048;
+  return (int)ch;
+}
+
+size_t f2_smem(const AttnJob& job, int chunk2) {
+  const Geom& g = job.geo;
+  return (size_t)chunk2 * g.G * 4 + (size_t)chunk2 * (g.n_codes / 64) * 8 + 16 +
+         (size_t)8 * g.n_codes * g.G * 4;
+}
+
+template <int R, int G>
+cudaError_t launch_f1(const FastArgs& a, int S, cudaStream_t st) {
+  constexpr int JC = R <= 12 ? 32 : 16;
+  constexpr int JS = 64 / JC;
+  const size_t sm = f1_smem(R, JC);
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(k_fast_score<R, JC, G>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  dim3 grid((unsigned)((a.n + a.chunk - 1) / a.chunk), S * JS);
+  k_fast_score<R, JC, G><<<grid, kF1Threads, sm, st>>>(a);
+  count_launch();
+  return cudaGetLastError();
+}
+
+template <int NC, int G, int JS>
+cudaError_t launch_f2(const FastArgs& a, size_t sm, cudaStream_t st) {
+  static size_t attr = 0;
+  if (sm > attr) {
+    cudaError_t e = cudaFuncSetAttribute(k_fast_value<NC, G, JS>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if (e != cudaSuccess) return e;
+    attr = sm;
+  }
+  dim3 grid((unsigned)((a.n + a.chunk2 - 1) / a.chunk2), a.S);
+  k_fast_value<NC, G, JS><<<grid, kThreads, sm, st>>>(a);
+  count_launch();
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+bool fast_path_applies(const AttnJob& job) {
+  const Geom& g = job.geo;
+  if (getenv("CVQ_DISABLE_FAST")) return false;
+  return g.d == 128 && g.groups == 1 && g.L == 64 && (g.R == 11 || g.R == 21) &&
+         (g.n_codes == 128 || g.n_codes == 256) && (g.G == 1 || g.G == 4) && job.n > 0;
+}
+
+size_t fast_scratch_bytes(const AttnJob& job, int* n_chunks) {
+  const int JS = 64 / jc_for(job.geo.R);
+  const int c2 = f2_chunk(job);
+  *n_chunks = (int)((job.n + c2 - 1) / c2);
+  const size_t ps = (size_t)job.S * JS * job.n * job.geo.G * sizeof(float);
+  return (ps + 255) / 256 * 256;
+}
+
+cudaError_t run_attention_fast(const AttnJob& job, const float* q, float* pm, float* pl,
+                               float* po, int n_chunks, void* scratch, cudaStream_t st,
+                               cudaEvent_t* prof, float* scores_out) {
+  const Geom& g = job.geo;
+  FastArgs a{};
+  a.kpool = job.kpool;
+  a.kstride = job.kstride;
+  a.vpool = job.vpool;
+  a.vstride = job.vstride;
+  a.cb = job.cb_key;
+  a.cbv = job.cb_val;
+  a.n_slots = job.n_slots;
+  a.q = q;
+  a.thetas = job.thetas;
+  a.t = job.t;
+  a.pos0 = job.pos0;
+  a.n = job.n;
+  a.chunk = f1_chunk(job);
+  a.chunk2 = f2_chunk(job);
+  a.S = job.S;
+  a.ps = static_cast<float*>(scratch);
+  a.scores_out = scores_out;
+  a.pm = pm;
+  a.pl = pl;
+  a.po = po;
+  (void)n_chunks;
+  cudaError_t e;
+  if (prof) cudaEventRecord(prof[0], st);
+  if (g.R == 11)
+    e = g.G == 4 ? launch_f1<11, 4>(a, job.S, st) : launch_f1<11, 1>(a, job.S, st);
+  else
+    e = g.G == 4 ? launch_f1<21, 4>(a, job.S, st) : launch_f1<21, 1>(a, job.S, st);
+  if (prof) cudaEventRecord(prof[1], st);
+  if (e != cudaSuccess) return e;
+  const size_t sm2 = f2_smem(job, a.chunk2);
+  const int JS = 64 / jc_for(g.R);
+  if (g.n_codes == 128) {
+    if (g.G == 4)
+      e = JS == 2 ? launch_f2<128, 4, 2>(a, sm2, st) : launch_f2<128, 4, 4>(a, sm2, st);
+    else
+      e = JS == 2 ? launch_f2<128, 1, 2>(a, sm2, st) : launch_f2<128, 1, 4>(a, sm2, st);
+  } else {
+    if (g.G == 4)
+      e = JS == 2 ? launch_f2<256, 4, 2>(a, sm2, st) : launch_f2<256, 4, 4>(a, sm2, st);
+    else
+      e = JS == 2 ? launch_f2<256, 1, 2>(a, sm2, st) : launch_f2<256, 1, 4>(a, sm2, st);
+  }
+  return e;
 }
 
 }  // namespace cvq

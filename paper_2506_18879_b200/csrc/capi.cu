@@ -353,8 +353,9 @@ CVQ_API cvq_status cvq_cache_create(cvq_context* ctx, const cvq_cache_desc* d, c
   c->n_slots = (int)(d->n_layers * d->n_kv_heads);
   const Geom& g = c->geo;
   // stream strides rounded to 32 B so 128-token tiles stay 32-B aligned
-  c->kstride = (words_for_bits(d->capacity * (uint64_t)g.bpt) + 4 + 3) / 4 * 4;
-  c->vstride = (words_for_bits(d->capacity * (uint64_t)g.n_codes) + 4 + 3) / 4 * 4;
+  const uint64_t cap128 = (d->capacity + 127) / 128 * 128;  // whole 128-token tiles
+  c->kstride = (words_for_bits(cap128 * (uint64_t)g.bpt) + 4 + 3) / 4 * 4;
+  c->vstride = (words_for_bits(cap128 * (uint64_t)g.n_codes) + 4 + 3) / 4 * 4;
   c->key_set.assign(c->n_slots, 0);
   c->val_set.assign(c->n_slots, 0);
   c->enc_set.assign(c->n_slots, 0);

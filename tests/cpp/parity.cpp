@@ -1,0 +1,170 @@
+// parity.cpp -- the drop-in claim, tested from C++: one binary links the
+// UNMODIFIED reference library (oracle/_ref/libcvq_ref.so, built from
+// /root/reference sources) and libcvq_b200.so through include/commvq_gpu.hpp,
+// and runs the reference's pinned scenarios through both namespaces side by
+// side (test_attn.cpp, test_keyquant.cpp, test_valquant.cpp, test_cache.cpp).
+// Needs a B200.  Prints one [PASS]/[FAIL] line per check; exit code = #fails.
+#include <cmath>
+#include <cstdio>
+#include <filesystem>
+#include <memory>
+#include <string>
+
+#include "commvq/attn.hpp"
+#include "commvq/cache.hpp"
+#include "commvq/keyquant.hpp"
+#include "commvq/rng.hpp"
+#include "commvq/valquant.hpp"
+#include "commvq_gpu.hpp"
+
+using namespace commvq;
+
+static int g_fail = 0;
+static void report(bool ok, const std::string& name, const std::string& detail = "") {
+  std::printf("[%s] %s %s\n", ok ? "PASS" : "FAIL", name.c_str(), detail.c_str());
+  if (!ok) ++g_fail;
+}
+
+static double rel_err(const Vec& a, const Vec& b) {  // test_attn.cpp:87-94
+  double num = 0, den = 0;
+  for (size_t i = 0; i < a.size(); ++i) {
+    num += (a[i] - b[i]) * (a[i] - b[i]);
+    den += b[i] * b[i];
+  }
+  return std::sqrt(num / std::max(den, 1e-300));
+}
+
+static KeyCodebook rand_kcb(const KeyQuantConfig& c, Rng& r, double s = 1.0) {
+  KeyCodebook cb = KeyCodebook::zeros(c);
+  for (CommMat& m : cb.atoms) m = comm_mat(s * r.normal(), s * r.normal());
+  return cb;
+}
+
+int main() {
+  // 1. fused attention: reference vs GPU, incl. preset head shapes
+  {
+    Rng rng(303);
+    struct S { size_t d, g, L, R, n, nc; double sc; };
+    const S shapes[] = {{8, 2, 4, 2, 1024, 8, 1.0},  {64, 16, 64, 3, 4096, 32, 1.0},
+                        {128, 64, 64, 11, 8192, 128, 0.3}, {128, 64, 64, 21, 4096, 256, 0.3},
+                        {128, 64, 2048, 21, 64, 32, 1.0}};
+    double worst = 0;
+    for (const S& s : shapes) {
+      KeyQuantConfig cfg{s.d, s.g, s.L, s.R};
+      KeyCodebook kcb = rand_kcb(cfg, rng, s.sc);
+      KeyCodes kc = KeyCodes::empty(cfg, s.n);
+      for (auto& v : kc.a) v = static_cast<uint16_t>(rng.index(s.L));
+      for (auto& v : kc.b) v = static_cast<uint16_t>(rng.index(s.L));
+      ValueCodes vc = ValueCodes::empty(s.nc, s.n);
+      for (auto& b : vc.bits) b = rng.next_u64() & 1;
+      ValueCodebook vcb = ValueCodebook::zeros(s.nc, s.d);
+      for (double& v : vcb.rows.data) v = rng.normal() * (s.sc < 1 ? 1.0 / 16 : 1.0);
+      Vec q(s.d);
+      for (double& v : q) v = rng.normal();
+      RopeParams rope = RopeParams::make(s.d);
+      AttnInput in{q, s.n - 1, kc, vc, kcb, vcb, rope};
+      RopeTable t1(rope), t2(rope);
+      AttnResult ref = commvq::fused_attention(in, t1);
+      AttnResult gpu = commvq::gpu::fused_attention(in, t2);
+      worst = std::max(worst, rel_err(gpu.out, ref.out));
+      report(gpu.flops.to_json() == ref.flops.to_json(), "flop report json d=" + std::to_string(s.d));
+    }
+    report(worst <= 1e-4, "fused_attention gpu vs reference", "worst rel_err " + std::to_string(worst));
+  }
+  // 2. encoders bit-exact
+  {
+    KeyQuantConfig cfg{128, 64, 64, 11};
+    Rng rng(7);
+    KeyCodebook kcb = rand_kcb(cfg, rng, 0.3);
+    Mat keys(200, 128);
+    for (double& v : keys.data) v = rng.normal() * 0.5;
+    KeyCodes ref = commvq::encode_keys(keys, kcb);
+    KeyCodes gpu = commvq::gpu::encode_keys(keys, kcb);
+    report(ref.a == gpu.a && ref.b == gpu.b, "encode_keys bit-exact (1bit preset, 200 tokens)");
+    ValueEncoder enc = ValueEncoder::zeros(128, 256, 128);
+    for (double& v : enc.w1.data) v = 0.1 * rng.normal();
+    for (double& v : enc.w2.data) v = 0.1 * rng.normal();
+    bool same = true;
+    for (size_t i = 0; i < 50; ++i) {
+      Vec t(keys.row(i).begin(), keys.row(i).end());
+      EncoderOut a = commvq::encoder_forward(t, enc, EncoderMode::infer, 1.0);
+      EncoderOut b = commvq::gpu::encoder_forward(t, enc, EncoderMode::infer, 1.0);
+      same = same && a.bits == b.bits && a.logits == b.logits;
+    }
+    report(same, "encoder_forward infer bits+logits exact");
+    report(commvq::pack_key_codes(ref) == commvq::gpu::pack_key_codes(gpu), "pack_key_codes words");
+  }
+  // 3. cache: prefill / decode_step / CVQC interop both ways
+  {
+    KeyQuantConfig cfg{16, 2, 16, 2};
+    Rng rng(808);
+    auto kcb = std::make_shared<KeyCodebook>(rand_kcb(cfg, rng));
+    auto vcb = std::make_shared<ValueCodebook>(ValueCodebook::zeros(16, 16));
+    for (double& v : vcb->rows.data) v = 0.5 * rng.normal();
+    auto enc = std::make_shared<ValueEncoder>(ValueEncoder::zeros(16, 32, 16));
+    for (double& v : enc->w1.data) v = 0.4 * rng.normal();
+    for (double& v : enc->w2.data) v = 0.4 * rng.normal();
+    for (double& v : enc->b1) v = 0.1 * rng.normal();
+    for (double& v : enc->b2) v = 0.1 * rng.normal();
+    const size_t n = 512;
+    Mat keys(n, 16), values(n, 16), qs(n, 16);
+    for (double& v : keys.data) v = rng.normal();
+    for (double& v : values.data) v = rng.normal();
+    for (double& v : qs.data) v = rng.normal();
+    QuantizedKVCache ref(kcb, vcb, enc);
+    gpu::QuantizedKVCache gc(kcb, vcb, enc, n + 8);
+    double worst = 0;
+    for (size_t t = 0; t < n; ++t) {
+      Vec k(keys.row(t).begin(), keys.row(t).end()), v(values.row(t).begin(), values.row(t).end());
+      Vec q(qs.row(t).begin(), qs.row(t).end());
+      Vec a = ref.decode_step(k, v, q);
+      Vec b = gc.decode_step(k, v, q);
+      worst = std::max(worst, rel_err(b, a));
+    }
+    report(worst <= 1e-4, "decode_step incremental gpu vs reference", std::to_string(worst));
+    report(gc.packed_key_words() == ref.packed_keys().words() &&
+               gc.packed_value_words() == ref.packed_values().words(),
+           "incremental packed words identical");
+    auto pre = gpu::QuantizedKVCache::prefill(keys, values, kcb, vcb, enc);
+    report(pre->packed_key_words() == ref.packed_keys().words(), "gpu prefill == reference appends");
+    const auto dir = std::filesystem::temp_directory_path();
+    const std::string p1 = (dir / "cvq_gpu.cvqc").string(), p2 = (dir / "cvq_ref.cvqc").string();
+    gc.save(p1);
+    QuantizedKVCache back = QuantizedKVCache::load(p1, kcb, vcb, enc);
+    report(back.packed_keys().words() == ref.packed_keys().words(), "reference loads GPU CVQC");
+    ref.save(p2);
+    auto gback = gpu::QuantizedKVCache::load(p2, kcb, vcb, enc);
+    report(gback->packed_key_words() == ref.packed_keys().words() && gback->size() == n,
+           "GPU loads reference CVQC");
+    bool threw = false;
+    try {
+      gpu::QuantizedKVCache::load(p2 + ".missing", kcb, vcb, enc);
+    } catch (const IoError&) {
+      threw = true;
+    }
+    report(threw, "missing file -> IoError");
+    std::filesystem::remove(p1);
+    std::filesystem::remove(p2);
+  }
+  // 4. exceptions mirror the reference
+  {
+    KeyQuantConfig cfg{8, 2, 4, 1};
+    KeyCodebook kcb = KeyCodebook::zeros(cfg);
+    KeyCodes kc = KeyCodes::empty(cfg, 4);
+    ValueCodes vc = ValueCodes::empty(8, 4);
+    ValueCodebook vcb = ValueCodebook::zeros(8, 8);
+    Vec q(8, 0.1);
+    RopeParams rope = RopeParams::make(8);
+    RopeTable table(rope);
+    AttnInput early{q, 2, kc, vc, kcb, vcb, rope};
+    bool threw = false;
+    try {
+      gpu::fused_attention(early, table);
+    } catch (const std::invalid_argument&) {
+      threw = true;
+    }
+    report(threw, "query before cache -> invalid_argument");
+  }
+  std::printf("%d failure(s)\n", g_fail);
+  return g_fail;
+}

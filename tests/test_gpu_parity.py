@@ -335,3 +335,49 @@ def test_cache_2bit_encode_decode_sample(G):
     out = c.attention(q.reshape(1, 1, 1, 128).astype(np.float32))
     want, _, _ = P.fused_attention(kq, atoms, a, b, bits, vrows, q, n - 1)
     assert fx.rel_err(out.reshape(-1), want) <= 1e-4
+
+
+@pytest.mark.parametrize("preset,n", [("1bit", 1), ("1bit", 127), ("1bit", 129), ("1bit", 3001),
+                                      ("2bit", 5), ("2bit", 1000), ("2bit", 2177)])
+def test_fast_path_tiles_vs_oracle_and_generic(G, preset, n, monkeypatch):
+    """The specialised kernels (attn_fast.cu) on partial tiles / chunks, GQA=4,
+    two sequences x two layers; each q head vs the oracle, and fast == generic."""
+    kq = KQ(128, 64, 64, 11 if preset == "1bit" else 21)
+    nc = 128 if preset == "1bit" else 256
+    B, Ly, H, Gq = 2, 2, 2, 4
+    rng = P.rng(n + nc)
+    c = G.QuantizedKVCache(kq, nc, n_seqs=B, n_layers=Ly, n_kv_heads=H, q_per_kv=Gq, capacity=n)
+    books = {}
+    for layer in range(Ly):
+        for h in range(H):
+            atoms = rng.normal(2 * kq.n_atoms, 0.3)
+            vrows = rng.normal(nc * 128, 1 / 16).reshape(nc, 128)
+            c.set_key_codebook(layer, h, atoms)
+            c.set_value_quantizer(layer, h, vrows)
+            books[layer, h] = (atoms, vrows)
+    codes = {}
+    for sq in range(B):
+        for layer in range(Ly):
+            for h in range(H):
+                a, b = fx.random_key_codes(kq, n, rng=rng)
+                bits = fx.random_value_codes(nc, n, rng=rng)
+                c.import_stream(sq, layer, h, P.pack_key_codes(kq, a, b), P.pack_value_codes(bits), n)
+                codes[sq, layer, h] = (a, b, bits)
+    q = rng.normal(B * Ly * H * Gq * 128).reshape(B, Ly, H * Gq, 128).astype(np.float32)
+    t = n - 1 + 777
+    out = c.attention(q, t)
+    monkeypatch.setenv("CVQ_DISABLE_FAST", "1")
+    out_generic = c.attention(q, t)
+    monkeypatch.delenv("CVQ_DISABLE_FAST")
+    assert fx.rel_err(out, out_generic) <= 1e-5
+    worst = 0.0
+    for sq in range(B):
+        for layer in range(Ly):
+            for h in range(H):
+                atoms, vrows = books[layer, h]
+                a, b, bits = codes[sq, layer, h]
+                for j in range(Gq):
+                    want, _, _ = P.fused_attention(kq, atoms, a, b, bits, vrows,
+                                                   q[sq, layer, h * Gq + j].astype(np.float64), t)
+                    worst = max(worst, fx.rel_err(out[sq, layer, h * Gq + j], want))
+    assert worst <= 1e-4, worst
