@@ -157,6 +157,8 @@ def main():
     ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--keys", default="fp32", choices=["fp32", "fp16"],
+                    help="on-chip key-codebook precision (accumulation is fp32 either way)")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
     if args.impl == "reference":
@@ -177,8 +179,8 @@ def main():
     kq = G.KeyQuantConfig(d, g, L, R)
     S, rows = B * layers * H, B * layers * H * Gq
     # contiguous context shards, boundaries at multiples of 128 tokens
-    per = ((N + world - 1) // world + 127) // 128 * 128
-    lo, hi = min(N, rank * per), min(N, (rank + 1) * per)
+    from paper_2506_18879_b200.dist import gather_partials, shard_plan
+    lo, hi = shard_plan(N, world)[rank]
     n_local = hi - lo
     extra = args.steps + args.warmup + 8
     # a real (non-default) stream shared by torch and libcvq, so the CUDA
@@ -187,7 +189,8 @@ def main():
     torch.cuda.set_stream(stream)
     ctx = G.Context(local, stream.cuda_stream)
     cache = G.QuantizedKVCache(kq, nc, n_seqs=B, n_layers=layers, n_kv_heads=H, q_per_kv=Gq,
-                               capacity=n_local + extra, hidden=2 * nc, position_offset=lo, ctx=ctx)
+                               capacity=n_local + extra, hidden=2 * nc, position_offset=lo, ctx=ctx,
+                               keys_fp16=args.keys == "fp16")
     rs = np.random.default_rng(1234)
     for layer in range(layers):
         for h in range(H):
@@ -219,19 +222,12 @@ def main():
     m_p = torch.empty(rows, device="cuda")
     l_p = torch.empty(rows, device="cuda")
     o_p = torch.empty(rows, d, device="cuda")
-    gm = torch.empty(world, rows, device="cuda")
-    gl = torch.empty(world, rows, device="cuda")
-    go = torch.empty(world, rows, d, device="cuda")
-
     def step():
         if world == 1:
             cache.attention(q, t_q, out)
         else:
-            import torch.distributed as dist
             cache.attention_partial(q, m_p, l_p, o_p, t_q)
-            dist.all_gather_into_tensor(gm, m_p)
-            dist.all_gather_into_tensor(gl, l_p)
-            dist.all_gather_into_tensor(go.view(world, -1), o_p.view(-1))
+            gm, gl, go = gather_partials(m_p, l_p, o_p)  # NCCL all-gather, 520 B/row
             G.lse_combine(gm, gl, go, out, ctx)
 
     def barrier():
@@ -309,9 +305,10 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
             threads = os.cpu_count() or 1
-            v, secs, kind = cpu_reference(cfg, max(threads, 8), threads)
+            n_calls = 4 * threads  # ~0.5 s per call per core at 128K: ~2 s wall
+            v, secs, kind = cpu_reference(cfg, n_calls, threads)
             cpu = {"value": v, "unit": "KV-tokens/s", "cores": threads, "kind": kind,
-                   "sample": f"{max(threads, 8)} q-head fused_attention calls at N={N} "
+                   "sample": f"{n_calls} q-head fused_attention calls at N={N} "
                              f"({secs:.1f} s wall)"}
         except Exception as ex:  # reported, never fatal
             cpu = {"value": None, "unit": "KV-tokens/s", "cores": 0, "kind": "reference",
@@ -322,7 +319,8 @@ def main():
             "metric": "CommVQ decode-attention KV-tokens/s @128K ctx", "value": value,
             "unit": "KV-tokens/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
-            "vs_baseline": None, "dtype": "f32 (fp64-reduced phases; int codes)",
+            "vs_baseline": None,
+            "dtype": "f32 accumulate, %s key codebook (fp64-reduced phases; int codes)" % args.keys,
             "data": "synthetic (random codebooks, random packed codes, random q)",
             "config": {"workload": args.config, "n_layers": layers, "n_seqs": B,
                        "n_kv_heads": H, "q_per_kv": Gq, "context": N, "key": [d, g, L, R],

@@ -180,7 +180,14 @@ typedef struct cvq_cache_desc {
   uint64_t capacity;   /* max tokens per stream             */
   uint64_t position_offset;
   double rope_base;    /* RopeParams::base (rope.hpp:17)    */
+  uint32_t flags;      /* CVQ_CACHE_* below                 */
 } cvq_cache_desc;
+
+/* Keep the on-chip copy of the key codebook as fp16 (x, y) pairs with fp32
+ * accumulation: half the shared-memory traffic of the score kernel, output
+ * error ~1e-5 at the bench's codebook scale ("precision modes").
+ * Default (0): fp32 codebook. */
+#define CVQ_CACHE_KEYS_FP16 1u
 
 CVQ_API cvq_status cvq_cache_create(cvq_context* ctx, const cvq_cache_desc* d,
                                     cvq_cache** out);

@@ -85,7 +85,11 @@ class _Flops(C.Structure):
 class _Desc(C.Structure):
     _fields_ = [("key", _KC), ("n_codes", _u32), ("hidden", _u32), ("n_seqs", _u32),
                 ("n_layers", _u32), ("n_kv_heads", _u32), ("q_per_kv", _u32),
-                ("capacity", _u64), ("position_offset", _u64), ("rope_base", _d)]
+                ("capacity", _u64), ("position_offset", _u64), ("rope_base", _d),
+                ("flags", _u32)]
+
+
+CVQ_CACHE_KEYS_FP16 = 1
 
 
 @dataclass(frozen=True)
@@ -353,15 +357,18 @@ class QuantizedKVCache:
     """
 
     def __init__(self, kq, n_codes, n_seqs=1, n_layers=1, n_kv_heads=1, q_per_kv=1,
-                 capacity=1024, hidden=0, position_offset=0, rope_base=10000.0, ctx=None):
+                 capacity=1024, hidden=0, position_offset=0, rope_base=10000.0, ctx=None,
+                 keys_fp16=False):
         self.kq = _kc(kq)
         self.ctx = ctx or default_context()
         self.n_codes, self.hidden = n_codes, hidden
         self.n_seqs, self.n_layers, self.n_kv_heads, self.q_per_kv = (n_seqs, n_layers,
                                                                       n_kv_heads, q_per_kv)
         self.capacity, self.position_offset = capacity, position_offset
+        self.keys_fp16 = bool(keys_fp16)
         d = _Desc(self.kq._c(), n_codes, hidden, n_seqs, n_layers, n_kv_heads, q_per_kv,
-                  capacity, position_offset, rope_base)
+                  capacity, position_offset, rope_base,
+                  CVQ_CACHE_KEYS_FP16 if keys_fp16 else 0)
         h = _p()
         _check(_lib.cvq_cache_create(self.ctx.h, C.byref(d), C.byref(h)))
         self.h = h

@@ -45,6 +45,7 @@ struct FastArgs {
   const uint64_t* vpool;
   uint64_t vstride;
   const float2* cb;   // [slot][R][64][64]
+  const uint32_t* cbh;  // same, packed (x, y) half2 (fp16-codebook mode) or null
   const float* cbv;   // [slot][NC][128]
   int n_slots;
   const float* q;     // [S][G][128]
@@ -222,6 +223,161 @@ __global__ void __launch_bounds__(kF1Threads, 1) k_fast_score(FastArgs a) {
   }
 }
 
+
+// f32 += f16 (FHADD on sm_100a) for both halves of a packed (x, y) half2.
+__device__ __forceinline__ void hadd2_acc(float2& acc, uint32_t h2) {
+  asm("{.reg .b16 lo, hi;\n\tmov.b32 {lo, hi}, %2;\n\t"
+      "add.rn.f32.f16 %0, lo, %0;\n\tadd.rn.f32.f16 %1, hi, %1;}"
+      : "+f"(acc.x), "+f"(acc.y)
+      : "r"(h2));
+}
+
+// fp16-codebook variant of k_fast_score: the slice is stored as packed
+// (x, y) half2, accumulation stays fp32 (FHADD), so each gather moves half
+// the shared-memory bytes.  Each lane owns SPL consecutive subspaces; the 32
+// lanes of a warp decode one token per step.  JC = 32*SPL subspaces per CTA:
+// the whole 64-subspace codebook for R <= 13 (SPL = 2, no split).
+template <int R, int SPL, int G>
+__global__ void __launch_bounds__(kF1Threads, 1) k_fast_score_h(FastArgs a) {
+  constexpr int JC = 32 * SPL;
+  constexpr int JS = 64 / JC;
+  constexpr int NSTEP = 8;
+  constexpr int CW = ((2 * R + 15) / 16) * 16;
+  constexpr int WPT = 24 * R;
+  constexpr int NV = NSTEP * G;
+  static_assert(kF1Threads / 32 * 8 == kTile, "one pass per tile");
+  extern __shared__ __align__(16) unsigned char smem[];
+  uint32_t* cbs = reinterpret_cast<uint32_t*>(smem);                           // [R][64][JC] half2
+  uint64_t* wbuf = reinterpret_cast<uint64_t*>(smem + (size_t)R * 64 * JC * 4);  // [2][WPT]
+  uint8_t* codes = reinterpret_cast<uint8_t*>(wbuf + 2 * WPT);                 // [kTile][CW]
+
+  const int s = blockIdx.y / JS, js = blockIdx.y % JS;
+  const long long i0 = (long long)blockIdx.x * a.chunk;
+  const long long i1 = min(a.n, i0 + a.chunk);
+  if (i0 >= i1) return;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int slot = s % a.n_slots;
+
+  const uint32_t* cbg = a.cbh + (size_t)slot * R * 64 * 64 + js * JC;
+  for (int e = tid; e < R * 64 * (JC / 4); e += kF1Threads) {
+    const int row = e / (JC / 4), c4 = e % (JC / 4);
+    cp_async16(cbs + row * JC + 4 * c4, cbg + (size_t)row * 64 + 4 * c4);
+  }
+  cp_async_commit();
+  const uint64_t* kw = a.kpool + (size_t)s * a.kstride + (size_t)(i0 / kTile) * WPT;
+  const int ntiles = (int)((i1 - i0 + kTile - 1) / kTile);
+  auto load_tile = [&](int k, int buf) {
+    const uint64_t* src = kw + (size_t)k * WPT;
+    for (int e = tid; e < WPT / 2; e += kF1Threads) cp_async16(wbuf + buf * WPT + 2 * e, src + 2 * e);
+    cp_async_commit();
+  };
+  load_tile(0, 0);
+
+  double theta[SPL];
+  float2 stepm[SPL], w[G][SPL];
+#pragma unroll
+  for (int m = 0; m < SPL; ++m) {
+    const int j = js * JC + lane * SPL + m;
+    theta[m] = a.thetas[j];
+    double sn, cs;
+    sincos(theta[m], &sn, &cs);
+    stepm[m] = make_float2((float)cs, (float)sn);
+#pragma unroll
+    for (int h = 0; h < G; ++h) {
+      const float* qr = a.q + ((size_t)s * G + h) * 128;
+      w[h][m] = make_float2(qr[2 * j] * 0.08838834764831845f, -qr[2 * j + 1] * 0.08838834764831845f);
+    }
+  }
+  float* ps = a.ps + ((size_t)(s * JS + js) * a.n) * G;
+
+  for (int k = 0; k < ntiles; ++k) {
+    if (k + 1 < ntiles) {
+      load_tile(k + 1, (k + 1) & 1);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    const uint64_t* wt = wbuf + (k & 1) * WPT;
+    for (int e = tid; e < kTile * 2 * R; e += kF1Threads) {
+      const int tok = e / (2 * R), f = e % (2 * R);
+      const unsigned bit = (unsigned)e * 6u;
+      const unsigned wi = bit >> 6, off = bit & 63u;
+      unsigned long long v = wt[wi] >> off;
+      if (off > 58u) v |= wt[wi + 1] << (64u - off);
+      codes[tok * CW + f] = (uint8_t)(v & 63u);
+    }
+    __syncthreads();
+    const long long ti = i0 + (long long)k * kTile;
+    const int valid = (int)min((long long)kTile, i1 - ti);
+    const int tok0 = warp * 8;
+    if (tok0 < valid) {
+      float2 ph[SPL];
+#pragma unroll
+      for (int m = 0; m < SPL; ++m) ph[m] = phase_neg(a.t - (a.pos0 + ti + tok0), theta[m]);
+      float acc[NV];
+#pragma unroll
+      for (int st = 0; st < NSTEP; ++st) {
+        const int dlt = tok0 + st;
+        const uint4* cd = reinterpret_cast<const uint4*>(codes + dlt * CW);
+        uint4 cv[CW / 16];
+#pragma unroll
+        for (int c = 0; c < CW / 16; ++c) cv[c] = cd[c];
+        const uint32_t* cw = reinterpret_cast<const uint32_t*>(cv);
+        float2 ka[SPL], kb[SPL];
+#pragma unroll
+        for (int m = 0; m < SPL; ++m) ka[m] = kb[m] = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const uint32_t word = cw[(2 * r) >> 2];
+          const unsigned ca = __byte_perm(word, 0, 0x4440 | ((2 * r) & 3));
+          const unsigned cbb = __byte_perm(word, 0, 0x4440 | ((2 * r + 1) & 3));
+          const uint32_t* ra = cbs + (r * 64 + ca) * JC + lane * SPL;
+          const uint32_t* rb = cbs + (r * 64 + cbb) * JC + lane * SPL;
+          if constexpr (SPL == 2) {
+            const uint2 va = *reinterpret_cast<const uint2*>(ra);
+            const uint2 vb = *reinterpret_cast<const uint2*>(rb);
+            hadd2_acc(ka[0], va.x);
+            hadd2_acc(ka[1], va.y);
+            hadd2_acc(kb[0], vb.x);
+            hadd2_acc(kb[1], vb.y);
+          } else {
+            hadd2_acc(ka[0], *ra);
+            hadd2_acc(kb[0], *rb);
+          }
+        }
+        float part[G];
+#pragma unroll
+        for (int h = 0; h < G; ++h) part[h] = 0.f;
+#pragma unroll
+        for (int m = 0; m < SPL; ++m) {
+          const float kx = ka[m].x - kb[m].y, ky = ka[m].y + kb[m].x;
+          const float rx = ph[m].x * kx - ph[m].y * ky;
+          const float ry = ph[m].x * ky + ph[m].y * kx;
+#pragma unroll
+          for (int h = 0; h < G; ++h) part[h] += w[h][m].x * rx - w[h][m].y * ry;
+          const float nx = ph[m].x * stepm[m].x - ph[m].y * stepm[m].y;
+          ph[m].y = ph[m].x * stepm[m].y + ph[m].y * stepm[m].x;
+          ph[m].x = nx;
+        }
+#pragma unroll
+        for (int h = 0; h < G; ++h) acc[st * G + h] = part[h];
+      }
+      bool writer;
+      const int base = reduce_scatter<NV, 32>(acc, lane, writer);
+      constexpr int VPL = NV / 32 > 0 ? NV / 32 : 1;
+#pragma unroll
+      for (int m = 0; m < VPL; ++m) {
+        const int vi = base + m;
+        const int st = vi / G, h = vi % G;
+        const int dlt = tok0 + st;
+        if (writer && dlt < valid) ps[(ti + dlt) * G + h] = acc[m];
+      }
+    }
+    __syncthreads();
+  }
+}
+
 template <int NC, int G, int JS>
 __global__ void __launch_bounds__(kThreads) k_fast_value(FastArgs a) {
   constexpr int CPL = NC / 32;       // codes per lane
@@ -303,29 +459,33 @@ __global__ void __launch_bounds__(kThreads) k_fast_value(FastArgs a) {
     lh[tid] = v;
   }
   // z[c][h] += p_h(i) * bit_c(i); lane owns codes [CPL*lane, CPL*lane+CPL)
-  float z[CPL][G];
+  // heads in pairs so the conditional adds are packed fp32x2 (FADD2)
+  constexpr int G2 = (G + 1) / 2;
+  float2 z[CPL][G2];
 #pragma unroll
   for (int c = 0; c < CPL; ++c)
 #pragma unroll
-    for (int h = 0; h < G; ++h) z[c][h] = 0.f;
+    for (int h = 0; h < G2; ++h) z[c][h] = make_float2(0.f, 0.f);
   const int wsel = (CPL * lane) >> 6, sh = (CPL * lane) & 63;
 #pragma unroll 4
   for (int e = warp; e < cnt; e += kThreads / 32) {
     const unsigned bits = (unsigned)(vw[(size_t)e * WPTOK + wsel] >> sh);
-    float p[G];
+    float2 p[G2];
 #pragma unroll
-    for (int h = 0; h < G; ++h) p[h] = sc[e * G + h];
+    for (int h = 0; h < G2; ++h)
+      p[h] = make_float2(sc[e * G + 2 * h], 2 * h + 1 < G ? sc[e * G + 2 * h + 1] : 0.f);
 #pragma unroll
     for (int c = 0; c < CPL; ++c)
       if (bits & (1u << c)) {
 #pragma unroll
-        for (int h = 0; h < G; ++h) z[c][h] += p[h];
+        for (int h = 0; h < G2; ++h) add2(z[c][h], p[h]);
       }
   }
 #pragma unroll
   for (int c = 0; c < CPL; ++c)
 #pragma unroll
-    for (int h = 0; h < G; ++h) zr[((size_t)warp * NC + CPL * lane + c) * G + h] = z[c][h];
+    for (int h = 0; h < G; ++h)
+      zr[((size_t)warp * NC + CPL * lane + c) * G + h] = (h & 1) ? z[c][h / 2].y : z[c][h / 2].x;
   __syncthreads();
   for (int e = tid; e < NC * G; e += kThreads) {
     float v = 0.f;
@@ -350,14 +510,18 @@ __global__ void __launch_bounds__(kThreads) k_fast_value(FastArgs a) {
   }
 }
 
-int jc_for(int R) { return R <= 12 ? 32 : 16; }
+// subspace split (CTAs per stream) so the codebook slice fits in smem
+int js_for(const AttnJob& job) {
+  if (job.cb_key16) return job.geo.R <= 13 ? 1 : 2;  // fp16: 16 KiB per round
+  return job.geo.R <= 12 ? 2 : 4;                    // fp32: 32 KiB per round
+}
 
-size_t f1_smem(int R, int JC) {
-  return (size_t)R * 64 * JC * 8 + 2 * 24 * R * 8 + (size_t)kTile * (((2 * R + 15) / 16) * 16);
+size_t f1_smem(int R, int JC, int esize) {
+  return (size_t)R * 64 * JC * esize + 2 * 24 * R * 8 + (size_t)kTile * (((2 * R + 15) / 16) * 16);
 }
 
 int f1_chunk(const AttnJob& job) {
-  const int JS = 64 / jc_for(job.geo.R);
+  const int JS = js_for(job);
   long long want = (job.n * (long long)job.S * JS + 2 * 148 - 1) / (2 * 148);
   long long ch = (want + kTile - 1) / kTile * kTile;
   if (ch < 512) ch = 512;
@@ -379,37 +543,60 @@ size_t f2_smem(const AttnJob& job, int chunk2) {
          (size_t)8 * g.n_codes * g.G * 4;
 }
 
+template <class K>
+cudaError_t set_smem(K kernel, size_t sm, size_t& done) {
+  if (sm <= done) return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  if (e == cudaSuccess) done = sm;
+  return e;
+}
+
 template <int R, int G>
 cudaError_t launch_f1(const FastArgs& a, int S, cudaStream_t st) {
   constexpr int JC = R <= 12 ? 32 : 16;
   constexpr int JS = 64 / JC;
-  const size_t sm = f1_smem(R, JC);
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(k_fast_score<R, JC, G>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  const size_t sm = f1_smem(R, JC, 8);
+  static size_t done = 0;
+  cudaError_t e = set_smem(k_fast_score<R, JC, G>, sm, done);
+  if (e != cudaSuccess) return e;
   dim3 grid((unsigned)((a.n + a.chunk - 1) / a.chunk), S * JS);
   k_fast_score<R, JC, G><<<grid, kF1Threads, sm, st>>>(a);
   count_launch();
   return cudaGetLastError();
 }
 
+template <int R, int G>
+cudaError_t launch_f1h(const FastArgs& a, int S, cudaStream_t st) {
+  constexpr int SPL = R <= 13 ? 2 : 1;
+  constexpr int JS = 2 / SPL;
+  const size_t sm = f1_smem(R, 32 * SPL, 4);
+  static size_t done = 0;
+  cudaError_t e = set_smem(k_fast_score_h<R, SPL, G>, sm, done);
+  if (e != cudaSuccess) return e;
+  dim3 grid((unsigned)((a.n + a.chunk - 1) / a.chunk), S * JS);
+  k_fast_score_h<R, SPL, G><<<grid, kF1Threads, sm, st>>>(a);
+  count_launch();
+  return cudaGetLastError();
+}
+
 template <int NC, int G, int JS>
 cudaError_t launch_f2(const FastArgs& a, size_t sm, cudaStream_t st) {
-  static size_t attr = 0;
-  if (sm > attr) {
-    cudaError_t e = cudaFuncSetAttribute(k_fast_value<NC, G, JS>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    if (e != cudaSuccess) return e;
-    attr = sm;
-  }
+  static size_t done = 0;
+  cudaError_t e = set_smem(k_fast_value<NC, G, JS>, sm, done);
+  if (e != cudaSuccess) return e;
   dim3 grid((unsigned)((a.n + a.chunk2 - 1) / a.chunk2), a.S);
   k_fast_value<NC, G, JS><<<grid, kThreads, sm, st>>>(a);
   count_launch();
   return cudaGetLastError();
+}
+
+template <int NC, int G>
+cudaError_t launch_f2_js(const FastArgs& a, int JS, size_t sm, cudaStream_t st) {
+  switch (JS) {
+    case 1: return launch_f2<NC, G, 1>(a, sm, st);
+    case 2: return launch_f2<NC, G, 2>(a, sm, st);
+    default: return launch_f2<NC, G, 4>(a, sm, st);
+  }
 }
 
 }  // namespace
@@ -422,7 +609,7 @@ bool fast_path_applies(const AttnJob& job) {
 }
 
 size_t fast_scratch_bytes(const AttnJob& job, int* n_chunks) {
-  const int JS = 64 / jc_for(job.geo.R);
+  const int JS = js_for(job);
   const int c2 = f2_chunk(job);
   *n_chunks = (int)((job.n + c2 - 1) / c2);
   const size_t ps = (size_t)job.S * JS * job.n * job.geo.G * sizeof(float);
@@ -439,6 +626,7 @@ cudaError_t run_attention_fast(const AttnJob& job, const float* q, float* pm, fl
   a.vpool = job.vpool;
   a.vstride = job.vstride;
   a.cb = job.cb_key;
+  a.cbh = job.cb_key16;
   a.cbv = job.cb_val;
   a.n_slots = job.n_slots;
   a.q = q;
@@ -457,25 +645,25 @@ cudaError_t run_attention_fast(const AttnJob& job, const float* q, float* pm, fl
   (void)n_chunks;
   cudaError_t e;
   if (prof) cudaEventRecord(prof[0], st);
-  if (g.R == 11)
-    e = g.G == 4 ? launch_f1<11, 4>(a, job.S, st) : launch_f1<11, 1>(a, job.S, st);
-  else
-    e = g.G == 4 ? launch_f1<21, 4>(a, job.S, st) : launch_f1<21, 1>(a, job.S, st);
+  if (job.cb_key16) {
+    if (g.R == 11)
+      e = g.G == 4 ? launch_f1h<11, 4>(a, job.S, st) : launch_f1h<11, 1>(a, job.S, st);
+    else
+      e = g.G == 4 ? launch_f1h<21, 4>(a, job.S, st) : launch_f1h<21, 1>(a, job.S, st);
+  } else {
+    if (g.R == 11)
+      e = g.G == 4 ? launch_f1<11, 4>(a, job.S, st) : launch_f1<11, 1>(a, job.S, st);
+    else
+      e = g.G == 4 ? launch_f1<21, 4>(a, job.S, st) : launch_f1<21, 1>(a, job.S, st);
+  }
   if (prof) cudaEventRecord(prof[1], st);
   if (e != cudaSuccess) return e;
   const size_t sm2 = f2_smem(job, a.chunk2);
-  const int JS = 64 / jc_for(g.R);
-  if (g.n_codes == 128) {
-    if (g.G == 4)
-      e = JS == 2 ? launch_f2<128, 4, 2>(a, sm2, st) : launch_f2<128, 4, 4>(a, sm2, st);
-    else
-      e = JS == 2 ? launch_f2<128, 1, 2>(a, sm2, st) : launch_f2<128, 1, 4>(a, sm2, st);
-  } else {
-    if (g.G == 4)
-      e = JS == 2 ? launch_f2<256, 4, 2>(a, sm2, st) : launch_f2<256, 4, 4>(a, sm2, st);
-    else
-      e = JS == 2 ? launch_f2<256, 1, 2>(a, sm2, st) : launch_f2<256, 1, 4>(a, sm2, st);
-  }
+  const int JS = js_for(job);
+  if (g.n_codes == 128)
+    e = g.G == 4 ? launch_f2_js<128, 4>(a, JS, sm2, st) : launch_f2_js<128, 1>(a, JS, sm2, st);
+  else
+    e = g.G == 4 ? launch_f2_js<256, 4>(a, JS, sm2, st) : launch_f2_js<256, 1>(a, JS, sm2, st);
   return e;
 }
 

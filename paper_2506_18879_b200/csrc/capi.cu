@@ -7,11 +7,14 @@
 
 #include <cmath>
 #include <cstdio>
+#include <algorithm>
 #include <cstring>
 #include <string>
 #include <vector>
 
 #include "../../include/cvq.h"
+#include <cuda_fp16.h>
+
 #include "cvq_internal.cuh"
 
 namespace cvq {
@@ -55,6 +58,8 @@ struct DevBuf {
     if (bytes <= n) return cudaSuccess;
     if (p) cudaFree(p);
     p = nullptr;
+    // grow geometrically: decode steps add one token at a time
+    if (n) bytes = bytes + bytes / 2 > bytes ? bytes + bytes / 2 : bytes;
     n = 0;
     cudaError_t e = cudaMalloc(&p, bytes);
     if (e == cudaSuccess) n = bytes;
@@ -166,6 +171,7 @@ struct cvq_cache {
   double* base = nullptr;      // [slot][R][groups][L][L] (when it fits)
   double* maxnorm = nullptr;   // [slot][R][groups]
   float2* cbk = nullptr;       // [slot][R][L][subs]
+  uint32_t* cbk16 = nullptr;   // same, packed half2 (CVQ_CACHE_KEYS_FP16)
   float* cbv = nullptr;        // [slot][n_codes][d]
   double *w1 = nullptr, *b1 = nullptr, *w2 = nullptr, *b2 = nullptr;
   double* thetas = nullptr;
@@ -183,7 +189,7 @@ cvq_status ctx_check(cvq_context* ctx) {
 
 void free_cache(cvq_cache* c) {
   for (void* p : {(void*)c->kpool, (void*)c->vpool, (void*)c->atoms64, (void*)c->base,
-                  (void*)c->maxnorm, (void*)c->cbk, (void*)c->cbv, (void*)c->w1, (void*)c->b1,
+                  (void*)c->maxnorm, (void*)c->cbk, (void*)c->cbk16, (void*)c->cbv, (void*)c->w1, (void*)c->b1,
                   (void*)c->w2, (void*)c->b2, (void*)c->thetas})
     if (p) cudaFree(p);
   c->attn_scratch.release();
@@ -202,6 +208,7 @@ AttnJob make_job(const cvq_cache* c) {
   j.vstride = c->vstride;
   j.n_slots = c->n_slots;
   j.cb_key = c->cbk;
+  j.cb_key16 = c->cbk16;
   j.cb_val = c->cbv;
   j.thetas = c->thetas;
   j.n = (long long)c->length;
@@ -370,6 +377,8 @@ CVQ_API cvq_status cvq_cache_create(cvq_context* ctx, const cvq_cache_desc* d, c
   if (e == cudaSuccess) e = alloc((void**)&c->vpool, (size_t)c->S * c->vstride * 8);
   if (e == cudaSuccess) e = alloc((void**)&c->atoms64, na * 2 * sizeof(double));
   if (e == cudaSuccess) e = alloc((void**)&c->cbk, na * sizeof(float2));
+  if (e == cudaSuccess && (d->flags & CVQ_CACHE_KEYS_FP16))
+    e = alloc((void**)&c->cbk16, na * sizeof(uint32_t));
   if (e == cudaSuccess) e = alloc((void**)&c->cbv, (size_t)c->n_slots * g.n_codes * g.d * 4);
   if (e == cudaSuccess)
     e = alloc((void**)&c->maxnorm, (size_t)c->n_slots * g.R * g.groups * sizeof(double));
@@ -431,6 +440,21 @@ CVQ_API cvq_status cvq_cache_set_key_codebook(cvq_cache* c, uint32_t layer, uint
   std::vector<float> dl = atoms_to_decode_layout(g, xy);
   CU(cudaMemcpyAsync(c->cbk + (size_t)slot * na, dl.data(), dl.size() * sizeof(float),
                      cudaMemcpyHostToDevice, st));
+  std::vector<uint32_t> dh;
+  if (c->cbk16) {  // fp16 copy, rounded once from fp64
+    dh.resize(na);
+    for (int r = 0; r < g.R; ++r)
+      for (int jj = 0; jj < g.subs; ++jj)
+        for (int l = 0; l < g.L; ++l) {
+          const size_t src = (((size_t)r * g.subs + jj) * g.L + l) * 2;
+          const size_t dst = ((size_t)r * g.L + l) * g.subs + jj;
+          const uint32_t hx = __half_as_ushort(__double2half(xy[src]));
+          const uint32_t hy = __half_as_ushort(__double2half(xy[src + 1]));
+          dh[dst] = hx | (hy << 16);
+        }
+    CU(cudaMemcpyAsync(c->cbk16 + (size_t)slot * na, dh.data(), na * 4, cudaMemcpyHostToDevice,
+                       st));
+  }
   if (c->base) {
     CU(build_key_enc_tables(g, 1, c->atoms64 + (size_t)slot * na * 2,
                             c->base + (size_t)slot * g.R * g.groups * g.L * g.L,
@@ -567,8 +591,10 @@ cvq_status attention_common(cvq_cache* c, const float* q, uint64_t t, float* out
   const Geom& g = c->geo;
   AttnJob job = make_job(c);
   job.t = (long long)t;
-  const size_t need = attn_scratch_bytes(job, nullptr);
-  CU(c->attn_scratch.ensure(need));
+  AttnJob cap = job;  // size scratch for the full capacity once, not per step
+  cap.n = (long long)c->desc.capacity;
+  CU(c->attn_scratch.ensure(std::max(attn_scratch_bytes(job, nullptr),
+                                     attn_scratch_bytes(cap, nullptr))));
   const size_t qbytes = (size_t)c->S * g.G * g.d * sizeof(float);
   const void* qd = nullptr;
   TRY(to_device(c, c->stage_in, q, qbytes, where, &qd));

@@ -31,6 +31,7 @@ struct AttnJob {
   uint64_t vstride;
   int n_slots;                // codebook slot of stream s = s % n_slots
   const float2* cb_key;       // [slot][R][L][subs] complex atoms (x, y), fp32
+  const uint32_t* cb_key16;   // same as packed half2, or null (fp16-codebook mode)
   const float* cb_val;        // [slot][n_codes][d] fp32
   const double* thetas;       // [subs] fp64, rope.cpp:8-25
   long long n;                // tokens per stream

@@ -1,0 +1,91 @@
+"""World-size-2 gloo test of the context-sharded decode on CPU.
+
+Each rank takes its shard of every stream (paper_2506_18879_b200.dist
+.shard_plan), forms split-K partials (m, l, o) from the oracle's scores of
+its tokens, exchanges them with dist.gather_partials (the call bench.py makes
+over NCCL), and the LSE merge of the gathered partials must equal the
+oracle's unsharded fused_attention.  The merge restated here in numpy is the
+algebra of k_combine (attn.cu); the kernel itself is covered on the GPU.
+"""
+import os
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2506_18879_b200.dist import TILE, shard_plan
+
+
+def test_shard_plan_covers_and_aligns():
+    for n in (1, 127, 128, 1000, 131072, 1048576):
+        for w in (1, 2, 4, 8):
+            plan = shard_plan(n, w)
+            assert plan[0][0] == 0 and plan[-1][1] == n
+            for (lo, hi), (lo2, _) in zip(plan, plan[1:]):
+                assert hi == lo2 and (lo % TILE == 0 or lo == n)
+            assert all(hi >= lo for lo, hi in plan)
+
+
+def lse_merge(M, Lh, O):
+    """k_combine (attn.cu): sum_p o_p l_p e^{m_p - M} / sum_p l_p e^{m_p - M}."""
+    live = Lh > 0
+    Mx = np.where(live, M, -np.inf).max(0)
+    wts = np.where(live, Lh * np.exp(M - Mx), 0.0)
+    return (wts[..., None] * O).sum(0) / wts.sum(0)[..., None]
+
+
+def _worker(rank, world, port, result_dir):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle.oracle import KQ, Oracle
+        from paper_2506_18879_b200.dist import gather_partials
+        from tests import fixtures as fx
+
+        P = Oracle("port")
+        kq = KQ(16, 8, 16, 3)
+        nc, n, streams, gq = 16, 1000, 3, 2
+        rows = []
+        for s in range(streams):
+            rng = P.rng(100 + s)
+            atoms = rng.normal(2 * kq.n_atoms, 0.5)
+            a, b = fx.random_key_codes(kq, n, rng=rng)
+            bits = fx.random_value_codes(nc, n, rng=rng)
+            vrows = rng.normal(nc * 16).reshape(nc, 16)
+            for h in range(gq):
+                q = rng.normal(16)
+                rows.append((atoms, a, b, bits, vrows, q))
+        lo, hi = shard_plan(n, world)[rank]
+        t = n - 1
+        m = np.zeros(len(rows), np.float32)
+        l = np.zeros(len(rows), np.float32)
+        o = np.zeros((len(rows), 16), np.float32)
+        for i, (atoms, a, b, bits, vrows, q) in enumerate(rows):
+            sc = P.fused_scores(kq, atoms, a, b, bits, vrows, q, t)[lo:hi]
+            if hi > lo:
+                m[i] = sc.max()
+                p = np.exp(sc - m[i])
+                l[i] = p.sum()
+                o[i] = ((p @ bits[lo:hi]) @ vrows) / l[i]
+        M, Lh, O = gather_partials(torch.from_numpy(m), torch.from_numpy(l), torch.from_numpy(o))
+        out = lse_merge(M.numpy().astype(np.float64), Lh.numpy().astype(np.float64),
+                        O.numpy().astype(np.float64))
+        if rank == 0:
+            worst = 0.0
+            for i, (atoms, a, b, bits, vrows, q) in enumerate(rows):
+                want, _, _ = P.fused_attention(kq, atoms, a, b, bits, vrows, q, t)
+                worst = max(worst, fx.rel_err(out[i], want))
+            np.save(os.path.join(result_dir, "worst.npy"), np.array([worst]))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2])
+def test_sharded_decode_merges_to_unsharded(tmp_path, world):
+    port = 29500 + (os.getpid() % 1000)
+    mp.spawn(_worker, args=(world, port, str(tmp_path)), nprocs=world, join=True)
+    worst = float(np.load(tmp_path / "worst.npy")[0])
+    assert worst <= 1e-5, worst

@@ -337,16 +337,21 @@ def test_cache_2bit_encode_decode_sample(G):
     assert fx.rel_err(out.reshape(-1), want) <= 1e-4
 
 
+@pytest.mark.parametrize("keys", ["fp32", "fp16"])
 @pytest.mark.parametrize("preset,n", [("1bit", 1), ("1bit", 127), ("1bit", 129), ("1bit", 3001),
                                       ("2bit", 5), ("2bit", 1000), ("2bit", 2177)])
-def test_fast_path_tiles_vs_oracle_and_generic(G, preset, n, monkeypatch):
+def test_fast_path_tiles_vs_oracle_and_generic(G, preset, n, keys, monkeypatch):
     """The specialised kernels (attn_fast.cu) on partial tiles / chunks, GQA=4,
-    two sequences x two layers; each q head vs the oracle, and fast == generic."""
+    two sequences x two layers; each q head vs the oracle, and fast == generic.
+    Tolerance (north_star): outputs within 1e-3 relative; the fp32-codebook
+    mode is asserted at 1e-4, the fp16-codebook mode at the 1e-3 bar."""
     kq = KQ(128, 64, 64, 11 if preset == "1bit" else 21)
     nc = 128 if preset == "1bit" else 256
     B, Ly, H, Gq = 2, 2, 2, 4
+    tol = 1e-4 if keys == "fp32" else 1e-3
     rng = P.rng(n + nc)
-    c = G.QuantizedKVCache(kq, nc, n_seqs=B, n_layers=Ly, n_kv_heads=H, q_per_kv=Gq, capacity=n)
+    c = G.QuantizedKVCache(kq, nc, n_seqs=B, n_layers=Ly, n_kv_heads=H, q_per_kv=Gq, capacity=n,
+                           keys_fp16=keys == "fp16")
     books = {}
     for layer in range(Ly):
         for h in range(H):
@@ -369,7 +374,7 @@ def test_fast_path_tiles_vs_oracle_and_generic(G, preset, n, monkeypatch):
     monkeypatch.setenv("CVQ_DISABLE_FAST", "1")
     out_generic = c.attention(q, t)
     monkeypatch.delenv("CVQ_DISABLE_FAST")
-    assert fx.rel_err(out, out_generic) <= 1e-5
+    assert fx.rel_err(out, out_generic) <= (1e-5 if keys == "fp32" else tol)
     worst = 0.0
     for sq in range(B):
         for layer in range(Ly):
@@ -380,4 +385,37 @@ def test_fast_path_tiles_vs_oracle_and_generic(G, preset, n, monkeypatch):
                     want, _, _ = P.fused_attention(kq, atoms, a, b, bits, vrows,
                                                    q[sq, layer, h * Gq + j].astype(np.float64), t)
                     worst = max(worst, fx.rel_err(out[sq, layer, h * Gq + j], want))
-    assert worst <= 1e-4, worst
+    assert worst <= tol, worst
+
+
+@pytest.mark.parametrize("keys", ["fp32", "fp16"])
+@pytest.mark.parametrize("scale", [0.3, 1.0])
+def test_bench_shape_precision(G, keys, scale):
+    """BASELINE configs[0] shape (8 KV / 32 q heads, 8K, 1-bit) at the bench's
+    atom scale (0.3) and the reference tests' scale (1.0): outputs within the
+    north_star 1e-3 relative bar; scores within 1e-3 of max |s|."""
+    kq = KQ(128, 64, 64, 11)
+    nc, n, H, Gq = 128, 8192, 8, 4
+    rng = P.rng(int(scale * 10) + (keys == "fp16"))
+    c = G.QuantizedKVCache(kq, nc, n_kv_heads=H, q_per_kv=Gq, capacity=n, keys_fp16=keys == "fp16")
+    streams = []
+    for h in range(H):
+        atoms = rng.normal(2 * kq.n_atoms, scale)
+        vrows = rng.normal(nc * 128, 1 / 16).reshape(nc, 128)
+        a, b = fx.random_key_codes(kq, n, rng=rng)
+        bits = fx.random_value_codes(nc, n, rng=rng)
+        c.set_key_codebook(0, h, atoms)
+        c.set_value_quantizer(0, h, vrows)
+        c.import_stream(0, 0, h, P.pack_key_codes(kq, a, b), P.pack_value_codes(bits), n)
+        streams.append((atoms, vrows, a, b, bits))
+    q = rng.normal(H * Gq * 128).reshape(1, 1, H * Gq, 128).astype(np.float32)
+    out = c.attention(q)
+    worst = 0.0
+    for h in range(H):
+        atoms, vrows, a, b, bits = streams[h]
+        for j in range(Gq):
+            want, _, _ = P.fused_attention(kq, atoms, a, b, bits, vrows,
+                                           q[0, 0, h * Gq + j].astype(np.float64), n - 1)
+            worst = max(worst, fx.rel_err(out[0, 0, h * Gq + j], want))
+    print(keys, scale, "worst rel err", worst)
+    assert worst <= 1e-3, worst
