@@ -157,7 +157,7 @@ def main():
     ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--keys", default="fp32", choices=["fp32", "fp16"],
+    ap.add_argument("--keys", default="fp32", choices=["fp32", "fp16", "tc"],
                     help="on-chip key-codebook precision (accumulation is fp32 either way)")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
@@ -190,7 +190,7 @@ def main():
     ctx = G.Context(local, stream.cuda_stream)
     cache = G.QuantizedKVCache(kq, nc, n_seqs=B, n_layers=layers, n_kv_heads=H, q_per_kv=Gq,
                                capacity=n_local + extra, hidden=2 * nc, position_offset=lo, ctx=ctx,
-                               keys_fp16=args.keys == "fp16")
+                               keys=args.keys)
     rs = np.random.default_rng(1234)
     for layer in range(layers):
         for h in range(H):

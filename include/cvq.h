@@ -188,6 +188,11 @@ typedef struct cvq_cache_desc {
  * error ~1e-5 at the bench's codebook scale ("precision modes").
  * Default (0): fp32 codebook. */
 #define CVQ_CACHE_KEYS_FP16 1u
+/* Score with the tcgen05 tensor-core kernel: the key decode as a one-hot
+ * GEMM (fp16 codebook operand, fp32 accumulators in TMEM).  Same precision
+ * class as CVQ_CACHE_KEYS_FP16.  Head presets (d=128, g=64, L=64) only;
+ * other shapes use the generic path. */
+#define CVQ_CACHE_KEYS_TC 2u
 
 CVQ_API cvq_status cvq_cache_create(cvq_context* ctx, const cvq_cache_desc* d,
                                     cvq_cache** out);

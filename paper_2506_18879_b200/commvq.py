@@ -90,6 +90,7 @@ class _Desc(C.Structure):
 
 
 CVQ_CACHE_KEYS_FP16 = 1
+CVQ_CACHE_KEYS_TC = 2
 
 
 @dataclass(frozen=True)
@@ -358,17 +359,21 @@ class QuantizedKVCache:
 
     def __init__(self, kq, n_codes, n_seqs=1, n_layers=1, n_kv_heads=1, q_per_kv=1,
                  capacity=1024, hidden=0, position_offset=0, rope_base=10000.0, ctx=None,
-                 keys_fp16=False):
+                 keys_fp16=False, keys="fp32"):
+        """keys: on-chip key-codebook mode -- "fp32" (default), "fp16"
+        (CVQ_CACHE_KEYS_FP16) or "tc" (tcgen05 one-hot MMA, CVQ_CACHE_KEYS_TC)."""
         self.kq = _kc(kq)
         self.ctx = ctx or default_context()
         self.n_codes, self.hidden = n_codes, hidden
         self.n_seqs, self.n_layers, self.n_kv_heads, self.q_per_kv = (n_seqs, n_layers,
                                                                       n_kv_heads, q_per_kv)
         self.capacity, self.position_offset = capacity, position_offset
-        self.keys_fp16 = bool(keys_fp16)
+        if keys_fp16:
+            keys = "fp16"
+        self.keys = keys
+        flags = {"fp32": 0, "fp16": CVQ_CACHE_KEYS_FP16, "tc": CVQ_CACHE_KEYS_TC}[keys]
         d = _Desc(self.kq._c(), n_codes, hidden, n_seqs, n_layers, n_kv_heads, q_per_kv,
-                  capacity, position_offset, rope_base,
-                  CVQ_CACHE_KEYS_FP16 if keys_fp16 else 0)
+                  capacity, position_offset, rope_base, flags)
         h = _p()
         _check(_lib.cvq_cache_create(self.ctx.h, C.byref(d), C.byref(h)))
         self.h = h

@@ -512,6 +512,7 @@ __global__ void __launch_bounds__(kThreads) k_fast_value(FastArgs a) {
 
 // subspace split (CTAs per stream) so the codebook slice fits in smem
 int js_for(const AttnJob& job) {
+  if (job.cb_key_tc) return tc_blocks(job.geo.R);    // tcgen05: round blocks of 11
   if (job.cb_key16) return job.geo.R <= 13 ? 1 : 2;  // fp16: 16 KiB per round
   return job.geo.R <= 12 ? 2 : 4;                    // fp32: 32 KiB per round
 }
@@ -645,7 +646,9 @@ cudaError_t run_attention_fast(const AttnJob& job, const float* q, float* pm, fl
   (void)n_chunks;
   cudaError_t e;
   if (prof) cudaEventRecord(prof[0], st);
-  if (job.cb_key16) {
+  if (job.cb_key_tc) {
+    e = run_tc_score(job, q, a.ps, a.chunk, st);
+  } else if (job.cb_key16) {
     if (g.R == 11)
       e = g.G == 4 ? launch_f1h<11, 4>(a, job.S, st) : launch_f1h<11, 1>(a, job.S, st);
     else

@@ -172,6 +172,7 @@ struct cvq_cache {
   double* maxnorm = nullptr;   // [slot][R][groups]
   float2* cbk = nullptr;       // [slot][R][L][subs]
   uint32_t* cbk16 = nullptr;   // same, packed half2 (CVQ_CACHE_KEYS_FP16)
+  uint16_t* cbtc = nullptr;    // tcgen05 B operand [slot][R][8192] (CVQ_CACHE_KEYS_TC)
   float* cbv = nullptr;        // [slot][n_codes][d]
   double *w1 = nullptr, *b1 = nullptr, *w2 = nullptr, *b2 = nullptr;
   double* thetas = nullptr;
@@ -189,7 +190,7 @@ cvq_status ctx_check(cvq_context* ctx) {
 
 void free_cache(cvq_cache* c) {
   for (void* p : {(void*)c->kpool, (void*)c->vpool, (void*)c->atoms64, (void*)c->base,
-                  (void*)c->maxnorm, (void*)c->cbk, (void*)c->cbk16, (void*)c->cbv, (void*)c->w1, (void*)c->b1,
+                  (void*)c->maxnorm, (void*)c->cbk, (void*)c->cbk16, (void*)c->cbtc, (void*)c->cbv, (void*)c->w1, (void*)c->b1,
                   (void*)c->w2, (void*)c->b2, (void*)c->thetas})
     if (p) cudaFree(p);
   c->attn_scratch.release();
@@ -209,6 +210,7 @@ AttnJob make_job(const cvq_cache* c) {
   j.n_slots = c->n_slots;
   j.cb_key = c->cbk;
   j.cb_key16 = c->cbk16;
+  j.cb_key_tc = c->cbtc;
   j.cb_val = c->cbv;
   j.thetas = c->thetas;
   j.n = (long long)c->length;
@@ -379,6 +381,10 @@ CVQ_API cvq_status cvq_cache_create(cvq_context* ctx, const cvq_cache_desc* d, c
   if (e == cudaSuccess) e = alloc((void**)&c->cbk, na * sizeof(float2));
   if (e == cudaSuccess && (d->flags & CVQ_CACHE_KEYS_FP16))
     e = alloc((void**)&c->cbk16, na * sizeof(uint32_t));
+  // tcgen05 path: head presets only (d=128, one 64-subspace group, L=64)
+  const bool tc_ok = g.d == 128 && g.groups == 1 && g.L == 64;
+  if (e == cudaSuccess && (d->flags & CVQ_CACHE_KEYS_TC) && tc_ok)
+    e = alloc((void**)&c->cbtc, (size_t)c->n_slots * g.R * 8192 * sizeof(uint16_t));
   if (e == cudaSuccess) e = alloc((void**)&c->cbv, (size_t)c->n_slots * g.n_codes * g.d * 4);
   if (e == cudaSuccess)
     e = alloc((void**)&c->maxnorm, (size_t)c->n_slots * g.R * g.groups * sizeof(double));
@@ -454,6 +460,14 @@ CVQ_API cvq_status cvq_cache_set_key_codebook(cvq_cache* c, uint32_t layer, uint
         }
     CU(cudaMemcpyAsync(c->cbk16 + (size_t)slot * na, dh.data(), na * 4, cudaMemcpyHostToDevice,
                        st));
+  }
+  std::vector<uint16_t> dt;
+  if (c->cbtc) {  // canonical K-major B operand of the one-hot MMA
+    dt.assign((size_t)g.R * 8192, 0);
+    tc_build_codebook(g.R, g.L, g.subs, xy, dt.data(),
+                      [](double v) -> uint16_t { return __half_as_ushort(__double2half(v)); });
+    CU(cudaMemcpyAsync(c->cbtc + (size_t)slot * g.R * 8192, dt.data(), dt.size() * 2,
+                       cudaMemcpyHostToDevice, st));
   }
   if (c->base) {
     CU(build_key_enc_tables(g, 1, c->atoms64 + (size_t)slot * na * 2,

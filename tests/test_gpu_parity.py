@@ -337,7 +337,7 @@ def test_cache_2bit_encode_decode_sample(G):
     assert fx.rel_err(out.reshape(-1), want) <= 1e-4
 
 
-@pytest.mark.parametrize("keys", ["fp32", "fp16"])
+@pytest.mark.parametrize("keys", ["fp32", "fp16", "tc"])
 @pytest.mark.parametrize("preset,n", [("1bit", 1), ("1bit", 127), ("1bit", 129), ("1bit", 3001),
                                       ("2bit", 5), ("2bit", 1000), ("2bit", 2177)])
 def test_fast_path_tiles_vs_oracle_and_generic(G, preset, n, keys, monkeypatch):
@@ -351,7 +351,7 @@ def test_fast_path_tiles_vs_oracle_and_generic(G, preset, n, keys, monkeypatch):
     tol = 1e-4 if keys == "fp32" else 1e-3
     rng = P.rng(n + nc)
     c = G.QuantizedKVCache(kq, nc, n_seqs=B, n_layers=Ly, n_kv_heads=H, q_per_kv=Gq, capacity=n,
-                           keys_fp16=keys == "fp16")
+                           keys=keys)
     books = {}
     for layer in range(Ly):
         for h in range(H):
@@ -388,7 +388,7 @@ def test_fast_path_tiles_vs_oracle_and_generic(G, preset, n, keys, monkeypatch):
     assert worst <= tol, worst
 
 
-@pytest.mark.parametrize("keys", ["fp32", "fp16"])
+@pytest.mark.parametrize("keys", ["fp32", "fp16", "tc"])
 @pytest.mark.parametrize("scale", [0.3, 1.0])
 def test_bench_shape_precision(G, keys, scale):
     """BASELINE configs[0] shape (8 KV / 32 q heads, 8K, 1-bit) at the bench's
@@ -397,7 +397,7 @@ def test_bench_shape_precision(G, keys, scale):
     kq = KQ(128, 64, 64, 11)
     nc, n, H, Gq = 128, 8192, 8, 4
     rng = P.rng(int(scale * 10) + (keys == "fp16"))
-    c = G.QuantizedKVCache(kq, nc, n_kv_heads=H, q_per_kv=Gq, capacity=n, keys_fp16=keys == "fp16")
+    c = G.QuantizedKVCache(kq, nc, n_kv_heads=H, q_per_kv=Gq, capacity=n, keys=keys)
     streams = []
     for h in range(H):
         atoms = rng.normal(2 * kq.n_atoms, scale)
