@@ -157,7 +157,9 @@ def main():
     ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--keys", default="fp32", choices=["fp32", "fp16", "tc"],
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"])
+    ap.add_argument("--no-prefill", action="store_true")
+    ap.add_argument("--keys", default="fp16", choices=["fp32", "fp16", "tc"],
                     help="on-chip key-codebook precision (accumulation is fp32 either way)")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
@@ -169,10 +171,16 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # --dist-backend gloo lets several ranks share one GPU (host-staged
+    # exchange) to exercise the sharded path where only one GPU is available
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
     from paper_2506_18879_b200 import commvq as G
 
     layers, B, H, Gq, N, d, g, L, R, nc = cfg
@@ -257,7 +265,7 @@ def main():
     launches = G.launch_count() - launches0
     if world > 1:
         import torch.distributed as dist
-        tt = torch.tensor([ms_total], device="cuda")
+        tt = torch.tensor([ms_total], device="cuda" if args.dist_backend == "nccl" else "cpu")
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         ms_total = float(tt.item())
     ms = ms_total / args.steps
@@ -301,6 +309,39 @@ def main():
                "d2h_bytes_per_step": int(oh.nbytes), "ms_per_step": e2e_ms,
                "path": "cvq_cache_decode_step (append k,v + attention) with pinned host buffers"}
 
+    # ---- prefill encode throughput (BASELINE configs[3], "C4"), sampled ----
+    prefill = None
+    if not args.no_prefill and world == 1:
+        del cache
+        torch.cuda.empty_cache()
+        n_pre, S_pre = 1024, layers * H  # one sequence: every (layer, kv head) stream
+        pc = G.QuantizedKVCache(kq, nc, n_seqs=1, n_layers=layers, n_kv_heads=H, q_per_kv=Gq,
+                                capacity=2 * n_pre, hidden=2 * nc, ctx=ctx, keys=args.keys)
+        rs2 = np.random.default_rng(77)
+        for layer in range(layers):
+            for h in range(H):
+                pc.set_key_codebook(layer, h, 0.3 * rs2.standard_normal(2 * kq.n_atoms))
+                pc.set_value_quantizer(
+                    layer, h, rs2.standard_normal((nc, d)) / 16,
+                    0.1 * rs2.standard_normal((d, 2 * nc)), np.zeros(2 * nc),
+                    0.1 * rs2.standard_normal((2 * nc, nc)), np.zeros(nc))
+        Kp = 0.5 * torch.randn(1, layers, H, n_pre, d, device="cuda", generator=gen)
+        Vp = torch.randn(1, layers, H, n_pre, d, device="cuda", generator=gen)
+        pc.prefill(Kp[:, :, :, :128].contiguous(), Vp[:, :, :, :128].contiguous())  # warm
+        torch.cuda.synchronize()
+        pe0, pe1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        pe0.record(stream)
+        pc.prefill(Kp[:, :, :, 128:].contiguous(), Vp[:, :, :, 128:].contiguous())
+        pe1.record(stream)
+        torch.cuda.synchronize()
+        p_ms = pe0.elapsed_time(pe1)
+        th = S_pre * (n_pre - 128) / (p_ms / 1e3)  # token-heads/s
+        prefill = {"token_heads_per_s": th, "kv_tokens_per_s": th / H, "unit": "KV-tokens/s",
+                   "sample": f"{n_pre - 128} tokens x {S_pre} streams, fp32 K/V on device",
+                   "c4_projected_s": 131072 * layers * H / th,
+                   "encoders": "bit-exact fp64 key search + value MLP, device packing"}
+        del pc
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
@@ -327,7 +368,7 @@ def main():
                        "n_codes": nc, "parallelism": f"context-shard x{world}",
                        "l2": "inputs (packed cache) larger than L2"},
             "kv_head_tokens_per_s": value * H, "roofline": roof, "clocks": clk.summary(),
-            "gpu_launches": launches, "e2e": e2e, "cpu_baseline": cpu,
+            "gpu_launches": launches, "e2e": e2e, "cpu_baseline": cpu, "prefill": prefill,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -234,14 +234,17 @@ __device__ __forceinline__ void hadd2_acc(float2& acc, uint32_t h2) {
 
 // fp16-codebook variant of k_fast_score: the slice is stored as packed
 // (x, y) half2, accumulation stays fp32 (FHADD), so each gather moves half
-// the shared-memory bytes.  Each lane owns SPL consecutive subspaces; the 32
-// lanes of a warp decode one token per step.  JC = 32*SPL subspaces per CTA:
-// the whole 64-subspace codebook for R <= 13 (SPL = 2, no split).
-template <int R, int SPL, int G>
+// the shared-memory bytes.  LPT lanes decode one token, each owning SPL
+// consecutive subspaces (SPL = 4: one 16-B LDS per row, so the per-gather
+// address and load instructions are shared by 4 subspaces); a warp decodes
+// TP = 32/LPT tokens per step.  JC = LPT*SPL subspaces per CTA: the whole
+// 64-subspace codebook for R <= 13 (no split).
+template <int R, int SPL, int LPT, int G>
 __global__ void __launch_bounds__(kF1Threads, 1) k_fast_score_h(FastArgs a) {
-  constexpr int JC = 32 * SPL;
+  constexpr int JC = LPT * SPL;
   constexpr int JS = 64 / JC;
-  constexpr int NSTEP = 8;
+  constexpr int TP = 32 / LPT;
+  constexpr int NSTEP = 8 / TP;  // 8 tokens per warp per tile
   constexpr int CW = ((2 * R + 15) / 16) * 16;
   constexpr int WPT = 24 * R;
   constexpr int NV = NSTEP * G;
@@ -256,6 +259,7 @@ __global__ void __launch_bounds__(kF1Threads, 1) k_fast_score_h(FastArgs a) {
   const long long i1 = min(a.n, i0 + a.chunk);
   if (i0 >= i1) return;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int tg = lane / LPT, ln = lane % LPT;
   const int slot = s % a.n_slots;
 
   const uint32_t* cbg = a.cbh + (size_t)slot * R * 64 * 64 + js * JC;
@@ -277,10 +281,10 @@ __global__ void __launch_bounds__(kF1Threads, 1) k_fast_score_h(FastArgs a) {
   float2 stepm[SPL], w[G][SPL];
 #pragma unroll
   for (int m = 0; m < SPL; ++m) {
-    const int j = js * JC + lane * SPL + m;
+    const int j = js * JC + ln * SPL + m;
     theta[m] = a.thetas[j];
     double sn, cs;
-    sincos(theta[m], &sn, &cs);
+    sincos((double)TP * theta[m], &sn, &cs);  // e^{+i TP theta}: next step's token
     stepm[m] = make_float2((float)cs, (float)sn);
 #pragma unroll
     for (int h = 0; h < G; ++h) {
@@ -289,6 +293,7 @@ __global__ void __launch_bounds__(kF1Threads, 1) k_fast_score_h(FastArgs a) {
     }
   }
   float* ps = a.ps + ((size_t)(s * JS + js) * a.n) * G;
+  const uint32_t* cb_lane = cbs + ln * SPL;
 
   for (int k = 0; k < ntiles; ++k) {
     if (k + 1 < ntiles) {
@@ -314,11 +319,11 @@ __global__ void __launch_bounds__(kF1Threads, 1) k_fast_score_h(FastArgs a) {
     if (tok0 < valid) {
       float2 ph[SPL];
 #pragma unroll
-      for (int m = 0; m < SPL; ++m) ph[m] = phase_neg(a.t - (a.pos0 + ti + tok0), theta[m]);
+      for (int m = 0; m < SPL; ++m) ph[m] = phase_neg(a.t - (a.pos0 + ti + tok0 + tg), theta[m]);
       float acc[NV];
 #pragma unroll
       for (int st = 0; st < NSTEP; ++st) {
-        const int dlt = tok0 + st;
+        const int dlt = tok0 + st * TP + tg;
         const uint4* cd = reinterpret_cast<const uint4*>(codes + dlt * CW);
         uint4 cv[CW / 16];
 #pragma unroll
@@ -332,9 +337,20 @@ __global__ void __launch_bounds__(kF1Threads, 1) k_fast_score_h(FastArgs a) {
           const uint32_t word = cw[(2 * r) >> 2];
           const unsigned ca = __byte_perm(word, 0, 0x4440 | ((2 * r) & 3));
           const unsigned cbb = __byte_perm(word, 0, 0x4440 | ((2 * r + 1) & 3));
-          const uint32_t* ra = cbs + (r * 64 + ca) * JC + lane * SPL;
-          const uint32_t* rb = cbs + (r * 64 + cbb) * JC + lane * SPL;
-          if constexpr (SPL == 2) {
+          const uint32_t* ra = cb_lane + (r * 64 + ca) * JC;
+          const uint32_t* rb = cb_lane + (r * 64 + cbb) * JC;
+          if constexpr (SPL == 4) {
+            const uint4 va = *reinterpret_cast<const uint4*>(ra);
+            const uint4 vb = *reinterpret_cast<const uint4*>(rb);
+            hadd2_acc(ka[0], va.x);
+            hadd2_acc(ka[1], va.y);
+            hadd2_acc(ka[2], va.z);
+            hadd2_acc(ka[3], va.w);
+            hadd2_acc(kb[0], vb.x);
+            hadd2_acc(kb[1], vb.y);
+            hadd2_acc(kb[2], vb.z);
+            hadd2_acc(kb[3], vb.w);
+          } else if constexpr (SPL == 2) {
             const uint2 va = *reinterpret_cast<const uint2*>(ra);
             const uint2 vb = *reinterpret_cast<const uint2*>(rb);
             hadd2_acc(ka[0], va.x);
@@ -364,13 +380,13 @@ __global__ void __launch_bounds__(kF1Threads, 1) k_fast_score_h(FastArgs a) {
         for (int h = 0; h < G; ++h) acc[st * G + h] = part[h];
       }
       bool writer;
-      const int base = reduce_scatter<NV, 32>(acc, lane, writer);
-      constexpr int VPL = NV / 32 > 0 ? NV / 32 : 1;
+      const int base = reduce_scatter<NV, LPT>(acc, lane, writer);
+      constexpr int VPL = NV / LPT > 0 ? NV / LPT : 1;
 #pragma unroll
       for (int m = 0; m < VPL; ++m) {
         const int vi = base + m;
         const int st = vi / G, h = vi % G;
-        const int dlt = tok0 + st;
+        const int dlt = tok0 + st * TP + tg;
         if (writer && dlt < valid) ps[(ti + dlt) * G + h] = acc[m];
       }
     }
@@ -568,14 +584,16 @@ cudaError_t launch_f1(const FastArgs& a, int S, cudaStream_t st) {
 
 template <int R, int G>
 cudaError_t launch_f1h(const FastArgs& a, int S, cudaStream_t st) {
-  constexpr int SPL = R <= 13 ? 2 : 1;
-  constexpr int JS = 2 / SPL;
-  const size_t sm = f1_smem(R, 32 * SPL, 4);
+  // 16 lanes x 4 subspaces per token; the whole codebook per CTA for R <= 13
+  constexpr int SPL = R <= 13 ? 4 : 2;
+  constexpr int LPT = 16;
+  constexpr int JS = 64 / (SPL * LPT);
+  const size_t sm = f1_smem(R, SPL * LPT, 4);
   static size_t done = 0;
-  cudaError_t e = set_smem(k_fast_score_h<R, SPL, G>, sm, done);
+  cudaError_t e = set_smem(k_fast_score_h<R, SPL, LPT, G>, sm, done);
   if (e != cudaSuccess) return e;
   dim3 grid((unsigned)((a.n + a.chunk - 1) / a.chunk), S * JS);
-  k_fast_score_h<R, SPL, G><<<grid, kF1Threads, sm, st>>>(a);
+  k_fast_score_h<R, SPL, LPT, G><<<grid, kF1Threads, sm, st>>>(a);
   count_launch();
   return cudaGetLastError();
 }

@@ -44,8 +44,13 @@ def gather_partials(m, l, o, group=None):
         dist.all_gather_into_tensor(M, m.contiguous(), group=group)
         dist.all_gather_into_tensor(Lh, l.contiguous(), group=group)
         dist.all_gather_into_tensor(O.view(world, rows * d), o.contiguous().view(-1), group=group)
-    else:  # gloo has no all_gather_into_tensor: list form into views of the same buffers
-        dist.all_gather(list(M.unbind(0)), m.contiguous(), group=group)
-        dist.all_gather(list(Lh.unbind(0)), l.contiguous(), group=group)
-        dist.all_gather(list(O.unbind(0)), o.contiguous(), group=group)
+    else:  # gloo: host tensors, list form into views of the same buffers
+        hm, hl, ho = (x.contiguous().cpu() for x in (m, l, o))
+        HM, HL, HO = (torch.empty(t.shape, dtype=t.dtype) for t in (M, Lh, O))
+        dist.all_gather(list(HM.unbind(0)), hm, group=group)
+        dist.all_gather(list(HL.unbind(0)), hl, group=group)
+        dist.all_gather(list(HO.unbind(0)), ho, group=group)
+        M.copy_(HM)
+        Lh.copy_(HL)
+        O.copy_(HO)
     return M, Lh, O
