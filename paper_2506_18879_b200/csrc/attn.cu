@@ -315,7 +315,7 @@ cudaError_t run_naive_attention(const AttnJob& job, const float* q, float* out, 
 bool fast_path_applies(const AttnJob& job);
 size_t fast_scratch_bytes(const AttnJob& job, int* n_chunks);
 cudaError_t run_attention_fast(const AttnJob& job, const float* q, float* pm,
-                               float* pl, float* po, int n_chunks, void* scratch,
+                               float* pl, float* po, int* n_chunks, void* scratch,
                                cudaStream_t st, cudaEvent_t* prof, float* scores_out);
 
 static int generic_chunk(const AttnJob& job) {
@@ -361,7 +361,7 @@ cudaError_t run_attention(const AttnJob& job, const float* q, float* out,
     pm = reinterpret_cast<float*>(p + extra);
     pl = pm + (size_t)nc * rows;
     po = pl + (size_t)nc * rows;
-    e = run_attention_fast(job, q, pm, pl, po, nc, p, st, prof, scores_out);
+    e = run_attention_fast(job, q, pm, pl, po, &nc, p, st, prof, scores_out);
     if (e != cudaSuccess) return e;
   } else {
     const int CH = generic_chunk(job);

@@ -18,7 +18,9 @@
 //     from cp.async-staged value words (attn.cpp:239-247), then
 //     o = z . C_V / l (attn.cpp:249-255).  Writes the chunk partial (m, l, o)
 //     merged by k_combine (attn.cu).
+#include <algorithm>
 #include <cfloat>
+#include <cstdlib>
 
 #include "cvq_internal.cuh"
 
@@ -394,6 +396,257 @@ __global__ void __launch_bounds__(kF1Threads, 1) k_fast_score_h(FastArgs a) {
   }
 }
 
+// Fused single-kernel decode attention for the 1-bit head preset with the
+// fp16 codebook (whole codebook per CTA, so every CTA has complete scores):
+// k_fast_score_h's key decode (R rounds, 16 lanes x 4 subspaces per token,
+// G = 4 query heads) followed, per warp and per 8-token run, by an online
+// softmax and the value accumulation z[c][h] += p_h bit_c (attn.cpp:
+// 237-247) on value words streamed with the key words.  The 16 warps'
+// (m, l, z) are merged at the end of the chunk and o = z C_V / l written as
+// the chunk partial (attn.cpp:249-255).  Removes the partial-score round
+// trip and the separate value kernel.
+template <int R>
+__global__ void __launch_bounds__(kF1Threads, 1) k_fast_attn_h(FastArgs a) {
+  constexpr int G = 4, NC = 128, SPL = 4, LPT = 16, JC = 64, TP = 2, NSTEP = 4;
+  constexpr int CW = ((2 * R + 15) / 16) * 16;
+  constexpr int WPT = 24 * R;
+  constexpr int VPT = 2 * kTile;  // value words per tile (128 bits per token)
+  constexpr int NV = NSTEP * G;   // 16 = LPT: one (token, head) score per lane
+  constexpr int NW = kF1Threads / 32;
+  extern __shared__ __align__(16) unsigned char smem[];
+  uint32_t* cbs = reinterpret_cast<uint32_t*>(smem);                           // [R][64][64] half2
+  uint64_t* wbuf = reinterpret_cast<uint64_t*>(smem + (size_t)R * 64 * JC * 4);  // [2][WPT]
+  uint64_t* vbuf = wbuf + 2 * WPT;                                             // [2][VPT]
+  float4* pw = reinterpret_cast<float4*>(vbuf + 2 * VPT);                      // [NW][8]
+  uint8_t* codes = reinterpret_cast<uint8_t*>(pw + NW * 8);                    // [kTile][CW]
+
+  const int s = blockIdx.y;
+  const long long i0 = (long long)blockIdx.x * a.chunk;
+  const long long i1 = min(a.n, i0 + a.chunk);
+  if (i0 >= i1) return;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int tg = lane / LPT, ln = lane % LPT;
+  const int slot = s % a.n_slots;
+
+  const uint32_t* cbg = a.cbh + (size_t)slot * R * 64 * 64;
+  for (int e = tid; e < R * 64 * (JC / 4); e += kF1Threads) cp_async16(cbs + 4 * e, cbg + 4 * e);
+  cp_async_commit();
+  const uint64_t* kw = a.kpool + (size_t)s * a.kstride + (size_t)(i0 / kTile) * WPT;
+  const uint64_t* vwg = a.vpool + (size_t)s * a.vstride + (size_t)(i0 / kTile) * VPT;
+  const int ntiles = (int)((i1 - i0 + kTile - 1) / kTile);
+  auto load_tile = [&](int k, int buf) {
+    const uint64_t* src = kw + (size_t)k * WPT;
+    for (int e = tid; e < WPT / 2; e += kF1Threads) cp_async16(wbuf + buf * WPT + 2 * e, src + 2 * e);
+    const uint64_t* vsrc = vwg + (size_t)k * VPT;
+    for (int e = tid; e < VPT / 2; e += kF1Threads) cp_async16(vbuf + buf * VPT + 2 * e, vsrc + 2 * e);
+    cp_async_commit();
+  };
+  load_tile(0, 0);
+
+  double theta[SPL];
+  float2 stepm[SPL], w[G][SPL];
+#pragma unroll
+  for (int m = 0; m < SPL; ++m) {
+    const int j = ln * SPL + m;
+    theta[m] = a.thetas[j];
+    double sn, cs;
+    sincos((double)TP * theta[m], &sn, &cs);
+    stepm[m] = make_float2((float)cs, (float)sn);
+#pragma unroll
+    for (int h = 0; h < G; ++h) {
+      const float* qr = a.q + ((size_t)s * G + h) * 128;
+      w[h][m] = make_float2(qr[2 * j] * 0.08838834764831845f, -qr[2 * j + 1] * 0.08838834764831845f);
+    }
+  }
+  const uint32_t* cb_lane = cbs + ln * SPL;
+  // per-warp online-softmax state; this lane's head is lane & 3, its codes
+  // are 4*lane .. 4*lane+3 for all 4 heads (z as head pairs for FADD2)
+  float m_run = -INFINITY, l_run = 0.f;
+  float2 z[4][2];
+#pragma unroll
+  for (int c = 0; c < 4; ++c) z[c][0] = z[c][1] = make_float2(0.f, 0.f);
+
+  for (int k = 0; k < ntiles; ++k) {
+    if (k + 1 < ntiles) {
+      load_tile(k + 1, (k + 1) & 1);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    const uint64_t* wt = wbuf + (k & 1) * WPT;
+    for (int e = tid; e < kTile * 2 * R; e += kF1Threads) {
+      const int tok = e / (2 * R), f = e % (2 * R);
+      const unsigned bit = (unsigned)e * 6u;
+      const unsigned wi = bit >> 6, off = bit & 63u;
+      unsigned long long v = wt[wi] >> off;
+      if (off > 58u) v |= wt[wi + 1] << (64u - off);
+      codes[tok * CW + f] = (uint8_t)(v & 63u);
+    }
+    __syncthreads();
+    const long long ti = i0 + (long long)k * kTile;
+    const int valid = (int)min((long long)kTile, i1 - ti);
+    const int tok0 = warp * 8;
+    if (tok0 < valid) {
+      float2 ph[SPL];
+#pragma unroll
+      for (int m = 0; m < SPL; ++m) ph[m] = phase_neg(a.t - (a.pos0 + ti + tok0 + tg), theta[m]);
+      float acc[NV];
+#pragma unroll
+      for (int st = 0; st < NSTEP; ++st) {
+        const int dlt = tok0 + st * TP + tg;
+        const uint4* cd = reinterpret_cast<const uint4*>(codes + dlt * CW);
+        uint4 cv[CW / 16];
+#pragma unroll
+        for (int c = 0; c < CW / 16; ++c) cv[c] = cd[c];
+        const uint32_t* cw = reinterpret_cast<const uint32_t*>(cv);
+        float2 ka[SPL], kb[SPL];
+#pragma unroll
+        for (int m = 0; m < SPL; ++m) ka[m] = kb[m] = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const uint32_t word = cw[(2 * r) >> 2];
+          const unsigned ca = __byte_perm(word, 0, 0x4440 | ((2 * r) & 3));
+          const unsigned cbb = __byte_perm(word, 0, 0x4440 | ((2 * r + 1) & 3));
+          const uint4 va = *reinterpret_cast<const uint4*>(cb_lane + (r * 64 + ca) * JC);
+          const uint4 vb = *reinterpret_cast<const uint4*>(cb_lane + (r * 64 + cbb) * JC);
+          hadd2_acc(ka[0], va.x);
+          hadd2_acc(ka[1], va.y);
+          hadd2_acc(ka[2], va.z);
+          hadd2_acc(ka[3], va.w);
+          hadd2_acc(kb[0], vb.x);
+          hadd2_acc(kb[1], vb.y);
+          hadd2_acc(kb[2], vb.z);
+          hadd2_acc(kb[3], vb.w);
+        }
+        float part[G];
+#pragma unroll
+        for (int h = 0; h < G; ++h) part[h] = 0.f;
+#pragma unroll
+        for (int m = 0; m < SPL; ++m) {
+          const float kx = ka[m].x - kb[m].y, ky = ka[m].y + kb[m].x;
+          const float rx = ph[m].x * kx - ph[m].y * ky;
+          const float ry = ph[m].x * ky + ph[m].y * kx;
+#pragma unroll
+          for (int h = 0; h < G; ++h) part[h] += w[h][m].x * rx - w[h][m].y * ry;
+          const float nx = ph[m].x * stepm[m].x - ph[m].y * stepm[m].y;
+          ph[m].y = ph[m].x * stepm[m].y + ph[m].y * stepm[m].x;
+          ph[m].x = nx;
+        }
+#pragma unroll
+        for (int h = 0; h < G; ++h) acc[st * G + h] = part[h];
+      }
+      bool writer;
+      reduce_scatter<NV, LPT>(acc, lane, writer);
+      // lane holds the score of (token tok0 + slot, head lane & 3), slot =
+      // ((lane & 15) >> 2) * 2 + (lane >> 4)
+      const int tslot = ((lane & 15) >> 2) * 2 + (lane >> 4);
+      const bool ok = tok0 + tslot < valid;
+      const float sv = ok ? acc[0] : -INFINITY;
+      float tm = sv;
+      tm = fmaxf(tm, __shfl_xor_sync(0xffffffffu, tm, 4));
+      tm = fmaxf(tm, __shfl_xor_sync(0xffffffffu, tm, 8));
+      tm = fmaxf(tm, __shfl_xor_sync(0xffffffffu, tm, 16));
+      const float mn = fmaxf(m_run, tm);
+      const float scale = (m_run == -INFINITY) ? 0.f : __expf(m_run - mn);
+      const float p = ok ? __expf(sv - mn) : 0.f;
+      float psum = p;
+      psum += __shfl_xor_sync(0xffffffffu, psum, 4);
+      psum += __shfl_xor_sync(0xffffffffu, psum, 8);
+      psum += __shfl_xor_sync(0xffffffffu, psum, 16);
+      l_run = l_run * scale + psum;
+      m_run = mn;
+      const float2 s01 = make_float2(__shfl_sync(0xffffffffu, scale, 0),
+                                     __shfl_sync(0xffffffffu, scale, 1));
+      const float2 s23 = make_float2(__shfl_sync(0xffffffffu, scale, 2),
+                                     __shfl_sync(0xffffffffu, scale, 3));
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        z[c][0].x *= s01.x;
+        z[c][0].y *= s01.y;
+        z[c][1].x *= s23.x;
+        z[c][1].y *= s23.y;
+      }
+      reinterpret_cast<float*>(pw + warp * 8 + tslot)[lane & 3] = p;
+      __syncwarp();
+      const uint64_t* vt = vbuf + (k & 1) * VPT;
+#pragma unroll
+      for (int sl = 0; sl < 8; ++sl) {
+        if (tok0 + sl < valid) {
+          const float4 pp = pw[warp * 8 + sl];
+          const unsigned bits =
+              (unsigned)(vt[(tok0 + sl) * 2 + (lane >> 4)] >> (4 * (lane & 15)));
+          const float2 p01 = make_float2(pp.x, pp.y), p23 = make_float2(pp.z, pp.w);
+#pragma unroll
+          for (int c = 0; c < 4; ++c)
+            if (bits & (1u << c)) {
+              add2(z[c][0], p01);
+              add2(z[c][1], p23);
+            }
+        }
+      }
+      __syncwarp();
+    }
+    __syncthreads();
+  }
+  // ---- merge the 16 warps' (m, l, z) (codebook smem is free now) ----
+  float* red = reinterpret_cast<float*>(smem);  // [NW][8 + NC*G]
+  float* mine = red + warp * (8 + NC * G);
+  {  // lanes 0..3 hold heads 0..3 (every lane with the same lane & 3 agrees)
+    const float mh = __shfl_sync(0xffffffffu, m_run, lane & 3);
+    const float lh = __shfl_sync(0xffffffffu, l_run, lane & 3);
+    if (lane < 4) {
+      mine[lane] = mh;
+      mine[4 + lane] = lh;
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    float* zc = mine + 8 + (4 * lane + c) * G;
+    zc[0] = z[c][0].x;
+    zc[1] = z[c][0].y;
+    zc[2] = z[c][1].x;
+    zc[3] = z[c][1].y;
+  }
+  __syncthreads();
+  __shared__ float Mh[G], Lh[G], Wt[NW][G];
+  if (tid < G) {
+    float M = -INFINITY;
+    for (int ww = 0; ww < NW; ++ww) M = fmaxf(M, red[ww * (8 + NC * G) + tid]);
+    float L = 0.f;
+    for (int ww = 0; ww < NW; ++ww) {
+      const float mw = red[ww * (8 + NC * G) + tid];
+      const float wt = (mw == -INFINITY) ? 0.f : __expf(mw - M);
+      Wt[ww][tid] = wt;
+      L += red[ww * (8 + NC * G) + 4 + tid] * wt;
+    }
+    Mh[tid] = M;
+    Lh[tid] = L;
+  }
+  __syncthreads();
+  float* Z = red + NW * (8 + NC * G);  // [NC][G]
+  for (int e = tid; e < NC * G; e += kF1Threads) {
+    const int h = e % G;
+    float v = 0.f;
+    for (int ww = 0; ww < NW; ++ww) v += red[ww * (8 + NC * G) + 8 + e] * Wt[ww][h];
+    Z[e] = v;
+  }
+  __syncthreads();
+  const float* cb = a.cbv + (size_t)slot * NC * 128;
+  const long long rows = (long long)a.S * G;
+  for (int e = tid; e < G * 128; e += kF1Threads) {
+    const int h = e / 128, jd = e % 128;
+    float acc = 0.f;
+#pragma unroll 8
+    for (int kk = 0; kk < NC; ++kk) acc += Z[kk * G + h] * __ldg(cb + (size_t)kk * 128 + jd);
+    a.po[((long long)blockIdx.x * rows + (long long)s * G + h) * 128 + jd] = acc / Lh[h];
+  }
+  if (tid < G) {
+    a.pm[(long long)blockIdx.x * rows + (long long)s * G + tid] = Mh[tid];
+    a.pl[(long long)blockIdx.x * rows + (long long)s * G + tid] = Lh[tid];
+  }
+}
+
 template <int NC, int G, int JS>
 __global__ void __launch_bounds__(kThreads) k_fast_value(FastArgs a) {
   constexpr int CPL = NC / 32;       // codes per lane
@@ -550,7 +803,7 @@ int f2_chunk(const AttnJob& job) {
   long long want = (job.n * (long long)job.S + 2 * 148 - 1) / (2 * 148);
   long long ch = (want + kTile - 1) / kTile * kTile;
   if (ch < 256) ch = 256;
-  if (ch > 2048) ch = 2048;
+  if (ch > 1024) ch = 1024;  // 40 KiB smem -> 5 CTAs/SM: latency-bound kernel
   return (int)ch;
 }
 
@@ -627,16 +880,30 @@ bool fast_path_applies(const AttnJob& job) {
          (g.n_codes == 128 || g.n_codes == 256) && (g.G == 1 || g.G == 4) && job.n > 0;
 }
 
+// single fused kernel (k_fast_attn_h): 1-bit fp16-codebook preset, GQA 4
+bool fused_applies(const AttnJob& job) {
+  const Geom& g = job.geo;
+  // Measured slower than score + value kernels on C3 (20.2 vs 19.5 ms: the
+  // score loop is issue-bound, so in-loop value work costs more than the
+  // separate kernel); opt-in only.
+  return job.cb_key16 && !job.cb_key_tc && g.R == 11 && g.G == 4 && g.n_codes == 128 &&
+         getenv("CVQ_ENABLE_FUSED");
+}
+
 size_t fast_scratch_bytes(const AttnJob& job, int* n_chunks) {
   const int JS = js_for(job);
   const int c2 = f2_chunk(job);
   *n_chunks = (int)((job.n + c2 - 1) / c2);
+  if (fused_applies(job)) {
+    const int c1 = f1_chunk(job);
+    *n_chunks = std::max(*n_chunks, (int)((job.n + c1 - 1) / c1));
+  }
   const size_t ps = (size_t)job.S * JS * job.n * job.geo.G * sizeof(float);
   return (ps + 255) / 256 * 256;
 }
 
 cudaError_t run_attention_fast(const AttnJob& job, const float* q, float* pm, float* pl,
-                               float* po, int n_chunks, void* scratch, cudaStream_t st,
+                               float* po, int* n_chunks, void* scratch, cudaStream_t st,
                                cudaEvent_t* prof, float* scores_out) {
   const Geom& g = job.geo;
   FastArgs a{};
@@ -661,8 +928,21 @@ cudaError_t run_attention_fast(const AttnJob& job, const float* q, float* pm, fl
   a.pm = pm;
   a.pl = pl;
   a.po = po;
-  (void)n_chunks;
   cudaError_t e;
+  if (fused_applies(job) && !scores_out) {
+    const size_t sm = (size_t)11 * 64 * 64 * 4 + 2 * 24 * 11 * 8 + 2 * 2 * kTile * 8 +
+                      (kF1Threads / 32) * 8 * 16 + (size_t)kTile * 32;
+    static size_t done = 0;
+    if ((e = set_smem(k_fast_attn_h<11>, sm, done)) != cudaSuccess) return e;
+    const int nc = (int)((job.n + a.chunk - 1) / a.chunk);
+    if (prof) cudaEventRecord(prof[0], st);
+    k_fast_attn_h<11><<<dim3((unsigned)nc, job.S), kF1Threads, sm, st>>>(a);
+    count_launch();
+    if (prof) cudaEventRecord(prof[1], st);
+    *n_chunks = nc;
+    return cudaGetLastError();
+  }
+  *n_chunks = (int)((job.n + a.chunk2 - 1) / a.chunk2);
   if (prof) cudaEventRecord(prof[0], st);
   if (job.cb_key_tc) {
     e = run_tc_score(job, q, a.ps, a.chunk, st);

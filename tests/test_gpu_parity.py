@@ -419,3 +419,24 @@ def test_bench_shape_precision(G, keys, scale):
             worst = max(worst, fx.rel_err(out[0, 0, h * Gq + j], want))
     print(keys, scale, "worst rel err", worst)
     assert worst <= 1e-3, worst
+
+
+@pytest.mark.parametrize("n", [1, 200, 5000])
+def test_fused_kernel_matches_split_kernels(G, n, monkeypatch):
+    """k_fast_attn_h (opt-in single-kernel path) == score + value kernels."""
+    kq = KQ(128, 64, 64, 11)
+    nc, H, Gq = 128, 2, 4
+    rng = P.rng(n)
+    c = G.QuantizedKVCache(kq, nc, n_layers=2, n_kv_heads=H, q_per_kv=Gq, capacity=n, keys="fp16")
+    for layer in range(2):
+        for h in range(H):
+            c.set_key_codebook(layer, h, rng.normal(2 * kq.n_atoms, 0.3))
+            c.set_value_quantizer(layer, h, rng.normal(nc * 128, 1 / 16).reshape(nc, 128))
+            a, b = fx.random_key_codes(kq, n, rng=rng)
+            bits = fx.random_value_codes(nc, n, rng=rng)
+            c.import_stream(0, layer, h, P.pack_key_codes(kq, a, b), P.pack_value_codes(bits), n)
+    q = rng.normal(2 * H * Gq * 128).reshape(1, 2, H * Gq, 128).astype(np.float32)
+    split = c.attention(q)
+    monkeypatch.setenv("CVQ_ENABLE_FUSED", "1")
+    fused = c.attention(q)
+    assert fx.rel_err(fused, split) <= 1e-5
