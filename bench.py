@@ -278,8 +278,19 @@ def main():
     bytes_per_launch = kvht_per_launch * BYTES_PER_KVHT[R]
     avg_main_ms = main_ms / max(main_n, 1)
     achieved = bytes_per_launch / (avg_main_ms / 1e3) / 1e9
+    # dram read+write bytes of the same kernel from the committed ncu capture
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            tr = json.load(f).get(f"{args.config}/{args.keys}")
+        if tr and world == 1:
+            traffic = tr["dram_bytes_per_launch"]
+    except Exception:
+        pass
     roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-            "frac": achieved / hbm, "traffic": None, "peak_source": src,
+            "frac": achieved / hbm, "traffic": traffic, "peak_source": src,
+            "traffic_note": "dram__bytes_read+write of the score kernel per launch "
+                            "(profiles/traffic.json); the value kernel reads the value words",
             "kernel_ms": avg_main_ms, "kernel_share_of_step": avg_main_ms / ms,
             "algorithmic_bytes_per_launch": bytes_per_launch,
             "kv_head_tokens_per_s_kernel": kvht_per_launch / (avg_main_ms / 1e3)}
