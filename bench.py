@@ -190,7 +190,7 @@ def main():
     from paper_2506_18879_b200.dist import gather_partials, shard_plan
     lo, hi = shard_plan(N, world)[rank]
     n_local = hi - lo
-    extra = args.steps + args.warmup + 8
+    extra = 2 * (args.steps + args.warmup) + 16  # room for the e2e decode steps' appends
     # a real (non-default) stream shared by torch and libcvq, so the CUDA
     # events below see the library's kernels
     stream = torch.cuda.Stream()
@@ -314,10 +314,19 @@ def main():
             cache.decode_step(k_pin, v_pin, q_pin, o_pin)
         torch.cuda.synchronize()
         e2e_ms = (time.perf_counter() - t0) * 1e3 / n_e2e
+        # breakdown: the append alone (encode + pack of one token per stream)
+        kd, vd = k_pin.cuda(), v_pin.cuda()
+        torch.cuda.synchronize()
+        t1 = time.perf_counter()
+        for _ in range(2):
+            cache.append(kd, vd)
+        torch.cuda.synchronize()
+        append_ms = (time.perf_counter() - t1) * 1e3 / 2
         n_now = cache.size()
         e2e = {"value": B * layers * n_now / (e2e_ms / 1e3), "unit": "KV-tokens/s",
                "h2d_bytes_per_step": int(kh.nbytes + vh.nbytes + qh.nbytes),
                "d2h_bytes_per_step": int(oh.nbytes), "ms_per_step": e2e_ms,
+               "append_ms": append_ms,
                "path": "cvq_cache_decode_step (append k,v + attention) with pinned host buffers"}
 
     # ---- prefill encode throughput (BASELINE configs[3], "C4"), sampled ----

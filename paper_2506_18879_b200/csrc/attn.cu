@@ -200,20 +200,28 @@ __global__ void k_combine(const float* __restrict__ m, const float* __restrict__
                           const float* __restrict__ o, int P, long long rows, int d,
                           float* __restrict__ out, float* __restrict__ m_out,
                           float* __restrict__ l_out) {
+  // part weights l_p e^{m_p - M} computed once per part (smem), then each
+  // thread sums its output column over the parts
+  extern __shared__ float wsh[];  // [P]
+  __shared__ float red[33];
   const long long row = blockIdx.x;
   float M = -FLT_MAX;
-  for (int p = 0; p < P; ++p)
+  for (int p = threadIdx.x; p < P; p += blockDim.x)
     if (l[p * rows + row] > 0.f) M = fmaxf(M, m[p * rows + row]);
-  float Lsum = 0.f;
-  for (int p = 0; p < P; ++p) {
+  M = block_reduce(M, true, red);
+  float Ls = 0.f;
+  for (int p = threadIdx.x; p < P; p += blockDim.x) {
     const float lp = l[p * rows + row];
-    if (lp > 0.f) Lsum += lp * expf(m[p * rows + row] - M);
+    const float wgt = lp > 0.f ? lp * expf(m[p * rows + row] - M) : 0.f;
+    wsh[p] = wgt;
+    Ls += wgt;
   }
+  const float Lsum = block_reduce(Ls, false, red);  // (its barriers publish wsh)
   for (int jd = threadIdx.x; jd < d; jd += blockDim.x) {
     float acc = 0.f;
     for (int p = 0; p < P; ++p) {
-      const float lp = l[p * rows + row];
-      if (lp > 0.f) acc += o[(p * rows + row) * d + jd] * (lp * expf(m[p * rows + row] - M));
+      const float wgt = wsh[p];
+      if (wgt != 0.f) acc += o[(p * rows + row) * d + jd] * wgt;
     }
     out[row * d + jd] = acc / Lsum;
   }
@@ -227,7 +235,8 @@ cudaError_t run_lse_combine(const float* m, const float* l, const float* o,
                             int n_parts, long long rows, int d, float* out,
                             float* m_out, float* l_out, cudaStream_t st) {
   if (rows == 0) return cudaSuccess;
-  k_combine<<<(unsigned)rows, 128, 0, st>>>(m, l, o, n_parts, rows, d, out, m_out, l_out);
+  k_combine<<<(unsigned)rows, 128, (size_t)n_parts * sizeof(float), st>>>(m, l, o, n_parts, rows,
+                                                                          d, out, m_out, l_out);
   count_launch();
   return cudaGetLastError();
 }

@@ -285,6 +285,155 @@ k_encode_keys_brute(Geom g, int n_slots, const double* __restrict__ atoms,
     }
 }
 
+
+// Decode-step key encoder: one 128-thread CTA per (token, stream), the
+// round's slice and screen table read straight from L2 (no smem staging --
+// appends encode one token per stream).  Same screen + exact re-check as
+// k_encode_keys_table; requires 2L <= 128 (L <= 64).
+constexpr int kSmallThreads = 128;
+
+__device__ __forceinline__ void block_argmin2(double& b1, int& c1, double& b2, double* rv, int* rc) {
+  // per-warp: argmin with smallest index, runner-up = min over the rest
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double v = b1;
+  int c = c1;
+  warp_argmin(v, c);
+  double ru = (c1 == c) ? b2 : b1;
+  for (int o = 16; o; o >>= 1) ru = fmin(ru, __shfl_xor_sync(0xffffffffu, ru, o));
+  if (lane == 0) {
+    rv[warp] = v;
+    rc[warp] = c;
+    rv[4 + warp] = ru;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double gv = rv[0], gr = rv[4];
+    int gc = rc[0];
+    for (int w = 1; w < kSmallThreads / 32; ++w) {
+      // merge (gv, gc, gr) with (rv[w], rc[w], rv[4+w])
+      if (rv[w] < gv || (rv[w] == gv && rc[w] < gc)) {
+        gr = fmin(gv, fmin(gr, rv[4 + w]));
+        gv = rv[w];
+        gc = rc[w];
+      } else {
+        gr = fmin(gr, fmin(rv[w], rv[4 + w]));
+      }
+    }
+    rv[8] = gv;
+    rv[9] = gr;
+    rc[8] = gc;
+  }
+  __syncthreads();
+  b1 = rv[8];
+  b2 = rv[9];
+  c1 = rc[8];
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(kSmallThreads)
+k_encode_keys_small(Geom g, int n_slots, const double* __restrict__ atoms,
+                    const double* __restrict__ base, const double* __restrict__ maxnorm,
+                    const void* __restrict__ keys, int dtype, long long s_stride, long long n,
+                    uint16_t* __restrict__ a_out, uint16_t* __restrict__ b_out) {
+  extern __shared__ double sm[];
+  double* P = sm;               // [d]
+  double* PU = P + g.d;         // [L]
+  double* PV = PU + g.L;        // [L]
+  __shared__ double rv[12];
+  __shared__ int rc[12];
+  const int s = blockIdx.y, tid = threadIdx.x;
+  const long long i = blockIdx.x;
+  const int slot = s % n_slots;
+  for (int e = tid; e < g.d; e += blockDim.x)
+    P[e] = load_elem(keys, dtype, (long long)s * s_stride + i * g.d + e);
+  __syncthreads();
+  const int L = g.L, gs = g.g, w2 = 2 * g.g;
+  for (int r = 0; r < g.R; ++r) {
+    for (int grp = 0; grp < g.groups; ++grp) {
+      const double2* U = reinterpret_cast<const double2*>(atoms) +
+                         ((size_t)(slot * g.R + r) * g.subs + (size_t)grp * gs) * L;
+      const double* B = base + ((size_t)(slot * g.R + r) * g.groups + grp) * L * L;
+      const double mn = maxnorm[(size_t)(slot * g.R + r) * g.groups + grp];
+      double* p = P + grp * w2;
+      if (tid < 2 * L) {  // threads [0,L): p.u_l, [L,2L): p.v_l
+        const int l = tid % L;
+        const bool isv = tid >= L;
+        double acc = 0.0;
+        for (int si = 0; si < gs; ++si) {
+          const double2 u = __ldg(U + (size_t)si * L + l);
+          const double px = p[2 * si], py = p[2 * si + 1];
+          acc = isv ? fma(py, u.x, fma(-px, u.y, acc)) : fma(px, u.x, fma(py, u.y, acc));
+        }
+        (isv ? PV : PU)[l] = acc;
+      }
+      double pn = 0.0;
+      if (tid < 32) {
+        for (int e = tid; e < w2; e += 32) pn = fma(p[e], p[e], pn);
+        for (int o = 16; o; o >>= 1) pn += __shfl_xor_sync(0xffffffffu, pn, o);
+        if (tid == 0) rv[10] = pn;
+      }
+      __syncthreads();
+      pn = rv[10];
+      int chosen;
+      bool exact = !(pn < 1e300) || !(mn < 1e150);
+      double gb = 0.0, margin = 0.0;
+      if (!exact) {
+        double b1 = INFINITY, b2 = INFINITY;
+        int c1 = 0x7fffffff;
+        for (int c = tid; c < L * L; c += blockDim.x) {
+          const int aa = c / L, bb = c % L;
+          const double sc = __ldg(B + c) - 2.0 * PU[aa] - 2.0 * PV[bb];
+          if (sc < b1 || (sc == b1 && c < c1)) {
+            b2 = b1;
+            b1 = sc;
+            c1 = c;
+          } else if (sc < b2) {
+            b2 = sc;
+          }
+        }
+        block_argmin2(b1, c1, b2, rv, rc);
+        const double scale = sqrt(pn) + 2.0 * mn;
+        margin = kMarginRel * scale * scale * fmax(1.0, w2 / 128.0);
+        gb = b1;
+        chosen = c1;
+        exact = !(b2 > b1 + margin);
+      }
+      if (exact) {  // re-evaluate every candidate within the margin exactly
+        const bool all = !(pn < 1e300) || !(mn < 1e150);
+        double best = INFINITY;
+        int bc = 0x7fffffff;
+        for (int c = tid; c < L * L; c += blockDim.x) {
+          const int aa = c / L, bb = c % L;
+          if (!all) {
+            const double sc = __ldg(B + c) - 2.0 * PU[aa] - 2.0 * PV[bb];
+            if (!(sc <= gb + margin)) continue;
+          }
+          const double dd = exact_dist(p, U, L, gs, aa, bb);
+          if (dd < best || (dd == best && c < bc)) {
+            best = dd;
+            bc = c;
+          }
+        }
+        double dummy = INFINITY;
+        block_argmin2(best, bc, dummy, rv, rc);
+        chosen = (bc == 0x7fffffff) ? 0 : bc;
+      }
+      const int ca = chosen / L, cb = chosen % L;
+      if (tid == 0) {
+        const size_t idx = ((size_t)s * n + i) * (g.R * g.groups) + (size_t)r * g.groups + grp;
+        a_out[idx] = (uint16_t)ca;
+        b_out[idx] = (uint16_t)cb;
+      }
+      for (int si = tid; si < gs; si += blockDim.x) {
+        const double2 ua = __ldg(U + (size_t)si * L + ca), ub = __ldg(U + (size_t)si * L + cb);
+        p[2 * si] = __dsub_rn(p[2 * si], __dadd_rn(ua.x, -ub.y));
+        p[2 * si + 1] = __dsub_rn(p[2 * si + 1], __dadd_rn(ua.y, ub.x));
+      }
+      __syncthreads();
+    }
+  }
+}
+
 static size_t table_smem(const Geom& g) {
   return sizeof(double) * (2 * (size_t)g.g * g.L + (size_t)g.L * g.L + (size_t)kEncTok * g.d +
                            2 * (size_t)kEncWarps * g.L);
@@ -296,7 +445,12 @@ cudaError_t run_encode_keys(const Geom& g, int S, int n_slots, const KeyEncTable
   if (n <= 0 || S <= 0) return cudaSuccess;
   const size_t sm = table_smem(g);
   cudaError_t e;
-  if (tab.base != nullptr && sm <= 200 * 1024) {
+  if (tab.base != nullptr && n < 8 && 2 * g.L <= kSmallThreads) {
+    // decode-step appends: a CTA per token, no 96-KiB slice staging per round
+    dim3 grid((unsigned)n, S);
+    k_encode_keys_small<<<grid, kSmallThreads, sizeof(double) * (g.d + 2 * g.L), st>>>(
+        g, n_slots, tab.atoms, tab.base, tab.maxnorm, keys, dtype, s_stride, n, a, b);
+  } else if (tab.base != nullptr && sm <= 200 * 1024) {
     static bool attr = false;
     if (!attr) {
       e = cudaFuncSetAttribute(k_encode_keys_table, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -320,22 +474,22 @@ cudaError_t run_encode_keys(const Geom& g, int S, int n_slots, const KeyEncTable
 bool key_tables_fit(const Geom& g) { return table_smem(g) <= 200 * 1024 && g.L <= 1024; }
 
 // ------------------------------------------------------------ values
-constexpr int kValTok = 16;
-
-// One CTA per (16-token tile, stream), blockDim = max(hidden, n_codes)
-// rounded to a warp multiple (<= 1024).
+// One CTA per (TV-token tile, stream), blockDim = max(hidden, n_codes)
+// rounded to a warp multiple (<= 1024).  TV = 16 for prefill (weights read
+// once per 16 tokens), TV = 1 for decode-step appends.
+template <int TV>
 __global__ void k_encode_values(Geom g, int n_slots, ValEncWeights w,
                                 const void* __restrict__ vals, int dtype, long long s_stride,
                                 long long n, uint8_t* __restrict__ bits,
                                 double* __restrict__ logits, int* __restrict__ err) {
   extern __shared__ double sm[];
-  double* T = sm;                              // [kValTok][d]
-  double* H = T + (size_t)kValTok * g.d;       // [kValTok][hidden]
+  double* T = sm;                          // [TV][d]
+  double* H = T + (size_t)TV * g.d;        // [TV][hidden]
   const int s = blockIdx.y, tid = threadIdx.x;
-  const long long i0 = (long long)blockIdx.x * kValTok;
-  const int nt = (int)min((long long)kValTok, n - i0);
+  const long long i0 = (long long)blockIdx.x * TV;
+  const int nt = (int)min((long long)TV, n - i0);
   const int slot = s % n_slots;
-  for (int e = tid; e < kValTok * g.d; e += blockDim.x)
+  for (int e = tid; e < TV * g.d; e += blockDim.x)
     T[e] = (e / g.d < nt)
                ? load_elem(vals, dtype, (long long)s * s_stride + (i0 + e / g.d) * g.d + e % g.d)
                : 0.0;
@@ -345,20 +499,20 @@ __global__ void k_encode_values(Geom g, int n_slots, ValEncWeights w,
   const double* w2 = w.w2 + (size_t)slot * g.hidden * g.n_codes;
   const double* b2 = w.b2 + (size_t)slot * g.n_codes;
   for (int j = tid; j < g.hidden; j += blockDim.x) {  // valquant.cpp:52-62
-    double h[kValTok];
+    double h[TV];
 #pragma unroll
-    for (int k = 0; k < kValTok; ++k) h[k] = 0.0;
+    for (int k = 0; k < TV; ++k) h[k] = 0.0;
     for (int i = 0; i < g.d; ++i) {
-      const double wv = w1[(size_t)i * g.hidden + j];
+      const double wv = __ldg(w1 + (size_t)i * g.hidden + j);
 #pragma unroll
-      for (int k = 0; k < kValTok; ++k) {
+      for (int k = 0; k < TV; ++k) {
         const double ti = T[k * g.d + i];
         if (ti != 0.0) h[k] = __dadd_rn(h[k], __dmul_rn(ti, wv));
       }
     }
     const double bj = b1[j];
 #pragma unroll
-    for (int k = 0; k < kValTok; ++k) {
+    for (int k = 0; k < TV; ++k) {
       double v = __dadd_rn(h[k], bj);
       if (v < 0.0) v = 0.0;
       H[k * g.hidden + j] = v;
@@ -366,13 +520,13 @@ __global__ void k_encode_values(Geom g, int n_slots, ValEncWeights w,
   }
   __syncthreads();
   for (int c = tid; c < g.n_codes; c += blockDim.x) {  // valquant.cpp:63-69, 98
-    double lg[kValTok];
+    double lg[TV];
 #pragma unroll
-    for (int k = 0; k < kValTok; ++k) lg[k] = 0.0;
+    for (int k = 0; k < TV; ++k) lg[k] = 0.0;
     for (int j = 0; j < g.hidden; ++j) {
-      const double wv = w2[(size_t)j * g.n_codes + c];
+      const double wv = __ldg(w2 + (size_t)j * g.n_codes + c);
 #pragma unroll
-      for (int k = 0; k < kValTok; ++k) {
+      for (int k = 0; k < TV; ++k) {
         const double hj = H[k * g.hidden + j];
         if (hj != 0.0) lg[k] = __dadd_rn(lg[k], __dmul_rn(hj, wv));
       }
@@ -388,24 +542,34 @@ __global__ void k_encode_values(Geom g, int n_slots, ValEncWeights w,
   }
 }
 
+template <int TV>
+static cudaError_t launch_values(const Geom& g, int S, int n_slots, const ValEncWeights& w,
+                                 const void* vals, int dtype, long long s_stride, long long n,
+                                 uint8_t* bits, double* logits, int* err_flag, cudaStream_t st) {
+  int threads = ((g.hidden > g.n_codes ? g.hidden : g.n_codes) + 31) / 32 * 32;
+  if (threads > 1024) threads = 1024;
+  if (threads < 64) threads = 64;
+  const size_t sm = sizeof(double) * (size_t)TV * (g.d + g.hidden);
+  cudaError_t e;
+  if (sm > 48 * 1024) {
+    e = cudaFuncSetAttribute(k_encode_values<TV>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)sm);
+    if (e != cudaSuccess) return e;
+  }
+  dim3 grid((unsigned)((n + TV - 1) / TV), S);
+  k_encode_values<TV><<<grid, threads, sm, st>>>(g, n_slots, w, vals, dtype, s_stride, n, bits,
+                                                 logits, err_flag);
+  count_launch();
+  return cudaGetLastError();
+}
+
 cudaError_t run_encode_values(const Geom& g, int S, int n_slots, const ValEncWeights& w,
                               const void* vals, int dtype, long long s_stride, long long n,
                               uint8_t* bits, double* logits, int* err_flag, cudaStream_t st) {
   if (n <= 0 || S <= 0) return cudaSuccess;
-  int threads = ((g.hidden > g.n_codes ? g.hidden : g.n_codes) + 31) / 32 * 32;
-  if (threads > 1024) threads = 1024;
-  if (threads < 64) threads = 64;
-  const size_t sm = sizeof(double) * (size_t)kValTok * (g.d + g.hidden);
-  cudaError_t e;
-  if (sm > 48 * 1024) {
-    e = cudaFuncSetAttribute(k_encode_values, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    if (e != cudaSuccess) return e;
-  }
-  dim3 grid((unsigned)((n + kValTok - 1) / kValTok), S);
-  k_encode_values<<<grid, threads, sm, st>>>(g, n_slots, w, vals, dtype, s_stride, n, bits, logits,
-                                             err_flag);
-  count_launch();
-  return cudaGetLastError();
+  if (n < 16)  // decode-step appends: one token per CTA, no wasted lanes
+    return launch_values<1>(g, S, n_slots, w, vals, dtype, s_stride, n, bits, logits, err_flag, st);
+  return launch_values<16>(g, S, n_slots, w, vals, dtype, s_stride, n, bits, logits, err_flag, st);
 }
 
 }  // namespace cvq

@@ -421,6 +421,26 @@ def test_bench_shape_precision(G, keys, scale):
     assert worst <= 1e-3, worst
 
 
+@pytest.mark.parametrize("shape", [(128, 64, 64, 11), (128, 64, 64, 21), (8, 2, 4, 2), (12, 3, 4, 2)])
+def test_encode_keys_small_batches_bit_exact(G, shape):
+    """n < 8 tokens take the decode-append encoder (k_encode_keys_small);
+    includes exact midpoints between two centers (near-ties)."""
+    kq = KQ(*shape)
+    rng = P.rng(sum(shape))
+    atoms = rng.normal(2 * kq.n_atoms, 0.3 if kq.d == 128 else 1.0)
+    for n in (1, 3, 7):
+        keys = P.gen_synth(n, kq.d, min(kq.d, 32), n)
+        if n == 3:  # midpoint of two round-0 centers, group 0 only
+            xy = atoms.reshape(kq.rounds, kq.subspaces, kq.n_levels, 2)
+            a1, b1, a2, b2 = rng.index(4, kq.n_levels).tolist()
+            for j in range(kq.group_size):
+                keys[0, 2 * j] = 0.5 * (xy[0, j, a1, 0] - xy[0, j, b1, 1] + xy[0, j, a2, 0] - xy[0, j, b2, 1])
+                keys[0, 2 * j + 1] = 0.5 * (xy[0, j, a1, 1] + xy[0, j, b1, 0] + xy[0, j, a2, 1] + xy[0, j, b2, 0])
+        ga, gb = G.encode_keys(kq, atoms, keys)
+        oa, ob = P.encode_keys(kq, atoms, keys)
+        assert (ga == oa).all() and (gb == ob).all(), (shape, n)
+
+
 @pytest.mark.parametrize("n", [1, 200, 5000])
 def test_fused_kernel_matches_split_kernels(G, n, monkeypatch):
     """k_fast_attn_h (opt-in single-kernel path) == score + value kernels."""

@@ -1,4 +1,5 @@
 set -x
-for dbg in 0 1 2 3; do
-CVQ_TC_DBG=$dbg timeout 600 python bench.py --steps 5 --warmup 2 --keys tc --no-cpu-baseline --no-e2e --no-prefill > gpurun_out/bench_tc_dbg$dbg.log 2>&1; echo dbg$dbg=$?
-done
+timeout 900 python -m pytest tests -m gpu -q -x > gpurun_out/pytest_gpu.log 2>&1; echo t=$?
+tail -n 3 gpurun_out/pytest_gpu.log
+timeout 300 python __graft_entry__.py smoke > gpurun_out/smoke.log 2>&1; echo smoke=$?
+timeout 600 python bench.py --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/bench_c3.log 2>&1; echo c3=$?
