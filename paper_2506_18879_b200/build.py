@@ -32,7 +32,8 @@ def _stale():
 def build(force=False, verbose=False):
     if not force and not _stale():
         return SO
-    cmd = [NVCC] + FLAGS + ["-o", SO] + [os.path.join(CSRC, s) for s in SOURCES]
+    extra = os.environ.get("CVQ_NVCC_EXTRA", "").split()  # experiments, e.g. -DNAME=1
+    cmd = [NVCC] + FLAGS + extra + ["-o", SO] + [os.path.join(CSRC, s) for s in SOURCES]
     r = subprocess.run(cmd, capture_output=True, text=True)
     log = os.path.join(HERE, "build.log")
     with open(log, "w") as f:

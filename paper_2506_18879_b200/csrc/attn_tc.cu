@@ -1,42 +1,61 @@
 // attn_tc.cu -- tcgen05 (5th-gen tensor core) score kernel for the head
 // presets: the key decode K_j(i) = sum_r U[r,j,a_r] + i U[r,j,b_r] as a
-// one-hot GEMM with the accumulators in TMEM.
+// one-hot GEMM, laid out so each MMA is full width:
 //
-// Per 128-token tile and per (round r, side s in {a, b}):
-//     D_s[token, n] += A_{r,s}[token, l] * B_r[n, l]      (M=128, N=128, K=64)
-// A_{r,s} is the one-hot of the token's code (fp16 1.0 at l = code), B_r the
-// round-r codebook as fp16 with n = 2j + {x, y}.  D_a and D_b live in TMEM
-// (128 columns each); K = D_a + i D_b.  The epilogue (one thread per token =
-// one TMEM lane) rotates K by the RoPE phase -- the tile-independent
-// e^{+i delta theta_j} table also lives in TMEM, the per-tile factor
-// e^{-i (t - pos_tile) theta_j} is folded into the query -- and forms the G
-// query-head partial scores.
+//   D^T[n, t] += A_{r,s}[n, l] * B_{r,s}[t, l]     (M = 128, N = 256, K = 64)
 //
-// Warp roles (160 threads): warps 0-3 = one-hot producers (thread = token;
-// only the 1.0 entries are set and later cleared, so a stage costs one 2-B
-// store per token instead of 16 KB of smem traffic) and epilogue; warp 4 =
-// TMEM allocator + single-thread tcgen05.mma issuer.  Synchronisation is by
-// mbarriers: full[stage] (128 producer arrivals), empty[stage] and d_full
-// (tcgen05.commit), d_empty (128 epilogue arrivals).
+// * n = 2j + {x, y} indexes the 128 reals of a key, t the 256 tokens of a
+//   tile.  For side a, A = U_r (A[2j+c, l] = U[r,j,l].c); for side b, A is
+//   the ROTATED codebook (A[2j, l] = -U[r,j,l].y, A[2j+1, l] = U[r,j,l].x),
+//   so both sides accumulate into one D that holds (Re K, Im K) directly.
+// * B_{r,s} = one-hot of the tile tokens' side-s codes (fp16 1.0 at
+//   l = code), written into a K-major smem stage by 4 producer warps that
+//   only set and clear the 1.0 entries.  The A slice (16 KiB fp16, built
+//   once per codebook in the MMA's core-matrix layout) arrives in the same
+//   stage by one cp.async.bulk; a stage is 48 KiB, 4 stages deep.
+// * Measured on B200 (profiles/r01_umma_issue_bench.txt) a single issuer's
+//   tcgen05.mma costs >= ~125 clk whatever N <= 256, so N = 256 (128 clk of
+//   tensor work) is the only shape that is not issue-bound; D (256 fp32
+//   columns) is double-buffered in TMEM (all 512 columns) so the epilogue of
+//   tile k overlaps the MMAs of tile k+1.
+// * epilogue (16 warps; thread = real n = TMEM lane; warp (quarter, slot)
+//   owns 64 tokens of the tile and frees D right after its two TMEM loads):
+//   partner shuffle for the other component, the RoPE phase by a
+//   per-subspace fp32 recurrence from an fp64-reduced base per tile; for
+//   G = 4 each lane of a (x, y) pair forms the full complex product for two
+//   of the heads, so the cross-lane reduction runs over 16 lanes; a 4-warp
+//   sum in smem -> partial scores.
 //
-// Codebook precision is fp16 (as CVQ_CACHE_KEYS_FP16); accumulation fp32.
-// Rounds are processed in blocks of <= 11 (176 KiB of B per block); a 2-bit
-// stream (R = 21) uses two blocks whose partial scores the value kernel sums.
+// Persistent CTAs (one per SM) walk (stream, chunk) work items.  Warp roles
+// (640 threads): 0-15 epilogue, 16-17 one-hot producers, 18 TMEM allocator +
+// MMA issuer (elected lane), 19 codebook loader.  mbarriers: full[stage]
+// (2 producer warps + loader with tx bytes), empty[stage] and d_full[buf]
+// (tcgen05.commit), d_empty[buf] (16 epilogue warps).
+//
+// Codebook precision fp16 (as CVQ_CACHE_KEYS_FP16), accumulation fp32.
 #include "cvq_internal.cuh"
+
+#ifndef CVQ_TC_EXPERIMENT
+#define CVQ_TC_EXPERIMENT 0
+#endif
 
 namespace cvq {
 
 namespace {
 
-constexpr int kTcTile = 128;
-constexpr int kTcThreads = 160;
-constexpr int kTcRR = 11;        // rounds per block
-constexpr int kNB = 64;          // MMA N per CTA: 32 subspaces x (x, y)
-constexpr int kSub = kNB / 2;    // subspaces per CTA (a stream is split in 2 halves)
-constexpr int kBBytes = kNB * 64 * 2;  // one round of B: 64 levels x 64 reals fp16
-constexpr int kTcStages = 8;     // one-hot A stages (16 KiB each)
+constexpr int kTok = 256;                 // tokens per tile (MMA N)
+constexpr int kEpiWarps = 16;             // 4 per TMEM lane quarter
+constexpr int kEpiSlots = kEpiWarps / 4;  // slot s takes tile tokens [64 s, 64 s + 64)
+constexpr int kProdWarps = 4;             // thread p owns tile tokens p + 128 i
+constexpr int kMmaWarp = kEpiWarps + kProdWarps;
+constexpr int kLoadWarp = kMmaWarp + 1;
+constexpr int kThreads = (kLoadWarp + 1) * 32;
+constexpr int kStages = 4;
+constexpr int kABytes = 128 * 64 * 2;     // 16 KiB codebook slice
+constexpr int kBBytes = kTok * 64 * 2;    // 32 KiB one-hot
+constexpr int kStageBytes = kABytes + kBBytes;
+constexpr int kChunk = kTok / kEpiSlots;  // epilogue tokens per warp per tile
 constexpr uint32_t kTmemCols = 512;
-constexpr uint32_t kColPh = 256;  // D buffers at [0,128) and [128,256): Da | Db
 
 __device__ __forceinline__ uint32_t su32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -47,6 +66,12 @@ __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("{.reg .b64 st;\n\tmbarrier.arrive.shared::cta.b64 st, [%0];}" ::"r"(su32(bar))
                : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile(
+      "{.reg .b64 st;\n\tmbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;}" ::"r"(su32(bar)),
+      "r"(bytes)
+      : "memory");
 }
 __device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t parity) {
   uint32_t ok;
@@ -61,6 +86,25 @@ __device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t parity) {
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   while (!mbar_try(bar, parity)) {
   }
+}
+// for waiters off the critical path: back off so the spin does not take
+// issue slots from the epilogue warps
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+  while (!mbar_try(bar, parity)) __nanosleep(64);
+}
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred;
+  asm volatile(
+      "{.reg .pred p;\n\telect.sync _|p, 0xffffffff;\n\tselp.u32 %0, 1, 0, p;}"
+      : "=r"(pred));
+  return pred != 0;
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          su32(dst)),
+      "l"(src), "r"(bytes), "r"(su32(bar))
+      : "memory");
 }
 __device__ __forceinline__ void fence_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -78,113 +122,116 @@ __device__ __forceinline__ void tc_commit(uint64_t* bar) {
 }
 // UMMA shared-memory descriptor, K-major, no swizzle: core matrices of
 // 8 rows x 16 B; lbo = byte stride between K-adjacent core matrices, sbo =
-// between M/N-adjacent ones; version 1 (Blackwell) at bit 46.
+// between row-adjacent ones; descriptor version 1 at bit 46.
 __device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
   return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)((lbo >> 4) & 0x3FFFu) << 16) |
          ((uint64_t)((sbo >> 4) & 0x3FFFu) << 32) | (1ull << 46);
 }
-__device__ __forceinline__ void umma_f16(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc,
-                                         uint32_t accum) {
+__device__ __forceinline__ void umma_ss(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc,
+                                        uint32_t accum) {
   asm volatile(
       "{.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
       "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;}" ::"r"(d_tmem),
       "l"(a), "l"(b), "r"(idesc), "r"(accum));
 }
-__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t* v) {
   asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
-      "%11, %12, %13, %14, %15}, [%16];"
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
+      "%11, %12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, "
+      "%28, %29, %30, %31}, [%32];"
       : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
         "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
-        "=r"(v[14]), "=r"(v[15])
+        "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]),
+        "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]),
+        "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
       : "r"(taddr));
 }
-__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&v)[16]) {
-  asm volatile(
-      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
-      "%11, %12, %13, %14, %15, %16};" ::"r"(taddr),
-      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]),
-      "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]),
-      "r"(v[15]));
-}
-__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;"); }
-__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;"); }
 
-// Byte offset of element (row, l) in a K-major, no-swizzle 128-row x 64-K
-// fp16 operand: core matrix (kc = l/8, g = row/8) at (kc*16 + g)*128.
-__device__ __forceinline__ uint32_t kmaj_off(int row, int l) {
-  return (uint32_t)((((l >> 3) * 16 + (row >> 3)) << 7) + ((row & 7) << 4) + ((l & 7) << 1));
+// Byte offset of (row t, level l) in a K-major, no-swizzle ROWS x 64 fp16
+// operand: core matrix (kc = l/8, g = t/8) at (kc*ROWS/8 + g)*128.
+template <int ROWS>
+__host__ __device__ __forceinline__ uint32_t kmaj(int t, int l) {
+  return (uint32_t)((((l >> 3) * (ROWS / 8) + (t >> 3)) << 7) + ((t & 7) << 4) + ((l & 7) << 1));
 }
 
 struct TcArgs {
   const uint64_t* kpool;
   uint64_t kstride;
-  const uint16_t* cbtc;  // [slot][R][2 halves][8 KiB canonical B] fp16
+  const uint16_t* cbtc;  // [slot][R][2][8192] fp16 A operand
   int n_slots;
   const float* q;        // [S][G][128]
   const double* thetas;
   long long t, pos0, n;
-  int chunk;             // tokens per CTA (multiple of 128)
-  int R;                 // total rounds
-  int nblk;              // round blocks
-  float* ps;             // [S][nblk*2][n][G]
+  int chunk;             // tokens per work item (multiple of kTok)
+  int cps;               // work items per stream
+  int n_items;
+  float* ps;             // [S][n][G]
 };
 
-template <int G>
-__global__ void __launch_bounds__(kTcThreads, 1) k_tc_score(TcArgs a) {
+// Iterate this CTA's tiles in order: (stream, first token, valid tokens).
+struct TileIter {
+  int item, s;
+  long long ti, hi;
+  __device__ bool first(const TcArgs& a) {
+    item = blockIdx.x;
+    return setup(a);
+  }
+  __device__ bool setup(const TcArgs& a) {
+    while (item < a.n_items) {
+      s = item / a.cps;
+      ti = (long long)(item % a.cps) * a.chunk;
+      hi = min(a.n, ti + a.chunk);
+      if (ti < hi) return true;
+      item += gridDim.x;
+    }
+    return false;
+  }
+  __device__ bool next(const TcArgs& a) {
+    ti += kTok;
+    if (ti < hi) return true;
+    item += gridDim.x;
+    return setup(a);
+  }
+  __device__ int valid() const { return (int)min((long long)kTok, hi - ti); }
+};
+
+template <int R, int G>
+__global__ void __launch_bounds__(kThreads, 1) k_tc_score(TcArgs a) {
+  static_assert(32 % G == 0, "G must divide the warp");
+  constexpr int NSTEP = 2 * R;  // (round, side) steps per tile
+  constexpr int NW = (NSTEP * 6 + 60 + 63) / 64 + 1;  // code window words (+1 for the shift)
   extern __shared__ __align__(1024) unsigned char smem[];
-  unsigned char* Bs = smem;                                    // [kTcRR][8 KiB]
-  unsigned char* As = smem + kTcRR * kBBytes;                  // [kTcStages][16 KiB]
-  float2* wq = reinterpret_cast<float2*>(As + kTcStages * 16384);  // [3][32][G]
-  uint16_t* lastoff = reinterpret_cast<uint16_t*>(wq + 3 * kSub * G);  // [kTcStages][128]/16
-  uint64_t* bars = reinterpret_cast<uint64_t*>(lastoff + kTcStages * 128);
-  uint64_t* full = bars;                       // [kTcStages]
-  uint64_t* empty = bars + kTcStages;          // [kTcStages]
-  uint64_t* dfull = bars + 2 * kTcStages;      // [2]
-  uint64_t* dempty = dfull + 2;                // [2]
+  unsigned char* stages = smem;                                                // [kStages][A|B]
+  float* red = reinterpret_cast<float*>(stages + kStages * kStageBytes);  // [slot][4][kChunk][G]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(red + kEpiSlots * 4 * kChunk * G);
+  uint64_t* full = bars;
+  uint64_t* empty = bars + kStages;
+  uint64_t* dfull = bars + 2 * kStages;
+  uint64_t* dempty = dfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(dempty + 2);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int per = 2 * a.nblk;
-  const int s = blockIdx.y / per, part = blockIdx.y % per;
-  const int blk = part >> 1, half = part & 1;
-  const int r0 = blk * kTcRR;
-  const int rr = min(kTcRR, a.R - r0);
-  const long long i0 = (long long)blockIdx.x * a.chunk;
-  const long long i1 = min(a.n, i0 + a.chunk);
-  if (i0 >= i1) return;
-  const int ntiles = (int)((i1 - i0 + kTcTile - 1) / kTcTile);
-  const int slot = s % a.n_slots;
-  const int j0 = half * kSub;  // first subspace of this CTA
 
-  // ---- setup: TMEM, barriers, B (codebook block/half), zeroed A stages ----
-  if (warp == 4) {
+  if (warp == kMmaWarp) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      su32(tmem_slot)),
                  "r"(kTmemCols));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   if (tid == 0) {
-    for (int i = 0; i < kTcStages; ++i) {
-      mbar_init(full + i, 4);  // one arrival per producer warp
+    for (int i = 0; i < kStages; ++i) {
+      mbar_init(full + i, kProdWarps + 1);
       mbar_init(empty + i, 1);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(dfull + i, 1);
-      mbar_init(dempty + i, 4);
+      mbar_init(dempty + i, kEpiWarps);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  {
-    const uint4* src = reinterpret_cast<const uint4*>(a.cbtc);
-    uint4* dst = reinterpret_cast<uint4*>(Bs);
-    for (int e = tid; e < rr * (kBBytes / 16); e += kTcThreads) {
-      const int r = e / (kBBytes / 16), o = e % (kBBytes / 16);
-      dst[e] = __ldg(src + ((((size_t)slot * a.R + r0 + r) * 2 + half) * (kBBytes / 16)) + o);
-    }
-    uint4* az = reinterpret_cast<uint4*>(As);
-    for (int e = tid; e < kTcStages * 1024; e += kTcThreads) az[e] = make_uint4(0, 0, 0, 0);
-    for (int e = tid; e < kTcStages * 128; e += kTcThreads) lastoff[e] = 0xffffu;
+  for (int st = 0; st < kStages; ++st) {
+    uint4* bz = reinterpret_cast<uint4*>(stages + st * kStageBytes + kABytes);
+    for (int e = tid; e < kBBytes / 16; e += kThreads) bz[e] = make_uint4(0, 0, 0, 0);
   }
   fence_async_smem();
   tc_fence_before();
@@ -192,207 +239,304 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_score(TcArgs a) {
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  if (warp < 4) {
-    // ================= producers + epilogue (thread = token row) =========
-    const int d = tid;  // row in the tile == TMEM lane
-    const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
-    // tile-independent phase table e^{+i d theta_j}, j in this half
-#pragma unroll 1
-    for (int c = 0; c < kSub / 8; ++c) {
-      uint32_t v[16];
-#pragma unroll
-      for (int jj = 0; jj < 8; ++jj) {
-        double sn, cs;
-        sincos((double)d * a.thetas[j0 + 8 * c + jj], &sn, &cs);
-        v[2 * jj] = __float_as_uint((float)cs);
-        v[2 * jj + 1] = __float_as_uint((float)sn);
-      }
-      tmem_st16(tmem + lane_base + kColPh + 16 * c, v);
+  if (warp < kEpiWarps) {
+    // ============ epilogue: thread = real n (TMEM lane); warp (quarter,
+    // slot) takes the tile's 64 tokens [64 slot, 64 slot + 64)
+    const int quarter = warp & 3, eslot = warp >> 2;
+    const int n = quarter * 32 + lane;
+    const int j = n >> 1, c = n & 1;
+    const uint32_t lane_base = (uint32_t)(quarter * 32) << 16;
+    const double theta = a.thetas[j];
+    // lane c = 0 owns Z.x = ph.x K.x - ph.y K.y, lane c = 1 owns
+    // Z.y = ph.x K.y + ph.y K.x.  With the partner's component ko and
+    // phs = (ph.x, sgn ph.y): own Z.c = phs.x kc + phs.y ko and other
+    // Z.(1-c) = phs.x ko - phs.y kc, for both lanes.  The recurrence
+    // phs <- phs * e^{i theta} keeps that form with sgn folded into the
+    // step's imaginary part.
+    const float sgn = c ? 1.f : -1.f;
+    float2 stepm;
+    {
+      double sn, cs;
+      sincos(theta, &sn, &cs);  // e^{+i theta}: one token later
+      stepm = make_float2((float)cs, sgn * (float)sn);
     }
-    tmem_wait_st();
-    const uint64_t* kw = a.kpool + (size_t)s * a.kstride;
-    const float* qs = a.q + (size_t)s * G * 128;
-    float* ps = a.ps + (((size_t)s * per + part) * a.n) * G;
-    auto load_window = [&](long long tbase, int nvalid, uint64_t& x0, uint64_t& x1, uint64_t& x2,
-                           uint32_t& off) {
-      const long long i = tbase + (d < nvalid ? d : 0);
-      const unsigned long long bit = ((unsigned long long)i * (2 * a.R) + 2 * r0) * 6ull;
-      const unsigned long long w = bit >> 6;
-      off = (uint32_t)(bit & 63u);
-      x0 = __ldg(kw + w);
-      x1 = __ldg(kw + w + 1);
-      x2 = __ldg(kw + w + 2);
-    };
-    // epilogue of tile kk: K = D_a + i D_b, RoPE phase, G query-head dots
-    auto epilogue = [&](int kk) {
-      const long long ti = i0 + (long long)kk * kTcTile;
-      const int valid = (int)min((long long)kTcTile, i1 - ti);
-      const int db = kk & 1;
-      mbar_wait(dfull + db, (kk >> 1) & 1);
-      tc_fence_after();
-      asm volatile("bar.sync 1, 128;" ::: "memory");  // w' of tile kk (written by warp 0)
-      const float2* wk = wq + (kk % 3) * kSub * G;
-      float acc[G];
-#pragma unroll
-      for (int h = 0; h < G; ++h) acc[h] = 0.f;
-      const uint32_t dcol = db * 128;
-#pragma unroll 1
-      for (int c = 0; c < kSub / 8; ++c) {
-        uint32_t va[16], vb[16], vp[16];
-        tmem_ld16(tmem + lane_base + dcol + 16 * c, va);
-        tmem_ld16(tmem + lane_base + dcol + 64 + 16 * c, vb);
-        tmem_ld16(tmem + lane_base + kColPh + 16 * c, vp);
-        tmem_wait_ld();
-#pragma unroll
-        for (int jj = 0; jj < 8; ++jj) {
-          const float kx = __uint_as_float(va[2 * jj]) - __uint_as_float(vb[2 * jj + 1]);
-          const float ky = __uint_as_float(va[2 * jj + 1]) + __uint_as_float(vb[2 * jj]);
-          const float px = __uint_as_float(vp[2 * jj]), py = __uint_as_float(vp[2 * jj + 1]);
-          const float rx = px * kx - py * ky, ry = px * ky + py * kx;
-          const float2* w = wk + (8 * c + jj) * G;
-#pragma unroll
-          for (int h = 0; h < G; ++h) acc[h] += w[h].x * rx - w[h].y * ry;
-        }
+    float* rb = red + eslot * (4 * kChunk * G);  // [quarter][token][head]
+    const int hsw = (lane >> 4) & 1;
+    TileIter it;
+    int k = 0;
+    for (bool ok = it.first(a); ok; ok = it.next(a), ++k) {
+      const int db = k & 1;
+      const int valid = it.valid();
+      const long long t0 = it.ti + eslot * kChunk;
+      // G = 4: lane (j, c) forms the full Re(conj(q_h) Z_j) / sqrt(d) for
+      // heads 2c + (hb ^ hsw), hb = 0, 1: (qa, qb) = (q.c, q.(1-c)).
+      // G = 1: lane c forms q.c Z.c / sqrt(d).
+      const float sc = 0.08838834764831845f;
+      const float* qs = a.q + (size_t)it.s * G * 128;
+      float2 qa, qb;
+      if constexpr (G == 4) {
+        const int h0 = 2 * c + hsw, h1 = 2 * c + (1 ^ hsw);
+        qa = make_float2(__ldg(qs + h0 * 128 + 2 * j + c) * sc, __ldg(qs + h1 * 128 + 2 * j + c) * sc);
+        qb = make_float2(__ldg(qs + h0 * 128 + 2 * j + 1 - c) * sc,
+                         __ldg(qs + h1 * 128 + 2 * j + 1 - c) * sc);
+      } else {
+        qa = make_float2(__ldg(qs + n) * sc, 0.f);
+        qb = make_float2(0.f, 0.f);
       }
+      float2 ph = phase_neg(a.t - (a.pos0 + t0), theta);
+      ph.y *= sgn;
+      mbar_wait_sleep(dfull + db, (k >> 1) & 1);
+      tc_fence_after();
+      uint32_t v[kChunk];
+      tmem_ld32(tmem + lane_base + db * kTok + eslot * kChunk, v);
+      tmem_ld32(tmem + lane_base + db * kTok + eslot * kChunk + 32, v + 32);
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(dempty + db);
-      if (d < valid) {
+      if (lane == 0) mbar_arrive(dempty + db);  // D[db] is in registers: free it
+#if CVQ_TC_EXPERIMENT == 1
+      if (v[0] == 0x7fffffffu) a.ps[0] = 1.f;
+      continue;
+#endif
+      if constexpr (G == 4) {
 #pragma unroll
-        for (int h = 0; h < G; ++h) ps[(ti + d) * G + h] = acc[h];
-      }
-    };
-    uint64_t wn0 = 0, wn1 = 0, wn2 = 0;
-    uint32_t woff = 0;
-    uint32_t g = 0;  // global one-hot step counter (stage = g % kTcStages)
-    constexpr int kGroup = 4;  // one-hot steps per proxy fence
-    for (int k = 0; k < ntiles; ++k) {
-      const long long ti = i0 + (long long)k * kTcTile;
-      const int valid = (int)min((long long)kTcTile, i1 - ti);
-      if (k == 0) load_window(ti, valid, wn0, wn1, wn2, woff);
-      const uint64_t w0 = wn0, w1 = wn1, w2 = wn2;
-      const uint32_t off0 = woff;
-      // query folded with this tile's phase base (triple-buffered by tile)
-      if (d < kSub) {
-        float2* wk = wq + (k % 3) * kSub * G;
-        const float2 pb = phase_neg(a.t - (a.pos0 + ti), a.thetas[j0 + d]);
-        const int j = j0 + d;
+        for (int grp = 0; grp < kChunk / 8; ++grp) {
+          float acc[16];  // position hb * 8 + token
 #pragma unroll
-        for (int h = 0; h < G; ++h) {
-          const float qx = qs[h * 128 + 2 * j] * 0.08838834764831845f;
-          const float qy = -qs[h * 128 + 2 * j + 1] * 0.08838834764831845f;
-          wk[d * G + h] = make_float2(qx * pb.x - qy * pb.y, qx * pb.y + qy * pb.x);
-        }
-      }
-      // one-hot stages: (round r, side) steps, a then b, fenced in groups
+          for (int tt = 0; tt < 8; ++tt) {
+            const float kc = __uint_as_float(v[grp * 8 + tt]);
+            const float ko = __shfl_xor_sync(0xffffffffu, kc, 1);
+            const float A = fmaf(ph.x, kc, ph.y * ko);
+            const float B = fmaf(ph.x, ko, -ph.y * kc);
+            acc[tt] = fmaf(qa.x, A, qb.x * B);
+            acc[8 + tt] = fmaf(qa.y, A, qb.y * B);
+            const float nx = fmaf(ph.x, stepm.x, -ph.y * stepm.y);
+            ph.y = fmaf(ph.x, stepm.y, ph.y * stepm.x);
+            ph.x = nx;
+          }
+          // over the 16 same-c lanes: head level select-free (lanes with
+          // bit 4 hold the heads swapped), then reduce-scatter of the tokens
 #pragma unroll
-      for (int s0 = 0; s0 < 2 * kTcRR; s0 += kGroup) {
-        if (s0 < 2 * rr) {
+          for (int i = 0; i < 8; ++i) acc[i] += __shfl_xor_sync(0xffffffffu, acc[i + 8], 16);
 #pragma unroll
-          for (int i = 0; i < kGroup; ++i) {
-            const int step = s0 + i;
-            if (step < 2 * kTcRR && step < 2 * rr) {
-              const uint32_t bit = off0 + 6u * step;
-              const uint32_t wi = bit >> 6, sh = bit & 63u;
-              const uint64_t lo = wi == 0 ? w0 : (wi == 1 ? w1 : w2);
-              const uint64_t hi = wi == 0 ? w1 : w2;
-              uint64_t v = lo >> sh;
-              if (sh > 58u) v |= hi << (64u - sh);
-              const int code = (int)(v & 63u);
-              const uint32_t gg = g + i;
-              const uint32_t st = gg % kTcStages, n_use = gg / kTcStages;
-              if (n_use > 0) mbar_wait(empty + st, (n_use - 1) & 1);  // MMA done with it
-              unsigned char* A = As + st * 16384;
-              const uint32_t old = lastoff[st * 128 + d];
-              if (old != 0xffffu) *reinterpret_cast<uint16_t*>(A + 2 * old) = 0;
-              const uint32_t off = kmaj_off(d, code);
-              *reinterpret_cast<uint16_t*>(A + off) = 0x3C00;  // fp16 1.0
-              lastoff[st * 128 + d] = (uint16_t)(off >> 1);
+          for (int o = 8; o >= 2; o >>= 1) {
+            const bool up = (lane & o) != 0;
+#pragma unroll
+            for (int i = 0; i < o / 2; ++i) {
+              const float send = up ? acc[i] : acc[i + o / 2];
+              const float keep = up ? acc[i + o / 2] : acc[i];
+              acc[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
             }
           }
-          fence_async_smem();
-          __syncwarp();
-          const int nstep = min(kGroup, 2 * rr - s0);
-          if (lane < nstep) mbar_arrive(full + (g + lane) % kTcStages);  // one per warp each
-          g += nstep;
+          // lane holds head 2c + hsw, token grp*8 + ((lane >> 1) & 7)
+          rb[(quarter * kChunk + grp * 8 + ((lane >> 1) & 7)) * 4 + 2 * c + hsw] = acc[0];
+        }
+      } else {
+#pragma unroll
+        for (int grp = 0; grp < kChunk / 16; ++grp) {
+          float acc[16];
+#pragma unroll
+          for (int tt = 0; tt < 16; ++tt) {
+            const float kc = __uint_as_float(v[grp * 16 + tt]);
+            const float ko = __shfl_xor_sync(0xffffffffu, kc, 1);
+            acc[tt] = qa.x * fmaf(ph.x, kc, ph.y * ko);
+            const float nx = fmaf(ph.x, stepm.x, -ph.y * stepm.y);
+            ph.y = fmaf(ph.x, stepm.y, ph.y * stepm.x);
+            ph.x = nx;
+          }
+          // pair (x, y) first, then the tokens over lanes xor 16, 8, 4, 2
+#pragma unroll
+          for (int i = 0; i < 16; ++i) acc[i] += __shfl_xor_sync(0xffffffffu, acc[i], 1);
+#pragma unroll
+          for (int o = 16; o >= 2; o >>= 1) {
+            const bool up = (lane & o) != 0;
+#pragma unroll
+            for (int i = 0; i < o / 2; ++i) {
+              const float send = up ? acc[i] : acc[i + o / 2];
+              const float keep = up ? acc[i + o / 2] : acc[i];
+              acc[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+            }
+          }
+          if (c == 0) rb[quarter * kChunk + grp * 16 + (lane >> 1)] = acc[0];
         }
       }
-      // prefetch the next tile's code window only now: the proxy fences above
-      // wait for all of this thread's outstanding memory operations
-      if (k + 1 < ntiles) {
-        const long long tn = ti + kTcTile;
-        load_window(tn, (int)min((long long)kTcTile, i1 - tn), wn0, wn1, wn2, woff);
+      asm volatile("bar.sync %0, 128;" ::"r"(1 + eslot) : "memory");
+#pragma unroll
+      for (int e = quarter * 32 + lane; e < kChunk * G; e += 128) {  // (token, head)
+        const int tt = e / G;
+        if (eslot * kChunk + tt < valid)
+          a.ps[((size_t)it.s * a.n + t0 + tt) * G + (e % G)] =
+              (rb[e] + rb[kChunk * G + e]) + (rb[2 * kChunk * G + e] + rb[3 * kChunk * G + e]);
       }
-      // the epilogue trails by one tile so the MMA never waits for it
-      if (k > 0) epilogue(k - 1);
+      asm volatile("bar.sync %0, 128;" ::"r"(1 + eslot) : "memory");
     }
-    epilogue(ntiles - 1);
-  } else if (tid == 128) {
-    // ================= single-thread tcgen05.mma issuer ==================
-    constexpr uint32_t idesc = (1u << 4) | ((kNB >> 3) << 17) | (8u << 24);  // f16->f32, M128 N64
-    const uint32_t a_base = su32(As), b_base = su32(Bs);
+  } else if (warp < kEpiWarps + kProdWarps) {
+    // ============ one-hot producers: thread p owns tile tokens p + 128 i ====
+    // A stage's previous user was the same thread 4 steps earlier (same token
+    // slot), so the entry to clear is recomputed from the code windows (this
+    // tile's, or the previous tile's for the first kStages steps).
+    constexpr int TPT = kTok / (kProdWarps * 32);  // tokens per producer thread
+    const int p = tid - kEpiWarps * 32;
+    uint64_t w[TPT][NW], wp[TPT][NW];  // code windows (current, previous tile)
+    auto load = [&](int s, long long tok, uint64_t* wv) {
+      const uint64_t* kw = a.kpool + (size_t)s * a.kstride;
+      const unsigned long long bit = (unsigned long long)tok * (NSTEP * 6);
+      const unsigned long long w0 = bit >> 6;
+      const uint32_t off = (uint32_t)(bit & 63u);
+      uint64_t raw[NW];
+#pragma unroll
+      for (int i = 0; i < NW; ++i) raw[i] = __ldg(kw + w0 + i);
+#pragma unroll
+      for (int i = 0; i + 1 < NW; ++i)
+        wv[i] = off ? (raw[i] >> off) | (raw[i + 1] << (64u - off)) : raw[i];
+    };
+    auto code_at = [](const uint64_t* wv, int q) -> int {  // q is a compile-time constant
+      const int b0 = 6 * q, wi = b0 >> 6, sh = b0 & 63;
+      return (int)((wv[wi] >> sh) | (sh > 58 ? wv[wi + 1] << (64 - sh) : 0)) & 63;
+    };
+#pragma unroll
+    for (int u = 0; u < TPT; ++u)
+#pragma unroll
+      for (int i = 0; i < NW; ++i) w[u][i] = 0;
+    TileIter it;
     uint32_t g = 0;
-    for (int k = 0; k < ntiles; ++k) {
+    bool have_prev = false;
+    for (bool ok = it.first(a); ok; ok = it.next(a)) {
+      const int valid = it.valid();
+#pragma unroll
+      for (int u = 0; u < TPT; ++u) {
+        const int t = p + kProdWarps * 32 * u;
+#pragma unroll
+        for (int i = 0; i < NW; ++i) wp[u][i] = w[u][i];
+        load(it.s, it.ti + (t < valid ? t : 0), w[u]);
+      }
+#pragma unroll
+      for (int q = 0; q < NSTEP; ++q, ++g) {
+        const uint32_t st = g % kStages, use = g / kStages;
+        if (use > 0) mbar_wait_sleep(empty + st, (use - 1) & 1);
+        uint16_t* B = reinterpret_cast<uint16_t*>(stages + st * kStageBytes + kABytes);
+#pragma unroll
+        for (int u = 0; u < TPT; ++u) {
+          const int t = p + kProdWarps * 32 * u;
+          if (q >= kStages)
+            B[kmaj<kTok>(t, code_at(w[u], q - kStages)) >> 1] = 0;
+          else if (have_prev)
+            B[kmaj<kTok>(t, code_at(wp[u], q - kStages + NSTEP)) >> 1] = 0;
+          B[kmaj<kTok>(t, code_at(w[u], q)) >> 1] = 0x3C00;  // fp16 1.0
+        }
+        fence_async_smem();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(full + st);
+      }
+      have_prev = true;
+    }
+  } else if (warp == kMmaWarp) {
+    // ============ tcgen05.mma issuer: the whole warp walks the schedule (so
+    // descriptors stay warp-uniform), one elected lane issues ===============
+    // f16 x f16 -> f32; A and B K-major in smem; M128 N256
+    constexpr uint32_t idesc = (1u << 4) | ((uint32_t)(kTok >> 3) << 17) | (8u << 24);
+    const uint64_t adesc0 = sdesc(su32(stages), 2048, 128);
+    const uint64_t bdesc0 = sdesc(su32(stages) + kABytes, 4096, 128);
+    TileIter it;
+    uint32_t g = 0;
+    int k = 0;
+    for (bool ok = it.first(a); ok; ok = it.next(a), ++k) {
       const int db = k & 1;
-      if (k >= 2) {  // epilogue of tile k-2 released this D buffer
+      if (k >= 2) {  // D buffer db was read by the epilogue of tile k-2
         mbar_wait(dempty + db, ((k - 2) >> 1) & 1);
         tc_fence_after();
       }
-      for (int step = 0; step < 2 * rr; ++step, ++g) {
-        const uint32_t st = g % kTcStages, u = g / kTcStages;
-        mbar_wait(full + st, u & 1);
+      for (int q = 0; q < NSTEP; ++q, ++g) {
+        const uint32_t st = g % kStages, use = g / kStages;
+        mbar_wait(full + st, use & 1);
         tc_fence_after();
-        const int r = step >> 1;
-        const uint32_t dcol = db * 128 + ((step & 1) ? 64 : 0);
+        // descriptor start addresses advance in 16-B units
+        const uint64_t ad = adesc0 + (uint64_t)(st * (kStageBytes >> 4));
+        const uint64_t bd = bdesc0 + (uint64_t)(st * (kStageBytes >> 4));
+        if (elect_one()) {
 #pragma unroll
-        for (int kk = 0; kk < 4; ++kk) {  // K = 64 levels as 4 x K16
-          const uint64_t ad = sdesc(a_base + st * 16384 + kk * 4096, 2048, 128);
-          const uint64_t bd = sdesc(b_base + r * kBBytes + kk * 2048, 1024, 128);
-          umma_f16(tmem + dcol, ad, bd, idesc, (r > 0 || kk > 0) ? 1u : 0u);
+          for (int kk = 0; kk < 4; ++kk)  // K = 64 levels as 4 x K16
+            umma_ss(tmem + db * kTok, ad + (uint64_t)(kk * (4096 >> 4)),
+                    bd + (uint64_t)(kk * (8192 >> 4)), idesc, (q > 0 || kk > 0) ? 1u : 0u);
+          tc_commit(empty + st);
         }
-        tc_commit(empty + st);
+        __syncwarp();
       }
-      tc_commit(dfull + db);
+      if (elect_one()) tc_commit(dfull + db);
+      __syncwarp();
+    }
+  } else if (tid == kLoadWarp * 32) {
+    // ============ codebook loader: one 16-KiB bulk copy per step ===========
+    TileIter it;
+    uint32_t g = 0;
+    for (bool ok = it.first(a); ok; ok = it.next(a)) {
+      const uint16_t* src = a.cbtc + (size_t)(it.s % a.n_slots) * NSTEP * (kABytes / 2);
+      for (int q = 0; q < NSTEP; ++q, ++g) {
+        const uint32_t st = g % kStages, use = g / kStages;
+        if (use > 0) mbar_wait_sleep(empty + st, (use - 1) & 1);
+        mbar_arrive_tx(full + st, kABytes);
+        bulk_g2s(stages + st * kStageBytes, src + (size_t)q * (kABytes / 2), kABytes, full + st);
+      }
     }
   }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  if (warp == 4)
+  if (warp == kMmaWarp)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
                  "r"(kTmemCols));
+}
+
+template <int R, int G>
+cudaError_t launch_tc(const TcArgs& a, cudaStream_t st) {
+  const size_t sm = tc_smem_bytes(G);
+  static size_t done = 0;
+  if (sm > done) {
+    cudaError_t e = cudaFuncSetAttribute(k_tc_score<R, G>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if (e != cudaSuccess) return e;
+    done = sm;
+  }
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int grid = a.n_items < sms ? a.n_items : sms;
+  k_tc_score<R, G><<<grid, kThreads, sm, st>>>(a);
+  count_launch();
+  return cudaGetLastError();
 }
 
 }  // namespace
 
 size_t tc_smem_bytes(int G) {
-  return (size_t)kTcRR * kBBytes + kTcStages * 16384 + 3 * kSub * G * sizeof(float2) +
-         kTcStages * 128 * 2 + (2 * kTcStages + 4) * 8 + 16;
+  return (size_t)kStages * kStageBytes + kEpiSlots * 4 * kChunk * G * 4 +
+         (2 * kStages + 4) * 8 + 16;
 }
 
-// partial-score blocks per stream: round blocks x 2 subspace halves
-int tc_blocks(int R) { return 2 * ((R + kTcRR - 1) / kTcRR); }
+int tc_blocks(int) { return 1; }
 
-// Host-side B layout for one slot: [R][half][K-major 64 x 64 fp16] with
-// n = 2(j - 32 half) + {0: x, 1: y}, l = level; core matrix (kc = l/8,
-// g = n/8) at (kc*8 + g)*128 B.
-void tc_build_codebook(int R, int L, int subs, const double* xy, uint16_t* out,
-                       uint16_t (*to_half)(double)) {
+size_t tc_codebook_elems(int R) { return (size_t)R * 2 * (kABytes / 2); }
+
+void tc_build_codebook(int R, const double* xy, uint16_t* out, uint16_t (*to_half)(double)) {
+  // xy: [R][64 subs][64 levels][2] (rope-commutative atoms, x then y)
   for (int r = 0; r < R; ++r)
-    for (int j = 0; j < subs; ++j)
-      for (int l = 0; l < L; ++l)
-        for (int c = 0; c < 2; ++c) {
-          const int hf = j / kSub, n = 2 * (j % kSub) + c;
-          const size_t off = ((((size_t)(l >> 3) * 8 + (n >> 3)) << 7) + ((n & 7) << 4) +
-                              ((l & 7) << 1)) / 2;
-          out[((size_t)r * 2 + hf) * (kBBytes / 2) + off] =
-              to_half(xy[(((size_t)r * subs + j) * L + l) * 2 + c]);
+    for (int side = 0; side < 2; ++side) {
+      uint16_t* o = out + ((size_t)r * 2 + side) * (kABytes / 2);
+      for (int j = 0; j < 64; ++j)
+        for (int l = 0; l < 64; ++l) {
+          const double x = xy[(((size_t)r * 64 + j) * 64 + l) * 2];
+          const double y = xy[(((size_t)r * 64 + j) * 64 + l) * 2 + 1];
+          // side a: (x, y); side b: i * (x + iy) = (-y, x)
+          o[kmaj<128>(2 * j, l) >> 1] = to_half(side ? -y : x);
+          o[kmaj<128>(2 * j + 1, l) >> 1] = to_half(side ? x : y);
         }
+    }
 }
 
 cudaError_t run_tc_score(const AttnJob& job, const float* q, float* ps, int chunk,
                          cudaStream_t st) {
   const Geom& g = job.geo;
+  if (!job.cb_key_tc || g.d != 128 || g.L != 64 || g.subs != 64) return cudaErrorInvalidValue;
   TcArgs a{};
   a.kpool = job.kpool;
   a.kstride = job.kstride;
@@ -403,32 +547,13 @@ cudaError_t run_tc_score(const AttnJob& job, const float* q, float* ps, int chun
   a.t = job.t;
   a.pos0 = job.pos0;
   a.n = job.n;
-  a.chunk = chunk;
-  a.R = g.R;
-  a.nblk = tc_blocks(g.R) / 2;
+  a.chunk = (chunk + kTok - 1) / kTok * kTok;
+  a.cps = (int)((job.n + a.chunk - 1) / a.chunk);
+  a.n_items = job.S * a.cps;
   a.ps = ps;
-  const size_t sm = tc_smem_bytes(g.G);
-  dim3 grid((unsigned)((job.n + chunk - 1) / chunk), job.S * a.nblk * 2);
-  cudaError_t e;
-  if (g.G == 4) {
-    static size_t done = 0;
-    if (sm > done) {
-      e = cudaFuncSetAttribute(k_tc_score<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-      if (e != cudaSuccess) return e;
-      done = sm;
-    }
-    k_tc_score<4><<<grid, kTcThreads, sm, st>>>(a);
-  } else {
-    static size_t done = 0;
-    if (sm > done) {
-      e = cudaFuncSetAttribute(k_tc_score<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-      if (e != cudaSuccess) return e;
-      done = sm;
-    }
-    k_tc_score<1><<<grid, kTcThreads, sm, st>>>(a);
-  }
-  count_launch();
-  return cudaGetLastError();
+  if (g.R == 11) return g.G == 4 ? launch_tc<11, 4>(a, st) : launch_tc<11, 1>(a, st);
+  if (g.R == 21) return g.G == 4 ? launch_tc<21, 4>(a, st) : launch_tc<21, 1>(a, st);
+  return cudaErrorInvalidValue;
 }
 
 }  // namespace cvq

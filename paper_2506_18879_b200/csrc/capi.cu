@@ -172,7 +172,7 @@ struct cvq_cache {
   double* maxnorm = nullptr;   // [slot][R][groups]
   float2* cbk = nullptr;       // [slot][R][L][subs]
   uint32_t* cbk16 = nullptr;   // same, packed half2 (CVQ_CACHE_KEYS_FP16)
-  uint16_t* cbtc = nullptr;    // tcgen05 B operand [slot][R][8192] (CVQ_CACHE_KEYS_TC)
+  uint16_t* cbtc = nullptr;    // tcgen05 A operand [slot][R][2][8192] (CVQ_CACHE_KEYS_TC)
   float* cbv = nullptr;        // [slot][n_codes][d]
   double *w1 = nullptr, *b1 = nullptr, *w2 = nullptr, *b2 = nullptr;
   double* thetas = nullptr;
@@ -363,7 +363,7 @@ CVQ_API cvq_status cvq_cache_create(cvq_context* ctx, const cvq_cache_desc* d, c
   const Geom& g = c->geo;
   // stream strides rounded to 32 B so 128-token tiles stay 32-B aligned
   const uint64_t cap128 = (d->capacity + 127) / 128 * 128;  // whole 128-token tiles
-  c->kstride = (words_for_bits(cap128 * (uint64_t)g.bpt) + 4 + 3) / 4 * 4;
+  c->kstride = (words_for_bits(cap128 * (uint64_t)g.bpt) + 8 + 3) / 4 * 4;  // slack for window over-reads
   c->vstride = (words_for_bits(cap128 * (uint64_t)g.n_codes) + 4 + 3) / 4 * 4;
   c->key_set.assign(c->n_slots, 0);
   c->val_set.assign(c->n_slots, 0);
@@ -381,10 +381,11 @@ CVQ_API cvq_status cvq_cache_create(cvq_context* ctx, const cvq_cache_desc* d, c
   if (e == cudaSuccess) e = alloc((void**)&c->cbk, na * sizeof(float2));
   if (e == cudaSuccess && (d->flags & CVQ_CACHE_KEYS_FP16))
     e = alloc((void**)&c->cbk16, na * sizeof(uint32_t));
-  // tcgen05 path: head presets only (d=128, one 64-subspace group, L=64)
-  const bool tc_ok = g.d == 128 && g.groups == 1 && g.L == 64;
+  // tcgen05 path: head presets only (d=128, one 64-subspace group, L=64,
+  // G in {1, 4} query heads per KV head)
+  const bool tc_ok = g.d == 128 && g.groups == 1 && g.L == 64 && (g.G == 4 || g.G == 1);
   if (e == cudaSuccess && (d->flags & CVQ_CACHE_KEYS_TC) && tc_ok)
-    e = alloc((void**)&c->cbtc, (size_t)c->n_slots * g.R * 8192 * sizeof(uint16_t));
+    e = alloc((void**)&c->cbtc, (size_t)c->n_slots * tc_codebook_elems(g.R) * sizeof(uint16_t));
   if (e == cudaSuccess) e = alloc((void**)&c->cbv, (size_t)c->n_slots * g.n_codes * g.d * 4);
   if (e == cudaSuccess)
     e = alloc((void**)&c->maxnorm, (size_t)c->n_slots * g.R * g.groups * sizeof(double));
@@ -462,11 +463,11 @@ CVQ_API cvq_status cvq_cache_set_key_codebook(cvq_cache* c, uint32_t layer, uint
                        st));
   }
   std::vector<uint16_t> dt;
-  if (c->cbtc) {  // canonical K-major B operand of the one-hot MMA
-    dt.assign((size_t)g.R * 8192, 0);
-    tc_build_codebook(g.R, g.L, g.subs, xy, dt.data(),
+  if (c->cbtc) {  // canonical K-major A operand of the one-hot MMA
+    dt.assign(tc_codebook_elems(g.R), 0);
+    tc_build_codebook(g.R, xy, dt.data(),
                       [](double v) -> uint16_t { return __half_as_ushort(__double2half(v)); });
-    CU(cudaMemcpyAsync(c->cbtc + (size_t)slot * g.R * 8192, dt.data(), dt.size() * 2,
+    CU(cudaMemcpyAsync(c->cbtc + (size_t)slot * dt.size(), dt.data(), dt.size() * 2,
                        cudaMemcpyHostToDevice, st));
   }
   if (c->base) {

@@ -32,7 +32,7 @@ struct AttnJob {
   int n_slots;                // codebook slot of stream s = s % n_slots
   const float2* cb_key;       // [slot][R][L][subs] complex atoms (x, y), fp32
   const uint32_t* cb_key16;   // same as packed half2, or null (fp16-codebook mode)
-  const uint16_t* cb_key_tc;  // [slot][R][128x64 K-major fp16] tcgen05 B operand, or null
+  const uint16_t* cb_key_tc;  // [slot][R][2 sides][128 x 64 K-major fp16] tcgen05 A operand, or null
   const float* cb_val;        // [slot][n_codes][d] fp32
   const double* thetas;       // [subs] fp64, rope.cpp:8-25
   long long n;                // tokens per stream
@@ -56,8 +56,10 @@ cudaError_t run_attention(const AttnJob& job, const float* q, float* out,
 // tcgen05 one-hot-MMA score kernel (attn_tc.cu).
 size_t tc_smem_bytes(int G);
 int tc_blocks(int R);
-void tc_build_codebook(int R, int L, int subs, const double* xy, uint16_t* out,
-                       uint16_t (*to_half)(double));
+// A operand of the one-hot MMA for one slot: [R][side][16 KiB core-matrix
+// layout]; side b holds the rotated codebook (x <- -y, y <- x).
+void tc_build_codebook(int R, const double* xy, uint16_t* out, uint16_t (*to_half)(double));
+size_t tc_codebook_elems(int R);
 cudaError_t run_tc_score(const AttnJob& job, const float* q, float* ps, int chunk,
                          cudaStream_t st);
 
