@@ -51,6 +51,7 @@ constexpr int kMmaWarp = kEpiWarps + kProdWarps;
 constexpr int kLoadWarp = kMmaWarp + 1;
 constexpr int kThreads = (kLoadWarp + 1) * 32;
 constexpr int kStages = 4;
+constexpr int kPGroup = 2;                // producer steps per proxy fence
 constexpr int kABytes = 128 * 64 * 2;     // 16 KiB codebook slice
 constexpr int kBBytes = kTok * 64 * 2;    // 32 KiB one-hot
 constexpr int kStageBytes = kABytes + kBBytes;
@@ -410,23 +411,29 @@ __global__ void __launch_bounds__(kThreads, 1) k_tc_score(TcArgs a) {
         for (int i = 0; i < NW; ++i) wp[u][i] = w[u][i];
         load(it.s, it.ti + (t < valid ? t : 0), w[u]);
       }
+      // kPGroup steps per proxy fence + arrival round (NSTEP is even)
 #pragma unroll
-      for (int q = 0; q < NSTEP; ++q, ++g) {
-        const uint32_t st = g % kStages, use = g / kStages;
-        if (use > 0) mbar_wait_sleep(empty + st, (use - 1) & 1);
-        uint16_t* B = reinterpret_cast<uint16_t*>(stages + st * kStageBytes + kABytes);
+      for (int q0 = 0; q0 < NSTEP; q0 += kPGroup) {
 #pragma unroll
-        for (int u = 0; u < TPT; ++u) {
-          const int t = p + kProdWarps * 32 * u;
-          if (q >= kStages)
-            B[kmaj<kTok>(t, code_at(w[u], q - kStages)) >> 1] = 0;
-          else if (have_prev)
-            B[kmaj<kTok>(t, code_at(wp[u], q - kStages + NSTEP)) >> 1] = 0;
-          B[kmaj<kTok>(t, code_at(w[u], q)) >> 1] = 0x3C00;  // fp16 1.0
+        for (int q = q0; q < q0 + kPGroup; ++q) {
+          const uint32_t gq = g + (q - q0);
+          const uint32_t st = gq % kStages, use = gq / kStages;
+          if (use > 0) mbar_wait_sleep(empty + st, (use - 1) & 1);
+          uint16_t* B = reinterpret_cast<uint16_t*>(stages + st * kStageBytes + kABytes);
+#pragma unroll
+          for (int u = 0; u < TPT; ++u) {
+            const int t = p + kProdWarps * 32 * u;
+            if (q >= kStages)
+              B[kmaj<kTok>(t, code_at(w[u], q - kStages)) >> 1] = 0;
+            else if (have_prev)
+              B[kmaj<kTok>(t, code_at(wp[u], q - kStages + NSTEP)) >> 1] = 0;
+            B[kmaj<kTok>(t, code_at(w[u], q)) >> 1] = 0x3C00;  // fp16 1.0
+          }
         }
         fence_async_smem();
         __syncwarp();
-        if (lane == 0) mbar_arrive(full + st);
+        if (lane < kPGroup) mbar_arrive(full + (g + lane) % kStages);
+        g += kPGroup;
       }
       have_prev = true;
     }
