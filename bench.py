@@ -36,6 +36,7 @@ CONFIGS = {
     "c5": (1, 1, 8, 4, 1048576, 128, 64, 64, 21, 256),
 }
 BYTES_PER_KVHT = {11: 32.5, 21: 63.5}
+TENSOR_NOMINAL_TFLOPS = 2250.0  # B200 dense fp16/bf16, /opt/skills/guides/B200_PROFILING.md
 
 
 def peaks():
@@ -159,8 +160,9 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"])
     ap.add_argument("--no-prefill", action="store_true")
-    ap.add_argument("--keys", default="fp16", choices=["fp32", "fp16", "tc"],
-                    help="on-chip key-codebook precision (accumulation is fp32 either way)")
+    ap.add_argument("--keys", default="tc", choices=["fp32", "fp16", "tc"],
+                    help="score kernel: tc = tcgen05 one-hot MMA (fp16 codebook), fp16 / fp32 = "
+                         "CUDA-core gather with that codebook precision; fp32 accumulation always")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
     if args.impl == "reference":
@@ -287,13 +289,28 @@ def main():
             traffic = tr["dram_bytes_per_launch"]
     except Exception:
         pass
-    roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-            "frac": achieved / hbm, "traffic": traffic, "peak_source": src,
-            "traffic_note": "dram__bytes_read+write of the score kernel per launch "
-                            "(profiles/traffic.json); the value kernel reads the value words",
-            "kernel_ms": avg_main_ms, "kernel_share_of_step": avg_main_ms / ms,
-            "algorithmic_bytes_per_launch": bytes_per_launch,
-            "kv_head_tokens_per_s_kernel": kvht_per_launch / (avg_main_ms / 1e3)}
+    common = {"traffic": traffic,
+              "traffic_note": "dram__bytes_read+write of the score kernel per launch "
+                              "(profiles/traffic.json); the value kernel reads the value words",
+              "kernel_ms": avg_main_ms, "kernel_share_of_step": avg_main_ms / ms,
+              "algorithmic_bytes_per_launch": bytes_per_launch,
+              "kv_head_tokens_per_s_kernel": kvht_per_launch / (avg_main_ms / 1e3)}
+    if args.keys == "tc":
+        # one-hot MMA: per KV-head-token 2 * 128 reals * (2 sides * 64 levels) * R
+        # = 4*R*L*d flops, executed on the tensor pipe
+        flops = kvht_per_launch * 4.0 * R * L * d
+        ach_tf = flops / (avg_main_ms / 1e3) / 1e12
+        roof = {"bound": "tensor", "achieved": ach_tf, "peak": TENSOR_NOMINAL_TFLOPS,
+                "unit": "TFLOP/s", "frac": ach_tf / TENSOR_NOMINAL_TFLOPS,
+                "peak_source": "B200_PROFILING.md nominal dense fp16 (2.25 PFLOP/s); "
+                               "MEASURED_PEAKS bf16 burst %.1f is a power-capped dense cuBLAS "
+                               "run at lower SM clocks" % tflops,
+                "frac_vs_measured_bf16_burst": ach_tf / tflops,
+                "algorithmic_flops_per_launch": flops,
+                "hbm_achieved_gbs": achieved, "hbm_frac": achieved / hbm, **common}
+    else:
+        roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                "frac": achieved / hbm, "peak_source": src, **common}
 
     # ---- e2e through the C-ABI with host buffers (decode_step) ----
     e2e = None
@@ -381,7 +398,9 @@ def main():
             "unit": "KV-tokens/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None,
-            "dtype": "f32 accumulate, %s key codebook (fp64-reduced phases; int codes)" % args.keys,
+            "dtype": ("f16 one-hot x f16 codebook MMA, f32 accumulate (fp64-reduced phases; int codes)"
+                      if args.keys == "tc" else
+                      "f32 accumulate, %s key codebook (fp64-reduced phases; int codes)" % args.keys),
             "data": "synthetic (random codebooks, random packed codes, random q)",
             "config": {"workload": args.config, "n_layers": layers, "n_seqs": B,
                        "n_kv_heads": H, "q_per_kv": Gq, "context": N, "key": [d, g, L, R],

@@ -18,6 +18,8 @@
 #include <cfloat>
 #include <cmath>
 
+#include <algorithm>
+
 #include "cvq_internal.cuh"
 
 namespace cvq {
@@ -83,26 +85,6 @@ k_score_generic(Geom g, const uint64_t* __restrict__ kpool, uint64_t kstride,
 constexpr int kValThreads = 256;
 constexpr int kValKpt = 4;  // codes per thread -> n_codes <= 1024
 
-__device__ __forceinline__ float block_reduce(float v, bool is_max, float* red) {
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  for (int o = 16; o; o >>= 1) {
-    float u = __shfl_xor_sync(0xffffffffu, v, o);
-    v = is_max ? fmaxf(v, u) : v + u;
-  }
-  __syncthreads();
-  if (lane == 0) red[wid] = v;
-  __syncthreads();
-  const int nw = blockDim.x >> 5;
-  v = (threadIdx.x < nw) ? red[threadIdx.x] : (is_max ? -FLT_MAX : 0.f);
-  if (wid == 0)
-    for (int o = 16; o; o >>= 1) {
-      float u = __shfl_xor_sync(0xffffffffu, v, o);
-      v = is_max ? fmaxf(v, u) : v + u;
-    }
-  if (threadIdx.x == 0) red[32] = v;
-  __syncthreads();
-  return red[32];
-}
 
 template <int MAXG>
 __global__ void __launch_bounds__(kValThreads)
@@ -326,6 +308,9 @@ size_t fast_scratch_bytes(const AttnJob& job, int* n_chunks);
 cudaError_t run_attention_fast(const AttnJob& job, const float* q, float* pm,
                                float* pl, float* po, int* n_chunks, void* scratch,
                                cudaStream_t st, cudaEvent_t* prof, float* scores_out);
+cudaError_t run_fast_combine(const AttnJob& job, const float* pm, const float* pl,
+                             const float* pz, int n_parts, float* out, float* m_out,
+                             float* l_out, cudaStream_t st);
 
 static int generic_chunk(const AttnJob& job) {
   long long want = (job.n * (long long)job.S + 591) / 592;  // >= ~4 CTAs/SM
@@ -342,7 +327,8 @@ size_t attn_scratch_bytes(const AttnJob& job, int* n_chunks_out) {
     int nc = 0;
     size_t extra = fast_scratch_bytes(job, &nc);
     if (n_chunks_out) *n_chunks_out = nc;
-    return extra + (size_t)nc * rows * (2 + g.d) * sizeof(float) + 256;
+    // partials (m, l, z[n_codes]) per chunk and row
+    return extra + (size_t)nc * rows * (2 + std::max(g.d, g.n_codes)) * sizeof(float) + 256;
   }
   const int CH = generic_chunk(job);
   const int nc = (int)((job.n + CH - 1) / CH);
@@ -402,6 +388,16 @@ cudaError_t run_attention(const AttnJob& job, const float* q, float* out,
   }
   float* mo = m;
   float* lo = l;
+  if (fast) {  // partials hold unnormalised z: merge, then the codebook product
+    if (out) {
+      e = run_fast_combine(job, pm, pl, po, nc, out, mo, lo, st);
+      if (e != cudaSuccess) return e;
+      if (o) e = cudaMemcpyAsync(o, out, (size_t)rows * g.d * sizeof(float), cudaMemcpyDeviceToDevice, st);
+      return e;
+    }
+    if (o) return run_fast_combine(job, pm, pl, po, nc, o, mo, lo, st);
+    return cudaSuccess;
+  }
   if (out) {
     e = run_lse_combine(pm, pl, po, nc, rows, g.d, out, mo, lo, st);
     if (e != cudaSuccess) return e;

@@ -15,9 +15,10 @@
 //     butterfly reduce-scatter.  Writes partial scores [S][JS][n][G].
 //  F2 k_fast_value  grid (context chunks, stream).  Sums the JS partial
 //     scores, softmax statistics of the chunk, z[k][h] += p_h(i) bit_k(i)
-//     from cp.async-staged value words (attn.cpp:239-247), then
-//     o = z . C_V / l (attn.cpp:249-255).  Writes the chunk partial (m, l, o)
-//     merged by k_combine (attn.cu).
+//     from cp.async-staged value words (attn.cpp:239-247).  Writes the chunk
+//     partial (m, l, z), unnormalised.
+//  k_combine_project  one CTA per (stream, q head) row: LSE merge of the
+//     chunk partials, then o = z . C_V / L (attn.cpp:249-255) once per row.
 #include <algorithm>
 #include <cfloat>
 #include <cstdlib>
@@ -632,14 +633,10 @@ __global__ void __launch_bounds__(kF1Threads, 1) k_fast_attn_h(FastArgs a) {
     Z[e] = v;
   }
   __syncthreads();
-  const float* cb = a.cbv + (size_t)slot * NC * 128;
   const long long rows = (long long)a.S * G;
-  for (int e = tid; e < G * 128; e += kF1Threads) {
-    const int h = e / 128, jd = e % 128;
-    float acc = 0.f;
-#pragma unroll 8
-    for (int kk = 0; kk < NC; ++kk) acc += Z[kk * G + h] * __ldg(cb + (size_t)kk * 128 + jd);
-    a.po[((long long)blockIdx.x * rows + (long long)s * G + h) * 128 + jd] = acc / Lh[h];
+  for (int e = tid; e < G * NC; e += kF1Threads) {  // unnormalised z (k_combine_project)
+    const int h = e / NC, kk = e % NC;
+    a.po[((long long)blockIdx.x * rows + (long long)s * G + h) * NC + kk] = Z[kk * G + h];
   }
   if (tid < G) {
     a.pm[(long long)blockIdx.x * rows + (long long)s * G + tid] = Mh[tid];
@@ -762,15 +759,12 @@ __global__ void __launch_bounds__(kThreads) k_fast_value(FastArgs a) {
     zr[e] = v;  // warp-0 slot reused for the total
   }
   __syncthreads();
-  const float* cb = a.cbv + (size_t)(s % a.n_slots) * NC * 128;
+  // unnormalised z of this chunk; the value codebook product happens once per
+  // row after the merge (k_combine_project)
   const long long rows = (long long)a.S * G;
-  for (int e = tid; e < G * 128; e += kThreads) {
-    const int h = e / 128, jd = e % 128;
-    float acc = 0.f;
-#pragma unroll 8
-    for (int k = 0; k < NC; ++k) acc += zr[k * G + h] * __ldg(cb + (size_t)k * 128 + jd);
-    const long long row = (long long)s * G + h;
-    a.po[((long long)blockIdx.x * rows + row) * 128 + jd] = acc / lh[h];
+  for (int e = tid; e < G * NC; e += kThreads) {
+    const int h = e / NC, k = e % NC;
+    a.po[((long long)blockIdx.x * rows + (long long)s * G + h) * NC + k] = zr[k * G + h];
   }
   if (tid < G) {
     const long long row = (long long)s * G + tid;
@@ -871,7 +865,71 @@ cudaError_t launch_f2_js(const FastArgs& a, int JS, size_t sm, cudaStream_t st) 
   }
 }
 
+// Merge of the chunk partials (m_p, l_p, z_p) of one row (flash-decoding
+// LSE merge; the reference softmax is global, linalg.cpp:63-75), then the
+// value codebook product o = z . C_V / L once per row (attn.cpp:249-256).
+template <int NC>
+__global__ void __launch_bounds__(128) k_combine_project(
+    const float* __restrict__ m, const float* __restrict__ l, const float* __restrict__ z,
+    int P, long long rows, int G, const float* __restrict__ cbv, int n_slots,
+    float* __restrict__ out, float* __restrict__ m_out, float* __restrict__ l_out) {
+  extern __shared__ float wsh[];  // [P] part weights e^{m_p - M}
+  __shared__ float zs[NC];
+  __shared__ float red[33];
+  const long long row = blockIdx.x;
+  float M = -FLT_MAX;
+  for (int p = threadIdx.x; p < P; p += blockDim.x)
+    if (l[p * rows + row] > 0.f) M = fmaxf(M, m[p * rows + row]);
+  M = block_reduce(M, true, red);
+  float Ls = 0.f;
+  for (int p = threadIdx.x; p < P; p += blockDim.x) {
+    const float lp = l[p * rows + row];
+    const float wgt = lp > 0.f ? expf(m[p * rows + row] - M) : 0.f;
+    wsh[p] = wgt;
+    Ls += lp * wgt;
+  }
+  const float Lsum = block_reduce(Ls, false, red);  // (its barriers publish wsh)
+#pragma unroll
+  for (int k = threadIdx.x; k < NC; k += 128) {
+    float acc = 0.f;
+    for (int p = 0; p < P; ++p) {
+      const float wgt = wsh[p];
+      if (wgt != 0.f) acc += z[(p * rows + row) * NC + k] * wgt;
+    }
+    zs[k] = acc;
+  }
+  __syncthreads();
+  const float* cb = cbv + (size_t)((row / G) % n_slots) * NC * 128;
+  const int jd = threadIdx.x;
+  float acc = 0.f;
+#pragma unroll 8
+  for (int k = 0; k < NC; ++k) acc += zs[k] * __ldg(cb + (size_t)k * 128 + jd);
+  out[row * 128 + jd] = acc / Lsum;
+  if (jd == 0) {
+    if (m_out) m_out[row] = M;
+    if (l_out) l_out[row] = Lsum;
+  }
+}
+
 }  // namespace
+
+cudaError_t run_fast_combine(const AttnJob& job, const float* pm, const float* pl,
+                             const float* pz, int n_parts, float* out, float* m_out,
+                             float* l_out, cudaStream_t st) {
+  const long long rows = (long long)job.S * job.geo.G;
+  if (rows == 0) return cudaSuccess;
+  const size_t sm = (size_t)n_parts * sizeof(float);
+  if (job.geo.n_codes == 128)
+    k_combine_project<128><<<(unsigned)rows, 128, sm, st>>>(pm, pl, pz, n_parts, rows, job.geo.G,
+                                                            job.cb_val, job.n_slots, out, m_out,
+                                                            l_out);
+  else
+    k_combine_project<256><<<(unsigned)rows, 128, sm, st>>>(pm, pl, pz, n_parts, rows, job.geo.G,
+                                                            job.cb_val, job.n_slots, out, m_out,
+                                                            l_out);
+  count_launch();
+  return cudaGetLastError();
+}
 
 bool fast_path_applies(const AttnJob& job) {
   const Geom& g = job.geo;

@@ -3,6 +3,8 @@
 // capi.cu).  Not part of the public C-ABI (include/cvq.h).
 #pragma once
 
+#include <cfloat>
+
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -62,6 +64,28 @@ void tc_build_codebook(int R, const double* xy, uint16_t* out, uint16_t (*to_hal
 size_t tc_codebook_elems(int R);
 cudaError_t run_tc_score(const AttnJob& job, const float* q, float* ps, int chunk,
                          cudaStream_t st);
+
+// Block-wide max / sum; every thread gets the result (contains barriers).
+__device__ __forceinline__ float block_reduce(float v, bool is_max, float* red) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int o = 16; o; o >>= 1) {
+    float u = __shfl_xor_sync(0xffffffffu, v, o);
+    v = is_max ? fmaxf(v, u) : v + u;
+  }
+  __syncthreads();
+  if (lane == 0) red[wid] = v;
+  __syncthreads();
+  const int nw = blockDim.x >> 5;
+  v = (threadIdx.x < nw) ? red[threadIdx.x] : (is_max ? -FLT_MAX : 0.f);
+  if (wid == 0)
+    for (int o = 16; o; o >>= 1) {
+      float u = __shfl_xor_sync(0xffffffffu, v, o);
+      v = is_max ? fmaxf(v, u) : v + u;
+    }
+  if (threadIdx.x == 0) red[32] = v;
+  __syncthreads();
+  return red[32];
+}
 
 // Log-sum-exp merge (device), parts-major.
 cudaError_t run_lse_combine(const float* m, const float* l, const float* o,
