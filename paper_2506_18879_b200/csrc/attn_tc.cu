@@ -148,6 +148,25 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t* v) {
       : "r"(taddr));
 }
 
+// packed fp32x2 arithmetic (FMUL2 / FFMA2 on sm_100a); the scalar operand is
+// broadcast to both halves
+__device__ __forceinline__ float2 fmul2(float2 a, float b) {
+  uint64_t d;
+  asm("{.reg .b64 a, b;\n\tmov.b64 a, {%1, %2};\n\tmov.b64 b, {%3, %3};\n\t"
+      "mul.rn.f32x2 %0, a, b;}"
+      : "=l"(d)
+      : "f"(a.x), "f"(a.y), "f"(b));
+  return make_float2(__uint_as_float((uint32_t)d), __uint_as_float((uint32_t)(d >> 32)));
+}
+__device__ __forceinline__ float2 ffma2(float2 a, float b, float2 c) {
+  uint64_t d;
+  asm("{.reg .b64 a, b, c;\n\tmov.b64 a, {%1, %2};\n\tmov.b64 b, {%3, %3};\n\t"
+      "mov.b64 c, {%4, %5};\n\tfma.rn.f32x2 %0, a, b, c;}"
+      : "=l"(d)
+      : "f"(a.x), "f"(a.y), "f"(b), "f"(c.x), "f"(c.y));
+  return make_float2(__uint_as_float((uint32_t)d), __uint_as_float((uint32_t)(d >> 32)));
+}
+
 // Byte offset of (row t, level l) in a K-major, no-swizzle ROWS x 64 fp16
 // operand: core matrix (kc = l/8, g = t/8) at (kc*ROWS/8 + g)*128.
 template <int ROWS>
@@ -300,6 +319,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_tc_score(TcArgs a) {
       continue;
 #endif
       if constexpr (G == 4) {
+        // acc_h = qa_h A + qb_h B with A = phs.x kc + phs.y ko and
+        // B = phs.x ko - phs.y kc equals al_h kc + be_h ko where
+        // al_h + i be_h = (qa_h + i qb_h)(phs.x + i phs.y); (al, be) follow the
+        // same per-token rotation as the phase.  Both heads of the lane ride
+        // in packed fp32x2 (FMUL2 / FFMA2 with scalar-broadcast operands).
+        float2 al = make_float2(qa.x * ph.x - qb.x * ph.y, qa.y * ph.x - qb.y * ph.y);
+        float2 be = make_float2(qa.x * ph.y + qb.x * ph.x, qa.y * ph.y + qb.y * ph.x);
+        const float nsy = -stepm.y;
 #pragma unroll
         for (int grp = 0; grp < kChunk / 8; ++grp) {
           float acc[16];  // position hb * 8 + token
@@ -307,13 +334,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_tc_score(TcArgs a) {
           for (int tt = 0; tt < 8; ++tt) {
             const float kc = __uint_as_float(v[grp * 8 + tt]);
             const float ko = __shfl_xor_sync(0xffffffffu, kc, 1);
-            const float A = fmaf(ph.x, kc, ph.y * ko);
-            const float B = fmaf(ph.x, ko, -ph.y * kc);
-            acc[tt] = fmaf(qa.x, A, qb.x * B);
-            acc[8 + tt] = fmaf(qa.y, A, qb.y * B);
-            const float nx = fmaf(ph.x, stepm.x, -ph.y * stepm.y);
-            ph.y = fmaf(ph.x, stepm.y, ph.y * stepm.x);
-            ph.x = nx;
+            const float2 r = ffma2(be, ko, fmul2(al, kc));
+            acc[tt] = r.x;
+            acc[8 + tt] = r.y;
+            const float2 nal = ffma2(al, stepm.x, fmul2(be, nsy));
+            be = ffma2(al, stepm.y, fmul2(be, stepm.x));
+            al = nal;
           }
           // over the 16 same-c lanes: head level select-free (lanes with
           // bit 4 hold the heads swapped), then reduce-scatter of the tokens
