@@ -189,9 +189,10 @@ typedef struct cvq_cache_desc {
  * Default (0): fp32 codebook. */
 #define CVQ_CACHE_KEYS_FP16 1u
 /* Score with the tcgen05 tensor-core kernel: the key decode as a one-hot
- * GEMM (fp16 codebook operand, fp32 accumulators in TMEM).  Same precision
- * class as CVQ_CACHE_KEYS_FP16.  Head presets (d=128, g=64, L=64) only;
- * other shapes use the generic path. */
+ * GEMM (fp16 codebook operand, fp32 accumulators in TMEM); the fastest mode
+ * on B200 (bench.py default).  Same precision class as CVQ_CACHE_KEYS_FP16.
+ * Head presets (d=128, g=64, L=64, R in {11, 21}, 1 or 4 query heads per KV
+ * head); other shapes run the CUDA-core kernels. */
 #define CVQ_CACHE_KEYS_TC 2u
 
 CVQ_API cvq_status cvq_cache_create(cvq_context* ctx, const cvq_cache_desc* d,
