@@ -46,7 +46,7 @@ namespace {
 constexpr int kTok = 256;                 // tokens per tile (MMA N)
 constexpr int kEpiWarps = 16;             // 4 per TMEM lane quarter
 constexpr int kEpiSlots = kEpiWarps / 4;  // slot s takes tile tokens [64 s, 64 s + 64)
-constexpr int kProdWarps = 4;             // thread p owns tile tokens p + 128 i
+constexpr int kProdWarps = 2;             // thread p owns tile tokens p + 64 i
 constexpr int kMmaWarp = kEpiWarps + kProdWarps;
 constexpr int kLoadWarp = kMmaWarp + 1;
 constexpr int kThreads = (kLoadWarp + 1) * 32;
