@@ -797,7 +797,9 @@ int f2_chunk(const AttnJob& job) {
   long long want = (job.n * (long long)job.S + 2 * 148 - 1) / (2 * 148);
   long long ch = (want + kTile - 1) / kTile * kTile;
   if (ch < 256) ch = 256;
-  if (ch > 1024) ch = 1024;  // 40 KiB smem -> 5 CTAs/SM: latency-bound kernel
+  // 48 KiB smem -> 4 CTAs/SM (latency-bound kernel); measured on C3: 1024 and
+  // 2048 tie, 512 and 4096 are slower
+  if (ch > 1024) ch = 1024;
   return (int)ch;
 }
 
