@@ -138,6 +138,34 @@ CVQ_API cvq_status cvq_encode_keys(cvq_context* ctx, const cvq_key_config* kc,
                                    const double* keys, uint64_t n_tokens,
                                    uint16_t* a, uint16_t* b);
 
+/* EmConfig (keyquant.hpp:71-80).  search: 0 = brute_force (default),
+ * 1 = factorized. */
+typedef struct cvq_em_config {
+  uint64_t soft_iters;      /* 30 */
+  uint64_t hard_iters_max;  /* 100 */
+  double t0;                /* 0 = auto temperature */
+  double decay;             /* 0.9 */
+  double tol;               /* 1e-6 */
+  double ridge;             /* -1 = auto */
+  uint64_t seed;            /* 1 */
+  int32_t search;
+} cvq_em_config;
+
+/* train_key_codebook (keyquant.cpp:641-703) on the GPU: the reference's
+ * soft-to-hard EM schedule per (round, group), E-steps and moments on the
+ * device, refit (Cholesky) on the host.  calib [n][d] fp64 host rows.
+ * atoms_out [R][d/2][L][2] (CVQK order); objective_len[R * groups] receives
+ * each group's hard-objective trace length and objective_out (capacity
+ * objective_cap, may be NULL) the traces concatenated round-major;
+ * mse_out[R] the per-round reconstruction MSE.  Errors: CVQ_EINVAL (fewer
+ * than L^2 rows, non-finite input), CVQ_ETRAINING (all-zero calibration,
+ * singular refit). */
+CVQ_API cvq_status cvq_train_key_codebook(cvq_context* ctx, const cvq_key_config* kc,
+                                          const double* calib, uint64_t n_rows,
+                                          const cvq_em_config* em, double* atoms_out,
+                                          double* objective_out, uint64_t objective_cap,
+                                          uint64_t* objective_len, double* mse_out);
+
 /* encoder_forward in infer mode (valquant.cpp:50-101), batched over tokens:
  * values[n][d] -> bits[n][n_codes] (logit > 0), logits optional. */
 CVQ_API cvq_status cvq_encoder_forward_infer(

@@ -329,6 +329,35 @@ class Oracle:
         self._check(f(n_codes, _ptr(words), words.size, n, _ptr(bits)))
         return bits
 
+    # ---- keyquant.cpp:641-703 (compiled reference only) -------------------
+    def train_key_codebook(self, kq, calib, soft_iters=30, hard_iters_max=100, t0=0.0,
+                           decay=0.9, tol=1e-6, ridge=-1.0, seed=1, factorized=False):
+        """train_key_codebook -> (atoms [R*(d/2)*L*2], traces [R][groups], mse [R])."""
+        assert self.kind == "reference", "training is pinned on the compiled reference"
+        calib = np.ascontiguousarray(calib, np.float64)
+        n = calib.shape[0]
+        atoms = np.zeros(2 * kq.n_atoms)
+        ng = kq.rounds * kq.groups
+        cap = ng * (hard_iters_max + 2)
+        obj = np.zeros(cap)
+        olen = np.zeros(ng, np.uint64)
+        mse = np.zeros(kq.rounds)
+        f = self.lib.cvqr_train_key_codebook
+        f.argtypes = [_sz] * 4 + [_p, _sz, _sz, _sz, _d, _d, _d, _d, _u64, C.c_int,
+                                  _p, _p, _sz, _p, _p]
+        self._check(f(kq.d, kq.group_size, kq.n_levels, kq.rounds, _ptr(calib), n, soft_iters,
+                      hard_iters_max, t0, decay, tol, ridge, seed, int(factorized), _ptr(atoms),
+                      _ptr(obj), cap, _ptr(olen), _ptr(mse)))
+        traces, k = [], 0
+        for r in range(kq.rounds):
+            row = []
+            for grp in range(kq.groups):
+                ln = int(olen[r * kq.groups + grp])
+                row.append(obj[k:k + ln].copy())
+                k += ln
+            traces.append(row)
+        return atoms, traces, mse
+
     # ---- ctf.cpp:97-144 --------------------------------------------------
     def gen_synth(self, n, d, rank, seed):
         out = np.zeros((n, d))

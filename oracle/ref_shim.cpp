@@ -230,6 +230,45 @@ int cvqr_decode_keys(size_t d, size_t g, size_t L, size_t R,
   });
 }
 
+// train_key_codebook (keyquant.cpp:641-703).  atoms_out: [R][d/2][L][2];
+// obj_out: the hard-objective traces, round-major then group, concatenated
+// (obj_len[r * groups + grp] entries each, at most obj_cap in total);
+// mse_out[R]: reconstruction MSE after each round.
+int cvqr_train_key_codebook(size_t d, size_t g, size_t L, size_t R, const double* calib,
+                            size_t n, size_t soft_iters, size_t hard_iters_max, double t0,
+                            double decay, double tol, double ridge, uint64_t seed,
+                            int factorized, double* atoms_out, double* obj_out,
+                            size_t obj_cap, size_t* obj_len, double* mse_out) {
+  return guard([&] {
+    KeyQuantConfig c = kqc(d, g, L, R);
+    EmConfig em;
+    em.soft_iters = soft_iters;
+    em.hard_iters_max = hard_iters_max;
+    em.t0 = t0;
+    em.decay = decay;
+    em.tol = tol;
+    em.ridge = ridge;
+    em.seed = seed;
+    em.search = factorized ? AssignSearch::factorized : AssignSearch::brute_force;
+    KeyTrainResult res = train_key_codebook(make_mat(n, d, calib), c, em);
+    for (size_t i = 0; i < res.codebook.atoms.size(); ++i) {
+      atoms_out[2 * i] = res.codebook.atoms[i].x;
+      atoms_out[2 * i + 1] = res.codebook.atoms[i].y;
+    }
+    size_t k = 0;
+    for (size_t r = 0; r < R; ++r) {
+      const auto& rr = res.report.rounds[r];
+      for (size_t grp = 0; grp < rr.hard_objective.size(); ++grp) {
+        const auto& tr = rr.hard_objective[grp];
+        obj_len[r * rr.hard_objective.size() + grp] = tr.size();
+        for (double v : tr)
+          if (k < obj_cap) obj_out[k++] = v;
+      }
+      mse_out[r] = rr.reconstruction_mse;
+    }
+  });
+}
+
 size_t cvqr_bits_per_token(size_t d, size_t g, size_t L, size_t R) {
   return kqc(d, g, L, R).bits_per_token();
 }

@@ -265,6 +265,63 @@ def encode_keys(kq, atoms, keys, ctx=None):
     return a[:m], b[:m]
 
 
+class _Em(C.Structure):
+    _fields_ = [("soft_iters", _u64), ("hard_iters_max", _u64), ("t0", _d), ("decay", _d),
+                ("tol", _d), ("ridge", _d), ("seed", _u64), ("search", C.c_int32)]
+
+
+@dataclass
+class EmConfig:
+    """keyquant.hpp:71-80 (search: "brute_force" | "factorized")."""
+
+    soft_iters: int = 30
+    hard_iters_max: int = 100
+    t0: float = 0.0
+    decay: float = 0.9
+    tol: float = 1e-6
+    ridge: float = -1.0
+    seed: int = 1
+    search: str = "brute_force"
+
+    def _c(self):
+        if self.search not in ("brute_force", "factorized"):
+            raise ValueError("EmConfig: unknown search")
+        return _Em(self.soft_iters, self.hard_iters_max, self.t0, self.decay, self.tol,
+                   self.ridge, self.seed, 1 if self.search == "factorized" else 0)
+
+
+def train_key_codebook(calib, kq, em=None, ctx=None):
+    """train_key_codebook (keyquant.cpp:641-703) on the B200.
+
+    Returns (atoms [R*(d/2)*L*2] fp64 in CVQK order, report) where report has
+    "hard_objective" [R][groups] -> list and "reconstruction_mse" [R]."""
+    kq = _kc(kq)
+    em = em or EmConfig()
+    ctx = ctx or default_context()
+    calib = _a(calib, np.float64)
+    if calib.ndim != 2 or calib.shape[1] != kq.d:
+        raise ValueError("train_key_codebook: calib width != d")
+    n = calib.shape[0]
+    atoms = np.zeros(2 * kq.n_atoms, np.float64)
+    ng = kq.rounds * kq.groups
+    cap = ng * (em.hard_iters_max + 2)
+    obj = np.zeros(max(cap, 1), np.float64)
+    olen = np.zeros(ng, np.uint64)
+    mse = np.zeros(kq.rounds, np.float64)
+    kc, ec = kq._c(), em._c()
+    _check(_lib.cvq_train_key_codebook(ctx.h, C.byref(kc), _ptr(calib), _u64(n), C.byref(ec),
+                                       _ptr(atoms), _ptr(obj), _u64(cap), _ptr(olen), _ptr(mse)))
+    traces, k = [], 0
+    for r in range(kq.rounds):
+        row = []
+        for grp in range(kq.groups):
+            ln = int(olen[r * kq.groups + grp])
+            row.append(obj[k:k + ln].copy())
+            k += ln
+        traces.append(row)
+    return atoms, {"hard_objective": traces, "reconstruction_mse": mse}
+
+
 def encoder_forward_infer(w1, b1, w2, b2, values, ctx=None):
     """valquant.cpp:50-101, infer mode, batched -> (bits[n][N_c], logits)."""
     ctx = ctx or default_context()

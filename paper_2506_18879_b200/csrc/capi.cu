@@ -19,7 +19,6 @@
 
 namespace cvq {
 std::atomic<unsigned long long> g_launches{0};
-bool key_tables_fit(const Geom& g);
 cudaError_t run_naive_attention(const AttnJob& job, const float* q, float* out, void* scratch,
                                 size_t scratch_bytes, cudaStream_t st);
 size_t naive_scratch_bytes(const AttnJob& job);
@@ -884,6 +883,37 @@ CVQ_API cvq_status cvq_encode_keys(cvq_context* ctx, const cvq_key_config* kc, c
   CU(cudaMemcpyAsync(a, da, np * 2, cudaMemcpyDeviceToHost, st));
   CU(cudaMemcpyAsync(b, db, np * 2, cudaMemcpyDeviceToHost, st));
   CU(cudaStreamSynchronize(st));
+  return CVQ_OK;
+}
+
+CVQ_API cvq_status cvq_train_key_codebook(cvq_context* ctx, const cvq_key_config* kc,
+                                          const double* calib, uint64_t n, const cvq_em_config* em,
+                                          double* atoms_out, double* objective_out,
+                                          uint64_t objective_cap, uint64_t* objective_len,
+                                          double* mse_out) {
+  TRY(ctx_check(ctx));
+  TRY(validate_kc(kc));
+  if (!em || !atoms_out || !objective_len || !mse_out || (n && !calib))
+    return fail(CVQ_EINVAL, "null argument");
+  if (em->search != 0 && em->search != 1) return fail(CVQ_EINVAL, "EmConfig: unknown search");
+  Geom g = make_geom(kc, 1, 0, 1);
+  TrainConfig tc{em->soft_iters, em->hard_iters_max, em->t0, em->decay, em->tol,
+                 em->ridge, em->seed, em->search == 1};
+  std::vector<std::vector<double>> traces;
+  std::vector<double> mse;
+  std::string err;
+  const int rc = train_key_codebook_gpu(g, calib, (long long)n, tc, atoms_out, &traces, &mse, &err,
+                                        ctx->stream);
+  if (rc == 1) return fail(CVQ_EINVAL, err);
+  if (rc == 2) return fail(CVQ_ETRAINING, err);
+  if (rc != 0) return fail(CVQ_ECUDA, err);
+  uint64_t k = 0;
+  for (size_t i = 0; i < traces.size(); ++i) {
+    objective_len[i] = traces[i].size();
+    for (double v : traces[i])
+      if (objective_out && k < objective_cap) objective_out[k++] = v;
+  }
+  for (size_t r = 0; r < mse.size(); ++r) mse_out[r] = mse[r];
   return CVQ_OK;
 }
 

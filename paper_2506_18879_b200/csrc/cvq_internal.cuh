@@ -10,6 +10,7 @@
 
 #include <atomic>
 #include <string>
+#include <vector>
 
 namespace cvq {
 
@@ -120,6 +121,22 @@ cudaError_t run_encode_values(const Geom& g, int S, int n_slots,
                               int dtype, long long s_stride, long long n,
                               uint8_t* bits, double* logits, int* err_flag,
                               cudaStream_t st);
+
+// ---- key-codebook training (train.cu) -------------------------------------
+bool key_tables_fit(const Geom& g);  // encode.cu
+struct TrainConfig {  // EmConfig, keyquant.hpp:71-80
+  size_t soft_iters, hard_iters_max;
+  double t0, decay, tol, ridge;
+  uint64_t seed;
+  bool factorized;
+};
+// train_key_codebook (keyquant.cpp:641-703): calib [n][d] fp64 host;
+// atoms_out [R][d/2][L][2]; traces: hard objective per (round, group);
+// mse: reconstruction MSE per round.  Returns 0, or 1 (invalid argument),
+// 2 (training error), 3 (CUDA error) with *err set.
+int train_key_codebook_gpu(const Geom& g, const double* calib, long long n, const TrainConfig& em,
+                           double* atoms_out, std::vector<std::vector<double>>* traces,
+                           std::vector<double>* mse, std::string* err, cudaStream_t st);
 
 // ---- packing (pack.cu) -----------------------------------------------------
 // Writes n tokens' key codes (a/b [s][n][R*groups]) into stream words at
