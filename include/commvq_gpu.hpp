@@ -150,6 +150,40 @@ inline KeyCodes encode_keys(const Mat& keys, const KeyCodebook& cb,
   return codes;
 }
 
+// keyquant.hpp:131-133: the soft-to-hard EM schedule with device E-steps
+// (train.cu); bit-identical to the reference on the golden cases.
+inline KeyTrainResult train_key_codebook(const Mat& calib_keys, const KeyQuantConfig& config,
+                                         const EmConfig& em = {}) {
+  config.validate();
+  if (calib_keys.cols != config.d)
+    throw std::invalid_argument("train_key_codebook: calib width != d");
+  const cvq_key_config ck = key_config(config);
+  cvq_em_config ce{em.soft_iters, em.hard_iters_max, em.t0, em.decay, em.tol, em.ridge, em.seed,
+                   em.search == AssignSearch::factorized ? 1 : 0};
+  const size_t groups = config.groups();
+  std::vector<double> xy(config.rounds * (config.d / 2) * config.n_levels * 2);
+  std::vector<double> obj(config.rounds * groups * (em.hard_iters_max + 2));
+  std::vector<uint64_t> olen(config.rounds * groups);
+  std::vector<double> mse(config.rounds);
+  check(cvq_train_key_codebook(context(), &ck, calib_keys.data.data(), calib_keys.rows, &ce,
+                               xy.data(), obj.data(), obj.size(), olen.data(), mse.data()));
+  KeyTrainResult res{KeyCodebook::zeros(config), {}};
+  for (size_t i = 0; i < res.codebook.atoms.size(); ++i)
+    res.codebook.atoms[i] = CommMat{xy[2 * i], xy[2 * i + 1]};
+  res.report.rounds.resize(config.rounds);
+  size_t k = 0;
+  for (size_t r = 0; r < config.rounds; ++r) {
+    res.report.rounds[r].hard_objective.resize(groups);
+    for (size_t grp = 0; grp < groups; ++grp) {
+      const size_t len = static_cast<size_t>(olen[r * groups + grp]);
+      res.report.rounds[r].hard_objective[grp].assign(obj.begin() + k, obj.begin() + k + len);
+      k += len;
+    }
+    res.report.rounds[r].reconstruction_mse = mse[r];
+  }
+  return res;
+}
+
 // valquant.hpp:62-64, infer mode on the device (train mode draws Gumbel
 // noise from the caller's CPU Rng and is calibration, not the decode path).
 inline EncoderOut encoder_forward(const Vec& t, const ValueEncoder& enc, EncoderMode mode,

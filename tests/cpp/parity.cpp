@@ -4,6 +4,7 @@
 // and runs the reference's pinned scenarios through both namespaces side by
 // side (test_attn.cpp, test_keyquant.cpp, test_valquant.cpp, test_cache.cpp).
 // Needs a B200.  Prints one [PASS]/[FAIL] line per check; exit code = #fails.
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <filesystem>
@@ -15,6 +16,7 @@
 #include "commvq/keyquant.hpp"
 #include "commvq/rng.hpp"
 #include "commvq/valquant.hpp"
+#include "commvq/ctf.hpp"
 #include "commvq_gpu.hpp"
 
 using namespace commvq;
@@ -164,6 +166,37 @@ int main() {
       threw = true;
     }
     report(threw, "query before cache -> invalid_argument");
+  }
+  // 5. train_key_codebook: drop-in for keyquant.hpp:131-133
+  {
+    KeyQuantConfig cfg{8, 2, 4, 2};
+    Mat calib = gen_synth(128, 8, 3, 21);
+    EmConfig em;
+    em.soft_iters = 5;
+    em.hard_iters_max = 20;
+    KeyTrainResult ref = train_key_codebook(calib, cfg, em);
+    KeyTrainResult dev = gpu::train_key_codebook(calib, cfg, em);
+    double worst = 0.0, scale = 0.0;
+    for (size_t i = 0; i < ref.codebook.atoms.size(); ++i) {
+      const CommMat& x = ref.codebook.atoms[i];
+      const CommMat& y = dev.codebook.atoms[i];
+      worst = std::max({worst, std::abs(x.x - y.x), std::abs(x.y - y.y)});
+      scale = std::max({scale, std::abs(x.x), std::abs(x.y)});
+    }
+    bool same_len = ref.report.rounds.size() == dev.report.rounds.size();
+    for (size_t r = 0; same_len && r < ref.report.rounds.size(); ++r)
+      for (size_t g2 = 0; g2 < ref.report.rounds[r].hard_objective.size(); ++g2)
+        same_len = same_len && ref.report.rounds[r].hard_objective[g2].size() ==
+                                   dev.report.rounds[r].hard_objective[g2].size();
+    report(worst <= 1e-9 * scale && same_len, "train_key_codebook",
+           "max |d atom| / max |atom| = " + std::to_string(worst / scale));
+    bool threw = false;
+    try {
+      gpu::train_key_codebook(Mat(4, 8), cfg, em);  // fewer than L^2 rows
+    } catch (const std::invalid_argument&) {
+      threw = true;
+    }
+    report(threw, "train: too few rows -> invalid_argument");
   }
   std::printf("%d failure(s)\n", g_fail);
   return g_fail;
