@@ -184,6 +184,34 @@ inline KeyTrainResult train_key_codebook(const Mat& calib_keys, const KeyQuantCo
   return res;
 }
 
+// valquant.hpp:96-104: SGD on the reference's random stream (train_value.cu).
+inline ValueTrainResult train_value_quantizer(const Mat& calib, size_t n_codes,
+                                              const ValTrainConfig& cfg = {},
+                                              const ValueCodebook* init_codebook = nullptr) {
+  if (init_codebook && (init_codebook->n_codes != n_codes || init_codebook->d != calib.cols))
+    throw std::invalid_argument("train_value_quantizer: init codebook shape mismatch");
+  const size_t d = calib.cols, H = cfg.hidden ? cfg.hidden : 2 * n_codes;
+  cvq_val_train_config c{cfg.steps,  cfg.batch, cfg.step_size, cfg.gumbel_t_start,
+                         cfg.gumbel_t_end, cfg.hidden, cfg.seed, cfg.checkpoint_every,
+                         cfg.freeze_codebook ? 1 : 0};
+  ValueTrainResult res;
+  res.encoder = ValueEncoder::zeros(d, H, n_codes);
+  res.codebook = ValueCodebook::zeros(n_codes, d);
+  std::vector<double> curve(cfg.steps ? cfg.steps : 1);
+  uint64_t len = 0, steps_run = 0;
+  int32_t diverged = 0;
+  check(cvq_train_value_quantizer(
+      context(), calib.data.data(), calib.rows, static_cast<uint32_t>(d),
+      static_cast<uint32_t>(n_codes), &c, init_codebook ? init_codebook->rows.data.data() : nullptr,
+      res.encoder.w1.data.data(), res.encoder.b1.data(), res.encoder.w2.data.data(),
+      res.encoder.b2.data(), res.codebook.rows.data.data(), curve.data(), &len, &diverged,
+      &steps_run));
+  res.loss_curve.assign(curve.begin(), curve.begin() + static_cast<long>(len));
+  res.diverged = diverged != 0;
+  res.steps_run = static_cast<size_t>(steps_run);
+  return res;
+}
+
 // valquant.hpp:62-64, infer mode on the device (train mode draws Gumbel
 // noise from the caller's CPU Rng and is calibration, not the decode path).
 inline EncoderOut encoder_forward(const Vec& t, const ValueEncoder& enc, EncoderMode mode,

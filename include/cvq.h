@@ -166,6 +166,34 @@ CVQ_API cvq_status cvq_train_key_codebook(cvq_context* ctx, const cvq_key_config
                                           double* objective_out, uint64_t objective_cap,
                                           uint64_t* objective_len, double* mse_out);
 
+/* ValTrainConfig (valquant.hpp:76-86). */
+typedef struct cvq_val_train_config {
+  uint64_t steps;            /* 10000 */
+  uint64_t batch;            /* 256 */
+  double step_size;          /* 1e-3 */
+  double gumbel_t_start;     /* 1.0 */
+  double gumbel_t_end;       /* 0.1 */
+  uint64_t hidden;           /* 0 -> 2 * n_codes */
+  uint64_t seed;             /* 1 */
+  uint64_t checkpoint_every; /* 100 */
+  int32_t freeze_codebook;
+} cvq_val_train_config;
+
+/* train_value_quantizer (valquant.cpp:172-383) on the GPU: SGD with
+ * straight-through Gumbel-sigmoid gradients on the reference's random
+ * stream; reductions in the reference order.  calib [n][d] fp64 host rows;
+ * init_codebook [n_codes][d] or NULL.  Outputs: w1 [d][H], b1 [H],
+ * w2 [H][n_codes], b2 [n_codes], codebook [n_codes][d] with
+ * H = hidden ? hidden : 2 n_codes; loss_curve[steps] (curve_len entries
+ * written), diverged, steps_run.  Errors: CVQ_EINVAL (valquant.cpp:175-200). */
+CVQ_API cvq_status cvq_train_value_quantizer(cvq_context* ctx, const double* calib,
+                                             uint64_t n_rows, uint32_t d, uint32_t n_codes,
+                                             const cvq_val_train_config* cfg,
+                                             const double* init_codebook, double* w1, double* b1,
+                                             double* w2, double* b2, double* codebook,
+                                             double* loss_curve, uint64_t* curve_len,
+                                             int32_t* diverged, uint64_t* steps_run);
+
 /* encoder_forward in infer mode (valquant.cpp:50-101), batched over tokens:
  * values[n][d] -> bits[n][n_codes] (logit > 0), logits optional. */
 CVQ_API cvq_status cvq_encoder_forward_infer(

@@ -358,6 +358,33 @@ class Oracle:
             traces.append(row)
         return atoms, traces, mse
 
+    # ---- valquant.cpp:172-383 (compiled reference only) -------------------
+    def train_value_quantizer(self, calib, n_codes, steps=10000, batch=256, step_size=1e-3,
+                              t_start=1.0, t_end=0.1, hidden=0, seed=1, checkpoint_every=100,
+                              freeze=False, init_codebook=None):
+        assert self.kind == "reference", "training is pinned on the compiled reference"
+        calib = np.ascontiguousarray(calib, np.float64)
+        n, d = calib.shape
+        H = hidden or 2 * n_codes
+        out = {"w1": np.zeros((d, H)), "b1": np.zeros(H), "w2": np.zeros((H, n_codes)),
+               "b2": np.zeros(n_codes), "codebook": np.zeros((n_codes, d))}
+        curve = np.zeros(max(steps, 1))
+        clen, sr = _sz(0), _sz(0)
+        dv = C.c_int(0)
+        init = None if init_codebook is None else np.ascontiguousarray(init_codebook, np.float64)
+        f = self.lib.cvqr_train_value_quantizer
+        f.argtypes = [_p, _sz, _sz, _sz, _sz, _sz, _d, _d, _d, _sz, _u64, _sz, C.c_int, _p,
+                      _p, _p, _p, _p, _p, _p, C.POINTER(_sz), C.POINTER(C.c_int), C.POINTER(_sz)]
+        self._check(f(_ptr(calib), n, d, n_codes, steps, batch, step_size, t_start, t_end, hidden,
+                      seed, checkpoint_every, int(freeze), _ptr(init) if init is not None else None,
+                      _ptr(out["w1"]), _ptr(out["b1"]), _ptr(out["w2"]), _ptr(out["b2"]),
+                      _ptr(out["codebook"]), _ptr(curve), C.byref(clen), C.byref(dv),
+                      C.byref(sr)))
+        out["loss_curve"] = curve[:clen.value].copy()
+        out["diverged"] = bool(dv.value)
+        out["steps_run"] = int(sr.value)
+        return out
+
     # ---- ctf.cpp:97-144 --------------------------------------------------
     def gen_synth(self, n, d, rank, seed):
         out = np.zeros((n, d))

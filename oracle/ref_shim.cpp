@@ -269,6 +269,43 @@ int cvqr_train_key_codebook(size_t d, size_t g, size_t L, size_t R, const double
   });
 }
 
+// train_value_quantizer (valquant.cpp:172-383).  Outputs as the reference's
+// ValueTrainResult: w1 [d][H], b1 [H], w2 [H][C], b2 [C], cb [C][d],
+// loss_curve (curve_len entries), diverged, steps_run.
+int cvqr_train_value_quantizer(const double* calib, size_t n, size_t d, size_t n_codes,
+                               size_t steps, size_t batch, double step_size, double t_start,
+                               double t_end, size_t hidden, uint64_t seed,
+                               size_t checkpoint_every, int freeze, const double* init_cb,
+                               double* w1, double* b1, double* w2, double* b2, double* cb,
+                               double* loss_curve, size_t* curve_len, int* diverged,
+                               size_t* steps_run) {
+  return guard([&] {
+    ValTrainConfig cfg;
+    cfg.steps = steps;
+    cfg.batch = batch;
+    cfg.step_size = step_size;
+    cfg.gumbel_t_start = t_start;
+    cfg.gumbel_t_end = t_end;
+    cfg.hidden = hidden;
+    cfg.seed = seed;
+    cfg.checkpoint_every = checkpoint_every;
+    cfg.freeze_codebook = freeze != 0;
+    ValueCodebook init;
+    if (init_cb) init = make_vcb(n_codes, d, init_cb);
+    ValueTrainResult r =
+        train_value_quantizer(make_mat(n, d, calib), n_codes, cfg, init_cb ? &init : nullptr);
+    std::memcpy(w1, r.encoder.w1.data.data(), r.encoder.w1.data.size() * 8);
+    std::memcpy(b1, r.encoder.b1.data(), r.encoder.b1.size() * 8);
+    std::memcpy(w2, r.encoder.w2.data.data(), r.encoder.w2.data.size() * 8);
+    std::memcpy(b2, r.encoder.b2.data(), r.encoder.b2.size() * 8);
+    std::memcpy(cb, r.codebook.rows.data.data(), r.codebook.rows.data.size() * 8);
+    std::memcpy(loss_curve, r.loss_curve.data(), r.loss_curve.size() * 8);
+    *curve_len = r.loss_curve.size();
+    *diverged = r.diverged ? 1 : 0;
+    *steps_run = r.steps_run;
+  });
+}
+
 size_t cvqr_bits_per_token(size_t d, size_t g, size_t L, size_t R) {
   return kqc(d, g, L, R).bits_per_token();
 }

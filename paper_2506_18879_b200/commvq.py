@@ -322,6 +322,61 @@ def train_key_codebook(calib, kq, em=None, ctx=None):
     return atoms, {"hard_objective": traces, "reconstruction_mse": mse}
 
 
+class _ValCfg(C.Structure):
+    _fields_ = [("steps", _u64), ("batch", _u64), ("step_size", _d), ("gumbel_t_start", _d),
+                ("gumbel_t_end", _d), ("hidden", _u64), ("seed", _u64),
+                ("checkpoint_every", _u64), ("freeze_codebook", C.c_int32)]
+
+
+@dataclass
+class ValTrainConfig:
+    """valquant.hpp:76-86."""
+
+    steps: int = 10000
+    batch: int = 256
+    step_size: float = 1e-3
+    gumbel_t_start: float = 1.0
+    gumbel_t_end: float = 0.1
+    hidden: int = 0
+    seed: int = 1
+    checkpoint_every: int = 100
+    freeze_codebook: bool = False
+
+    def _c(self):
+        return _ValCfg(self.steps, self.batch, self.step_size, self.gumbel_t_start,
+                       self.gumbel_t_end, self.hidden, self.seed, self.checkpoint_every,
+                       int(self.freeze_codebook))
+
+
+def train_value_quantizer(calib, n_codes, cfg=None, init_codebook=None, ctx=None):
+    """train_value_quantizer (valquant.cpp:172-383) on the B200 -> dict with
+    w1 [d][H], b1, w2 [H][n_codes], b2, codebook [n_codes][d], loss_curve,
+    diverged, steps_run (ValueTrainResult, valquant.hpp:88-94)."""
+    cfg = cfg or ValTrainConfig()
+    ctx = ctx or default_context()
+    calib = _a(calib, np.float64)
+    if calib.ndim != 2:
+        raise ValueError("train_value_quantizer: calib must be 2-D")
+    n, d = calib.shape
+    H = cfg.hidden or 2 * n_codes
+    out = {"w1": np.zeros((d, H)), "b1": np.zeros(H), "w2": np.zeros((H, n_codes)),
+           "b2": np.zeros(n_codes), "codebook": np.zeros((n_codes, d))}
+    curve = np.zeros(max(cfg.steps, 1))
+    clen, sr = _u64(0), _u64(0)
+    dv = C.c_int32(0)
+    init = None if init_codebook is None else _a(init_codebook, np.float64)
+    c = cfg._c()
+    _check(_lib.cvq_train_value_quantizer(
+        ctx.h, _ptr(calib) if n else None, _u64(n), _u32(d), _u32(n_codes), C.byref(c),
+        _ptr(init) if init is not None else None, _ptr(out["w1"]), _ptr(out["b1"]),
+        _ptr(out["w2"]), _ptr(out["b2"]), _ptr(out["codebook"]), _ptr(curve), C.byref(clen),
+        C.byref(dv), C.byref(sr)))
+    out["loss_curve"] = curve[:clen.value].copy()
+    out["diverged"] = bool(dv.value)
+    out["steps_run"] = int(sr.value)
+    return out
+
+
 def encoder_forward_infer(w1, b1, w2, b2, values, ctx=None):
     """valquant.cpp:50-101, infer mode, batched -> (bits[n][N_c], logits)."""
     ctx = ctx or default_context()

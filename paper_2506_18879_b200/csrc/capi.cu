@@ -917,6 +917,33 @@ CVQ_API cvq_status cvq_train_key_codebook(cvq_context* ctx, const cvq_key_config
   return CVQ_OK;
 }
 
+CVQ_API cvq_status cvq_train_value_quantizer(cvq_context* ctx, const double* calib, uint64_t n,
+                                             uint32_t d, uint32_t n_codes,
+                                             const cvq_val_train_config* cfg,
+                                             const double* init_codebook, double* w1, double* b1,
+                                             double* w2, double* b2, double* codebook,
+                                             double* loss_curve, uint64_t* curve_len,
+                                             int32_t* diverged, uint64_t* steps_run) {
+  TRY(ctx_check(ctx));
+  if (!cfg || !w1 || !b1 || !w2 || !b2 || !codebook || !loss_curve || !curve_len || !diverged ||
+      !steps_run || (n && !calib))
+    return fail(CVQ_EINVAL, "null argument");
+  ValTrainCfg vc{cfg->steps, cfg->batch, cfg->step_size, cfg->gumbel_t_start, cfg->gumbel_t_end,
+                 cfg->hidden, cfg->seed, cfg->checkpoint_every, cfg->freeze_codebook != 0};
+  std::string err;
+  int dv = 0;
+  long long sr = 0, cl = 0;
+  const int rc = train_value_quantizer_gpu(calib, (long long)n, (int)d, (int)n_codes, vc,
+                                           init_codebook, w1, b1, w2, b2, codebook, loss_curve,
+                                           &dv, &sr, &cl, &err, ctx->stream);
+  if (rc == 1) return fail(CVQ_EINVAL, err);
+  if (rc != 0) return fail(CVQ_ECUDA, err);
+  *diverged = dv;
+  *steps_run = (uint64_t)sr;
+  *curve_len = (uint64_t)cl;
+  return CVQ_OK;
+}
+
 CVQ_API cvq_status cvq_encoder_forward_infer(cvq_context* ctx, uint32_t d, uint32_t hidden,
                                              uint32_t n_codes, const double* w1, const double* b1,
                                              const double* w2, const double* b2,

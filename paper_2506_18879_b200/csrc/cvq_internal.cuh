@@ -138,6 +138,24 @@ int train_key_codebook_gpu(const Geom& g, const double* calib, long long n, cons
                            double* atoms_out, std::vector<std::vector<double>>* traces,
                            std::vector<double>* mse, std::string* err, cudaStream_t st);
 
+// ---- value-quantizer training (train_value.cu) -----------------------------
+struct ValTrainCfg {  // ValTrainConfig, valquant.hpp:76-86
+  size_t steps, batch;
+  double step_size, t_start, t_end;
+  size_t hidden;
+  uint64_t seed;
+  size_t checkpoint_every;
+  bool freeze_codebook;
+};
+// train_value_quantizer (valquant.cpp:172-383).  calib [n][d] host; outputs
+// host arrays (w1 [d][H], b1 [H], w2 [H][C], b2 [C], cb [C][d], loss_curve
+// [steps]).  Returns 0, 1 (invalid argument) or 3 (CUDA) with *err set.
+int train_value_quantizer_gpu(const double* calib, long long n, int d, int n_codes,
+                              const ValTrainCfg& cfg, const double* init_cb, double* w1,
+                              double* b1, double* w2, double* b2, double* cb, double* loss_curve,
+                              int* diverged, long long* steps_run, long long* curve_len,
+                              std::string* err, cudaStream_t st);
+
 // ---- packing (pack.cu) -----------------------------------------------------
 // Writes n tokens' key codes (a/b [s][n][R*groups]) into stream words at
 // token offset tok0 (read-modify-write of boundary words).

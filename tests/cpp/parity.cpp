@@ -198,6 +198,30 @@ int main() {
     }
     report(threw, "train: too few rows -> invalid_argument");
   }
+  // 6. train_value_quantizer: drop-in for valquant.hpp:96-104
+  {
+    Mat calib = gen_synth(96, 8, 3, 22);
+    ValTrainConfig cfg;
+    cfg.steps = 150;
+    cfg.batch = 16;
+    cfg.step_size = 1e-2;
+    ValueTrainResult ref = train_value_quantizer(calib, 8, cfg);
+    ValueTrainResult dev = gpu::train_value_quantizer(calib, 8, cfg);
+    double worst = 0.0, scale = 0.0;
+    auto cmp = [&](const std::vector<double>& a, const std::vector<double>& b) {
+      for (size_t i = 0; i < a.size(); ++i) {
+        worst = std::max(worst, std::abs(a[i] - b[i]));
+        scale = std::max(scale, std::abs(a[i]));
+      }
+    };
+    cmp(ref.encoder.w1.data, dev.encoder.w1.data);
+    cmp(ref.encoder.w2.data, dev.encoder.w2.data);
+    cmp(ref.codebook.rows.data, dev.codebook.rows.data);
+    const bool same = ref.steps_run == dev.steps_run && ref.diverged == dev.diverged &&
+                      ref.loss_curve.size() == dev.loss_curve.size();
+    report(same && worst <= 1e-9 * scale, "train_value_quantizer",
+           "max |d param| / max |param| = " + std::to_string(worst / scale));
+  }
   std::printf("%d failure(s)\n", g_fail);
   return g_fail;
 }

@@ -65,6 +65,29 @@ def main():
                                      "point_iterations_per_s": cpit / cpu_s}
             line["speedup"] = (pit / gpu_s) / (cpit / cpu_s)
     print(json.dumps(line))
+    # ---- value quantizer (valquant.cpp:172-383): default ValTrainConfig,
+    # d = 128, n_codes = 128 (1-bit), H = 256
+    vcal = synth(args.n, 128, 32, 4)
+    vcfg = G.ValTrainConfig()
+    G.train_value_quantizer(vcal[:1024], 128, G.ValTrainConfig(steps=5))  # warm
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    r = G.train_value_quantizer(vcal, 128, vcfg)
+    torch.cuda.synchronize()
+    vg = time.perf_counter() - t0
+    vline = {"metric": "value-quantizer SGD steps/s (d=128, n_codes=128, batch=256)",
+             "gpu": {"steps": r["steps_run"], "seconds": vg, "steps_per_s": r["steps_run"] / vg,
+                     "final_loss": float(r["loss_curve"][-1])}}
+    if not args.no_cpu:
+        from oracle.oracle import Oracle, have_ref
+        if have_ref():
+            t1 = time.perf_counter()
+            Oracle("reference").train_value_quantizer(vcal, 128, steps=20)
+            vc = time.perf_counter() - t1
+            vline["cpu_reference"] = {"steps": 20, "seconds": vc, "cores": 1,
+                                      "steps_per_s": 20 / vc}
+            vline["speedup"] = (r["steps_run"] / vg) / (20 / vc)
+    print(json.dumps(vline))
 
 
 if __name__ == "__main__":
