@@ -35,9 +35,6 @@
 // Codebook precision fp16 (as CVQ_CACHE_KEYS_FP16), accumulation fp32.
 #include "cvq_internal.cuh"
 
-#ifndef CVQ_TC_EXPERIMENT
-#define CVQ_TC_EXPERIMENT 0
-#endif
 
 namespace cvq {
 
@@ -314,10 +311,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_tc_score(TcArgs a) {
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(dempty + db);  // D[db] is in registers: free it
-#if CVQ_TC_EXPERIMENT == 1
-      if (v[0] == 0x7fffffffu) a.ps[0] = 1.f;
-      continue;
-#endif
       if constexpr (G == 4) {
         // acc_h = qa_h A + qb_h B with A = phs.x kc + phs.y ko and
         // B = phs.x ko - phs.y kc equals al_h kc + be_h ko where
