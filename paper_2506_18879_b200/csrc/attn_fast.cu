@@ -651,7 +651,13 @@ __global__ void __launch_bounds__(kThreads) k_fast_value(FastArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   float* sc = reinterpret_cast<float*>(smem);                                 // [chunk2][G]
   uint64_t* vw = reinterpret_cast<uint64_t*>(sc + (size_t)a.chunk2 * G);     // [chunk2][WPTOK]
-  float* zr = reinterpret_cast<float*>(vw + (size_t)a.chunk2 * WPTOK);       // [8][NC][G]
+  // per-warp z partials [8][NC][G] alias the score / value-word staging,
+  // which is dead once the accumulate loop is done (fewer smem bytes per CTA
+  // -> more resident CTAs for this latency-bound kernel)
+  const size_t stage_bytes = (size_t)a.chunk2 * (G * 4 + WPTOK * 8);
+  float* zr = stage_bytes >= (size_t)8 * NC * G * 4
+                  ? reinterpret_cast<float*>(smem)
+                  : reinterpret_cast<float*>(vw + (size_t)a.chunk2 * WPTOK);
   __shared__ float red[8][G];
   __shared__ float mh[G], lh[G];
   const int s = blockIdx.y;
@@ -747,6 +753,7 @@ __global__ void __launch_bounds__(kThreads) k_fast_value(FastArgs a) {
         for (int h = 0; h < G2; ++h) add2(z[c][h], p[h]);
       }
   }
+  __syncthreads();  // all warps are done with sc / vw (zr may alias them)
 #pragma unroll
   for (int c = 0; c < CPL; ++c)
 #pragma unroll
@@ -797,7 +804,7 @@ int f2_chunk(const AttnJob& job) {
   long long want = (job.n * (long long)job.S + 2 * 148 - 1) / (2 * 148);
   long long ch = (want + kTile - 1) / kTile * kTile;
   if (ch < 256) ch = 256;
-  // 48 KiB smem -> 4 CTAs/SM (latency-bound kernel); measured on C3: 1024 and
+  // 32 KiB smem -> 6 CTAs/SM (latency-bound kernel); measured on C3: 1024 and
   // 2048 tie, 512 and 4096 are slower
   if (ch > 1024) ch = 1024;
   return (int)ch;
@@ -805,8 +812,9 @@ int f2_chunk(const AttnJob& job) {
 
 size_t f2_smem(const AttnJob& job, int chunk2) {
   const Geom& g = job.geo;
-  return (size_t)chunk2 * g.G * 4 + (size_t)chunk2 * (g.n_codes / 64) * 8 + 16 +
-         (size_t)8 * g.n_codes * g.G * 4;
+  const size_t stage = (size_t)chunk2 * g.G * 4 + (size_t)chunk2 * (g.n_codes / 64) * 8;
+  const size_t zr = (size_t)8 * g.n_codes * g.G * 4;
+  return (stage >= zr ? stage : stage + zr) + 16;  // zr aliases the staging when it fits
 }
 
 template <class K>
