@@ -189,7 +189,7 @@ def main():
     kq = G.KeyQuantConfig(d, g, L, R)
     S, rows = B * layers * H, B * layers * H * Gq
     # contiguous context shards, boundaries at multiples of 128 tokens
-    from paper_2506_18879_b200.dist import gather_partials, shard_plan
+    from paper_2506_18879_b200.dist import gather_packed, packed_views, shard_plan
     lo, hi = shard_plan(N, world)[rank]
     n_local = hi - lo
     extra = 2 * (args.steps + args.warmup) + 16  # room for the e2e decode steps' appends
@@ -229,16 +229,16 @@ def main():
     q = torch.randn(B, layers, H * Gq, d, device="cuda", generator=gen)
     out = torch.empty_like(q)
     t_q = N - 1  # global query position (last cached token)
-    m_p = torch.empty(rows, device="cuda")
-    l_p = torch.empty(rows, device="cuda")
-    o_p = torch.empty(rows, d, device="cuda")
+    # this rank's partials (m, l, o) in one packed block -> one all-gather
+    pk = torch.empty(rows * (d + 2), device="cuda")
+    m_p, l_p, o_p = packed_views(pk, rows, d)
     def step():
         if world == 1:
             cache.attention(q, t_q, out)
         else:
             cache.attention_partial(q, m_p, l_p, o_p, t_q)
-            gm, gl, go = gather_partials(m_p, l_p, o_p)  # NCCL all-gather, 520 B/row
-            G.lse_combine(gm, gl, go, out, ctx)
+            parts = gather_packed(pk)  # NCCL all-gather, 520 B/row
+            G.lse_combine_packed(parts, rows, d, out, ctx)
 
     def barrier():
         if world > 1:

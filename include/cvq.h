@@ -302,6 +302,14 @@ CVQ_API cvq_status cvq_lse_combine(cvq_context* ctx, const float* m,
                                    uint32_t n_parts, uint64_t rows, uint32_t d,
                                    float* out);
 
+/* Same merge over packed per-part blocks [m (rows) | l (rows) | o (rows x d)]
+ * at parts + p * rows * (d + 2): one all-gather of such blocks (the layout
+ * cvq_cache_attention_partial writes when m, l, o point into one buffer)
+ * feeds it directly. */
+CVQ_API cvq_status cvq_lse_combine_packed(cvq_context* ctx, const float* parts,
+                                          uint32_t n_parts, uint64_t rows, uint32_t d,
+                                          float* out);
+
 /* QuantizedKVCache::decode_step (cache.cpp:287-296): append k, v then attend
  * q at the new last position.  All buffers in `where`. */
 CVQ_API cvq_status cvq_cache_decode_step(cvq_cache* c, const void* k,

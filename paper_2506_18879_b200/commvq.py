@@ -597,6 +597,17 @@ class QuantizedKVCache:
         _check(_lib.cvq_cache_set_length(self.h, _u64(n)))
 
 
+def lse_combine_packed(parts, rows, d, out, ctx=None):
+    """Device tensor parts [P][rows*(d+2)] of packed [m | l | o] blocks ->
+    out [rows][d] (cvq_lse_combine_packed)."""
+    ctx = ctx or default_context()
+    P = parts.shape[0]
+    if parts.numel() != P * rows * (d + 2):
+        raise ValueError("lse_combine_packed: parts must be [P][rows*(d+2)]")
+    _check(_lib.cvq_lse_combine_packed(ctx.h, _p(parts.data_ptr()), _u32(P), _u64(rows), _u32(d),
+                                       _p(out.data_ptr())))
+
+
 def lse_combine(m, l, o, out, ctx=None):
     """Device tensors m, l [P][rows], o [P][rows][d] -> out [rows][d]."""
     ctx = ctx or default_context()

@@ -178,10 +178,11 @@ k_value_generic(Geom g, const uint64_t* __restrict__ vpool, uint64_t vstride,
 // --------------------------------------------------------------- combine
 // out = sum_p o_p l_p e^{m_p - M} / sum_p l_p e^{m_p - M}  (flash-decoding
 // merge; the reference softmax is global, linalg.cpp:63-75).
+// Part p's m / l rows at p * sm, its o rows at p * so (elements).
 __global__ void k_combine(const float* __restrict__ m, const float* __restrict__ l,
                           const float* __restrict__ o, int P, long long rows, int d,
-                          float* __restrict__ out, float* __restrict__ m_out,
-                          float* __restrict__ l_out) {
+                          long long sm, long long so, float* __restrict__ out,
+                          float* __restrict__ m_out, float* __restrict__ l_out) {
   // part weights l_p e^{m_p - M} computed once per part (smem), then each
   // thread sums its output column over the parts
   extern __shared__ float wsh[];  // [P]
@@ -189,12 +190,12 @@ __global__ void k_combine(const float* __restrict__ m, const float* __restrict__
   const long long row = blockIdx.x;
   float M = -FLT_MAX;
   for (int p = threadIdx.x; p < P; p += blockDim.x)
-    if (l[p * rows + row] > 0.f) M = fmaxf(M, m[p * rows + row]);
+    if (l[p * sm + row] > 0.f) M = fmaxf(M, m[p * sm + row]);
   M = block_reduce(M, true, red);
   float Ls = 0.f;
   for (int p = threadIdx.x; p < P; p += blockDim.x) {
-    const float lp = l[p * rows + row];
-    const float wgt = lp > 0.f ? lp * expf(m[p * rows + row] - M) : 0.f;
+    const float lp = l[p * sm + row];
+    const float wgt = lp > 0.f ? lp * expf(m[p * sm + row] - M) : 0.f;
     wsh[p] = wgt;
     Ls += wgt;
   }
@@ -203,7 +204,7 @@ __global__ void k_combine(const float* __restrict__ m, const float* __restrict__
     float acc = 0.f;
     for (int p = 0; p < P; ++p) {
       const float wgt = wsh[p];
-      if (wgt != 0.f) acc += o[(p * rows + row) * d + jd] * wgt;
+      if (wgt != 0.f) acc += o[p * so + row * d + jd] * wgt;
     }
     out[row * d + jd] = acc / Lsum;
   }
@@ -215,10 +216,13 @@ __global__ void k_combine(const float* __restrict__ m, const float* __restrict__
 
 cudaError_t run_lse_combine(const float* m, const float* l, const float* o,
                             int n_parts, long long rows, int d, float* out,
-                            float* m_out, float* l_out, cudaStream_t st) {
+                            float* m_out, float* l_out, cudaStream_t st,
+                            long long part_stride) {
   if (rows == 0) return cudaSuccess;
-  k_combine<<<(unsigned)rows, 128, (size_t)n_parts * sizeof(float), st>>>(m, l, o, n_parts, rows,
-                                                                          d, out, m_out, l_out);
+  const long long sm = part_stride ? part_stride : rows;
+  const long long so = part_stride ? part_stride : rows * d;
+  k_combine<<<(unsigned)rows, 128, (size_t)n_parts * sizeof(float), st>>>(
+      m, l, o, n_parts, rows, d, sm, so, out, m_out, l_out);
   count_launch();
   return cudaGetLastError();
 }

@@ -89,9 +89,12 @@ __device__ __forceinline__ float block_reduce(float v, bool is_max, float* red) 
 }
 
 // Log-sum-exp merge (device), parts-major.
+// part_stride 0: m, l [parts][rows], o [parts][rows][d]; otherwise part p's
+// m, l and o rows start at p * part_stride (packed exchange buffers).
 cudaError_t run_lse_combine(const float* m, const float* l, const float* o,
                             int n_parts, long long rows, int d, float* out,
-                            float* m_out, float* l_out, cudaStream_t st);
+                            float* m_out, float* l_out, cudaStream_t st,
+                            long long part_stride = 0);
 
 // ---- encoders (encode.cu) -------------------------------------------------
 // Per slot: atoms fp64 [R][subs][L][2] -> screen tables.

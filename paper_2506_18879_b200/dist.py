@@ -2,7 +2,6 @@
 
 Each rank holds a contiguous range of every stream's tokens (boundaries on
 128-token tiles so packed records stay 32-B aligned), attends with
-cvq_cache_attention_partial -> (m, l, o) per row, and the partials of all
 ranks are all-gathered (NCCL over NVLink on GPUs; any torch.distributed
 backend works) and merged with the LSE combine kernel (cvq_lse_combine).
 """
@@ -54,3 +53,26 @@ def gather_partials(m, l, o, group=None):
         Lh.copy_(HL)
         O.copy_(HO)
     return M, Lh, O
+
+
+def packed_views(buf, rows, d):
+    """(m, l, o) views into one packed block buf [rows*(d+2)]."""
+    return buf[:rows], buf[rows:2 * rows], buf[2 * rows:].view(rows, d)
+
+
+def gather_packed(buf, group=None):
+    """All-gather this rank's packed block [rows*(d+2)] -> [world][rows*(d+2)]
+    in rank order (one collective), the input of cvq_lse_combine_packed."""
+    import torch
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    out = torch.empty((world, buf.numel()), dtype=buf.dtype, device=buf.device)
+    if dist.get_backend(group) == "nccl":
+        dist.all_gather_into_tensor(out, buf.contiguous(), group=group)
+    else:  # gloo: host tensors
+        hb = buf.contiguous().cpu()
+        HO = torch.empty((world, hb.numel()), dtype=hb.dtype)
+        dist.all_gather(list(HO.unbind(0)), hb, group=group)
+        out.copy_(HO)
+    return out

@@ -2,8 +2,10 @@
 
 Each rank takes its shard of every stream (paper_2506_18879_b200.dist
 .shard_plan), forms split-K partials (m, l, o) from the oracle's scores of
-its tokens, exchanges them with dist.gather_partials (the call bench.py makes
-over NCCL), and the LSE merge of the gathered partials must equal the
+its tokens into one packed block [m | l | o], exchanges the blocks with
+dist.gather_packed (the single collective bench.py makes over NCCL; the
+three-tensor gather_partials must agree), and the LSE merge of the gathered
+partials must equal the
 oracle's unsharded fused_attention.  The merge restated here in numpy is the
 algebra of k_combine (attn.cu); the kernel itself is covered on the GPU.
 """
@@ -42,7 +44,7 @@ def _worker(rank, world, port, result_dir):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         from oracle.oracle import KQ, Oracle
-        from paper_2506_18879_b200.dist import gather_partials
+        from paper_2506_18879_b200.dist import gather_packed, gather_partials, packed_views
         from tests import fixtures as fx
 
         P = Oracle("port")
@@ -60,9 +62,9 @@ def _worker(rank, world, port, result_dir):
                 rows.append((atoms, a, b, bits, vrows, q))
         lo, hi = shard_plan(n, world)[rank]
         t = n - 1
-        m = np.zeros(len(rows), np.float32)
-        l = np.zeros(len(rows), np.float32)
-        o = np.zeros((len(rows), 16), np.float32)
+        pk = torch.zeros(len(rows) * (16 + 2))
+        mt, lt, ot = packed_views(pk, len(rows), 16)
+        m, l, o = mt.numpy(), lt.numpy(), ot.numpy()  # views: writes land in pk
         for i, (atoms, a, b, bits, vrows, q) in enumerate(rows):
             sc = P.fused_scores(kq, atoms, a, b, bits, vrows, q, t)[lo:hi]
             if hi > lo:
@@ -70,9 +72,13 @@ def _worker(rank, world, port, result_dir):
                 p = np.exp(sc - m[i])
                 l[i] = p.sum()
                 o[i] = ((p @ bits[lo:hi]) @ vrows) / l[i]
-        M, Lh, O = gather_partials(torch.from_numpy(m), torch.from_numpy(l), torch.from_numpy(o))
-        out = lse_merge(M.numpy().astype(np.float64), Lh.numpy().astype(np.float64),
-                        O.numpy().astype(np.float64))
+        parts = gather_packed(pk).numpy().astype(np.float64)  # [world][rows*(d+2)]
+        R = len(rows)
+        M, Lh, O = parts[:, :R], parts[:, R:2 * R], parts[:, 2 * R:].reshape(world, R, 16)
+        M3, L3, O3 = gather_partials(mt, lt, ot)
+        assert np.array_equal(M3.numpy(), M.astype(np.float32))
+        assert np.array_equal(O3.numpy(), O.astype(np.float32))
+        out = lse_merge(M, Lh, O)
         if rank == 0:
             worst = 0.0
             for i, (atoms, a, b, bits, vrows, q) in enumerate(rows):

@@ -460,3 +460,60 @@ def test_fused_kernel_matches_split_kernels(G, n, monkeypatch):
     monkeypatch.setenv("CVQ_ENABLE_FUSED", "1")
     fused = c.attention(q)
     assert fx.rel_err(fused, split) <= 1e-5
+
+
+@pytest.mark.parametrize("keys", ["fp32", "tc"])
+def test_context_shards_merge_to_full_cache(G, keys):
+    """SURVEY.md 8e on one GPU: the context split over 3 caches (global
+    positions via position_offset), each attention_partial written into a
+    packed [m | l | o] block, merged by cvq_lse_combine_packed, equals the
+    unsharded cache's attention and the oracle (3 ranks' worth of shards;
+    the 4th block is an empty shard, l = 0, which the merge skips)."""
+    import torch
+    from paper_2506_18879_b200.dist import packed_views, shard_plan
+    kq = KQ(128, 64, 64, 11)
+    nc, n, H, Gq = 128, 1000, 2, 4
+    rng = P.rng(777)
+    books = [(rng.normal(2 * kq.n_atoms, 0.3), rng.normal(nc * 128, 1 / 16).reshape(nc, 128))
+             for _ in range(H)]
+    codes = []
+    for h in range(H):
+        a, b = fx.random_key_codes(kq, n, rng=rng)
+        codes.append((a, b, fx.random_value_codes(nc, n, rng=rng)))
+    q = rng.normal(H * Gq * 128).reshape(1, 1, H * Gq, 128).astype(np.float32)
+    t = n - 1 + 55
+    plan = shard_plan(n, 4)  # last shard empty for n = 1000
+    rows, d = H * Gq, 128
+    parts = torch.zeros((len(plan), rows * (d + 2)), device="cuda")
+    full = G.QuantizedKVCache(kq, nc, n_kv_heads=H, q_per_kv=Gq, capacity=n, keys=keys)
+    for h in range(H):
+        full.set_key_codebook(0, h, books[h][0])
+        full.set_value_quantizer(0, h, books[h][1])
+        a, b, bits = codes[h]
+        full.import_stream(0, 0, h, P.pack_key_codes(kq, a, b), P.pack_value_codes(bits), n)
+    want = full.attention(q, t).reshape(rows, d)
+    qd = torch.from_numpy(q.reshape(rows, d)).cuda()
+    for r, (lo, hi) in enumerate(plan):
+        if hi == lo:
+            continue  # empty shard: its block stays m = l = 0
+        c = G.QuantizedKVCache(kq, nc, n_kv_heads=H, q_per_kv=Gq, capacity=hi - lo,
+                               position_offset=lo, keys=keys)
+        for h in range(H):
+            c.set_key_codebook(0, h, books[h][0])
+            c.set_value_quantizer(0, h, books[h][1])
+            a, b, bits = codes[h]
+            kr = lambda x: x.reshape(n, -1)[lo:hi].reshape(-1)  # noqa: E731
+            c.import_stream(0, 0, h, P.pack_key_codes(kq, kr(a), kr(b)),
+                            P.pack_value_codes(bits.reshape(n, nc)[lo:hi]), hi - lo)
+        m, l, o = packed_views(parts[r], rows, d)
+        c.attention_partial(qd, m, l, o, t)
+    out = torch.empty(rows, d, device="cuda")
+    G.lse_combine_packed(parts, rows, d, out)
+    got = out.cpu().numpy()
+    assert fx.rel_err(got, want) <= 1e-5
+    for h in range(H):
+        a, b, bits = codes[h]
+        for j in range(Gq):
+            ref, _, _ = P.fused_attention(kq, books[h][0], a, b, bits, books[h][1],
+                                          q[0, 0, h * Gq + j].astype(np.float64), t)
+            assert fx.rel_err(got[h * Gq + j], ref) <= (1e-4 if keys == "fp32" else 1e-3)
