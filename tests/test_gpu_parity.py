@@ -517,3 +517,36 @@ def test_context_shards_merge_to_full_cache(G, keys):
             ref, _, _ = P.fused_attention(kq, books[h][0], a, b, bits, books[h][1],
                                           q[0, 0, h * Gq + j].astype(np.float64), t)
             assert fx.rel_err(got[h * Gq + j], ref) <= (1e-4 if keys == "fp32" else 1e-3)
+
+
+@pytest.mark.parametrize("preset,n", [("1bit", 300), ("1bit", 4099), ("2bit", 777)])
+@pytest.mark.parametrize("keys", ["fp16", "tc"])
+def test_mha_one_query_head_per_stream(G, preset, n, keys):
+    """G = 1 (one query head per KV stream, MHA-shaped): the G = 1 variants
+    of the tcgen05 kernel (select-based reduce-scatter) and of the fp16
+    CUDA-core kernel vs the oracle, 3 streams."""
+    kq = KQ(128, 64, 64, 11 if preset == "1bit" else 21)
+    nc = 128 if preset == "1bit" else 256
+    H = 3
+    rng = P.rng(31 + n)
+    c = G.QuantizedKVCache(kq, nc, n_kv_heads=H, q_per_kv=1, capacity=n, keys=keys)
+    streams = []
+    for h in range(H):
+        atoms = rng.normal(2 * kq.n_atoms, 0.3)
+        vrows = rng.normal(nc * 128, 1 / 16).reshape(nc, 128)
+        a, b = fx.random_key_codes(kq, n, rng=rng)
+        bits = fx.random_value_codes(nc, n, rng=rng)
+        c.set_key_codebook(0, h, atoms)
+        c.set_value_quantizer(0, h, vrows)
+        c.import_stream(0, 0, h, P.pack_key_codes(kq, a, b), P.pack_value_codes(bits), n)
+        streams.append((atoms, vrows, a, b, bits))
+    q = rng.normal(H * 128).reshape(1, 1, H, 128).astype(np.float32)
+    t = n - 1 + 3
+    out = c.attention(q, t)
+    worst = 0.0
+    for h in range(H):
+        atoms, vrows, a, b, bits = streams[h]
+        want, _, _ = P.fused_attention(kq, atoms, a, b, bits, vrows,
+                                       q[0, 0, h].astype(np.float64), t)
+        worst = max(worst, fx.rel_err(out[0, 0, h], want))
+    assert worst <= 1e-3, worst
