@@ -1,5 +1,3 @@
-for v in 0 1 0 1; do
-if [ $v = 1 ]; then export CVQ_F2_NOALIAS=1; else unset CVQ_F2_NOALIAS; fi
-timeout 300 python bench.py --config c3 --steps 10 --warmup 3 --no-cpu-baseline --no-prefill --no-e2e > gpurun_out/b.log 2>&1
-echo "noalias=$v $(grep -o '"ms_per_step": [0-9.]*\|"kernel_ms": [0-9.]*' gpurun_out/b.log | tr '\n' ' ')"
-done
+timeout 600 python -m pytest tests/test_gpu_parity.py tests/test_golden.py -m gpu -q -x -k "encode or prefill or golden or 2bit" > gpurun_out/pt.log 2>&1; echo t=$?; tail -1 gpurun_out/pt.log
+timeout 300 python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/b.log 2>&1; echo b=$?
+grep -o '"token_heads_per_s": [0-9.e+]*\|"c4_projected_s": [0-9.]*' gpurun_out/b.log
