@@ -220,7 +220,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_tc_score(TcArgs a) {
   extern __shared__ __align__(1024) unsigned char smem[];
   unsigned char* stages = smem;                                                // [kStages][A|B]
   float* red = reinterpret_cast<float*>(stages + kStages * kStageBytes);  // [slot][4][kChunk][G]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(red + kEpiSlots * 4 * kChunk * G);
+  // raw key-code windows of the NEXT tile, prefetched by the producers with
+  // cp.async while the current tile is produced: [kTok][NW] words
+  uint64_t* wbuf = reinterpret_cast<uint64_t*>(red + kEpiSlots * 4 * kChunk * G);
+  uint64_t* bars = wbuf + (size_t)kTok * NW;
   uint64_t* full = bars;
   uint64_t* empty = bars + kStages;
   uint64_t* dfull = bars + 2 * kStages;
@@ -394,18 +397,36 @@ __global__ void __launch_bounds__(kThreads, 1) k_tc_score(TcArgs a) {
     // ============ one-hot producers: thread p owns tile tokens p + 128 i ====
     // A stage's previous user was the same thread 4 steps earlier (same token
     // slot), so the entry to clear is recomputed from the code windows (this
-    // tile's, or the previous tile's for the first kStages steps).
+    // tile's, or the previous tile's for the first kStages steps).  The next
+    // tile's code words are prefetched into smem during this tile.
     constexpr int TPT = kTok / (kProdWarps * 32);  // tokens per producer thread
     const int p = tid - kEpiWarps * 32;
     uint64_t w[TPT][NW], wp[TPT][NW];  // code windows (current, previous tile)
-    auto load = [&](int s, long long tok, uint64_t* wv) {
+    // the raw words of this thread's tokens of a tile -> wbuf (cp.async; a
+    // token past the end reads token 0's record, as the epilogue ignores it)
+    auto issue = [&](int s, long long ti, int valid) {
       const uint64_t* kw = a.kpool + (size_t)s * a.kstride;
-      const unsigned long long bit = (unsigned long long)tok * (NSTEP * 6);
-      const unsigned long long w0 = bit >> 6;
-      const uint32_t off = (uint32_t)(bit & 63u);
+#pragma unroll
+      for (int u = 0; u < TPT; ++u) {
+        const int t = p + kProdWarps * 32 * u;
+        const long long tok = ti + (t < valid ? t : 0);
+        const unsigned long long w0 = ((unsigned long long)tok * (NSTEP * 6)) >> 6;
+#pragma unroll
+        for (int i = 0; i < NW; ++i)
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(su32(wbuf + t * NW + i)),
+                       "l"(kw + w0 + i)
+                       : "memory");
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    // windows shifted so a token's code q sits at bit 6q
+    auto fetch = [&](long long ti, int valid, int u, uint64_t* wv) {
+      const int t = p + kProdWarps * 32 * u;
+      const long long tok = ti + (t < valid ? t : 0);
+      const uint32_t off = (uint32_t)(((unsigned long long)tok * (NSTEP * 6)) & 63u);
       uint64_t raw[NW];
 #pragma unroll
-      for (int i = 0; i < NW; ++i) raw[i] = __ldg(kw + w0 + i);
+      for (int i = 0; i < NW; ++i) raw[i] = wbuf[t * NW + i];
 #pragma unroll
       for (int i = 0; i + 1 < NW; ++i)
         wv[i] = off ? (raw[i] >> off) | (raw[i + 1] << (64u - off)) : raw[i];
@@ -421,15 +442,20 @@ __global__ void __launch_bounds__(kThreads, 1) k_tc_score(TcArgs a) {
     TileIter it;
     uint32_t g = 0;
     bool have_prev = false;
-    for (bool ok = it.first(a); ok; ok = it.next(a)) {
+    bool ok = it.first(a);
+    if (ok) issue(it.s, it.ti, it.valid());
+    while (ok) {
       const int valid = it.valid();
+      asm volatile("cp.async.wait_all;" ::: "memory");  // this thread's words of this tile
 #pragma unroll
       for (int u = 0; u < TPT; ++u) {
-        const int t = p + kProdWarps * 32 * u;
 #pragma unroll
         for (int i = 0; i < NW; ++i) wp[u][i] = w[u][i];
-        load(it.s, it.ti + (t < valid ? t : 0), w[u]);
+        fetch(it.ti, valid, u, w[u]);
       }
+      TileIter nx = it;  // prefetch the next tile's words behind this tile's steps
+      const bool okn = nx.next(a);
+      if (okn) issue(nx.s, nx.ti, nx.valid());
       // kPGroup steps per proxy fence + arrival round (NSTEP is even)
 #pragma unroll
       for (int q0 = 0; q0 < NSTEP; q0 += kPGroup) {
@@ -455,6 +481,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_tc_score(TcArgs a) {
         g += kPGroup;
       }
       have_prev = true;
+      it = nx;
+      ok = okn;
     }
   } else if (warp == kMmaWarp) {
     // ============ tcgen05.mma issuer: the whole warp walks the schedule (so
@@ -515,7 +543,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_tc_score(TcArgs a) {
 
 template <int R, int G>
 cudaError_t launch_tc(const TcArgs& a, cudaStream_t st) {
-  const size_t sm = tc_smem_bytes(G);
+  const size_t sm = tc_smem_bytes(G, R);
   static size_t done = 0;
   if (sm > done) {
     cudaError_t e = cudaFuncSetAttribute(k_tc_score<R, G>,
@@ -534,8 +562,9 @@ cudaError_t launch_tc(const TcArgs& a, cudaStream_t st) {
 
 }  // namespace
 
-size_t tc_smem_bytes(int G) {
-  return (size_t)kStages * kStageBytes + kEpiSlots * 4 * kChunk * G * 4 +
+size_t tc_smem_bytes(int G, int R) {
+  const int nw = (2 * R * 6 + 60 + 63) / 64 + 1;  // = NW of k_tc_score<R, G>
+  return (size_t)kStages * kStageBytes + kEpiSlots * 4 * kChunk * G * 4 + (size_t)kTok * nw * 8 +
          (2 * kStages + 4) * 8 + 16;
 }
 

@@ -57,7 +57,7 @@ cudaError_t run_attention(const AttnJob& job, const float* q, float* out,
                           cudaStream_t st, cudaEvent_t* prof = nullptr);
 
 // tcgen05 one-hot-MMA score kernel (attn_tc.cu).
-size_t tc_smem_bytes(int G);
+size_t tc_smem_bytes(int G, int R);
 int tc_blocks(int R);
 // A operand of the one-hot MMA for one slot: [R][side][16 KiB core-matrix
 // layout]; side b holds the rotated codebook (x <- -y, y <- x).
