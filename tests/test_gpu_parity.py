@@ -550,3 +550,38 @@ def test_mha_one_query_head_per_stream(G, preset, n, keys):
                                        q[0, 0, h].astype(np.float64), t)
         worst = max(worst, fx.rel_err(out[0, 0, h], want))
     assert worst <= 1e-3, worst
+
+
+def test_tc_at_bench_scale_vs_fp32_and_oracle(G):
+    """The default tcgen05 path at the C3 context length (128K tokens, 16
+    persistent work items per stream, 4 streams x 4 q heads): all rows vs the
+    fp32-codebook CUDA-core path on the same cache contents, and two rows vs
+    the oracle's fused_attention (bench-shape tolerance 1e-3)."""
+    kq = KQ(128, 64, 64, 11)
+    nc, n, H, Gq = 128, 131072, 4, 4
+    rng = P.rng(128)
+    caches = {k: G.QuantizedKVCache(kq, nc, n_kv_heads=H, q_per_kv=Gq, capacity=n, keys=k)
+              for k in ("tc", "fp32")}
+    streams = []
+    for h in range(H):
+        atoms = rng.normal(2 * kq.n_atoms, 0.3)
+        vrows = rng.normal(nc * 128, 1 / 16).reshape(nc, 128)
+        a, b = fx.random_key_codes(kq, n, rng=rng)
+        bits = fx.random_value_codes(nc, n, rng=rng)
+        kw, vw = P.pack_key_codes(kq, a, b), P.pack_value_codes(bits)
+        for c in caches.values():
+            c.set_key_codebook(0, h, atoms)
+            c.set_value_quantizer(0, h, vrows)
+            c.import_stream(0, 0, h, kw, vw, n)
+        streams.append((atoms, vrows, a, b, bits))
+    q = rng.normal(H * Gq * 128).reshape(1, 1, H * Gq, 128).astype(np.float32)
+    t = n - 1
+    out_tc = caches["tc"].attention(q, t)
+    out_32 = caches["fp32"].attention(q, t)
+    assert fx.rel_err(out_tc, out_32) <= 1e-3
+    for h, j in ((0, 0), (H - 1, Gq - 1)):
+        atoms, vrows, a, b, bits = streams[h]
+        want, _, _ = P.fused_attention(kq, atoms, a, b, bits, vrows,
+                                       q[0, 0, h * Gq + j].astype(np.float64), t)
+        assert fx.rel_err(out_tc[0, 0, h * Gq + j], want) <= 1e-3
+        assert fx.rel_err(out_32[0, 0, h * Gq + j], want) <= 1e-4
