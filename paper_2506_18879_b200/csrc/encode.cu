@@ -33,6 +33,9 @@ namespace cvq {
 // rounding of the screen and of the reference sum is ~4*(2g+4)*2^-53 of that
 // scale (< 6e-14 at g = 64); 1e-11 leaves a ~90x safety factor.
 constexpr double kMarginRel = 1e-11;
+// fp32 screen: worst-case error 3 * 2^-24 of scale^2 per value (see the
+// table kernel), 3.6e-7 pair to pair; 4e-6 leaves an 11x safety factor.
+constexpr double kMarginRel32 = 4e-6;
 
 // ---------------------------------------------------------------- tables
 // base[a][b] = |u_a|^2 + |v_b|^2 + 2 u_a.v_b per (slot, round, group) and
@@ -118,16 +121,26 @@ __device__ __forceinline__ void warp_argmin(double& v, int& c) {
 
 // Exact search over all pairs (or those whose screen value is <= thr when
 // use_thr) for one token; U may be shared or global.
-__device__ int exact_search(const double* p, const double2* U, int L, int gsz,
-                            const double* B, const double* PU, const double* PV, bool use_thr,
-                            double thr) {
+__device__ __forceinline__ double screen_val(const double* B, const double* PU, const double* PV,
+                                             int L, int a, int b) {
+  return B[(size_t)a * L + b] - 2.0 * PU[a] - 2.0 * PV[b];
+}
+// fp32 screen: (B - 2 pu) by one FMA, then - 2 pv (2 pv exact): two roundings
+__device__ __forceinline__ float screen_val(const float* B, const float* PU, const float* PV, int L,
+                                            int a, int b) {
+  return fmaf(-2.f, PU[a], B[(size_t)a * L + b]) - 2.f * PV[b];
+}
+
+template <class T>
+__device__ int exact_search(const double* p, const double2* U, int L, int gsz, const T* B,
+                            const T* PU, const T* PV, bool use_thr, T thr) {
   const int lane = threadIdx.x & 31;
   double best = INFINITY;
   int bc = 0x7fffffff;
   for (int c = lane; c < L * L; c += 32) {
     const int a = c / L, b = c % L;
     if (use_thr) {
-      const double sc = B[(size_t)a * L + b] - 2.0 * PU[a] - 2.0 * PV[b];
+      const T sc = screen_val(B, PU, PV, L, a, b);
       if (!(sc <= thr)) continue;
     }
     const double d = exact_dist(p, U, L, gsz, a, b);
@@ -160,6 +173,9 @@ k_encode_keys_table(Geom g, int n_slots, const double* __restrict__ atoms,
   double* P = B + (size_t)g.L * g.L;                    // [kEncTok][d]
   double* PU = P + (size_t)kEncTok * g.d;               // [warps][L]
   double* PV = PU + (size_t)kEncWarps * g.L;            // [warps][L]
+  float* Bf = reinterpret_cast<float*>(PV + (size_t)kEncWarps * g.L);  // [L][L] fp32 screen table
+  float* PUf = Bf + (size_t)g.L * g.L;                  // [warps][L]
+  float* PVf = PUf + (size_t)kEncWarps * g.L;           // [warps][L]
   const int s = blockIdx.y, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const long long i0 = (long long)blockIdx.x * kEncTok;
   const int nt = (int)min((long long)kEncTok, n - i0);
@@ -174,11 +190,17 @@ k_encode_keys_table(Geom g, int n_slots, const double* __restrict__ atoms,
                           ((size_t)(slot * g.R + r) * g.subs + (size_t)grp * gs) * L;
       for (int e = tid; e < gs * L; e += blockDim.x) U[e] = Ug[e];
       const double* Bg = base + ((size_t)(slot * g.R + r) * g.groups + grp) * L * L;
-      for (int e = tid; e < L * L; e += blockDim.x) B[e] = Bg[e];
+      for (int e = tid; e < L * L; e += blockDim.x) {
+        const double bv = Bg[e];
+        B[e] = bv;
+        Bf[e] = (float)bv;
+      }
       const double mn = maxnorm[(size_t)(slot * g.R + r) * g.groups + grp];
       __syncthreads();
       double* pu = PU + warp * L;
       double* pv = PV + warp * L;
+      float* puf = PUf + warp * L;
+      float* pvf = PVf + warp * L;
       for (int tk = warp; tk < nt; tk += kEncWarps) {
         double* p = P + (size_t)tk * g.d + grp * w2;
         for (int l = lane; l < L; l += 32) {
@@ -191,14 +213,59 @@ k_encode_keys_table(Geom g, int n_slots, const double* __restrict__ atoms,
           }
           pu[l] = su;
           pv[l] = sv;
+          puf[l] = (float)su;
+          pvf[l] = (float)sv;
         }
         double pn = 0.0;
         for (int e = lane; e < w2; e += 32) pn = fma(p[e], p[e], pn);
         for (int o = 16; o; o >>= 1) pn += __shfl_xor_sync(0xffffffffu, pn, o);
         __syncwarp();
         int chosen;
+        const double scale = sqrt(pn) + 2.0 * mn;
+        const double scale2 = scale * scale * fmax(1.0, w2 / 128.0);
         if (!(pn < 1e300) || !(mn < 1e150)) {
           chosen = exact_search(p, U, L, gs, B, pu, pv, false, 0.0);
+        } else if (scale2 > 1e-30 && scale2 < 1e30) {
+          // fp32 screen (twice the pair rate of fp64).  Each screen value is
+          // within 3 * 2^-24 * scale^2 of the exact shifted distance (inputs
+          // rounded once to fp32, two fp32 roundings; |B| + 2|pu| + 2|pv| <=
+          // scale^2), so a pair-to-pair error below 3.6e-7 scale^2: with the
+          // 4e-6 margin every pair that can be the reference argmin is
+          // re-checked exactly whenever the screen is not decisive.
+          float b1 = INFINITY, b2 = INFINITY;
+          int c1 = 0x7fffffff;
+          for (int b = lane; b < L; b += 32) {
+            const float t2 = 2.f * pvf[b];
+            for (int a = 0; a < L; ++a) {
+              const float sc = fmaf(-2.f, puf[a], Bf[a * L + b]) - t2;
+              const int c = a * L + b;
+              if (sc < b1 || (sc == b1 && c < c1)) {
+                b2 = b1;
+                b1 = sc;
+                c1 = c;
+              } else if (sc < b2) {
+                b2 = sc;
+              }
+            }
+          }
+          float gb = b1;
+          int gc = c1;
+          for (int o = 16; o; o >>= 1) {
+            const float v2 = __shfl_xor_sync(0xffffffffu, gb, o);
+            const int c2 = __shfl_xor_sync(0xffffffffu, gc, o);
+            if (v2 < gb || (v2 == gb && c2 < gc)) {
+              gb = v2;
+              gc = c2;
+            }
+          }
+          float ru = (c1 == gc) ? b2 : b1;
+          for (int o = 16; o; o >>= 1) ru = fminf(ru, __shfl_xor_sync(0xffffffffu, ru, o));
+          const float margin = (float)(kMarginRel32 * scale2);
+          if (ru > gb + margin) {
+            chosen = gc;
+          } else {
+            chosen = exact_search(p, U, L, gs, Bf, puf, pvf, true, gb + margin);
+          }
         } else {
           // single pass: lane-local best and runner-up, then warp merge
           double b1 = INFINITY, b2 = INFINITY;
@@ -223,8 +290,7 @@ k_encode_keys_table(Geom g, int n_slots, const double* __restrict__ atoms,
           // runner-up over the warp: every lane's b2, plus other lanes' b1
           double ru = (c1 == gc) ? b2 : b1;
           for (int o = 16; o; o >>= 1) ru = fmin(ru, __shfl_xor_sync(0xffffffffu, ru, o));
-          const double scale = sqrt(pn) + 2.0 * mn;
-          const double margin = kMarginRel * scale * scale * fmax(1.0, w2 / 128.0);
+          const double margin = kMarginRel * scale2;
           if (ru > gb + margin) {
             chosen = gc;
           } else {
@@ -268,7 +334,7 @@ k_encode_keys_brute(Geom g, int n_slots, const double* __restrict__ atoms,
       const double2* U = reinterpret_cast<const double2*>(atoms) +
                          ((size_t)(slot * g.R + r) * g.subs + (size_t)grp * g.g) * g.L;
       double* pg = p + grp * 2 * g.g;
-      const int c = exact_search(pg, U, g.L, g.g, nullptr, nullptr, nullptr, false, 0.0);
+      const int c = exact_search<double>(pg, U, g.L, g.g, nullptr, nullptr, nullptr, false, 0.0);
       const int ca = c / g.L, cb = c % g.L;
       if (lane == 0) {
         const size_t idx = ((size_t)s * n + i) * (g.R * g.groups) + (size_t)r * g.groups + grp;
@@ -436,7 +502,8 @@ k_encode_keys_small(Geom g, int n_slots, const double* __restrict__ atoms,
 
 static size_t table_smem(const Geom& g) {
   return sizeof(double) * (2 * (size_t)g.g * g.L + (size_t)g.L * g.L + (size_t)kEncTok * g.d +
-                           2 * (size_t)kEncWarps * g.L);
+                           2 * (size_t)kEncWarps * g.L) +
+         sizeof(float) * ((size_t)g.L * g.L + 2 * (size_t)kEncWarps * g.L);
 }
 
 cudaError_t run_encode_keys(const Geom& g, int S, int n_slots, const KeyEncTables& tab,
