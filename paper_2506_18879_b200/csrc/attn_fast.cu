@@ -818,11 +818,8 @@ size_t f2_smem(const AttnJob& job, int chunk2) {
 }
 
 template <class K>
-cudaError_t set_smem(K kernel, size_t sm, size_t& done) {
-  if (sm <= done) return cudaSuccess;
-  cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  if (e == cudaSuccess) done = sm;
-  return e;
+cudaError_t set_smem(K kernel, size_t sm) {
+  return ensure_dyn_smem(reinterpret_cast<const void*>(kernel), sm);
 }
 
 template <int R, int G>
@@ -830,8 +827,7 @@ cudaError_t launch_f1(const FastArgs& a, int S, cudaStream_t st) {
   constexpr int JC = R <= 12 ? 32 : 16;
   constexpr int JS = 64 / JC;
   const size_t sm = f1_smem(R, JC, 8);
-  static size_t done = 0;
-  cudaError_t e = set_smem(k_fast_score<R, JC, G>, sm, done);
+  cudaError_t e = set_smem(k_fast_score<R, JC, G>, sm);
   if (e != cudaSuccess) return e;
   dim3 grid((unsigned)((a.n + a.chunk - 1) / a.chunk), S * JS);
   k_fast_score<R, JC, G><<<grid, kF1Threads, sm, st>>>(a);
@@ -846,8 +842,7 @@ cudaError_t launch_f1h(const FastArgs& a, int S, cudaStream_t st) {
   constexpr int LPT = 16;
   constexpr int JS = 64 / (SPL * LPT);
   const size_t sm = f1_smem(R, SPL * LPT, 4);
-  static size_t done = 0;
-  cudaError_t e = set_smem(k_fast_score_h<R, SPL, LPT, G>, sm, done);
+  cudaError_t e = set_smem(k_fast_score_h<R, SPL, LPT, G>, sm);
   if (e != cudaSuccess) return e;
   dim3 grid((unsigned)((a.n + a.chunk - 1) / a.chunk), S * JS);
   k_fast_score_h<R, SPL, LPT, G><<<grid, kF1Threads, sm, st>>>(a);
@@ -857,8 +852,7 @@ cudaError_t launch_f1h(const FastArgs& a, int S, cudaStream_t st) {
 
 template <int NC, int G, int JS>
 cudaError_t launch_f2(const FastArgs& a, size_t sm, cudaStream_t st) {
-  static size_t done = 0;
-  cudaError_t e = set_smem(k_fast_value<NC, G, JS>, sm, done);
+  cudaError_t e = set_smem(k_fast_value<NC, G, JS>, sm);
   if (e != cudaSuccess) return e;
   dim3 grid((unsigned)((a.n + a.chunk2 - 1) / a.chunk2), a.S);
   k_fast_value<NC, G, JS><<<grid, kThreads, sm, st>>>(a);
@@ -1000,8 +994,7 @@ cudaError_t run_attention_fast(const AttnJob& job, const float* q, float* pm, fl
   if (fused_applies(job) && !scores_out) {
     const size_t sm = (size_t)11 * 64 * 64 * 4 + 2 * 24 * 11 * 8 + 2 * 2 * kTile * 8 +
                       (kF1Threads / 32) * 8 * 16 + (size_t)kTile * 32;
-    static size_t done = 0;
-    if ((e = set_smem(k_fast_attn_h<11>, sm, done)) != cudaSuccess) return e;
+    if ((e = set_smem(k_fast_attn_h<11>, sm)) != cudaSuccess) return e;
     const int nc = (int)((job.n + a.chunk - 1) / a.chunk);
     if (prof) cudaEventRecord(prof[0], st);
     k_fast_attn_h<11><<<dim3((unsigned)nc, job.S), kF1Threads, sm, st>>>(a);

@@ -544,13 +544,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_tc_score(TcArgs a) {
 template <int R, int G>
 cudaError_t launch_tc(const TcArgs& a, cudaStream_t st) {
   const size_t sm = tc_smem_bytes(G, R);
-  static size_t done = 0;
-  if (sm > done) {
-    cudaError_t e = cudaFuncSetAttribute(k_tc_score<R, G>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    if (e != cudaSuccess) return e;
-    done = sm;
-  }
+  cudaError_t e = ensure_dyn_smem(reinterpret_cast<const void*>(k_tc_score<R, G>), sm);
+  if (e != cudaSuccess) return e;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);

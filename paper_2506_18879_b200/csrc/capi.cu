@@ -10,6 +10,8 @@
 #include <algorithm>
 #include <cstring>
 #include <string>
+#include <map>
+#include <mutex>
 #include <vector>
 
 #include "../../include/cvq.h"
@@ -18,6 +20,21 @@
 #include "cvq_internal.cuh"
 
 namespace cvq {
+
+cudaError_t ensure_dyn_smem(const void* kernel, size_t bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, size_t> done;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lock(mu);
+  size_t& have = done[{kernel, dev}];
+  if (bytes <= have) return cudaSuccess;
+  e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e == cudaSuccess) have = bytes;
+  return e;
+}
+
 std::atomic<unsigned long long> g_launches{0};
 cudaError_t run_naive_attention(const AttnJob& job, const float* q, float* out, void* scratch,
                                 size_t scratch_bytes, cudaStream_t st);

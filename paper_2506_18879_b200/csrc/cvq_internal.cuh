@@ -173,6 +173,11 @@ cudaError_t run_unpack_keys(const Geom& g, const uint64_t* words, long long n,
 cudaError_t run_unpack_values(const Geom& g, const uint64_t* words,
                               long long n, uint8_t* bits, cudaStream_t st);
 
+// cudaFuncAttributeMaxDynamicSharedMemorySize is per (kernel, device): the
+// largest value set so far is remembered per pair (capi.cu), so a process
+// driving several GPUs raises it on each device.
+cudaError_t ensure_dyn_smem(const void* kernel, size_t bytes);
+
 // Global launch counter (bench.py gpu_launches).
 extern std::atomic<unsigned long long> g_launches;
 inline void count_launch(unsigned long long k = 1) { g_launches += k; }

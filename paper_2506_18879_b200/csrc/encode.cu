@@ -518,13 +518,8 @@ cudaError_t run_encode_keys(const Geom& g, int S, int n_slots, const KeyEncTable
     k_encode_keys_small<<<grid, kSmallThreads, sizeof(double) * (g.d + 2 * g.L), st>>>(
         g, n_slots, tab.atoms, tab.base, tab.maxnorm, keys, dtype, s_stride, n, a, b);
   } else if (tab.base != nullptr && sm <= 200 * 1024) {
-    static bool attr = false;
-    if (!attr) {
-      e = cudaFuncSetAttribute(k_encode_keys_table, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               220 * 1024);
-      if (e != cudaSuccess) return e;
-      attr = true;
-    }
+    e = ensure_dyn_smem(reinterpret_cast<const void*>(k_encode_keys_table), sm);
+    if (e != cudaSuccess) return e;
     dim3 grid((unsigned)((n + kEncTok - 1) / kEncTok), S);
     k_encode_keys_table<<<grid, kEncWarps * 32, sm, st>>>(g, n_slots, tab.atoms, tab.base,
                                                          tab.maxnorm, keys, dtype, s_stride, n,
@@ -619,8 +614,7 @@ static cudaError_t launch_values(const Geom& g, int S, int n_slots, const ValEnc
   const size_t sm = sizeof(double) * (size_t)TV * (g.d + g.hidden);
   cudaError_t e;
   if (sm > 48 * 1024) {
-    e = cudaFuncSetAttribute(k_encode_values<TV>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)sm);
+    e = ensure_dyn_smem(reinterpret_cast<const void*>(k_encode_values<TV>), sm);
     if (e != cudaSuccess) return e;
   }
   dim3 grid((unsigned)((n + TV - 1) / TV), S);
