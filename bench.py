@@ -160,6 +160,9 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"])
     ap.add_argument("--no-prefill", action="store_true")
+    ap.add_argument("--merge", default="nccl", choices=["nccl", "peer"],
+                    help="N>1 shard merge: one NCCL all-gather of packed partials + combine, or "
+                         "peer: symmetric-memory blocks read by the combine kernel over NVLink")
     ap.add_argument("--keys", default="tc", choices=["fp32", "fp16", "tc"],
                     help="score kernel: tc = tcgen05 one-hot MMA (fp16 codebook), fp16 / fp32 = "
                          "CUDA-core gather with that codebook precision; fp32 accumulation always")
@@ -232,9 +235,18 @@ def main():
     # this rank's partials (m, l, o) in one packed block -> one all-gather
     pk = torch.empty(rows * (d + 2), device="cuda")
     m_p, l_p, o_p = packed_views(pk, rows, d)
+    peer = None
+    if world > 1 and args.merge == "peer":
+        from paper_2506_18879_b200.dist import PeerMerge
+        peer = PeerMerge(rows, d)
+
     def step():
         if world == 1:
             cache.attention(q, t_q, out)
+        elif peer is not None:  # the combine kernel reads the peers' blocks over NVLink
+            m_v, l_v, o_v = peer.views()
+            cache.attention_partial(q, m_v, l_v, o_v, t_q)
+            peer.merge(out, G, ctx)
         else:
             cache.attention_partial(q, m_p, l_p, o_p, t_q)
             parts = gather_packed(pk)  # NCCL all-gather, 520 B/row
@@ -405,6 +417,7 @@ def main():
             "config": {"workload": args.config, "n_layers": layers, "n_seqs": B,
                        "n_kv_heads": H, "q_per_kv": Gq, "context": N, "key": [d, g, L, R],
                        "n_codes": nc, "parallelism": f"context-shard x{world}",
+                       "merge": args.merge if world > 1 else None,
                        "l2": "inputs (packed cache) larger than L2"},
             "kv_head_tokens_per_s": value * H, "roofline": roof, "clocks": clk.summary(),
             "gpu_launches": launches, "e2e": e2e, "cpu_baseline": cpu, "prefill": prefill,

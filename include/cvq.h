@@ -310,6 +310,14 @@ CVQ_API cvq_status cvq_lse_combine_packed(cvq_context* ctx, const float* parts,
                                           uint32_t n_parts, uint64_t rows, uint32_t d,
                                           float* out);
 
+/* Same merge with part p's packed block at parts[p] + offset (floats), parts
+ * a DEVICE array of device pointers.  The pointers may address peer GPUs'
+ * memory (symmetric / IPC buffers mapped over NVLink): the combine kernel
+ * then gathers the partials itself, with no separate collective. */
+CVQ_API cvq_status cvq_lse_combine_ptrs(cvq_context* ctx, const float* const* parts,
+                                        uint64_t offset, uint32_t n_parts, uint64_t rows,
+                                        uint32_t d, float* out);
+
 /* QuantizedKVCache::decode_step (cache.cpp:287-296): append k, v then attend
  * q at the new last position.  All buffers in `where`. */
 CVQ_API cvq_status cvq_cache_decode_step(cvq_cache* c, const void* k,

@@ -608,6 +608,16 @@ def lse_combine_packed(parts, rows, d, out, ctx=None):
                                        _p(out.data_ptr())))
 
 
+def lse_combine_ptrs(ptrs_dev, offset, n_parts, rows, d, out, ctx=None):
+    """ptrs_dev: device int64 tensor (or raw device address) of n_parts
+    pointers to packed [m | l | o] blocks (peer buffers allowed); part p's
+    block starts at ptrs[p] + offset floats -> out [rows][d]."""
+    ctx = ctx or default_context()
+    addr = ptrs_dev if isinstance(ptrs_dev, int) else ptrs_dev.data_ptr()
+    _check(_lib.cvq_lse_combine_ptrs(ctx.h, _p(addr), _u64(offset), _u32(n_parts), _u64(rows),
+                                     _u32(d), _p(out.data_ptr())))
+
+
 def lse_combine(m, l, o, out, ctx=None):
     """Device tensors m, l [P][rows], o [P][rows][d] -> out [rows][d]."""
     ctx = ctx or default_context()

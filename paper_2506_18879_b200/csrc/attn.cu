@@ -214,6 +214,48 @@ __global__ void k_combine(const float* __restrict__ m, const float* __restrict__
   }
 }
 
+// Same merge, part p's packed block [m | l | o] read through parts[p] + off:
+// the parts may live in peer GPUs' memory (symmetric / IPC buffers mapped
+// over NVLink), so the gather is the combine's own loads -- no collective.
+__global__ void k_combine_ptrs(const float* const* __restrict__ parts, long long off, int P,
+                               long long rows, int d, float* __restrict__ out) {
+  extern __shared__ float wsh[];  // [P]
+  __shared__ float red[33];
+  const long long row = blockIdx.x;
+  float M = -FLT_MAX;
+  for (int p = threadIdx.x; p < P; p += blockDim.x) {
+    const float* b = parts[p] + off;
+    if (b[rows + row] > 0.f) M = fmaxf(M, b[row]);
+  }
+  M = block_reduce(M, true, red);
+  float Ls = 0.f;
+  for (int p = threadIdx.x; p < P; p += blockDim.x) {
+    const float* b = parts[p] + off;
+    const float lp = b[rows + row];
+    const float wgt = lp > 0.f ? lp * expf(b[row] - M) : 0.f;
+    wsh[p] = wgt;
+    Ls += wgt;
+  }
+  const float Lsum = block_reduce(Ls, false, red);
+  for (int jd = threadIdx.x; jd < d; jd += blockDim.x) {
+    float acc = 0.f;
+    for (int p = 0; p < P; ++p) {
+      const float wgt = wsh[p];
+      if (wgt != 0.f) acc += parts[p][off + 2 * rows + row * d + jd] * wgt;
+    }
+    out[row * d + jd] = acc / Lsum;
+  }
+}
+
+cudaError_t run_lse_combine_ptrs(const float* const* parts, long long off, int n_parts,
+                                 long long rows, int d, float* out, cudaStream_t st) {
+  if (rows == 0) return cudaSuccess;
+  k_combine_ptrs<<<(unsigned)rows, 128, (size_t)n_parts * sizeof(float), st>>>(parts, off, n_parts,
+                                                                               rows, d, out);
+  count_launch();
+  return cudaGetLastError();
+}
+
 cudaError_t run_lse_combine(const float* m, const float* l, const float* o,
                             int n_parts, long long rows, int d, float* out,
                             float* m_out, float* l_out, cudaStream_t st,

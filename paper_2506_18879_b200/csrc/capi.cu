@@ -677,6 +677,16 @@ CVQ_API cvq_status cvq_lse_combine_packed(cvq_context* ctx, const float* parts, 
   return CVQ_OK;
 }
 
+CVQ_API cvq_status cvq_lse_combine_ptrs(cvq_context* ctx, const float* const* parts,
+                                        uint64_t offset, uint32_t n_parts, uint64_t rows,
+                                        uint32_t d, float* out) {
+  TRY(ctx_check(ctx));
+  if (!parts || !out || n_parts == 0) return fail(CVQ_EINVAL, "lse_combine: bad argument");
+  CU(run_lse_combine_ptrs(parts, (long long)offset, (int)n_parts, (long long)rows, (int)d, out,
+                          ctx->stream));
+  return CVQ_OK;
+}
+
 CVQ_API cvq_status cvq_cache_decode_step(cvq_cache* c, const void* k, const void* v, int kv_dtype,
                                          const float* q, float* out, int where) {
   if (!c) return fail(CVQ_EINVAL, "null cache");

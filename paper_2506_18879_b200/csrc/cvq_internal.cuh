@@ -66,6 +66,11 @@ size_t tc_codebook_elems(int R);
 cudaError_t run_tc_score(const AttnJob& job, const float* q, float* ps, int chunk,
                          cudaStream_t st);
 
+// LSE merge over packed blocks reached through a device array of pointers
+// (parts[p] + off), e.g. peers' symmetric-memory buffers over NVLink.
+cudaError_t run_lse_combine_ptrs(const float* const* parts, long long off, int n_parts,
+                                 long long rows, int d, float* out, cudaStream_t st);
+
 // Block-wide max / sum; every thread gets the result (contains barriers).
 __device__ __forceinline__ float block_reduce(float v, bool is_max, float* red) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;

@@ -76,3 +76,41 @@ def gather_packed(buf, group=None):
         dist.all_gather(list(HO.unbind(0)), hb, group=group)
         out.copy_(HO)
     return out
+
+
+class PeerMerge:
+    """Context-shard merge over NVLink peer memory: no collective on the data
+    path.  Each rank's cvq_cache_attention_partial writes its packed
+    [m | l | o] block into a symmetric-memory buffer (torch symmetric memory,
+    mapped on every peer); a device-side barrier publishes the blocks; each
+    rank's combine kernel then reads all peers' blocks itself
+    (cvq_lse_combine_ptrs).  Double-buffered by step parity: a rank writes
+    step k+2's block only after the barrier of step k+1, which every peer
+    passes only after finishing its combine of step k (stream order)."""
+
+    def __init__(self, rows, d, group=None):
+        import torch
+        import torch.distributed as dist
+        import torch.distributed._symmetric_memory as symm
+
+        grp = group or dist.group.WORLD
+        self.rows, self.d = rows, d
+        self.block = rows * (d + 2)
+        self.buf = symm.empty(2 * self.block, dtype=torch.float32, device="cuda")
+        self.buf.zero_()
+        self.hdl = symm.rendezvous(self.buf, grp.group_name)
+        self.world = self.hdl.world_size
+        self.ptrs = self.hdl.buffer_ptrs_dev  # device array of the peers' buffer addresses
+        self.step = 0
+
+    def views(self):
+        """(m, l, o) of this step's local block."""
+        slot = self.step & 1
+        return packed_views(self.buf[slot * self.block:(slot + 1) * self.block], self.rows, self.d)
+
+    def merge(self, out, G, ctx):
+        """Publish this step's block and merge all ranks' blocks into out."""
+        slot = self.step & 1
+        self.hdl.barrier(channel=0)
+        G.lse_combine_ptrs(self.ptrs, slot * self.block, self.world, self.rows, self.d, out, ctx)
+        self.step += 1

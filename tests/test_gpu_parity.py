@@ -585,3 +585,55 @@ def test_tc_at_bench_scale_vs_fp32_and_oracle(G):
                                        q[0, 0, h * Gq + j].astype(np.float64), t)
         assert fx.rel_err(out_tc[0, 0, h * Gq + j], want) <= 1e-3
         assert fx.rel_err(out_32[0, 0, h * Gq + j], want) <= 1e-4
+
+
+def test_lse_combine_ptrs_over_separate_buffers(G):
+    """cvq_lse_combine_ptrs reads each part's packed block through a device
+    pointer table (peers' symmetric buffers in the multi-GPU path); here the
+    'peers' are separate local buffers with an offset, one part empty.  Must
+    equal the packed contiguous merge bit for bit."""
+    import torch
+    rows, d, Pn, off = 96, 128, 4, 7 * 1024
+    rng = np.random.default_rng(3)
+    blocks = []
+    for p in range(Pn):
+        b = torch.zeros(off + rows * (d + 2), device="cuda")
+        blk = b[off:]
+        blk[:rows] = torch.from_numpy(rng.normal(0, 3, rows).astype(np.float32)).cuda()
+        blk[rows:2 * rows] = 0.0 if p == 2 else torch.from_numpy(
+            rng.uniform(0.5, 4, rows).astype(np.float32)).cuda()
+        blk[2 * rows:] = torch.from_numpy(rng.normal(0, 1, rows * d).astype(np.float32)).cuda()
+        blocks.append(b)
+    ptrs = torch.tensor([b.data_ptr() for b in blocks], dtype=torch.int64, device="cuda")
+    out = torch.empty(rows, d, device="cuda")
+    G.lse_combine_ptrs(ptrs, off, Pn, rows, d, out)
+    packed = torch.stack([b[off:] for b in blocks])
+    want = torch.empty(rows, d, device="cuda")
+    G.lse_combine_packed(packed, rows, d, want)
+    torch.cuda.synchronize()
+    assert torch.equal(out, want)
+
+
+def test_peer_merge_world_one_roundtrip(G, tmp_path):
+    """dist.PeerMerge on a real symmetric-memory buffer (world size 1 on one
+    GPU): rendezvous, device barrier and the pointer-table combine, two steps
+    (both buffer parities); the merge of one block is its normalised o."""
+    import torch
+    import torch.distributed as dist
+    from paper_2506_18879_b200.dist import PeerMerge
+    if not dist.is_initialized():
+        dist.init_process_group("nccl", init_method=f"file://{tmp_path}/pg", rank=0, world_size=1,
+                                device_id=torch.device("cuda", 0))
+    try:
+        pm = PeerMerge(64, 128)
+        for step in range(2):
+            m, l, o = pm.views()
+            m.copy_(torch.randn(64, device="cuda"))
+            l.copy_(torch.rand(64, device="cuda") + 0.5)
+            o.copy_(torch.randn(64, 128, device="cuda"))
+            out = torch.empty(64, 128, device="cuda")
+            pm.merge(out, G, None)
+            torch.cuda.synchronize()
+            assert torch.allclose(out, o, rtol=1e-6, atol=1e-6), step
+    finally:
+        dist.destroy_process_group()
