@@ -229,7 +229,9 @@ def main():
                 pool[s, nw - 1] &= (1 << tail) - 1
     cache.set_length(n_local)
     torch.cuda.synchronize()
-    q = torch.randn(B, layers, H * Gq, d, device="cuda", generator=gen)
+    # the query is the same on every rank (broadcast); only the context shards differ
+    qgen = torch.Generator(device="cuda").manual_seed(7)
+    q = torch.randn(B, layers, H * Gq, d, device="cuda", generator=qgen)
     out = torch.empty_like(q)
     t_q = N - 1  # global query position (last cached token)
     # this rank's partials (m, l, o) in one packed block -> one all-gather
