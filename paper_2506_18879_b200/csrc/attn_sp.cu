@@ -1,0 +1,595 @@
+// attn_sp.cu -- 2:4-sparse tcgen05 score kernel for the 1-bit head preset
+// (R = 11 rounds, 64 levels, d = 128, one key group).  The key decode is the
+// same one-hot GEMM as attn_tc.cu, turned so the one-hot is the A operand:
+//
+//   D[t, n] += A_{r,s}[t, l] * B_r[n, l]     (M = 128 tokens, N = 64, K = 64)
+//
+// A one-hot row has a single non-zero per 64 levels, so it is 2:4 sparse and
+// runs on tcgen05.mma.sp (K = 32 logical per instruction, half the physical
+// MACs of a dense K = 32).  Measured on B200 (profiles/r01_umma_sparse_*):
+// sparse M128 x N64 with A in TMEM issues every 32 clk from ONE thread with
+// warp-uniform operands, twice the dense rate, and a 64-row B slice (4 KiB
+// per K = 32) is exactly the 128 B/clk the tensor core reads from smem.
+//
+// * B_r = the round-r codebook as two 64-row blocks, X (rows j: U[r,j,l].x)
+//   and Y (rows 64 + j: U[r,j,l].y), K-major fp16 -- 16 KiB per round, all
+//   11 rounds RESIDENT in smem (176 KiB; reloaded only when a CTA's stream
+//   changes codebook slot).  Nothing is re-streamed per tile.
+// * D = [Re K | Im K] (2 x 64 fp32 columns).  Side a adds X into Re and Y
+//   into Im; side b (K += i U[b]) adds -Y into Re (instruction-descriptor
+//   negate-A) and X into Im: 4 MMAs (N = 64) per (round, side, K-half).
+// * A = compressed one-hot in TMEM (lane = token): per K = 32 half, 8
+//   columns of fp16 pairs, group g = (c & 31) / 4 holds 1.0 in slot c & 1;
+//   the metadata column selects index pair (0,1) or (2,3) from bit 1 of c
+//   -- one column per (round, side); its lane L = m0 + 8 k1 + 16 m2 holds
+//   K-half k1 of rows m0 + 16 m2 (low 16 bits) and m0 + 8 + 16 m2 (high).  4
+//   producer warps (one per TMEM lane quarter, thread = token) write both
+//   with tcgen05.st; 6 round stages (both sides: 32 + 2 metadata columns),
+//   one mbarrier round trip per round.
+// * D double-buffered (TMEM columns 0-255); epilogue = 16 warps, warp
+//   (quarter, slot) owns tokens [32 quarter, +32) x subspaces [16 slot, +16):
+//   z = E[lane][j] K_j with the per-lane phase table E = e^{+i lane theta_j},
+//   score_h += Re(w_hj z) where w_hj = conj(q_hj) e^{-i(t - p0 - 32 quarter)
+//   theta_j} / sqrt(d) is per warp (fp64-based at a work item's first tile,
+//   advanced by e^{+i 128 theta_j} per tile); a 4-warp smem sum per quarter.
+//
+// Codebook precision fp16 (as CVQ_CACHE_KEYS_FP16), accumulation fp32.
+#include <cuda_fp16.h>
+
+#include "cvq_internal.cuh"
+
+namespace cvq {
+
+namespace {
+
+constexpr int kTok = 128;                 // tokens per tile (MMA M)
+constexpr int kEpiWarps = 16;
+constexpr int kProdWarps = 8;             // warp 16 + p: TMEM lane quarter p & 3, rounds r = p >> 2 (mod 2)
+constexpr int kMmaWarp = kEpiWarps + kProdWarps;  // MMA issuer + codebook loader
+constexpr int kThreads = (kMmaWarp + 1) * 32;
+constexpr int kAStages = 6;               // round stages: both sides of one round (32 + 2 metadata columns)
+constexpr uint32_t kACol0 = 256;          // round stage st: side s at columns 256 + 32 st + 16 s
+constexpr uint32_t kMetaCol0 = 448;       // its metadata: column 448 + 4 st + 2 s
+constexpr int kRoundBytes = 128 * 64 * 2;  // 16 KiB [X; Y] x 64 levels
+constexpr uint32_t kTmemCols = 512;
+
+__device__ __forceinline__ uint32_t su32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("{.reg .b64 st;\n\tmbarrier.arrive.shared::cta.b64 st, [%0];}" ::"r"(su32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile(
+      "{.reg .b64 st;\n\tmbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;}" ::"r"(su32(bar)),
+      "r"(bytes)
+      : "memory");
+}
+__device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;}"
+      : "=r"(ok)
+      : "r"(su32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  while (!mbar_try(bar, parity)) {
+  }
+}
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+  while (!mbar_try(bar, parity)) __nanosleep(64);
+}
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred;
+  asm volatile(
+      "{.reg .pred p;\n\telect.sync _|p, 0xffffffff;\n\tselp.u32 %0, 1, 0, p;}"
+      : "=r"(pred));
+  return pred != 0;
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          su32(dst)),
+      "l"(src), "r"(bytes), "r"(su32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   su32(bar))
+               : "memory");
+}
+__device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)((lbo >> 4) & 0x3FFFu) << 16) |
+         ((uint64_t)((sbo >> 4) & 0x3FFFu) << 32) | (1ull << 46);
+}
+// D[tmem] (+)= A[a_tmem] (2:4 compressed, metadata at e_tmem) x B[b_desc]
+__device__ __forceinline__ void umma_sp_ts(uint32_t d, uint32_t a, uint64_t b, uint32_t idesc,
+                                           uint32_t accum, uint32_t e) {
+  asm volatile(
+      "{.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.sp.cta_group::1.kind::f16 [%0], [%1], %2, [%5], %3, p;}" ::"r"(d),
+      "r"(a), "l"(b), "r"(idesc), "r"(accum), "r"(e));
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t* v) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
+      "%11, %12, %13, %14, %15}, [%16];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+        "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+        "=r"(v[14]), "=r"(v[15])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t* v) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
+      "%11, %12, %13, %14, %15, %16};" ::"r"(taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]),
+      "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]),
+      "r"(v[15])
+      : "memory");
+}
+__device__ __forceinline__ void tmem_st1(uint32_t taddr, uint32_t v) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" ::"r"(taddr), "r"(v) : "memory");
+}
+__device__ __forceinline__ float2 ffma2(float2 a, float b, float2 c) {
+  uint64_t d;
+  asm("{.reg .b64 a, b, c;\n\tmov.b64 a, {%1, %2};\n\tmov.b64 b, {%3, %3};\n\t"
+      "mov.b64 c, {%4, %5};\n\tfma.rn.f32x2 %0, a, b, c;}"
+      : "=l"(d)
+      : "f"(a.x), "f"(a.y), "f"(b), "f"(c.x), "f"(c.y));
+  return make_float2(__uint_as_float((uint32_t)d), __uint_as_float((uint32_t)(d >> 32)));
+}
+
+// Byte offset of (row, level) in the K-major no-swizzle 128 x 64 fp16 round
+// block: core matrix (level / 8, row / 8) at ((level / 8) * 16 + row / 8) * 128.
+__host__ __device__ __forceinline__ uint32_t kmaj128(int row, int l) {
+  return (uint32_t)((((l >> 3) * 16 + (row >> 3)) << 7) + ((row & 7) << 4) + ((l & 7) << 1));
+}
+
+struct SpArgs {
+  const uint64_t* kpool;
+  uint64_t kstride;
+  const uint16_t* cb;    // slot s: cb + s * slot_elems = [R][128 x 64] fp16 B blocks
+  size_t slot_elems;
+  int n_slots;
+  const float* q;        // [S][G][128]
+  const double* thetas;
+  long long t, pos0, n;
+  int chunk;             // tokens per work item (multiple of kTok)
+  int cps;               // work items per stream
+  int n_items;
+  float* ps;             // [S][n][G]
+};
+
+// This CTA's tiles in order; each CTA owns a contiguous range of work items
+// (so consecutive items mostly share a stream and its codebook slot).
+struct SpIter {
+  int item, end, s;
+  long long ti, hi;
+  bool item_start;
+  __device__ bool first(const SpArgs& a) {
+    const int per = a.n_items / (int)gridDim.x, rem = a.n_items % (int)gridDim.x;
+    const int b = (int)blockIdx.x;
+    item = b * per + min(b, rem);
+    end = item + per + (b < rem ? 1 : 0);
+    return setup(a);
+  }
+  __device__ bool setup(const SpArgs& a) {
+    while (item < end) {
+      s = item / a.cps;
+      ti = (long long)(item % a.cps) * a.chunk;
+      hi = min(a.n, ti + a.chunk);
+      item_start = true;
+      if (ti < hi) return true;
+      ++item;
+    }
+    return false;
+  }
+  __device__ bool next(const SpArgs& a) {
+    ti += kTok;
+    item_start = false;
+    if (ti < hi) return true;
+    ++item;
+    return setup(a);
+  }
+  __device__ int valid() const { return (int)min((long long)kTok, hi - ti); }
+  __device__ bool last_of_item() const { return ti + kTok >= hi; }
+};
+
+template <int R, int G>
+__global__ void __launch_bounds__(kThreads, 1) k_sp_score(SpArgs a) {
+  static_assert(G == 1 || G == 4, "heads per KV stream");
+  constexpr int NSTEP = 2 * R;
+  constexpr int NW = (NSTEP * 6 + 63 + 63) / 64;  // raw words covering a token's record
+  extern __shared__ __align__(1024) unsigned char smem[];
+  unsigned char* cbs = smem;                                             // [R][16 KiB]
+  float2* etab = reinterpret_cast<float2*>(cbs + R * kRoundBytes);         // [64 j][32 lanes]
+  float* wtab = reinterpret_cast<float*>(etab + 64 * 32);                 // [warp][16 j][2G]
+  float* red = wtab + kEpiWarps * 16 * 2 * G;                             // [2][4 q][4 e][32][G]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(red + 2 * 16 * 32 * G);
+  uint64_t* afull = bars;
+  uint64_t* aempty = bars + kAStages;
+  uint64_t* dfull = bars + 2 * kAStages;
+  uint64_t* dempty = dfull + 2;
+  uint64_t* cbfull = dempty + 2;
+  uint64_t* cbempty = cbfull + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(cbempty + 1);
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+
+  if (warp == kMmaWarp) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     su32(tmem_slot)),
+                 "r"(kTmemCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (tid == 0) {
+    for (int i = 0; i < kAStages; ++i) {
+      mbar_init(afull + i, 4);  // one producer warp per lane quarter
+      mbar_init(aempty + i, 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(dfull + i, 1);
+      mbar_init(dempty + i, kEpiWarps);
+    }
+    mbar_init(cbfull, 1);
+    mbar_init(cbempty, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  // per-lane phase table e^{+i lane theta_j}
+  for (int e = tid; e < 64 * 32; e += kThreads) {
+    const int j = e >> 5, ln = e & 31;
+    double sn, cs;
+    sincos((double)ln * a.thetas[j], &sn, &cs);
+    etab[e] = make_float2((float)cs, (float)sn);
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp < kEpiWarps) {
+    // ============ epilogue: lane = token 32 quarter + lane of the tile,
+    // warp slot e = subspaces [16 e, 16 e + 16) ==========================
+    const int quarter = warp & 3, eslot = warp >> 2;
+    const uint32_t lane_base = (uint32_t)(quarter * 32) << 16;
+    // lanes (jj = lane & 15, half = lane >> 4) keep the phase of subspace
+    // 16 e + jj and produce w for heads 2 half, 2 half + 1 (G = 4)
+    const int jl = eslot * 16 + (lane & 15), hh = lane >> 4;
+    const double theta = a.thetas[jl];
+    float2 step;
+    {
+      double sn, cs;
+      sincos((double)kTok * theta, &sn, &cs);  // e^{+i 128 theta}: one tile later
+      step = make_float2((float)cs, (float)sn);
+    }
+    float* wt = wtab + warp * (16 * 2 * G);
+    const float sc = 0.08838834764831845f;  // 1 / sqrt(128)
+    float2 ph = make_float2(1.f, 0.f);
+    float2 qv[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+    SpIter it;
+    int k = 0;
+    for (bool ok = it.first(a); ok; ok = it.next(a), ++k) {
+      const int db = k & 1;
+      if (it.item_start) {
+        ph = phase_neg(a.t - (a.pos0 + it.ti + 32 * quarter), theta);
+        const float* qs = a.q + (size_t)it.s * G * 128;
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const int h = (G == 4) ? 2 * hh + u : 0;
+          qv[u] = make_float2(__ldg(qs + h * 128 + 2 * jl) * sc, __ldg(qs + h * 128 + 2 * jl + 1) * sc);
+        }
+      } else {
+        ph = make_float2(ph.x * step.x - ph.y * step.y, ph.x * step.y + ph.y * step.x);
+      }
+      // w = conj(q) ph; stored as (w.x, -w.y) so Re(w z) = w.x z.x + (-w.y) z.y
+      if (G == 4 || hh == 0) {
+        float o[4];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const float wx = qv[u].x * ph.x + qv[u].y * ph.y;
+          const float wy = qv[u].x * ph.y - qv[u].y * ph.x;
+          o[u] = wx;
+          o[2 + u] = -wy;
+        }
+        if constexpr (G == 4) {
+          // [jj][half]: (wx_h0, wx_h1, -wy_h0, -wy_h1)
+          reinterpret_cast<float4*>(wt)[(lane & 15) * 2 + hh] = make_float4(o[0], o[1], o[2], o[3]);
+        } else {
+          reinterpret_cast<float2*>(wt)[lane & 15] = make_float2(o[0], o[2]);
+        }
+      }
+      __syncwarp();
+      mbar_wait_sleep(dfull + db, (k >> 1) & 1);
+      tc_fence_after();
+      uint32_t re[16], im[16];
+      tmem_ld16(tmem + lane_base + db * 128 + eslot * 16, re);
+      tmem_ld16(tmem + lane_base + db * 128 + 64 + eslot * 16, im);
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(dempty + db);  // D[db] is in registers: free it
+      const float2* E = etab + eslot * 16 * 32 + lane;
+      float* rb = red + (size_t)((db * 4 + quarter) * 4) * 32 * G;  // [e][lane][G]
+      if constexpr (G == 4) {
+        float2 acc01 = make_float2(0.f, 0.f), acc23 = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int jj = 0; jj < 16; ++jj) {
+          const float2 ej = E[jj * 32];
+          const float kr = __uint_as_float(re[jj]), ki = __uint_as_float(im[jj]);
+          const float zx = ej.x * kr - ej.y * ki;
+          const float zy = ej.x * ki + ej.y * kr;
+          const float4 w01 = reinterpret_cast<const float4*>(wt)[jj * 2];
+          const float4 w23 = reinterpret_cast<const float4*>(wt)[jj * 2 + 1];
+          acc01 = ffma2(make_float2(w01.x, w01.y), zx, acc01);
+          acc01 = ffma2(make_float2(w01.z, w01.w), zy, acc01);
+          acc23 = ffma2(make_float2(w23.x, w23.y), zx, acc23);
+          acc23 = ffma2(make_float2(w23.z, w23.w), zy, acc23);
+        }
+        reinterpret_cast<float4*>(rb)[eslot * 32 + lane] = make_float4(acc01.x, acc01.y, acc23.x, acc23.y);
+      } else {
+        float acc = 0.f;
+#pragma unroll
+        for (int jj = 0; jj < 16; ++jj) {
+          const float2 ej = E[jj * 32];
+          const float kr = __uint_as_float(re[jj]), ki = __uint_as_float(im[jj]);
+          const float2 w = reinterpret_cast<const float2*>(wt)[jj];
+          acc = fmaf(w.x, ej.x * kr - ej.y * ki, acc);
+          acc = fmaf(w.y, ej.x * ki + ej.y * kr, acc);
+        }
+        rb[eslot * 32 + lane] = acc;
+      }
+      asm volatile("bar.sync %0, 128;" ::"r"(1 + quarter) : "memory");
+      // warp slot e writes head e (G = 4) / slot 0 writes the head (G = 1)
+      const int tok = 32 * quarter + lane;
+      if (eslot < G && tok < it.valid()) {
+        float v = 0.f;
+#pragma unroll
+        for (int e2 = 0; e2 < 4; ++e2) v += rb[(e2 * 32 + lane) * G + eslot];
+        a.ps[((size_t)it.s * a.n + it.ti + tok) * G + eslot] = v;
+      }
+    }
+  } else if (warp < kEpiWarps + kProdWarps) {
+    // ============ one-hot producers: thread = token 32 quarter + lane; warp
+    // sub = 0 / 1 takes the even / odd rounds (both sides), so two chains of
+    // tcgen05.st -> wait::st per lane quarter run concurrently ===========
+    const int p = warp - kEpiWarps, quarter = p & 3, sub = p >> 2;
+    const uint32_t lane_base = (uint32_t)(quarter * 32) << 16;
+    const int t = quarter * 32 + lane;
+    auto load_raw = [&](const SpIter& x, uint64_t* raw, uint32_t& off) {
+      const uint64_t* kw = a.kpool + (size_t)x.s * a.kstride;
+      const long long tok = x.ti + (t < x.valid() ? t : 0);
+      const unsigned long long b0 = (unsigned long long)tok * (NSTEP * 6);
+      off = (uint32_t)(b0 & 63u);
+#pragma unroll
+      for (int i = 0; i < NW; ++i) raw[i] = __ldg(kw + (b0 >> 6) + i);
+    };
+    uint64_t raw[NW], nraw[NW];
+    uint32_t off = 0, noff = 0;
+    SpIter it;
+    int k = 0;
+    bool ok = it.first(a);
+    if (ok) load_raw(it, raw, off);
+    const int src = (lane & 7) | (lane & 16);
+    while (ok) {
+      uint64_t w[NW];  // token record at bit 0
+#pragma unroll
+      for (int i = 0; i < NW; ++i)
+        w[i] = off ? (raw[i] >> off) | (i + 1 < NW ? raw[i + 1] << (64u - off) : 0ull) : raw[i];
+      SpIter nx = it;
+      const bool okn = nx.next(a);
+      if (okn) load_raw(nx, nraw, noff);
+      // this warp's rounds r = sub, sub + 2, ...: their 12-bit (a, b) fields
+      // packed back to back into (pk0, pk1)
+      uint64_t pk0 = 0, pk1 = 0;
+#pragma unroll
+      for (int r = 0, i = 0; r < R; ++r) {
+        if ((r & 1) != sub) continue;
+        const int b0 = 12 * r, wi = b0 >> 6, sh = b0 & 63;
+        const uint64_t f = ((w[wi] >> sh) | (sh > 52 ? w[wi + 1] << (64 - sh) : 0ull)) & 0xFFFull;
+        if (i < 5) pk0 |= f << (12 * i);
+        else pk1 |= f << (12 * (i - 5));
+        ++i;
+      }
+#pragma unroll 1
+      for (int r = sub; r < R; r += 2) {
+        const uint32_t fld = (uint32_t)pk0 & 0xFFFu;
+        pk0 = (pk0 >> 12) | (pk1 << 48);
+        pk1 >>= 12;
+        // round stage of global round g = R tile + r
+        const uint32_t g = (uint32_t)(R * k + r), st = g % kAStages, use = g / kAStages;
+        if (use > 0) {
+          mbar_wait(aempty + st, (use - 1) & 1u);
+          tc_fence_after();
+        }
+#pragma unroll
+        for (int s2 = 0; s2 < 2; ++s2) {
+          const uint32_t c = (fld >> (6 * s2)) & 63u;
+          uint32_t v[16];
+          const uint32_t col = ((c >> 5) << 3) | ((c & 31) >> 2);
+          const uint32_t one = (c & 1) ? 0x3C000000u : 0x00003C00u;  // fp16 1.0 in slot c & 1
+#pragma unroll
+          for (int i = 0; i < 16; ++i) v[i] = (col == (uint32_t)i) ? one : 0u;
+          // metadata word of TMEM lane L = m0 + 8 k1 + 16 m2 (measured,
+          // profiles/r01_umma_sparse_lanemap.txt): bits [16 m1, 16 m1 + 16)
+          // are the 4 group nibbles of K-half k1 for row m0 + 8 m1 + 16 m2.
+          // Every group of a row uses pair (2,3) / (0,1) from bit 1 of c.
+          const uint32_t hb = (c >> 1) & 1u;
+          const uint32_t ba = __shfl_sync(0xffffffffu, hb, src);
+          const uint32_t bb = __shfl_sync(0xffffffffu, hb, src | 8);
+          const uint32_t meta =
+              (ba ? 0x0000EEEEu : 0x00004444u) | (bb ? 0xEEEE0000u : 0x44440000u);
+          tmem_st16(tmem + lane_base + kACol0 + 32 * st + 16 * s2, v);
+          tmem_st1(tmem + lane_base + kMetaCol0 + 4 * st + 2 * s2, meta);
+        }
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(afull + st);
+      }
+#pragma unroll
+      for (int i = 0; i < NW; ++i) raw[i] = nraw[i];
+      off = noff;
+      it = nx;
+      ok = okn;
+      ++k;
+    }
+  } else if (warp == kMmaWarp) {
+    // ============ tcgen05.mma.sp issuer (warp-uniform walk, elected lane) ==
+    // f16 x f16 -> f32, sparse A from TMEM, B K-major in smem; M128 N64
+    constexpr uint32_t idesc = (1u << 2) | (1u << 4) | ((64u >> 3) << 17) | (8u << 24);
+    constexpr uint32_t kNegA = 1u << 13;
+    const uint64_t bdesc0 = sdesc(su32(cbs), 2048, 128);
+    SpIter it;
+    uint32_t nload = 0, gr = 0;  // gr: global round counter
+    int k = 0, prev_slot = -1;
+    for (bool ok = it.first(a); ok; ok = it.next(a), ++k) {
+      const int db = k & 1;
+      if (it.item_start) {
+        const int slot = it.s % a.n_slots;
+        if (slot != prev_slot) {
+          // (re)load the resident codebook: once every MMA reading the old
+          // one has completed (rare: work items are contiguous per CTA)
+          if (nload > 0) {
+            if (elect_one()) tc_commit(cbempty);
+            __syncwarp();
+            mbar_wait(cbempty, (nload - 1) & 1);
+          }
+          if (elect_one()) {
+            const uint16_t* src = a.cb + (size_t)slot * a.slot_elems;
+            mbar_arrive_tx(cbfull, R * kRoundBytes);
+            for (int r = 0; r < R; ++r)
+              bulk_g2s(cbs + r * kRoundBytes, src + (size_t)r * (kRoundBytes / 2), kRoundBytes,
+                       cbfull);
+          }
+          __syncwarp();
+          mbar_wait(cbfull, nload & 1);
+          ++nload;
+          prev_slot = slot;
+        }
+      }
+      if (k >= 2) {  // D buffer db was read by the epilogue of tile k-2
+        mbar_wait(dempty + db, ((k - 2) >> 1) & 1);
+        tc_fence_after();
+      }
+      const uint32_t dcol = tmem + (uint32_t)db * 128u;
+      // compact loop (instruction-cache friendly): one barrier round trip
+      // per round (8 MMAs: 2 sides x 2 K-halves x Re/Im)
+      uint64_t br = bdesc0;
+#pragma unroll 1
+      for (int r = 0; r < R; ++r, br += (uint64_t)(kRoundBytes >> 4), ++gr) {
+        const uint32_t st = gr % kAStages, use = gr / kAStages;
+        mbar_wait(afull + st, use & 1u);
+        tc_fence_after();
+        if (elect_one()) {
+#pragma unroll
+          for (int s = 0; s < 2; ++s) {
+            const uint32_t a_tm = tmem + kACol0 + 32 * st + 16 * s;
+            const uint32_t e_tm = tmem + kMetaCol0 + 4 * st + 2 * s;
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+#pragma unroll
+              for (int blk = 0; blk < 2; ++blk) {
+                // side a: Re += X, Im += Y;  side b: Re -= Y, Im += X
+                const int rows = s ? (blk ? 0 : 64) : (blk ? 64 : 0);
+                const uint64_t bd = br + (uint64_t)((h * 4 * 2048 + rows * 16) >> 4);
+                umma_sp_ts(dcol + blk * 64, a_tm + h * 8, bd,
+                           idesc | ((s && !blk) ? kNegA : 0u),
+                           (s > 0 || h > 0 || r > 0) ? 1u : 0u, e_tm);
+              }
+            }
+          }
+          tc_commit(aempty + st);
+        }
+        __syncwarp();
+      }
+      if (elect_one()) tc_commit(dfull + db);
+      __syncwarp();
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == kMmaWarp)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                 "r"(kTmemCols));
+}
+
+size_t sp_smem(int G, int R) {
+  return (size_t)R * kRoundBytes + 64 * 32 * 8 + (size_t)kEpiWarps * 16 * 2 * G * 4 +
+         (size_t)2 * 16 * 32 * G * 4 + (2 * kAStages + 6) * 8 + 16;
+}
+
+template <int R, int G>
+cudaError_t launch_sp(const SpArgs& a, cudaStream_t st) {
+  const size_t sm = sp_smem(G, R);
+  cudaError_t e = ensure_dyn_smem(reinterpret_cast<const void*>(k_sp_score<R, G>), sm);
+  if (e != cudaSuccess) return e;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int grid = a.n_items < sms ? a.n_items : sms;
+  k_sp_score<R, G><<<grid, kThreads, sm, st>>>(a);
+  count_launch();
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+bool sp_supported(int R) { return R == 11; }
+
+size_t sp_codebook_elems(int R) { return sp_supported(R) ? (size_t)R * (kRoundBytes / 2) : 0; }
+
+void sp_build_codebook(int R, const double* xy, uint16_t* out, uint16_t (*to_half)(double)) {
+  // xy: [R][64 subs][64 levels][2]; out: [R][X rows 0-63 | Y rows 64-127][64 levels]
+  for (int r = 0; r < R; ++r) {
+    uint16_t* o = out + (size_t)r * (kRoundBytes / 2);
+    for (int j = 0; j < 64; ++j)
+      for (int l = 0; l < 64; ++l) {
+        const double x = xy[(((size_t)r * 64 + j) * 64 + l) * 2];
+        const double y = xy[(((size_t)r * 64 + j) * 64 + l) * 2 + 1];
+        o[kmaj128(j, l) >> 1] = to_half(x);
+        o[kmaj128(64 + j, l) >> 1] = to_half(y);
+      }
+  }
+}
+
+cudaError_t run_sp_score(const AttnJob& job, const uint16_t* cb, size_t slot_elems,
+                         const float* q, float* ps, int chunk, cudaStream_t st) {
+  const Geom& g = job.geo;
+  if (!cb || g.d != 128 || g.L != 64 || g.subs != 64 || !sp_supported(g.R))
+    return cudaErrorInvalidValue;
+  SpArgs a{};
+  a.kpool = job.kpool;
+  a.kstride = job.kstride;
+  a.cb = cb;
+  a.slot_elems = slot_elems;
+  a.n_slots = job.n_slots;
+  a.q = q;
+  a.thetas = job.thetas;
+  a.t = job.t;
+  a.pos0 = job.pos0;
+  a.n = job.n;
+  a.chunk = (chunk + kTok - 1) / kTok * kTok;
+  a.cps = (int)((job.n + a.chunk - 1) / a.chunk);
+  a.n_items = job.S * a.cps;
+  a.ps = ps;
+  if (g.G == 4) return launch_sp<11, 4>(a, st);
+  if (g.G == 1) return launch_sp<11, 1>(a, st);
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace cvq

@@ -33,6 +33,8 @@
 // (tcgen05.commit), d_empty[buf] (16 epilogue warps).
 //
 // Codebook precision fp16 (as CVQ_CACHE_KEYS_FP16), accumulation fp32.
+#include <cstdlib>
+
 #include "cvq_internal.cuh"
 
 
@@ -174,7 +176,8 @@ __host__ __device__ __forceinline__ uint32_t kmaj(int t, int l) {
 struct TcArgs {
   const uint64_t* kpool;
   uint64_t kstride;
-  const uint16_t* cbtc;  // [slot][R][2][8192] fp16 A operand
+  const uint16_t* cbtc;  // slot s at cbtc + s * slot_elems: [R][2][8192] fp16 A operand
+  size_t slot_elems;
   int n_slots;
   const float* q;        // [S][G][128]
   const double* thetas;
@@ -524,7 +527,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_tc_score(TcArgs a) {
     TileIter it;
     uint32_t g = 0;
     for (bool ok = it.first(a); ok; ok = it.next(a)) {
-      const uint16_t* src = a.cbtc + (size_t)(it.s % a.n_slots) * NSTEP * (kABytes / 2);
+      const uint16_t* src = a.cbtc + (size_t)(it.s % a.n_slots) * a.slot_elems;
       for (int q = 0; q < NSTEP; ++q, ++g) {
         const uint32_t st = g % kStages, use = g / kStages;
         if (use > 0) mbar_wait_sleep(empty + st, (use - 1) & 1);
@@ -565,7 +568,9 @@ size_t tc_smem_bytes(int G, int R) {
 
 int tc_blocks(int) { return 1; }
 
-size_t tc_codebook_elems(int R) { return (size_t)R * 2 * (kABytes / 2); }
+// per slot: the dense layout [R][2][8192], then (R = 11) the sparse kernel's
+// [R][X | Y][64] blocks (attn_sp.cu)
+size_t tc_codebook_elems(int R) { return (size_t)R * 2 * (kABytes / 2) + sp_codebook_elems(R); }
 
 void tc_build_codebook(int R, const double* xy, uint16_t* out, uint16_t (*to_half)(double)) {
   // xy: [R][64 subs][64 levels][2] (rope-commutative atoms, x then y)
@@ -581,16 +586,25 @@ void tc_build_codebook(int R, const double* xy, uint16_t* out, uint16_t (*to_hal
           o[kmaj<128>(2 * j + 1, l) >> 1] = to_half(side ? x : y);
         }
     }
+  if (sp_supported(R)) sp_build_codebook(R, xy, out + (size_t)R * 2 * (kABytes / 2), to_half);
 }
 
 cudaError_t run_tc_score(const AttnJob& job, const float* q, float* ps, int chunk,
                          cudaStream_t st) {
   const Geom& g = job.geo;
   if (!job.cb_key_tc || g.d != 128 || g.L != 64 || g.subs != 64) return cudaErrorInvalidValue;
+  const size_t slot_elems = tc_codebook_elems(g.R);
+  // 2:4-sparse kernel where it applies (CVQ_TC_DENSE=1 keeps the dense one)
+  const char* fd = getenv("CVQ_TC_DENSE");
+  const bool force_dense = fd && fd[0] == '1';
+  if (sp_supported(g.R) && !force_dense)
+    return run_sp_score(job, job.cb_key_tc + (size_t)g.R * 2 * (kABytes / 2), slot_elems, q, ps,
+                        chunk, st);
   TcArgs a{};
   a.kpool = job.kpool;
   a.kstride = job.kstride;
   a.cbtc = job.cb_key_tc;
+  a.slot_elems = slot_elems;
   a.n_slots = job.n_slots;
   a.q = q;
   a.thetas = job.thetas;

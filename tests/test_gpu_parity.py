@@ -552,6 +552,33 @@ def test_mha_one_query_head_per_stream(G, preset, n, keys):
     assert worst <= 1e-3, worst
 
 
+@pytest.mark.parametrize("Gq,n", [(4, 1), (4, 127), (4, 129), (4, 8197), (1, 300), (1, 20000)])
+def test_sparse_tc_matches_dense_tc(G, Gq, n, monkeypatch):
+    """The 2:4-sparse tcgen05 kernel (attn_sp.cu, 1-bit preset) against the
+    dense one-hot tcgen05 kernel (CVQ_TC_DENSE=1) on the same cache: same
+    fp16 codebook, fp32 accumulation in another order, so outputs agree to
+    1e-5 relative; 3 layers x 2 KV heads exercise codebook-slot reloads."""
+    kq = KQ(128, 64, 64, 11)
+    nc, Ly, H = 128, 3, 2
+    rng = P.rng(n + Gq)
+    c = G.QuantizedKVCache(kq, nc, n_layers=Ly, n_kv_heads=H, q_per_kv=Gq, capacity=n, keys="tc")
+    for layer in range(Ly):
+        for h in range(H):
+            c.set_key_codebook(layer, h, rng.normal(2 * kq.n_atoms, 0.3))
+            c.set_value_quantizer(layer, h, rng.normal(nc * 128, 1 / 16).reshape(nc, 128))
+            a, b = fx.random_key_codes(kq, n, rng=rng)
+            bits = fx.random_value_codes(nc, n, rng=rng)
+            c.import_stream(0, layer, h, P.pack_key_codes(kq, a, b), P.pack_value_codes(bits), n)
+    q = rng.normal(Ly * H * Gq * 128).reshape(1, Ly, H * Gq, 128).astype(np.float32)
+    t = n + 4000
+    out_sp = c.attention(q, t)
+    monkeypatch.setenv("CVQ_TC_DENSE", "1")
+    out_dense = c.attention(q, t)
+    monkeypatch.delenv("CVQ_TC_DENSE")
+    assert np.isfinite(out_sp).all()
+    assert fx.rel_err(out_sp, out_dense) <= 1e-5
+
+
 def test_tc_at_bench_scale_vs_fp32_and_oracle(G):
     """The default tcgen05 path at the C3 context length (128K tokens, 16
     persistent work items per stream, 4 streams x 4 q heads): all rows vs the

@@ -1,0 +1,209 @@
+// Microbenchmark of the MMA issue pattern a tokens-in-M sparse score kernel
+// would use: I issuer warps (whole warp walks the loop, one elected lane
+// issues, warp-uniform operands), each with its own accumulator, B walking
+// 4 x 16 KiB stages, A from smem or TMEM.  Reports SM clocks per MMA per SM.
+#include <cstdio>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+__device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)((lbo >> 4) & 0x3FFFu) << 16) |
+         ((uint64_t)((sbo >> 4) & 0x3FFFu) << 32) | (1ull << 46);
+}
+__device__ __forceinline__ bool elect_one() {
+  uint32_t p;
+  asm volatile("{.reg .pred p;\n\telect.sync _|p, 0xffffffff;\n\tselp.u32 %0, 1, 0, p;}" : "=r"(p));
+  return p != 0;
+}
+template <int SPARSE, int ATM, int N>
+__global__ void kb(int issuers, int tiles, long long* out) {
+  extern __shared__ __align__(1024) unsigned char sm[];
+  __shared__ uint32_t slot;
+  __shared__ __align__(8) uint64_t bar[8];
+  const int tid = threadIdx.x, warp = tid >> 5;
+  for (int i = tid; i < 80 * 1024 / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(sm)[i] = 0;
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(&slot)), "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (tid < 8) asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(&bar[tid])), "r"(1));
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = slot;
+  if (warp < 4) {
+    const uint32_t z = 0, m = 0x44444444u;
+    for (int c = 256; c < 512; ++c)
+      asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" ::"r"(tmem + ((uint32_t)(warp * 32) << 16) + c),
+                   "r"(c >= 448 ? m : z) : "memory");
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const int w = __shfl_sync(0xffffffffu, warp, 0);
+  if (w < issuers) {
+    const uint32_t idesc = (1u << 4) | ((uint32_t)(N >> 3) << 17) | (8u << 24) | (SPARSE ? (1u << 2) : 0u);
+    const uint32_t d = tmem + (uint32_t)(w * (N == 256 ? 0 : 128));
+    const uint32_t a_tm = tmem + 384 + (uint32_t)(w * 16);
+    const uint32_t te = tmem + 448 + (uint32_t)w;
+    const uint32_t sA = su32(sm + 65536);  // 16 KiB A region
+    const uint32_t sB = su32(sm);          // 4 x 16 KiB B stages
+    const int per_tile = SPARSE ? 44 : 88;
+    long long t0 = clock64();
+    for (int t = 0; t < tiles; ++t) {
+      for (int i = 0; i < per_tile; ++i) {
+        const uint32_t stage = (uint32_t)((i >> 1) & 3);
+        const uint32_t half = (uint32_t)(i & 1);
+        const uint64_t bd = sdesc(sB + stage * 16384 + half * (SPARSE ? 4 : 2) * 128, 128 * 16, 128);
+        const uint64_t ad = sdesc(sA + half * 4096, 128 * 16, 128);
+        if (elect_one()) {
+          if (SPARSE && ATM)
+            asm volatile("{.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                         "tcgen05.mma.sp.cta_group::1.kind::f16 [%0], [%1], %2, [%5], %3, p;}" ::"r"(d),
+                         "r"(a_tm + half * 8), "l"(bd), "r"(idesc), "r"(i), "r"(te));
+          else if (SPARSE)
+            asm volatile("{.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                         "tcgen05.mma.sp.cta_group::1.kind::f16 [%0], %1, %2, [%5], %3, p;}" ::"r"(d),
+                         "l"(ad), "l"(bd), "r"(idesc), "r"(i), "r"(te));
+          else if (ATM)
+            asm volatile("{.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                         "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;}" ::"r"(d),
+                         "r"(a_tm + half * 8), "l"(bd), "r"(idesc), "r"(i));
+          else
+            asm volatile("{.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                         "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;}" ::"r"(d),
+                         "l"(ad), "l"(bd), "r"(idesc), "r"(i));
+        }
+        __syncwarp();
+      }
+    }
+    if (elect_one())
+      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(&bar[w])) : "memory");
+    uint32_t ok = 0;
+    while (!ok)
+      asm volatile("{.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;}"
+                   : "=r"(ok) : "r"(su32(&bar[w])), "r"(0) : "memory");
+    if (blockIdx.x == 0 && w == 0 && (tid & 31) == 0) out[0] = clock64() - t0;
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+}
+
+
+// Resident-codebook pattern: N = 64, 4 MMAs per (round, K32 half) into two
+// 64-column blocks (Re, Im), B walking an 11 x 16 KiB resident codebook,
+// A and metadata from TMEM stage regions, negate-A on one MMA in four.
+__global__ void kres(int tiles, int ms, long long* out) {
+  extern __shared__ __align__(1024) unsigned char sm[];
+  __shared__ uint32_t slot;
+  __shared__ __align__(8) uint64_t bar[8];
+  const int tid = threadIdx.x, warp = tid >> 5;
+  for (int i = tid; i < 176 * 1024 / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(sm)[i] = 0;
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(&slot)), "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (tid < 8) asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(&bar[tid])), "r"(1));
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = slot;
+  if (warp < 4) {
+    for (int c = 256; c < 512; ++c)
+      asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" ::"r"(tmem + ((uint32_t)(warp * 32) << 16) + c),
+                   "r"(c >= 448 ? 0x44444444u : 0u) : "memory");
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  if (warp == 0) {
+    const uint32_t idesc = (1u << 4) | (8u << 17) | (8u << 24) | (1u << 2);  // N = 64
+    const uint32_t sB = su32(sm);
+    long long t0 = clock64();
+    for (int t = 0; t < tiles; ++t) {
+      const uint32_t d = tmem + (uint32_t)((t & 1) * 128);
+      for (int r = 0; r < 11; ++r) {
+        for (int s = 0; s < 2; ++s) {
+          const uint32_t st = (uint32_t)((r * 2 + s) & 7);
+          const uint32_t a_tm = tmem + 256 + st * 16;
+          const uint32_t te = tmem + 448 + st * (uint32_t)ms;
+          for (int h = 0; h < 2; ++h) {
+            for (int blk = 0; blk < 2; ++blk) {
+              // side a: Re += X, Im += Y;  side b: Re -= Y, Im += X
+              const uint32_t rows = (uint32_t)(s ? (blk ? 0 : 64) : (blk ? 64 : 0));
+              const uint64_t bd = sdesc(sB + r * 16384 + h * 4 * 2048 + rows * 16, 2048, 128);
+              const uint32_t id = idesc | ((s && !blk) ? (1u << 13) : 0u);
+              if (elect_one())
+                asm volatile("{.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                             "tcgen05.mma.sp.cta_group::1.kind::f16 [%0], [%1], %2, [%5], %3, p;}" ::"r"(d + blk * 64),
+                             "r"(a_tm + h * 8), "l"(bd), "r"(id), "r"(r | s | h), "r"(te));
+              __syncwarp();
+            }
+          }
+        }
+      }
+    }
+    if (elect_one())
+      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(&bar[0])) : "memory");
+    uint32_t ok = 0;
+    while (!ok)
+      asm volatile("{.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;}"
+                   : "=r"(ok) : "r"(su32(&bar[0])), "r"(0) : "memory");
+    if (blockIdx.x == 0 && (tid & 31) == 0) out[0] = clock64() - t0;
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+}
+
+template <int SP, int ATM, int N>
+void run(int iss, long long* d) {
+  auto k = kb<SP, ATM, N>;
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+  const int tiles = 64;
+  k<<<148, 128, 96 * 1024>>>(iss, 2, d);
+  k<<<148, 128, 96 * 1024>>>(iss, tiles, d);
+  cudaError_t e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) { printf("err %s\n", cudaGetErrorString(e)); exit(1); }
+  long long cyc = 0;
+  cudaMemcpy(&cyc, d, 8, cudaMemcpyDeviceToHost);
+  const int per_tile = SP ? 44 : 88;
+  const double per = (double)cyc / ((double)tiles * per_tile * iss);
+  const double macs = 128.0 * N * (SP ? 32 : 16);
+  printf("%s A=%s N=%d issuers=%d: %.1f clk/mma per SM, %.0f logical MAC/clk (%.0f%% of dense), %.1f clk per 128 tok x 22 steps\n",
+         SP ? "sparse" : "dense ", ATM ? "tmem" : "smem", N, iss, per, macs / per, 100 * macs / per / 4096,
+         per * (SP ? 44 : 88) * (N == 256 && !SP ? 0.5 : 1.0) * (N == 128 && !SP ? 2.0 : 1.0));
+}
+int main() {
+  setvbuf(stdout, nullptr, _IONBF, 0);
+  long long* d;
+  cudaMalloc(&d, 8);
+  run<0, 0, 256>(1, d);
+  run<0, 1, 256>(1, d);
+  run<1, 0, 128>(1, d);
+  run<1, 1, 128>(1, d);
+  run<1, 1, 64>(1, d);
+  {
+    cudaFuncSetAttribute(kres, cudaFuncAttributeMaxDynamicSharedMemorySize, 176 * 1024);
+   for (int ms : {8, 4, 2, 1}) {
+    kres<<<148, 128, 176 * 1024>>>(2, ms, d);
+    kres<<<148, 128, 176 * 1024>>>(64, ms, d);
+    cudaError_t e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) { printf("err %s\n", cudaGetErrorString(e)); exit(1); }
+    long long cyc = 0;
+    cudaMemcpy(&cyc, d, 8, cudaMemcpyDeviceToHost);
+    printf("resident-codebook N=64 pattern: %.1f clk per 128-token tile (88 MMAs), %.1f clk/mma, %.2f clk/token\n",
+           cyc / 64.0, cyc / 64.0 / 88, cyc / 64.0 / 128);
+    printf("  (metadata column stride %d)\n", ms);
+   }
+  }
+  return 0;
+}
