@@ -314,11 +314,18 @@ def main():
         # = 4*R*L*d flops, executed on the tensor pipe
         flops = kvht_per_launch * 4.0 * R * L * d
         ach_tf = flops / (avg_main_ms / 1e3) / 1e12
-        roof = {"bound": "tensor", "achieved": ach_tf, "peak": TENSOR_NOMINAL_TFLOPS,
-                "unit": "TFLOP/s", "frac": ach_tf / TENSOR_NOMINAL_TFLOPS,
-                "peak_source": "B200_PROFILING.md nominal dense fp16 (2.25 PFLOP/s); "
-                               "MEASURED_PEAKS bf16 burst %.1f is a power-capped dense cuBLAS "
-                               "run at lower SM clocks" % tflops,
+        # R = 11: the one-hot is a 2:4-sparse A operand (tcgen05.mma.sp,
+        # attn_sp.cu) -- the ceiling is the sparse fp16 rate, twice the dense
+        sparse = R == 11 and os.environ.get("CVQ_TC_DENSE", "0") != "1"
+        peak_tf = TENSOR_NOMINAL_TFLOPS * (2 if sparse else 1)
+        roof = {"bound": "tensor", "achieved": ach_tf, "peak": peak_tf,
+                "unit": "TFLOP/s", "frac": ach_tf / peak_tf,
+                "kernel": "k_sp_score (2:4-sparse one-hot MMA)" if sparse else "k_tc_score (dense one-hot MMA)",
+                "peak_source": ("B200_PROFILING.md nominal fp16 %s (%.2f PFLOP/s, achieved counts the "
+                                "logical one-hot GEMM flops); MEASURED_PEAKS bf16 burst %.1f is a "
+                                "power-capped dense cuBLAS run at lower SM clocks"
+                                % ("2:4-sparse = 2 x dense" if sparse else "dense", peak_tf / 1e3, tflops)),
+                "frac_vs_dense_nominal": ach_tf / TENSOR_NOMINAL_TFLOPS,
                 "frac_vs_measured_bf16_burst": ach_tf / tflops,
                 "algorithmic_flops_per_launch": flops,
                 "hbm_achieved_gbs": achieved, "hbm_frac": achieved / hbm, **common}

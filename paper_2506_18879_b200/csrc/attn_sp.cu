@@ -24,8 +24,8 @@
 //   -- one column per (round, side); its lane L = m0 + 8 k1 + 16 m2 holds
 //   K-half k1 of rows m0 + 16 m2 (low 16 bits) and m0 + 8 + 16 m2 (high).  4
 //   producer warps (one per TMEM lane quarter, thread = token) write both
-//   with tcgen05.st; 6 round stages (both sides: 32 + 2 metadata columns),
-//   one mbarrier round trip per round.
+//   with tcgen05.st; 6 round stages (both sides: 32 + 2 metadata columns);
+//   the MMA warp takes rounds in pairs (16 MMAs per elected region).
 // * D double-buffered (TMEM columns 0-255); epilogue = 16 warps, warp
 //   (quarter, slot) owns tokens [32 quarter, +32) x subspaces [16 slot, +16):
 //   z = E[lane][j] K_j with the per-lane phase table E = e^{+i lane theta_j},
@@ -454,7 +454,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_sp_score(SpArgs a) {
     constexpr uint32_t kNegA = 1u << 13;
     const uint64_t bdesc0 = sdesc(su32(cbs), 2048, 128);
     SpIter it;
-    uint32_t nload = 0, gr = 0;  // gr: global round counter
+    uint32_t nload = 0, gst = 0, gph = 0;  // stage / parity of the next round
     int k = 0, prev_slot = -1;
     for (bool ok = it.first(a); ok; ok = it.next(a), ++k) {
       const int db = k & 1;
@@ -486,35 +486,56 @@ __global__ void __launch_bounds__(kThreads, 1) k_sp_score(SpArgs a) {
         tc_fence_after();
       }
       const uint32_t dcol = tmem + (uint32_t)db * 128u;
-      // compact loop (instruction-cache friendly): one barrier round trip
-      // per round (8 MMAs: 2 sides x 2 K-halves x Re/Im)
+      // rounds in pairs: one elected issue region of 16 MMAs (2 rounds x 2
+      // sides x 2 K-halves x Re/Im) per pair, so the per-region overhead
+      // (barrier waits, elect, reconvergence) is paid every 16 MMAs; each
+      // round's stage is released by its own commit
       uint64_t br = bdesc0;
 #pragma unroll 1
-      for (int r = 0; r < R; ++r, br += (uint64_t)(kRoundBytes >> 4), ++gr) {
-        const uint32_t st = gr % kAStages, use = gr / kAStages;
-        mbar_wait(afull + st, use & 1u);
+      for (int r = 0; r < R; r += 2) {
+        const bool two = r + 1 < R;
+        const uint32_t st0 = gst, ph0 = gph;
+        uint32_t st1 = gst + 1, ph1 = gph;
+        if (st1 == kAStages) {
+          st1 = 0;
+          ph1 ^= 1u;
+        }
+        mbar_wait(afull + st0, ph0);
+        if (two) mbar_wait(afull + st1, ph1);
         tc_fence_after();
         if (elect_one()) {
 #pragma unroll
-          for (int s = 0; s < 2; ++s) {
-            const uint32_t a_tm = tmem + kACol0 + 32 * st + 16 * s;
-            const uint32_t e_tm = tmem + kMetaCol0 + 4 * st + 2 * s;
+          for (int u = 0; u < 2; ++u) {
+            if (u == 1 && !two) break;
+            const uint32_t st = u ? st1 : st0;
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
+            for (int s = 0; s < 2; ++s) {
+              const uint32_t a_tm = tmem + kACol0 + 32 * st + 16 * s;
+              const uint32_t e_tm = tmem + kMetaCol0 + 4 * st + 2 * s;
 #pragma unroll
-              for (int blk = 0; blk < 2; ++blk) {
-                // side a: Re += X, Im += Y;  side b: Re -= Y, Im += X
-                const int rows = s ? (blk ? 0 : 64) : (blk ? 64 : 0);
-                const uint64_t bd = br + (uint64_t)((h * 4 * 2048 + rows * 16) >> 4);
-                umma_sp_ts(dcol + blk * 64, a_tm + h * 8, bd,
-                           idesc | ((s && !blk) ? kNegA : 0u),
-                           (s > 0 || h > 0 || r > 0) ? 1u : 0u, e_tm);
+              for (int h = 0; h < 2; ++h) {
+#pragma unroll
+                for (int blk = 0; blk < 2; ++blk) {
+                  // side a: Re += X, Im += Y;  side b: Re -= Y, Im += X
+                  const int rows = s ? (blk ? 0 : 64) : (blk ? 64 : 0);
+                  const uint64_t bd =
+                      br + (uint64_t)((u * kRoundBytes + h * 4 * 2048 + rows * 16) >> 4);
+                  umma_sp_ts(dcol + blk * 64, a_tm + h * 8, bd,
+                             idesc | ((s && !blk) ? kNegA : 0u),
+                             (u > 0 || s > 0 || h > 0 || r > 0) ? 1u : 0u, e_tm);
+                }
               }
             }
+            tc_commit(aempty + st);
           }
-          tc_commit(aempty + st);
         }
         __syncwarp();
+        br += (uint64_t)((2 * kRoundBytes) >> 4);
+        gst += two ? 2u : 1u;  // the stages of the rounds just issued
+        if (gst >= kAStages) {
+          gst -= kAStages;
+          gph ^= 1u;
+        }
       }
       if (elect_one()) tc_commit(dfull + db);
       __syncwarp();
