@@ -412,7 +412,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_sp_score(SpArgs a) {
         // round stage of global round g = R tile + r
         const uint32_t g = (uint32_t)(R * k + r), st = g % kAStages, use = g / kAStages;
         if (use > 0) {
-          mbar_wait(aempty + st, (use - 1) & 1u);
+          mbar_wait_sleep(aempty + st, (use - 1) & 1u);  // back off: spinning takes issue slots from the MMA warp
           tc_fence_after();
         }
 #pragma unroll
