@@ -579,6 +579,37 @@ def test_sparse_tc_matches_dense_tc(G, Gq, n, monkeypatch):
     assert fx.rel_err(out_sp, out_dense) <= 1e-5
 
 
+@pytest.mark.parametrize("dense", [False, True])
+def test_tc_long_context_phases_vs_oracle(G, dense, monkeypatch):
+    """Both tcgen05 score kernels far from the query (Delta ~ 1e6) and past
+    two 8192-token work items: the sparse kernel advances each warp's phases
+    by e^{i 128 theta} per tile from an fp64-reduced base per item, the dense
+    one per token from an fp64 base per tile.  Outputs vs the oracle within
+    the 1e-3 bar, with a non-zero position_offset and a ragged last tile."""
+    if dense:
+        monkeypatch.setenv("CVQ_TC_DENSE", "1")
+    kq = KQ(128, 64, 64, 11)
+    nc, n, Gq, off = 128, 16384 + 77, 4, 5
+    rng = P.rng(2024)
+    atoms = rng.normal(2 * kq.n_atoms, 0.3)
+    vrows = rng.normal(nc * 128, 1 / 16).reshape(nc, 128)
+    a, b = fx.random_key_codes(kq, n, rng=rng)
+    bits = fx.random_value_codes(nc, n, rng=rng)
+    c = G.QuantizedKVCache(kq, nc, n_kv_heads=1, q_per_kv=Gq, capacity=n, keys="tc",
+                           position_offset=off)
+    c.set_key_codebook(0, 0, atoms)
+    c.set_value_quantizer(0, 0, vrows)
+    c.import_stream(0, 0, 0, P.pack_key_codes(kq, a, b), P.pack_value_codes(bits), n)
+    q = rng.normal(Gq * 128).reshape(1, 1, Gq, 128).astype(np.float32)
+    t = off + n - 1 + 1_000_000
+    out = c.attention(q, t)
+    for j in range(Gq):
+        # the oracle's keys sit at positions 0..n-1: shift the query instead
+        want, _, _ = P.fused_attention(kq, atoms, a, b, bits, vrows,
+                                       q[0, 0, j].astype(np.float64), t - off)
+        assert fx.rel_err(out[0, 0, j], want) <= 1e-3, j
+
+
 def test_tc_at_bench_scale_vs_fp32_and_oracle(G):
     """The default tcgen05 path at the C3 context length (128K tokens, 16
     persistent work items per stream, 4 streams x 4 q heads): all rows vs the
