@@ -47,9 +47,9 @@ constexpr int kEpiWarps = 16;
 constexpr int kProdWarps = 8;             // warp 16 + p: TMEM lane quarter p & 3, rounds r = p >> 2 (mod 2)
 constexpr int kMmaWarp = kEpiWarps + kProdWarps;  // MMA issuer + codebook loader
 constexpr int kThreads = (kMmaWarp + 1) * 32;
-constexpr int kAStages = 6;               // round stages: both sides of one round (32 + 2 metadata columns)
+constexpr int kAStages = 6;               // round stages: both sides of one round (32 + 4 metadata columns)
 constexpr uint32_t kACol0 = 256;          // round stage st: side s at columns 256 + 32 st + 16 s
-constexpr uint32_t kMetaCol0 = 448;       // its metadata: column 448 + 4 st + 2 s
+constexpr uint32_t kMetaCol0 = kACol0 + 32 * kAStages;  // its metadata: column kMetaCol0 + 4 st + 2 s
 constexpr int kRoundBytes = 128 * 64 * 2;  // 16 KiB [X; Y] x 64 levels
 constexpr uint32_t kTmemCols = 512;
 
@@ -212,6 +212,7 @@ struct SpIter {
 template <int R, int G>
 __global__ void __launch_bounds__(kThreads, 1) k_sp_score(SpArgs a) {
   static_assert(G == 1 || G == 4, "heads per KV stream");
+  static_assert(kMetaCol0 + 4 * kAStages <= kTmemCols, "TMEM columns");
   constexpr int NSTEP = 2 * R;
   constexpr int NW = (NSTEP * 6 + 63 + 63) / 64;  // raw words covering a token's record
   extern __shared__ __align__(1024) unsigned char smem[];
