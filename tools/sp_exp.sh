@@ -1,4 +1,6 @@
-# A/B experiments on the sparse score kernel (compile-time switches);
+# A/B experiments on the sparse score kernel (compile-time switches; the round-1
+# switches SP_EXP_MMA_ONLY / NO_EPI / NO_STTM / NO_AWAIT / TIMING were measured
+# and then removed from attn_sp.cu);
 # SP_EXPS = comma-separated flag sets, e.g. "-DA,-DA -DB"
 IFS=',' read -ra SETS <<< "${SP_EXPS:-}"
 [ ${#SETS[@]} -eq 0 ] && SETS=("")

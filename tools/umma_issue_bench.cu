@@ -164,6 +164,105 @@ __global__ void kres(int tiles, int ms, long long* out) {
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
 }
 
+
+// kres with `nprod` extra warps hammering tcgen05.st (x16 zeros into the A
+// stage columns 256..447, wait::st each time) and `nld` warps doing
+// tcgen05.ld x16 of the accumulator columns: does TMEM store / load traffic
+// slow the sparse MMAs?
+__global__ void kres2(int tiles, int nprod, int nld, long long* out) {
+  extern __shared__ __align__(1024) unsigned char sm[];
+  __shared__ uint32_t slot;
+  __shared__ __align__(8) uint64_t bar[8];
+  __shared__ volatile int done;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  for (int i = tid; i < 176 * 1024 / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(sm)[i] = 0;
+  if (tid == 0) done = 0;
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(&slot)), "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (tid < 8) asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(&bar[tid])), "r"(1));
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = slot;
+  if (warp < 4) {
+    for (int c = 256; c < 512; ++c)
+      asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" ::"r"(tmem + ((uint32_t)(warp * 32) << 16) + c),
+                   "r"(c >= 448 ? 0x44444444u : 0u) : "memory");
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const int w = warp;
+  if (w == 4) {
+    const uint32_t idesc = (1u << 4) | (8u << 17) | (8u << 24) | (1u << 2);
+    const uint32_t sB = su32(sm);
+    long long t0 = clock64();
+    for (int t = 0; t < tiles; ++t) {
+      const uint32_t d = tmem + (uint32_t)((t & 1) * 128);
+      for (int r = 0; r < 11; ++r) {
+        for (int s = 0; s < 2; ++s) {
+          const uint32_t st = (uint32_t)((r * 2 + s) % 6);
+          const uint32_t a_tm = tmem + 256 + st * 32 + s * 16;
+          const uint32_t te = tmem + 448 + st * 4 + 2 * s;
+          for (int h = 0; h < 2; ++h) {
+            for (int blk = 0; blk < 2; ++blk) {
+              const uint32_t rows = (uint32_t)(s ? (blk ? 0 : 64) : (blk ? 64 : 0));
+              const uint64_t bd = sdesc(sB + r * 16384 + h * 4 * 2048 + rows * 16, 2048, 128);
+              const uint32_t id = idesc | ((s && !blk) ? (1u << 13) : 0u);
+              if (elect_one())
+                asm volatile("{.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                             "tcgen05.mma.sp.cta_group::1.kind::f16 [%0], [%1], %2, [%5], %3, p;}" ::"r"(d + blk * 64),
+                             "r"(a_tm + h * 8), "l"(bd), "r"(id), "r"(r | s | h), "r"(te));
+              __syncwarp();
+            }
+          }
+        }
+      }
+    }
+    if (elect_one())
+      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(&bar[0])) : "memory");
+    uint32_t ok = 0;
+    while (!ok)
+      asm volatile("{.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;}"
+                   : "=r"(ok) : "r"(su32(&bar[0])), "r"(0) : "memory");
+    if (blockIdx.x == 0 && (tid & 31) == 0) out[0] = clock64() - t0;
+    if ((tid & 31) == 0) done = 1;
+  } else if (w >= 8 && w < 8 + nprod) {
+    const uint32_t lane_base = (uint32_t)((w & 3) * 32) << 16;
+    uint32_t v[16];
+    for (int i = 0; i < 16; ++i) v[i] = 0u;
+    uint32_t st = 0;
+    while (!done) {
+      asm volatile("tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, %16};"
+                   ::"r"(tmem + lane_base + 256 + 16 * st), "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]),
+                   "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]) : "memory");
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      st = st == 11 ? 0 : st + 1;
+    }
+  } else if (w >= 24 && w < 24 + nld) {
+    const uint32_t lane_base = (uint32_t)((w & 3) * 32) << 16;
+    uint32_t acc = 0;
+    while (!done) {
+      uint32_t v[16];
+      asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15}, [%16];"
+                   : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+                     "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+                   : "r"(tmem + lane_base));
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      acc += v[0] ^ v[15];
+    }
+    if (acc == 12345u) out[1] = acc;
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+}
+
 template <int SP, int ATM, int N>
 void run(int iss, long long* d) {
   auto k = kb<SP, ATM, N>;
@@ -193,7 +292,7 @@ int main() {
   run<1, 1, 64>(1, d);
   {
     cudaFuncSetAttribute(kres, cudaFuncAttributeMaxDynamicSharedMemorySize, 176 * 1024);
-   for (int ms : {8, 4, 2, 1}) {
+   for (int ms : {4, 2}) {
     kres<<<148, 128, 176 * 1024>>>(2, ms, d);
     kres<<<148, 128, 176 * 1024>>>(64, ms, d);
     cudaError_t e = cudaDeviceSynchronize();
@@ -204,6 +303,22 @@ int main() {
            cyc / 64.0, cyc / 64.0 / 88, cyc / 64.0 / 128);
     printf("  (metadata column stride %d)\n", ms);
    }
+  }
+  {
+    cudaFuncSetAttribute(kres2, cudaFuncAttributeMaxDynamicSharedMemorySize, 176 * 1024);
+    long long* d2;
+    cudaMalloc(&d2, 16);
+    const int cfg[][2] = {{0, 0}, {8, 0}, {16, 0}, {0, 8}, {8, 8}};
+    for (auto& c : cfg) {
+      kres2<<<148, 1024, 176 * 1024>>>(2, c[0], c[1], d2);
+      kres2<<<148, 1024, 176 * 1024>>>(64, c[0], c[1], d2);
+      cudaError_t e = cudaDeviceSynchronize();
+      if (e != cudaSuccess) { printf("err %s\n", cudaGetErrorString(e)); exit(1); }
+      long long cyc = 0;
+      cudaMemcpy(&cyc, d2, 8, cudaMemcpyDeviceToHost);
+      printf("kres2 store-warps=%d load-warps=%d: %.1f clk per 128-token tile (88 sparse N=64 MMAs), %.1f clk/mma\n",
+             c[0], c[1], cyc / 64.0, cyc / 64.0 / 88);
+    }
   }
   return 0;
 }
