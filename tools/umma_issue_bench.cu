@@ -263,6 +263,95 @@ __global__ void kres2(int tiles, int nprod, int nld, long long* out) {
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
 }
 
+
+// kres with the per-round synchronisation of the real kernel: mode bit 0 =
+// tcgen05.commit to an mbarrier after every round (nobody waits on it), bit 1
+// = mbarrier try_wait on an already-completed barrier + tcgen05 fence before
+// every round, bit 2 = rounds issued in pairs (one elected region of 16).
+__global__ void kres3(int tiles, int mode, long long* out) {
+  extern __shared__ __align__(1024) unsigned char sm[];
+  __shared__ uint32_t slot;
+  __shared__ __align__(8) uint64_t bar[16];
+  const int tid = threadIdx.x, warp = tid >> 5;
+  for (int i = tid; i < 176 * 1024 / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(sm)[i] = 0;
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(&slot)), "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (tid < 16) asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(&bar[tid])), "r"(tid < 8 ? 1 : 1));
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  __syncthreads();
+  // complete phase 0 of barriers 8..15 (the "already full" stages)
+  if (tid >= 8 && tid < 16) asm volatile("{.reg .b64 st;\n\tmbarrier.arrive.shared::cta.b64 st, [%0];}" ::"r"(su32(&bar[tid])) : "memory");
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = slot;
+  if (warp < 4) {
+    for (int c = 256; c < 512; ++c)
+      asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" ::"r"(tmem + ((uint32_t)(warp * 32) << 16) + c),
+                   "r"(c >= 448 ? 0x44444444u : 0u) : "memory");
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  if (warp == 0) {
+    const uint32_t idesc = (1u << 4) | (8u << 17) | (8u << 24) | (1u << 2);
+    const uint32_t sB = su32(sm);
+    const int per = (mode & 4) ? 2 : 1;
+    long long t0 = clock64();
+    for (int t = 0; t < tiles; ++t) {
+      const uint32_t d = tmem + (uint32_t)((t & 1) * 128);
+#pragma unroll 1
+      for (int r0 = 0; r0 < 11; r0 += per) {
+        if (mode & 2) {
+          uint32_t ok = 0;
+          while (!ok)
+            asm volatile("{.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;}"
+                         : "=r"(ok) : "r"(su32(&bar[8 + (r0 % 6)])), "r"(0) : "memory");
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        }
+        if (elect_one()) {
+          for (int u = 0; u < per; ++u) {
+            const int r = r0 + u;
+            if (r >= 11) break;
+            for (int s = 0; s < 2; ++s) {
+              const uint32_t st = (uint32_t)(r % 6);
+              const uint32_t a_tm = tmem + 256 + st * 32 + s * 16;
+              const uint32_t te = tmem + 448 + st * 4 + 2 * s;
+              for (int h = 0; h < 2; ++h) {
+                for (int blk = 0; blk < 2; ++blk) {
+                  const uint32_t rows = (uint32_t)(s ? (blk ? 0 : 64) : (blk ? 64 : 0));
+                  const uint64_t bd = sdesc(sB + r * 16384 + h * 4 * 2048 + rows * 16, 2048, 128);
+                  const uint32_t id = idesc | ((s && !blk) ? (1u << 13) : 0u);
+                  asm volatile("{.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                               "tcgen05.mma.sp.cta_group::1.kind::f16 [%0], [%1], %2, [%5], %3, p;}" ::"r"(d + blk * 64),
+                               "r"(a_tm + h * 8), "l"(bd), "r"(id), "r"(r | s | h), "r"(te));
+                }
+              }
+            }
+            if (mode & 1)
+              asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(&bar[1 + (r % 6)])) : "memory");
+          }
+        }
+        __syncwarp();
+      }
+    }
+    if (elect_one())
+      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(&bar[0])) : "memory");
+    uint32_t ok = 0;
+    while (!ok)
+      asm volatile("{.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;}"
+                   : "=r"(ok) : "r"(su32(&bar[0])), "r"(0) : "memory");
+    if (blockIdx.x == 0 && (tid & 31) == 0) out[0] = clock64() - t0;
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+}
+
 template <int SP, int ATM, int N>
 void run(int iss, long long* d) {
   auto k = kb<SP, ATM, N>;
@@ -318,6 +407,21 @@ int main() {
       cudaMemcpy(&cyc, d2, 8, cudaMemcpyDeviceToHost);
       printf("kres2 store-warps=%d load-warps=%d: %.1f clk per 128-token tile (88 sparse N=64 MMAs), %.1f clk/mma\n",
              c[0], c[1], cyc / 64.0, cyc / 64.0 / 88);
+    }
+  }
+  {
+    cudaFuncSetAttribute(kres3, cudaFuncAttributeMaxDynamicSharedMemorySize, 176 * 1024);
+    long long* d3;
+    cudaMalloc(&d3, 16);
+    for (int mode : {0, 1, 2, 3, 4, 5, 7}) {
+      kres3<<<148, 128, 176 * 1024>>>(2, mode, d3);
+      kres3<<<148, 128, 176 * 1024>>>(64, mode, d3);
+      cudaError_t e = cudaDeviceSynchronize();
+      if (e != cudaSuccess) { printf("err %s\n", cudaGetErrorString(e)); exit(1); }
+      long long cyc = 0;
+      cudaMemcpy(&cyc, d3, 8, cudaMemcpyDeviceToHost);
+      printf("kres3 commit=%d wait+fence=%d pairs=%d: %.1f clk per tile, %.1f clk/mma\n", mode & 1, (mode >> 1) & 1,
+             (mode >> 2) & 1, cyc / 64.0, cyc / 64.0 / 88);
     }
   }
   return 0;
