@@ -316,7 +316,7 @@ def main():
         ach_tf = flops / (avg_main_ms / 1e3) / 1e12
         # R = 11: the one-hot is a 2:4-sparse A operand (tcgen05.mma.sp,
         # attn_sp.cu) -- the ceiling is the sparse fp16 rate, twice the dense
-        sparse = R == 11 and os.environ.get("CVQ_TC_DENSE", "0") != "1"
+        sparse = R in (11, 21) and os.environ.get("CVQ_TC_DENSE", "0") != "1"
         peak_tf = TENSOR_NOMINAL_TFLOPS * (2 if sparse else 1)
         roof = {"bound": "tensor", "achieved": ach_tf, "peak": peak_tf,
                 "unit": "TFLOP/s", "frac": ach_tf / peak_tf,

@@ -248,9 +248,9 @@ typedef struct cvq_cache_desc {
  * GEMM (fp16 codebook operand, fp32 accumulators in TMEM); the fastest mode
  * on B200 (bench.py default).  Same precision class as CVQ_CACHE_KEYS_FP16.
  * Head presets (d=128, g=64, L=64, R in {11, 21}, 1 or 4 query heads per KV
- * head); other shapes run the CUDA-core kernels.  R = 11 uses the 2:4-sparse
- * variant (one-hot as the sparse operand); the environment variable
- * CVQ_TC_DENSE=1 selects the dense kernel instead. */
+ * head); other shapes run the CUDA-core kernels.  Both presets use the
+ * 2:4-sparse variant (one-hot as the sparse operand); the environment
+ * variable CVQ_TC_DENSE=1 selects the dense kernel instead. */
 #define CVQ_CACHE_KEYS_TC 2u
 
 CVQ_API cvq_status cvq_cache_create(cvq_context* ctx, const cvq_cache_desc* d,

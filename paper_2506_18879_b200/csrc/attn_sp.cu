@@ -51,6 +51,7 @@ constexpr int kAStages = 6;               // round stages: both sides of one rou
 constexpr uint32_t kACol0 = 256;          // round stage st: side s at columns 256 + 32 st + 16 s
 constexpr uint32_t kMetaCol0 = kACol0 + 32 * kAStages;  // its metadata: column kMetaCol0 + 4 st + 2 s
 constexpr int kRoundBytes = 128 * 64 * 2;  // 16 KiB [X; Y] x 64 levels
+constexpr int kRPart = 11;                // rounds resident per CTA (176 KiB); 2-bit = 2 parts
 constexpr uint32_t kTmemCols = 512;
 
 __device__ __forceinline__ uint32_t su32(const void* p) {
@@ -169,15 +170,17 @@ struct SpArgs {
   const double* thetas;
   long long t, pos0, n;
   int chunk;             // tokens per work item (multiple of kTok)
-  int cps;               // work items per stream
+  int cps;               // work items per (stream, round part)
   int n_items;
-  float* ps;             // [S][n][G]
+  int rtot;              // rounds of the preset (11, 21)
+  int js;                // round parts of <= RP rounds (scores are linear in K)
+  float* ps;             // [S][js][n][G] partial scores
 };
 
 // This CTA's tiles in order; each CTA owns a contiguous range of work items
 // (so consecutive items mostly share a stream and its codebook slot).
 struct SpIter {
-  int item, end, s;
+  int item, end, s, part, r0, nr;  // stream, round part, its first round and round count
   long long ti, hi;
   bool item_start;
   __device__ bool first(const SpArgs& a) {
@@ -189,7 +192,10 @@ struct SpIter {
   }
   __device__ bool setup(const SpArgs& a) {
     while (item < end) {
-      s = item / a.cps;
+      s = item / (a.cps * a.js);
+      part = (item / a.cps) % a.js;
+      r0 = part * kRPart;
+      nr = min(kRPart, a.rtot - r0);
       ti = (long long)(item % a.cps) * a.chunk;
       hi = min(a.n, ti + a.chunk);
       item_start = true;
@@ -209,7 +215,7 @@ struct SpIter {
   __device__ bool last_of_item() const { return ti + kTok >= hi; }
 };
 
-template <int R, int G>
+template <int R, int G>  // R = rounds per part (kRPart)
 __global__ void __launch_bounds__(kThreads, 1) k_sp_score(SpArgs a) {
   static_assert(G == 1 || G == 4, "heads per KV stream");
   static_assert(kMetaCol0 + 4 * kAStages <= kTmemCols, "TMEM columns");
@@ -360,7 +366,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_sp_score(SpArgs a) {
         float v = 0.f;
 #pragma unroll
         for (int e2 = 0; e2 < 4; ++e2) v += rb[(e2 * 32 + lane) * G + eslot];
-        a.ps[((size_t)it.s * a.n + it.ti + tok) * G + eslot] = v;
+        a.ps[(((size_t)it.s * a.js + it.part) * a.n + it.ti + tok) * G + eslot] = v;
       }
     }
   } else if (warp < kEpiWarps + kProdWarps) {
@@ -373,7 +379,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_sp_score(SpArgs a) {
     auto load_raw = [&](const SpIter& x, uint64_t* raw, uint32_t& off) {
       const uint64_t* kw = a.kpool + (size_t)x.s * a.kstride;
       const long long tok = x.ti + (t < x.valid() ? t : 0);
-      const unsigned long long b0 = (unsigned long long)tok * (NSTEP * 6);
+      // this part's fields start 12 r0 bits into the token's 12 rtot-bit record
+      const unsigned long long b0 = (unsigned long long)tok * (12u * a.rtot) + 12u * x.r0;
       off = (uint32_t)(b0 & 63u);
 #pragma unroll
       for (int i = 0; i < NW; ++i) raw[i] = __ldg(kw + (b0 >> 6) + i);
@@ -381,7 +388,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_sp_score(SpArgs a) {
     uint64_t raw[NW], nraw[NW];
     uint32_t off = 0, noff = 0;
     SpIter it;
-    int k = 0;
+    uint32_t gbase = 0;  // rounds of the previous tiles (stage accounting)
     bool ok = it.first(a);
     if (ok) load_raw(it, raw, off);
     const int src = (lane & 7) | (lane & 16);
@@ -406,12 +413,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_sp_score(SpArgs a) {
         ++i;
       }
 #pragma unroll 1
-      for (int r = sub; r < R; r += 2) {
+      for (int r = sub; r < it.nr; r += 2) {
         const uint32_t fld = (uint32_t)pk0 & 0xFFFu;
         pk0 = (pk0 >> 12) | (pk1 << 48);
         pk1 >>= 12;
-        // round stage of global round g = R tile + r
-        const uint32_t g = (uint32_t)(R * k + r), st = g % kAStages, use = g / kAStages;
+        // round stage of this CTA's global round g
+        const uint32_t g = gbase + (uint32_t)r, st = g % kAStages, use = g / kAStages;
         if (use > 0) {
           mbar_wait_sleep(aempty + st, (use - 1) & 1u);  // back off: spinning takes issue slots from the MMA warp
           tc_fence_after();
@@ -444,9 +451,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_sp_score(SpArgs a) {
 #pragma unroll
       for (int i = 0; i < NW; ++i) raw[i] = nraw[i];
       off = noff;
+      gbase += (uint32_t)it.nr;
       it = nx;
       ok = okn;
-      ++k;
     }
   } else if (warp == kMmaWarp) {
     // ============ tcgen05.mma.sp issuer (warp-uniform walk, elected lane) ==
@@ -460,7 +467,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_sp_score(SpArgs a) {
     for (bool ok = it.first(a); ok; ok = it.next(a), ++k) {
       const int db = k & 1;
       if (it.item_start) {
-        const int slot = it.s % a.n_slots;
+        const int slot = (it.s % a.n_slots) * a.js + it.part;  // (codebook slot, round part)
         if (slot != prev_slot) {
           // (re)load the resident codebook: once every MMA reading the old
           // one has completed (rare: work items are contiguous per CTA)
@@ -470,9 +477,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_sp_score(SpArgs a) {
             mbar_wait(cbempty, (nload - 1) & 1);
           }
           if (elect_one()) {
-            const uint16_t* src = a.cb + (size_t)slot * a.slot_elems;
-            mbar_arrive_tx(cbfull, R * kRoundBytes);
-            for (int r = 0; r < R; ++r)
+            const uint16_t* src = a.cb + (size_t)(it.s % a.n_slots) * a.slot_elems +
+                                  (size_t)it.r0 * (kRoundBytes / 2);
+            mbar_arrive_tx(cbfull, (uint32_t)it.nr * kRoundBytes);
+            for (int r = 0; r < it.nr; ++r)
               bulk_g2s(cbs + r * kRoundBytes, src + (size_t)r * (kRoundBytes / 2), kRoundBytes,
                        cbfull);
           }
@@ -493,8 +501,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_sp_score(SpArgs a) {
       // round's stage is released by its own commit
       uint64_t br = bdesc0;
 #pragma unroll 1
-      for (int r = 0; r < R; r += 2) {
-        const bool two = r + 1 < R;
+      for (int r = 0; r < it.nr; r += 2) {
+        const bool two = r + 1 < it.nr;
         const uint32_t st0 = gst, ph0 = gph;
         uint32_t st1 = gst + 1, ph1 = gph;
         if (st1 == kAStages) {
@@ -571,7 +579,9 @@ cudaError_t launch_sp(const SpArgs& a, cudaStream_t st) {
 
 }  // namespace
 
-bool sp_supported(int R) { return R == 11; }
+bool sp_supported(int R) { return R == 11 || R == 21; }
+
+int sp_parts(int R) { return (R + kRPart - 1) / kRPart; }
 
 size_t sp_codebook_elems(int R) { return sp_supported(R) ? (size_t)R * (kRoundBytes / 2) : 0; }
 
@@ -607,10 +617,12 @@ cudaError_t run_sp_score(const AttnJob& job, const uint16_t* cb, size_t slot_ele
   a.n = job.n;
   a.chunk = (chunk + kTok - 1) / kTok * kTok;
   a.cps = (int)((job.n + a.chunk - 1) / a.chunk);
-  a.n_items = job.S * a.cps;
+  a.rtot = g.R;
+  a.js = sp_parts(g.R);
+  a.n_items = job.S * a.js * a.cps;
   a.ps = ps;
-  if (g.G == 4) return launch_sp<11, 4>(a, st);
-  if (g.G == 1) return launch_sp<11, 1>(a, st);
+  if (g.G == 4) return launch_sp<kRPart, 4>(a, st);
+  if (g.G == 1) return launch_sp<kRPart, 1>(a, st);
   return cudaErrorInvalidValue;
 }
 

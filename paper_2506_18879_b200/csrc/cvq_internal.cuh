@@ -68,6 +68,7 @@ cudaError_t run_tc_score(const AttnJob& job, const float* q, float* ps, int chun
 // 2:4-sparse tcgen05 score kernel (attn_sp.cu), R = 11: B blocks per slot
 // [R][X rows | Y rows][64 levels] fp16, built by sp_build_codebook.
 bool sp_supported(int R);
+int sp_parts(int R);  // round parts (<= 11 resident rounds each) -> partial-score slices
 size_t sp_codebook_elems(int R);
 void sp_build_codebook(int R, const double* xy, uint16_t* out, uint16_t (*to_half)(double));
 cudaError_t run_sp_score(const AttnJob& job, const uint16_t* cb, size_t slot_elems,

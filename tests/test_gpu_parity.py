@@ -552,14 +552,18 @@ def test_mha_one_query_head_per_stream(G, preset, n, keys):
     assert worst <= 1e-3, worst
 
 
-@pytest.mark.parametrize("Gq,n", [(4, 1), (4, 127), (4, 129), (4, 8197), (1, 300), (1, 20000)])
-def test_sparse_tc_matches_dense_tc(G, Gq, n, monkeypatch):
-    """The 2:4-sparse tcgen05 kernel (attn_sp.cu, 1-bit preset) against the
-    dense one-hot tcgen05 kernel (CVQ_TC_DENSE=1) on the same cache: same
-    fp16 codebook, fp32 accumulation in another order, so outputs agree to
-    1e-5 relative; 3 layers x 2 KV heads exercise codebook-slot reloads."""
-    kq = KQ(128, 64, 64, 11)
-    nc, Ly, H = 128, 3, 2
+@pytest.mark.parametrize("R,Gq,n", [(11, 4, 1), (11, 4, 127), (11, 4, 129), (11, 4, 8197),
+                                    (11, 1, 300), (11, 1, 20000), (21, 4, 1000), (21, 4, 9001),
+                                    (21, 1, 4099)])
+def test_sparse_tc_matches_dense_tc(G, R, Gq, n, monkeypatch):
+    """The 2:4-sparse tcgen05 kernel (attn_sp.cu) against the dense one-hot
+    tcgen05 kernel (CVQ_TC_DENSE=1) on the same cache: same fp16 codebook,
+    fp32 accumulation in another order, so outputs agree to 1e-5 relative.
+    3 layers x 2 KV heads exercise codebook-slot reloads; the 2-bit preset
+    (R = 21) runs as two round parts of 11 and 10 resident rounds whose
+    partial scores the value kernel sums."""
+    kq = KQ(128, 64, 64, R)
+    nc, Ly, H = (128 if R == 11 else 256), 3, 2
     rng = P.rng(n + Gq)
     c = G.QuantizedKVCache(kq, nc, n_layers=Ly, n_kv_heads=H, q_per_kv=Gq, capacity=n, keys="tc")
     for layer in range(Ly):
