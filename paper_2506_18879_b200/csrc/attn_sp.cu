@@ -33,8 +33,18 @@
 //   theta_j} / sqrt(d) is per warp (fp64-based at a work item's first tile,
 //   advanced by e^{+i 128 theta_j} per tile); a 4-warp smem sum per quarter.
 //
+// * CTA pairs (CVQ_TC_PAIR=1, experimental, off by default): clusters of 2
+//   with tcgen05 cta_group::2 -- one MMA covers 256 tokens x N = 128. Each
+//   CTA keeps half of B: rank 0 P = X, Q = Y; rank 1 P = Y, Q = -X, so side a
+//   is [X ; Y] over the P halves and side b is -[Y ; -X] over the Q halves
+//   (negate-A).  Producers of both CTAs arrive on the leader's stage
+//   barriers, the leader's commits multicast to both.  Exact (same parity
+//   tests), but 14.4 ms against 10.6 ms at C3.
+//
 // Codebook precision fp16 (as CVQ_CACHE_KEYS_FP16), accumulation fp32.
 #include <cuda_fp16.h>
+
+#include <cstdlib>
 
 #include "cvq_internal.cuh"
 
@@ -124,6 +134,39 @@ __device__ __forceinline__ void umma_sp_ts(uint32_t d, uint32_t a, uint64_t b, u
       "tcgen05.mma.sp.cta_group::1.kind::f16 [%0], [%1], %2, [%5], %3, p;}" ::"r"(d),
       "r"(a), "l"(b), "r"(idesc), "r"(accum), "r"(e));
 }
+// arrive on the mbarrier at the same smem offset in CTA `cta` of the cluster
+__device__ __forceinline__ void mbar_arrive_cluster(uint64_t* bar, uint32_t cta) {
+  asm volatile(
+      "{.reg .b32 ra;\n\tmapa.shared::cluster.u32 ra, %0, %1;\n\t"
+      "mbarrier.arrive.release.cluster.shared::cluster.b64 _, [ra];}" ::"r"(su32(bar)),
+      "r"(cta)
+      : "memory");
+}
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::
+                   : "memory");
+}
+// CTA-pair MMA (M = 256: 128 token rows of A in each CTA's TMEM, half of the
+// N rows of B in each CTA's smem), issued by the leader CTA only
+__device__ __forceinline__ void umma_sp_ts_pair(uint32_t d, uint32_t a, uint64_t b, uint32_t idesc,
+                                                uint32_t accum, uint32_t e) {
+  asm volatile(
+      "{.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.sp.cta_group::2.kind::f16 [%0], [%1], %2, [%5], %3, p;}" ::"r"(d),
+      "r"(a), "l"(b), "r"(idesc), "r"(accum), "r"(e));
+}
+__device__ __forceinline__ void tc_commit_pair(uint64_t* bar) {  // arrives in both CTAs
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 "
+      "[%0], %1;" ::"r"(su32(bar)),
+      "h"((uint16_t)3)
+      : "memory");
+}
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t* v) {
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
@@ -169,7 +212,7 @@ struct SpArgs {
   const float* q;        // [S][G][128]
   const double* thetas;
   long long t, pos0, n;
-  int chunk;             // tokens per work item (multiple of kTok)
+  int chunk;             // tokens per work item (multiple of 2 kTok)
   int cps;               // work items per (stream, round part)
   int n_items;
   int rtot;              // rounds of the preset (11, 21)
@@ -179,13 +222,20 @@ struct SpArgs {
 
 // This CTA's tiles in order; each CTA owns a contiguous range of work items
 // (so consecutive items mostly share a stream and its codebook slot).
+template <bool PAIR>
 struct SpIter {
+  // a CTA pair walks 256-token pair tiles; CTA `rank` takes tokens
+  // [ti + 128 rank, +128) of each
+  static constexpr int kStep = PAIR ? 2 * kTok : kTok;
   int item, end, s, part, r0, nr;  // stream, round part, its first round and round count
   long long ti, hi;
   bool item_start;
+  int rank;
   __device__ bool first(const SpArgs& a) {
-    const int per = a.n_items / (int)gridDim.x, rem = a.n_items % (int)gridDim.x;
-    const int b = (int)blockIdx.x;
+    rank = PAIR ? (int)(blockIdx.x & 1) : 0;
+    const int units = PAIR ? (int)gridDim.x / 2 : (int)gridDim.x;
+    const int per = a.n_items / units, rem = a.n_items % units;
+    const int b = PAIR ? (int)blockIdx.x / 2 : (int)blockIdx.x;
     item = b * per + min(b, rem);
     end = item + per + (b < rem ? 1 : 0);
     return setup(a);
@@ -205,17 +255,21 @@ struct SpIter {
     return false;
   }
   __device__ bool next(const SpArgs& a) {
-    ti += kTok;
+    ti += kStep;
     item_start = false;
     if (ti < hi) return true;
     ++item;
     return setup(a);
   }
-  __device__ int valid() const { return (int)min((long long)kTok, hi - ti); }
-  __device__ bool last_of_item() const { return ti + kTok >= hi; }
+  __device__ long long base() const { return ti + (long long)rank * kTok; }
+  // tokens of this CTA in the tile (0 for the second CTA of a short last tile)
+  __device__ int valid() const { return (int)max(0ll, min((long long)kTok, hi - base())); }
 };
 
-template <int R, int G>  // R = rounds per part (kRPart)
+// PAIR: CTA pairs (cluster of 2) with tcgen05 cta_group::2 -- one MMA covers
+// 256 tokens and N = 128 ([Re | Im] in one instruction per side), each CTA
+// holding half of the B rows (attn_sp.cu header, "CTA pairs").
+template <int R, int G, bool PAIR>  // R = rounds per part (kRPart)
 __global__ void __launch_bounds__(kThreads, 1) k_sp_score(SpArgs a) {
   static_assert(G == 1 || G == 4, "heads per KV stream");
   static_assert(kMetaCol0 + 4 * kAStages <= kTmemCols, "TMEM columns");
@@ -233,27 +287,37 @@ __global__ void __launch_bounds__(kThreads, 1) k_sp_score(SpArgs a) {
   uint64_t* dempty = dfull + 2;
   uint64_t* cbfull = dempty + 2;
   uint64_t* cbempty = cbfull + 1;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(cbempty + 1);
+  uint64_t* cbpeer = cbempty + 1;  // PAIR: the second CTA's codebook half is in
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(cbpeer + 1);
+  const uint32_t rank = PAIR ? cluster_rank() : 0u;
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
   if (warp == kMmaWarp) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                     su32(tmem_slot)),
-                 "r"(kTmemCols));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    if constexpr (PAIR) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                       su32(tmem_slot)),
+                   "r"(kTmemCols));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                       su32(tmem_slot)),
+                   "r"(kTmemCols));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
   }
   if (tid == 0) {
     for (int i = 0; i < kAStages; ++i) {
-      mbar_init(afull + i, 4);  // one producer warp per lane quarter
+      mbar_init(afull + i, PAIR ? 8 : 4);  // one producer warp per lane quarter (per CTA)
       mbar_init(aempty + i, 1);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(dfull + i, 1);
-      mbar_init(dempty + i, kEpiWarps);
+      mbar_init(dempty + i, PAIR ? 2 * kEpiWarps : kEpiWarps);
     }
     mbar_init(cbfull, 1);
     mbar_init(cbempty, 1);
+    mbar_init(cbpeer, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   // per-lane phase table e^{+i lane theta_j}
@@ -264,7 +328,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_sp_score(SpArgs a) {
     etab[e] = make_float2((float)cs, (float)sn);
   }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (PAIR) cluster_sync_all();  // barriers of both CTAs initialised
+  else __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
@@ -280,19 +345,19 @@ __global__ void __launch_bounds__(kThreads, 1) k_sp_score(SpArgs a) {
     float2 step;
     {
       double sn, cs;
-      sincos((double)kTok * theta, &sn, &cs);  // e^{+i 128 theta}: one tile later
+      sincos((double)SpIter<PAIR>::kStep * theta, &sn, &cs);  // e^{+i step theta}: one tile later
       step = make_float2((float)cs, (float)sn);
     }
     float* wt = wtab + warp * (16 * 2 * G);
     const float sc = 0.08838834764831845f;  // 1 / sqrt(128)
     float2 ph = make_float2(1.f, 0.f);
     float2 qv[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
-    SpIter it;
+    SpIter<PAIR> it;
     int k = 0;
     for (bool ok = it.first(a); ok; ok = it.next(a), ++k) {
       const int db = k & 1;
       if (it.item_start) {
-        ph = phase_neg(a.t - (a.pos0 + it.ti + 32 * quarter), theta);
+        ph = phase_neg(a.t - (a.pos0 + it.base() + 32 * quarter), theta);
         const float* qs = a.q + (size_t)it.s * G * 128;
 #pragma unroll
         for (int u = 0; u < 2; ++u) {
@@ -328,7 +393,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_sp_score(SpArgs a) {
       asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(dempty + db);  // D[db] is in registers: free it
+      if (lane == 0) {  // D[db] is in registers: free it
+        if constexpr (PAIR) mbar_arrive_cluster(dempty + db, 0);
+        else mbar_arrive(dempty + db);
+      }
       const float2* E = etab + eslot * 16 * 32 + lane;
       float* rb = red + (size_t)((db * 4 + quarter) * 4) * 32 * G;  // [e][lane][G]
       if constexpr (G == 4) {
@@ -366,7 +434,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_sp_score(SpArgs a) {
         float v = 0.f;
 #pragma unroll
         for (int e2 = 0; e2 < 4; ++e2) v += rb[(e2 * 32 + lane) * G + eslot];
-        a.ps[(((size_t)it.s * a.js + it.part) * a.n + it.ti + tok) * G + eslot] = v;
+        a.ps[(((size_t)it.s * a.js + it.part) * a.n + it.base() + tok) * G + eslot] = v;
       }
     }
   } else if (warp < kEpiWarps + kProdWarps) {
@@ -376,9 +444,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_sp_score(SpArgs a) {
     const int p = warp - kEpiWarps, quarter = p & 3, sub = p >> 2;
     const uint32_t lane_base = (uint32_t)(quarter * 32) << 16;
     const int t = quarter * 32 + lane;
-    auto load_raw = [&](const SpIter& x, uint64_t* raw, uint32_t& off) {
+    auto load_raw = [&](const SpIter<PAIR>& x, uint64_t* raw, uint32_t& off) {
       const uint64_t* kw = a.kpool + (size_t)x.s * a.kstride;
-      const long long tok = x.ti + (t < x.valid() ? t : 0);
+      // rows past the end reuse a valid token's record (the epilogue skips them)
+      const int v = x.valid();
+      const long long tok = v > 0 ? x.base() + (t < v ? t : 0) : x.ti;
       // this part's fields start 12 r0 bits into the token's 12 rtot-bit record
       const unsigned long long b0 = (unsigned long long)tok * (12u * a.rtot) + 12u * x.r0;
       off = (uint32_t)(b0 & 63u);
@@ -387,7 +457,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_sp_score(SpArgs a) {
     };
     uint64_t raw[NW], nraw[NW];
     uint32_t off = 0, noff = 0;
-    SpIter it;
+    SpIter<PAIR> it;
     uint32_t gbase = 0;  // rounds of the previous tiles (stage accounting)
     bool ok = it.first(a);
     if (ok) load_raw(it, raw, off);
@@ -397,7 +467,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_sp_score(SpArgs a) {
 #pragma unroll
       for (int i = 0; i < NW; ++i)
         w[i] = off ? (raw[i] >> off) | (i + 1 < NW ? raw[i + 1] << (64u - off) : 0ull) : raw[i];
-      SpIter nx = it;
+      SpIter<PAIR> nx = it;
       const bool okn = nx.next(a);
       if (okn) load_raw(nx, nraw, noff);
       // this warp's rounds r = sub, sub + 2, ...: their 12-bit (a, b) fields
@@ -446,7 +516,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_sp_score(SpArgs a) {
         asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(afull + st);
+        if (lane == 0) {  // (PAIR: the leader's barrier counts both CTAs' rows)
+          if constexpr (PAIR) mbar_arrive_cluster(afull + st, 0);
+          else mbar_arrive(afull + st);
+        }
       }
 #pragma unroll
       for (int i = 0; i < NW; ++i) raw[i] = nraw[i];
@@ -461,7 +534,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_sp_score(SpArgs a) {
     constexpr uint32_t idesc = (1u << 2) | (1u << 4) | ((64u >> 3) << 17) | (8u << 24);
     constexpr uint32_t kNegA = 1u << 13;
     const uint64_t bdesc0 = sdesc(su32(cbs), 2048, 128);
-    SpIter it;
+    SpIter<PAIR> it;
     uint32_t nload = 0, gst = 0, gph = 0;  // stage / parity of the next round
     int k = 0, prev_slot = -1;
     for (bool ok = it.first(a); ok; ok = it.next(a), ++k) {
@@ -472,23 +545,91 @@ __global__ void __launch_bounds__(kThreads, 1) k_sp_score(SpArgs a) {
           // (re)load the resident codebook: once every MMA reading the old
           // one has completed (rare: work items are contiguous per CTA)
           if (nload > 0) {
-            if (elect_one()) tc_commit(cbempty);
+            // PAIR: the leader's commit arrives in both CTAs
+            if (rank == 0 && elect_one()) {
+              if constexpr (PAIR) tc_commit_pair(cbempty);
+              else tc_commit(cbempty);
+            }
             __syncwarp();
             mbar_wait(cbempty, (nload - 1) & 1);
           }
           if (elect_one()) {
+            // PAIR: this CTA's half, [P | Q] per round (sp2 layout)
             const uint16_t* src = a.cb + (size_t)(it.s % a.n_slots) * a.slot_elems +
-                                  (size_t)it.r0 * (kRoundBytes / 2);
+                                  (size_t)it.r0 * (PAIR ? kRoundBytes : kRoundBytes / 2);
             mbar_arrive_tx(cbfull, (uint32_t)it.nr * kRoundBytes);
             for (int r = 0; r < it.nr; ++r)
-              bulk_g2s(cbs + r * kRoundBytes, src + (size_t)r * (kRoundBytes / 2), kRoundBytes,
-                       cbfull);
+              bulk_g2s(cbs + r * kRoundBytes,
+                       src + (PAIR ? (size_t)r * kRoundBytes + rank * (kRoundBytes / 2)
+                                   : (size_t)r * (kRoundBytes / 2)),
+                       kRoundBytes, cbfull);
           }
           __syncwarp();
           mbar_wait(cbfull, nload & 1);
+          if constexpr (PAIR) {
+            if (rank == 1) {
+              if (lane == 0) mbar_arrive_cluster(cbpeer, 0);
+            } else {
+              mbar_wait(cbpeer, nload & 1);
+            }
+          }
           ++nload;
           prev_slot = slot;
         }
+      }
+      if constexpr (PAIR) {
+        if (rank != 0) continue;  // the peer CTA only loads its codebook half
+        if (k >= 2) {  // D buffer db was read by both CTAs' epilogues of tile k-2
+          mbar_wait(dempty + db, ((k - 2) >> 1) & 1);
+          tc_fence_after();
+        }
+        // M = 256 (both CTAs' tokens), N = 128: side a = [X ; Y] (P halves),
+        // side b = -[Y ; -X] (Q halves, negate-A) -> [Re | Im] of every token
+        constexpr uint32_t idesc2 = (1u << 2) | (1u << 4) | ((128u >> 3) << 17) | (16u << 24);
+        const uint64_t pdesc0 = sdesc(su32(cbs), 1024, 128);
+        const uint32_t dcol = tmem + (uint32_t)db * 128u;
+#pragma unroll 1
+        for (int r = 0; r < it.nr; r += 2) {
+          const bool two = r + 1 < it.nr;
+          const uint32_t st0 = gst, ph0 = gph;
+          uint32_t st1 = gst + 1, ph1 = gph;
+          if (st1 == kAStages) {
+            st1 = 0;
+            ph1 ^= 1u;
+          }
+          mbar_wait(afull + st0, ph0);
+          if (two) mbar_wait(afull + st1, ph1);
+          tc_fence_after();
+          if (elect_one()) {
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+              if (u == 1 && !two) break;
+              const uint32_t st = u ? st1 : st0;
+              const uint64_t pr = pdesc0 + (uint64_t)(((r + u) * kRoundBytes) >> 4);
+#pragma unroll
+              for (int s2 = 0; s2 < 2; ++s2) {
+                const uint32_t a_tm = tmem + kACol0 + 32 * st + 16 * s2;
+                const uint32_t e_tm = tmem + kMetaCol0 + 4 * st + 2 * s2;
+#pragma unroll
+                for (int h = 0; h < 2; ++h)
+                  umma_sp_ts_pair(dcol, a_tm + h * 8,
+                                  pr + (uint64_t)((s2 * (kRoundBytes / 2) + h * 4 * 1024) >> 4),
+                                  idesc2 | (s2 ? kNegA : 0u),
+                                  (u > 0 || s2 > 0 || h > 0 || r > 0) ? 1u : 0u, e_tm);
+              }
+              tc_commit_pair(aempty + st);
+            }
+          }
+          __syncwarp();
+          gst += two ? 2u : 1u;
+          if (gst >= kAStages) {
+            gst -= kAStages;
+            gph ^= 1u;
+          }
+        }
+        if (elect_one()) tc_commit_pair(dfull + db);
+        __syncwarp();
+        continue;
       }
       if (k >= 2) {  // D buffer db was read by the epilogue of tile k-2
         mbar_wait(dempty + db, ((k - 2) >> 1) & 1);
@@ -551,30 +692,56 @@ __global__ void __launch_bounds__(kThreads, 1) k_sp_score(SpArgs a) {
     }
   }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (PAIR) cluster_sync_all();  // the leader's MMAs into this CTA's TMEM are done
+  else __syncthreads();
   tc_fence_after();
-  if (warp == kMmaWarp)
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
-                 "r"(kTmemCols));
+  if (warp == kMmaWarp) {
+    if constexpr (PAIR)
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                   "r"(kTmemCols));
+    else
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                   "r"(kTmemCols));
+  }
 }
 
 size_t sp_smem(int G, int R) {
   return (size_t)R * kRoundBytes + 64 * 32 * 8 + (size_t)kEpiWarps * 16 * 2 * G * 4 +
-         (size_t)2 * 16 * 32 * G * 4 + (2 * kAStages + 6) * 8 + 16;
+         (size_t)2 * 16 * 32 * G * 4 + (2 * kAStages + 7) * 8 + 16;
 }
 
-template <int R, int G>
+template <int R, int G, bool PAIR>
 cudaError_t launch_sp(const SpArgs& a, cudaStream_t st) {
   const size_t sm = sp_smem(G, R);
-  cudaError_t e = ensure_dyn_smem(reinterpret_cast<const void*>(k_sp_score<R, G>), sm);
+  const void* fn = reinterpret_cast<const void*>(k_sp_score<R, G, PAIR>);
+  cudaError_t e = ensure_dyn_smem(fn, sm);
   if (e != cudaSuccess) return e;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int grid = a.n_items < sms ? a.n_items : sms;
-  k_sp_score<R, G><<<grid, kThreads, sm, st>>>(a);
+  if constexpr (PAIR) {
+    // clusters of 2 CTAs (an SM pair each); one work-item range per pair
+    const int pairs = a.n_items < sms / 2 ? a.n_items : sms / 2;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(2 * pairs);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = sm;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    e = cudaLaunchKernelEx(&cfg, k_sp_score<R, G, PAIR>, a);
+  } else {
+    const int grid = a.n_items < sms ? a.n_items : sms;
+    k_sp_score<R, G, PAIR><<<grid, kThreads, sm, st>>>(a);
+    e = cudaGetLastError();
+  }
   count_launch();
-  return cudaGetLastError();
+  return e;
 }
 
 }  // namespace
@@ -583,31 +750,56 @@ bool sp_supported(int R) { return R == 11 || R == 21; }
 
 int sp_parts(int R) { return (R + kRPart - 1) / kRPart; }
 
-size_t sp_codebook_elems(int R) { return sp_supported(R) ? (size_t)R * (kRoundBytes / 2) : 0; }
+// per slot: the single-CTA layout [R][X | Y][64] (R x 8192 fp16), then the
+// CTA-pair layout [R][rank][P | Q][64 rows x 64 levels] (R x 16384 fp16):
+// rank 0 holds P = X, Q = Y; rank 1 holds P = Y, Q = -X, so the pair MMA over
+// the P halves is [X ; Y] and, negated, over the Q halves [-Y ; X].
+size_t sp_codebook_elems(int R) {
+  return sp_supported(R) ? (size_t)R * (kRoundBytes / 2) + (size_t)R * kRoundBytes : 0;
+}
+
+// (row, level) of a K-major no-swizzle 64 x 64 fp16 block
+static uint32_t kmaj64(int row, int l) {
+  return (uint32_t)((((l >> 3) * 8 + (row >> 3)) << 7) + ((row & 7) << 4) + ((l & 7) << 1));
+}
 
 void sp_build_codebook(int R, const double* xy, uint16_t* out, uint16_t (*to_half)(double)) {
   // xy: [R][64 subs][64 levels][2]; out: [R][X rows 0-63 | Y rows 64-127][64 levels]
+  uint16_t* pair = out + (size_t)R * (kRoundBytes / 2);
   for (int r = 0; r < R; ++r) {
     uint16_t* o = out + (size_t)r * (kRoundBytes / 2);
+    uint16_t* p0 = pair + (size_t)r * kRoundBytes;  // rank 0: P, Q
+    uint16_t* p1 = p0 + kRoundBytes / 2;            // rank 1: P, Q
     for (int j = 0; j < 64; ++j)
       for (int l = 0; l < 64; ++l) {
         const double x = xy[(((size_t)r * 64 + j) * 64 + l) * 2];
         const double y = xy[(((size_t)r * 64 + j) * 64 + l) * 2 + 1];
         o[kmaj128(j, l) >> 1] = to_half(x);
         o[kmaj128(64 + j, l) >> 1] = to_half(y);
+        p0[kmaj64(j, l) >> 1] = to_half(x);
+        p0[4096 + (kmaj64(j, l) >> 1)] = to_half(y);
+        p1[kmaj64(j, l) >> 1] = to_half(y);
+        p1[4096 + (kmaj64(j, l) >> 1)] = to_half(-x);
       }
   }
 }
 
+bool sp_pair_enabled() {
+  const char* e = getenv("CVQ_TC_PAIR");
+  return e && e[0] == '1';
+}
+
 cudaError_t run_sp_score(const AttnJob& job, const uint16_t* cb, size_t slot_elems,
                          const float* q, float* ps, int chunk, cudaStream_t st) {
+  // cb: slot 0's single-CTA layout; the pair layout follows it (sp_build_codebook)
+  const bool pair = sp_pair_enabled();
   const Geom& g = job.geo;
   if (!cb || g.d != 128 || g.L != 64 || g.subs != 64 || !sp_supported(g.R))
     return cudaErrorInvalidValue;
   SpArgs a{};
   a.kpool = job.kpool;
   a.kstride = job.kstride;
-  a.cb = cb;
+  a.cb = pair ? cb + (size_t)job.geo.R * (kRoundBytes / 2) : cb;
   a.slot_elems = slot_elems;
   a.n_slots = job.n_slots;
   a.q = q;
@@ -615,14 +807,19 @@ cudaError_t run_sp_score(const AttnJob& job, const uint16_t* cb, size_t slot_ele
   a.t = job.t;
   a.pos0 = job.pos0;
   a.n = job.n;
-  a.chunk = (chunk + kTok - 1) / kTok * kTok;
+  a.chunk = (chunk + 2 * kTok - 1) / (2 * kTok) * (2 * kTok);
   a.cps = (int)((job.n + a.chunk - 1) / a.chunk);
   a.rtot = g.R;
   a.js = sp_parts(g.R);
   a.n_items = job.S * a.js * a.cps;
   a.ps = ps;
-  if (g.G == 4) return launch_sp<kRPart, 4>(a, st);
-  if (g.G == 1) return launch_sp<kRPart, 1>(a, st);
+  if (pair) {
+    if (g.G == 4) return launch_sp<kRPart, 4, true>(a, st);
+    if (g.G == 1) return launch_sp<kRPart, 1, true>(a, st);
+  } else {
+    if (g.G == 4) return launch_sp<kRPart, 4, false>(a, st);
+    if (g.G == 1) return launch_sp<kRPart, 1, false>(a, st);
+  }
   return cudaErrorInvalidValue;
 }
 
