@@ -583,6 +583,34 @@ def test_sparse_tc_matches_dense_tc(G, R, Gq, n, monkeypatch):
     assert fx.rel_err(out_sp, out_dense) <= 1e-5
 
 
+@pytest.mark.parametrize("R,Gq,n", [(11, 4, 8197), (11, 1, 300), (21, 4, 1000), (11, 4, 129)])
+def test_pair_tc_matches_dense_tc(G, R, Gq, n, monkeypatch):
+    """The CTA-pair (tcgen05 cta_group::2) variant of the sparse kernel
+    (CVQ_TC_PAIR=1): each CTA of an SM pair holds half of the codebook rows
+    and 128 of the 256 tokens of a pair tile; ragged tiles leave the second
+    CTA empty.  Same cache, outputs vs the dense kernel within 1e-5."""
+    kq = KQ(128, 64, 64, R)
+    nc, Ly, H = (128 if R == 11 else 256), 2, 2
+    rng = P.rng(n + 7 * Gq)
+    c = G.QuantizedKVCache(kq, nc, n_layers=Ly, n_kv_heads=H, q_per_kv=Gq, capacity=n, keys="tc")
+    for layer in range(Ly):
+        for h in range(H):
+            c.set_key_codebook(layer, h, rng.normal(2 * kq.n_atoms, 0.3))
+            c.set_value_quantizer(layer, h, rng.normal(nc * 128, 1 / 16).reshape(nc, 128))
+            a, b = fx.random_key_codes(kq, n, rng=rng)
+            bits = fx.random_value_codes(nc, n, rng=rng)
+            c.import_stream(0, layer, h, P.pack_key_codes(kq, a, b), P.pack_value_codes(bits), n)
+    q = rng.normal(Ly * H * Gq * 128).reshape(1, Ly, H * Gq, 128).astype(np.float32)
+    t = n + 99
+    monkeypatch.setenv("CVQ_TC_PAIR", "1")
+    out_pair = c.attention(q, t)
+    monkeypatch.delenv("CVQ_TC_PAIR")
+    monkeypatch.setenv("CVQ_TC_DENSE", "1")
+    out_dense = c.attention(q, t)
+    assert np.isfinite(out_pair).all()
+    assert fx.rel_err(out_pair, out_dense) <= 1e-5
+
+
 @pytest.mark.parametrize("dense", [False, True])
 def test_tc_long_context_phases_vs_oracle(G, dense, monkeypatch):
     """Both tcgen05 score kernels far from the query (Delta ~ 1e6) and past
