@@ -352,6 +352,156 @@ __global__ void kres3(int tiles, int mode, long long* out) {
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
 }
 
+
+__device__ __forceinline__ bool mtry(uint64_t* b, uint32_t ph) {
+  uint32_t ok;
+  asm volatile("{.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;}"
+               : "=r"(ok) : "r"(su32(b)), "r"(ph) : "memory");
+  return ok != 0;
+}
+// The kernel's producer -> issuer handoff in isolation: 6 round stages in
+// TMEM, 8 producer warps (2 per lane quarter, even / odd rounds) writing 2 x
+// (16 A + 1 metadata) columns per round with tcgen05.st, wait::st, fence,
+// arrive; the MMA warp waits both stages of a round pair, issues 16 sparse
+// N = 64 MMAs in one elected region and commits each round's stage.
+// sleep_ns: producer backoff while waiting (0 = spin).
+__global__ void kres4(int tiles, int sleep_ns, int mode, long long* out) {
+  extern __shared__ __align__(1024) unsigned char sm[];
+  __shared__ uint32_t slot;
+  __shared__ __align__(8) uint64_t afull[6], aempty[6], fin;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  for (int i = tid; i < 176 * 1024 / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(sm)[i] = 0;
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(&slot)), "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (tid == 0) {
+    for (int i = 0; i < 6; ++i) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(&afull[i])), "r"(4));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(&aempty[i])), "r"(1));
+    }
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(&fin)), "r"(1));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = slot;
+  const int R = 11;
+  if (warp >= 8 && warp < 16) {  // producers
+    const int p = warp - 8, quarter = p & 3, sub = p >> 2;
+    const uint32_t lane_base = (uint32_t)(quarter * 32) << 16;
+    uint32_t v[16];
+    for (int i = 0; i < 16; ++i) v[i] = (i == (lane & 15)) ? 0x3C00u : 0u;
+    uint32_t gbase = 0;
+    for (int t = 0; t < tiles; ++t) {
+      for (int r = sub; r < R; r += 2) {
+        const uint32_t g = gbase + r, st = g % 6, use = g / 6;
+        if (use > 0) {
+          while (!mtry(&aempty[st], (use - 1) & 1)) if (sleep_ns) __nanosleep(64);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        }
+        for (int s2 = 0; s2 < 2; ++s2) {
+          asm volatile("tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, %16};"
+                       ::"r"(tmem + lane_base + 256 + 32 * st + 16 * s2), "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]),
+                       "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]),
+                       "r"(v[14]), "r"(v[15]) : "memory");
+          asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" ::"r"(tmem + lane_base + 448 + 4 * st + 2 * s2),
+                       "r"(0x44444444u) : "memory");
+        }
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) asm volatile("{.reg .b64 st;\n\tmbarrier.arrive.shared::cta.b64 st, [%0];}" ::"r"(su32(&afull[st])) : "memory");
+      }
+      gbase += R;
+    }
+  } else if (warp == 16 || (mode == 2 && warp == 17)) {  // MMA issuer(s)
+    const int iss = warp - 16;  // mode 2: warp iss takes round pairs p = iss (mod 2)
+    const uint32_t idesc = (1u << 4) | (8u << 17) | (8u << 24) | (1u << 2);
+    const uint64_t bdesc0 = sdesc(su32(sm), 2048, 128);
+    uint32_t gst = 0, gph = 0;
+    long long t0 = clock64();
+    for (int t = 0; t < tiles; ++t) {
+      const uint32_t dcol = tmem + (uint32_t)(t & 1) * 128u;
+#pragma unroll 1
+      for (int r = 0; r < R; r += 2) {
+        const bool two = r + 1 < R;
+        const uint32_t st0 = gst, ph0 = gph;
+        uint32_t st1 = gst + 1, ph1 = gph;
+        if (st1 == 6) { st1 = 0; ph1 ^= 1u; }
+        if (mode == 2 && ((r >> 1) & 1) != iss) {  // the other issuer's pair
+          gst += two ? 2u : 1u;
+          if (gst >= 6) { gst -= 6; gph ^= 1u; }
+          continue;
+        }
+        while (!mtry(&afull[st0], ph0)) {}
+        if (two) while (!mtry(&afull[st1], ph1)) {}
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        if (mode != 1) {
+        if (elect_one()) {
+          for (int u = 0; u < 2; ++u) {
+            if (u == 1 && !two) break;
+            const uint32_t st = u ? st1 : st0;
+            for (int s = 0; s < 2; ++s) {
+              const uint32_t a_tm = tmem + 256 + 32 * st + 16 * s;
+              const uint32_t e_tm = tmem + 448 + 4 * st + 2 * s;
+              for (int h = 0; h < 2; ++h)
+                for (int blk = 0; blk < 2; ++blk) {
+                  const int rows = s ? (blk ? 0 : 64) : (blk ? 64 : 0);
+                  const uint64_t bd = bdesc0 + (uint64_t)((((r + u) * 16384) + h * 4 * 2048 + rows * 16) >> 4);
+                  asm volatile("{.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                               "tcgen05.mma.sp.cta_group::1.kind::f16 [%0], [%1], %2, [%5], %3, p;}" ::"r"(dcol + blk * 64),
+                               "r"(a_tm + h * 8), "l"(bd), "r"(idesc | ((s && !blk) ? (1u << 13) : 0u)),
+                               "r"(mode == 2 ? 1 : ((u | s | h | r) ? 1 : 0)), "r"(e_tm));
+                }
+            }
+            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(&aempty[st])) : "memory");
+          }
+        }
+        __syncwarp();
+        } else {
+          for (int u = 0; u < 2; ++u) {
+            if (u == 1 && !two) break;
+            const uint32_t st = u ? st1 : st0;
+            for (int s = 0; s < 2; ++s) {
+              const uint32_t a_tm = tmem + 256 + 32 * st + 16 * s;
+              const uint32_t e_tm = tmem + 448 + 4 * st + 2 * s;
+              for (int h = 0; h < 2; ++h)
+                for (int blk = 0; blk < 2; ++blk) {
+                  const int rows = s ? (blk ? 0 : 64) : (blk ? 64 : 0);
+                  const uint64_t bd = bdesc0 + (uint64_t)((((r + u) * 16384) + h * 4 * 2048 + rows * 16) >> 4);
+                  if (elect_one())
+                    asm volatile("{.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                                 "tcgen05.mma.sp.cta_group::1.kind::f16 [%0], [%1], %2, [%5], %3, p;}" ::"r"(dcol + blk * 64),
+                                 "r"(a_tm + h * 8), "l"(bd), "r"(idesc | ((s && !blk) ? (1u << 13) : 0u)),
+                                 "r"((u | s | h | r) ? 1 : 0), "r"(e_tm));
+                  __syncwarp();
+                }
+            }
+            if (elect_one())
+              asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(&aempty[st])) : "memory");
+            __syncwarp();
+          }
+        }
+        gst += two ? 2u : 1u;
+        if (gst >= 6) { gst -= 6; gph ^= 1u; }
+      }
+    }
+    if (iss == 0) {
+      if (elect_one())
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(&fin)) : "memory");
+      __syncwarp();
+      while (!mtry(&fin, 0)) {}
+      if (blockIdx.x == 0 && lane == 0) out[0] = clock64() - t0;
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+}
+
 template <int SP, int ATM, int N>
 void run(int iss, long long* d) {
   auto k = kb<SP, ATM, N>;
@@ -422,6 +572,22 @@ int main() {
       cudaMemcpy(&cyc, d3, 8, cudaMemcpyDeviceToHost);
       printf("kres3 commit=%d wait+fence=%d pairs=%d: %.1f clk per tile, %.1f clk/mma\n", mode & 1, (mode >> 1) & 1,
              (mode >> 2) & 1, cyc / 64.0, cyc / 64.0 / 88);
+    }
+  }
+  {
+    cudaFuncSetAttribute(kres4, cudaFuncAttributeMaxDynamicSharedMemorySize, 176 * 1024);
+    long long* d4;
+    cudaMalloc(&d4, 16);
+    for (int md = 0; md < 3; ++md) {
+      const int sl = 1;
+      kres4<<<148, 576, 176 * 1024>>>(2, sl, md, d4);
+      kres4<<<148, 576, 176 * 1024>>>(64, sl, md, d4);
+      cudaError_t e = cudaDeviceSynchronize();
+      if (e != cudaSuccess) { printf("err %s\n", cudaGetErrorString(e)); exit(1); }
+      long long cyc = 0;
+      cudaMemcpy(&cyc, d4, 8, cudaMemcpyDeviceToHost);
+      printf("kres4 handoff (%s): %.1f clk per 128-token tile, %.1f clk/mma\n", md == 2 ? "2 issuers, alternate pairs" : md ? "per-MMA elect" : "16-MMA region",
+             cyc / 64.0, cyc / 64.0 / 88);
     }
   }
   return 0;
