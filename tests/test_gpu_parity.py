@@ -583,6 +583,32 @@ def test_sparse_tc_matches_dense_tc(G, R, Gq, n, monkeypatch):
     assert fx.rel_err(out_sp, out_dense) <= 1e-5
 
 
+@pytest.mark.parametrize("n", [128, 256, 8192, 8193])
+def test_sparse_tc_tile_boundaries_vs_oracle(G, n):
+    """Exact tile / work-item boundaries of the sparse kernel (128-token
+    tiles, 8192-token items) with a position offset: every q head of one KV
+    stream vs the oracle (1e-3 bar)."""
+    kq = KQ(128, 64, 64, 11)
+    nc, Gq, off = 128, 4, 1000
+    rng = P.rng(n + 31)
+    atoms = rng.normal(2 * kq.n_atoms, 0.3)
+    vrows = rng.normal(nc * 128, 1 / 16).reshape(nc, 128)
+    a, b = fx.random_key_codes(kq, n, rng=rng)
+    bits = fx.random_value_codes(nc, n, rng=rng)
+    c = G.QuantizedKVCache(kq, nc, n_kv_heads=1, q_per_kv=Gq, capacity=n, keys="tc",
+                           position_offset=off)
+    c.set_key_codebook(0, 0, atoms)
+    c.set_value_quantizer(0, 0, vrows)
+    c.import_stream(0, 0, 0, P.pack_key_codes(kq, a, b), P.pack_value_codes(bits), n)
+    q = rng.normal(Gq * 128).reshape(1, 1, Gq, 128).astype(np.float32)
+    t = off + n - 1
+    out = c.attention(q, t)
+    for j in range(Gq):
+        want, _, _ = P.fused_attention(kq, atoms, a, b, bits, vrows,
+                                       q[0, 0, j].astype(np.float64), t - off)
+        assert fx.rel_err(out[0, 0, j], want) <= 1e-3, j
+
+
 @pytest.mark.parametrize("R,Gq,n", [(11, 4, 8197), (11, 1, 300), (21, 4, 1000), (11, 4, 129)])
 def test_pair_tc_matches_dense_tc(G, R, Gq, n, monkeypatch):
     """The CTA-pair (tcgen05 cta_group::2) variant of the sparse kernel
