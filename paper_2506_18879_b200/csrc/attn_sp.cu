@@ -44,6 +44,7 @@
 // Codebook precision fp16 (as CVQ_CACHE_KEYS_FP16), accumulation fp32.
 #include <cuda_fp16.h>
 
+#include <algorithm>
 #include <cstdlib>
 
 #include "cvq_internal.cuh"
@@ -807,7 +808,17 @@ cudaError_t run_sp_score(const AttnJob& job, const uint16_t* cb, size_t slot_ele
   a.t = job.t;
   a.pos0 = job.pos0;
   a.n = job.n;
-  a.chunk = (chunk + 2 * kTok - 1) / (2 * kTok) * (2 * kTok);
+  // work items: up to 64 tiles (8192 tokens), fewer when the job is small so
+  // every SM gets >= 4 items (load balance within one item); a CTA's items
+  // are contiguous, so small items add no codebook reloads
+  (void)chunk;
+  {
+    const long long step = pair ? 2 * kTok : kTok;
+    const long long tiles = (long long)job.S * sp_parts(g.R) * ((job.n + step - 1) / step);
+    const long long units = pair ? 74 : 148;
+    const long long ct = std::max(1ll, std::min(64ll, tiles / (4 * units)));
+    a.chunk = (int)(ct * step);
+  }
   a.cps = (int)((job.n + a.chunk - 1) / a.chunk);
   a.rtot = g.R;
   a.js = sp_parts(g.R);
