@@ -98,7 +98,7 @@ __global__ void kb(int issuers, int tiles, long long* out) {
 // Resident-codebook pattern: N = 64, 4 MMAs per (round, K32 half) into two
 // 64-column blocks (Re, Im), B walking an 11 x 16 KiB resident codebook,
 // A and metadata from TMEM stage regions, negate-A on one MMA in four.
-__global__ void kres(int tiles, int ms, long long* out) {
+__global__ void kres(int tiles, int ms, long long* out, int rnd = 0) {
   extern __shared__ __align__(1024) unsigned char sm[];
   __shared__ uint32_t slot;
   __shared__ __align__(8) uint64_t bar[8];
@@ -116,9 +116,19 @@ __global__ void kres(int tiles, int ms, long long* out) {
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = slot;
   if (warp < 4) {
-    for (int c = 256; c < 512; ++c)
+    const int lane = tid & 31;
+    for (int c = 256; c < 512; ++c) {
+      uint32_t h = (uint32_t)(c * 2654435761u) ^ (uint32_t)((warp * 32 + lane) * 40503u);
+      h ^= h >> 13; h *= 0x5bd1e995u; h ^= h >> 15;
+      uint32_t v;
+      if (c >= 448) {  // metadata: each 16-bit half picks (0,1) or (2,3) for its row
+        v = rnd ? (((h & 1) ? 0x0000EEEEu : 0x00004444u) | ((h & 2) ? 0xEEEE0000u : 0x44440000u)) : 0x44444444u;
+      } else {  // A: a one-hot fp16 1.0 per row and stage (random column) or zeros
+        v = (rnd == 2 && ((h >> 4) & 15) == (uint32_t)(c & 15)) ? ((h & 4) ? 0x3C000000u : 0x3C00u) : 0u;
+      }
       asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" ::"r"(tmem + ((uint32_t)(warp * 32) << 16) + c),
-                   "r"(c >= 448 ? 0x44444444u : 0u) : "memory");
+                   "r"(v) : "memory");
+    }
     asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -531,16 +541,17 @@ int main() {
   run<1, 1, 64>(1, d);
   {
     cudaFuncSetAttribute(kres, cudaFuncAttributeMaxDynamicSharedMemorySize, 176 * 1024);
-   for (int ms : {4, 2}) {
-    kres<<<148, 128, 176 * 1024>>>(2, ms, d);
-    kres<<<148, 128, 176 * 1024>>>(64, ms, d);
+   for (int ms : {4, 2, 102, 202}) {
+    const int rnd = ms / 100;
+    kres<<<148, 128, 176 * 1024>>>(2, ms % 100, d, rnd);
+    kres<<<148, 128, 176 * 1024>>>(64, ms % 100, d, rnd);
     cudaError_t e = cudaDeviceSynchronize();
     if (e != cudaSuccess) { printf("err %s\n", cudaGetErrorString(e)); exit(1); }
     long long cyc = 0;
     cudaMemcpy(&cyc, d, 8, cudaMemcpyDeviceToHost);
     printf("resident-codebook N=64 pattern: %.1f clk per 128-token tile (88 MMAs), %.1f clk/mma, %.2f clk/token\n",
            cyc / 64.0, cyc / 64.0 / 88, cyc / 64.0 / 128);
-    printf("  (metadata column stride %d)\n", ms);
+    printf("  (metadata column stride %d, %s)\n", ms % 100, ms >= 200 ? "random metadata + random one-hot A" : ms >= 100 ? "random metadata per row" : "uniform metadata");
    }
   }
   {
