@@ -53,6 +53,21 @@ namespace cvq {
 
 namespace {
 
+#ifdef SP_TRACE
+// clock64 trace of CTA 0 over tiles [kTrK0, kTrK0 + 4) (tools/sp_trace.py)
+__device__ long long g_sptr[8192];
+constexpr int kTrK0 = 20;
+#define SPTR(idx) \
+  do { if (blockIdx.x == 0 && (threadIdx.x & 31) == 0) g_sptr[(idx)] = clock64(); } while (0)
+#define TRK(k) ((k) >= kTrK0 && (k) < kTrK0 + 4)
+// layout: MMA afull wait begin/end [tile][round]: 0 / 64; dempty begin/end
+// [tile]: 128 / 136; dfull commit 144; producer (quarter, sub) wait
+// begin/end/arrive [q][tile][round]: 256 / 512 / 768 (q*64 + tile*16 + r);
+// epilogue warp w: dfull wait begin/end, release, end [w][tile]: 1024 + w*16 + 4*f + tile
+#else
+#define SPTR(idx) do {} while (0)
+#define TRK(k) false
+#endif
 constexpr int kTok = 128;                 // tokens per tile (MMA M)
 constexpr int kEpiWarps = 16;
 constexpr int kProdWarps = 8;             // warp 16 + p: TMEM lane quarter p & 3, rounds r = p >> 2 (mod 2)
@@ -91,12 +106,52 @@ __device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t parity) {
       : "memory");
   return ok != 0;
 }
+__device__ __forceinline__ bool mbar_try_hint(uint64_t* bar, uint32_t parity);
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+#ifdef SP_R2_HINT_ALL
+  while (!mbar_try_hint(bar, parity)) {
+  }
+#else
   while (!mbar_try(bar, parity)) {
   }
+#endif
 }
+#if defined(SP_R2_HINT) || defined(SP_R2_HINT_ALL)
+// try_wait with a suspend-time hint: the warp sleeps in the barrier unit until
+// the phase completes (or ~the hint elapses) instead of re-issuing a poll loop
+__device__ __forceinline__ bool mbar_try_hint(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+      "selp.u32 %0, 1, 0, p;}"
+      : "=r"(ok)
+      : "r"(su32(bar)), "r"(parity), "r"(0x989680u)
+      : "memory");
+  return ok != 0;
+}
+#endif
+#ifdef SP_R2_HINT
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+  while (!mbar_try_hint(bar, parity)) {
+  }
+}
+#else
 __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
   while (!mbar_try(bar, parity)) __nanosleep(64);
+}
+#endif
+#ifndef SP_R2_ISS_SLEEP
+#define SP_R2_ISS_SLEEP 0
+#endif
+// the MMA warp's waits: with SP_R2_ISS_SLEEP > 0 it backs off between polls
+// (it shares SMSP 0 with lane quarter 0's producers)
+__device__ __forceinline__ void mbar_wait_iss(uint64_t* bar, uint32_t parity) {
+#ifdef SP_R2_HINT_ALL
+  mbar_wait(bar, parity);
+#else
+  while (!mbar_try(bar, parity))
+    if (SP_R2_ISS_SLEEP) __nanosleep(SP_R2_ISS_SLEEP);
+#endif
 }
 __device__ __forceinline__ bool elect_one() {
   uint32_t pred;
@@ -196,6 +251,73 @@ __device__ __forceinline__ float2 ffma2(float2 a, float b, float2 c) {
       : "=l"(d)
       : "f"(a.x), "f"(a.y), "f"(b), "f"(c.x), "f"(c.y));
   return make_float2(__uint_as_float((uint32_t)d), __uint_as_float((uint32_t)(d >> 32)));
+}
+
+// One round of the resident-codebook schedule as ONE asm block: elect.sync,
+// 8 predicated sparse MMAs (sides a/b x K halves x Re/Im blocks) and the
+// commit that frees the round's A stage.  No branch, so ptxas emits
+// @UP-predicated UTCHMMAs with no BSSY/BSYNC reconvergence (a BSYNC waits on
+// the UTCHMMA scoreboards, i.e. drains the MMA queue, ~200 clk per region;
+// tools/umma_pred_bench.cu, profiles/r02_umma_pred_bench.txt).
+//   side a: Re += X (rows 0-63), Im += Y (rows 64-127)
+//   side b: Re -= Y (negate-A), Im += X;  K half h at +8 A columns, +4 x 2048 B
+template <bool WS>
+__device__ __forceinline__ void sp_issue_round(uint32_t d, uint32_t a, uint32_t e, uint64_t br,
+                                               uint32_t idesc, uint32_t accum, uint64_t* bar) {
+#define SP_MMA(c) "@q tcgen05.mma" c
+  if constexpr (WS) {
+  asm volatile(
+      "{.reg .pred q, p, t;\n\t"
+      ".reg .b32 a1, a2, a3, d1, e1;\n\t"
+      ".reg .b64 b1, b2, b3;\n\t"
+      "elect.sync _|q, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %5, 0;\n\t"
+      "setp.eq.u32 t, %5, %5;\n\t"
+      "add.u32 a1, %1, 8;\n\tadd.u32 a2, %1, 16;\n\tadd.u32 a3, %1, 24;\n\t"
+      "add.u32 d1, %0, 64;\n\tadd.u32 e1, %2, 2;\n\t"
+      "add.u64 b1, %3, 64;\n\tadd.u64 b2, %3, 512;\n\tadd.u64 b3, %3, 576;\n\t"
+      SP_MMA(".ws.sp.cta_group::1.kind::f16.collector::b0::fill [%0], [%1], %3, [%2], %4, p;\n\t")
+      SP_MMA(".ws.sp.cta_group::1.kind::f16.collector::b1::fill [d1], [%1], b1, [%2], %4, p;\n\t")
+      SP_MMA(".ws.sp.cta_group::1.kind::f16.collector::b2::fill [%0], [a1], b2, [%2], %4, t;\n\t")
+      SP_MMA(".ws.sp.cta_group::1.kind::f16.collector::b3::fill [d1], [a1], b3, [%2], %4, t;\n\t")
+      SP_MMA(".ws.sp.cta_group::1.kind::f16.collector::b1::lastuse [%0], [a2], b1, [e1], %6, t;\n\t")
+      SP_MMA(".ws.sp.cta_group::1.kind::f16.collector::b0::lastuse [d1], [a2], %3, [e1], %4, t;\n\t")
+      SP_MMA(".ws.sp.cta_group::1.kind::f16.collector::b3::lastuse [%0], [a3], b3, [e1], %6, t;\n\t")
+      SP_MMA(".ws.sp.cta_group::1.kind::f16.collector::b2::lastuse [d1], [a3], b2, [e1], %4, t;\n\t")
+      "@q tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%7];}" ::"r"(d),
+      "r"(a), "r"(e), "l"(br), "r"(idesc), "r"(accum), "r"(idesc | (1u << 13)), "r"(su32(bar))
+      : "memory");
+  } else {
+  asm volatile(
+      "{.reg .pred q, p, t;\n\t"
+      ".reg .b32 a1, a2, a3, d1, e1;\n\t"
+      ".reg .b64 b1, b2, b3;\n\t"
+      "elect.sync _|q, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %5, 0;\n\t"
+      "setp.eq.u32 t, %5, %5;\n\t"
+      "add.u32 a1, %1, 8;\n\tadd.u32 a2, %1, 16;\n\tadd.u32 a3, %1, 24;\n\t"
+      "add.u32 d1, %0, 64;\n\tadd.u32 e1, %2, 2;\n\t"
+      "add.u64 b1, %3, 64;\n\tadd.u64 b2, %3, 512;\n\tadd.u64 b3, %3, 576;\n\t"
+      SP_MMA(".sp.cta_group::1.kind::f16 [%0], [%1], %3, [%2], %4, p;\n\t")
+      SP_MMA(".sp.cta_group::1.kind::f16 [d1], [%1], b1, [%2], %4, p;\n\t")
+      SP_MMA(".sp.cta_group::1.kind::f16 [%0], [a1], b2, [%2], %4, t;\n\t")
+      SP_MMA(".sp.cta_group::1.kind::f16 [d1], [a1], b3, [%2], %4, t;\n\t")
+      SP_MMA(".sp.cta_group::1.kind::f16 [%0], [a2], b1, [e1], %6, t;\n\t")
+      SP_MMA(".sp.cta_group::1.kind::f16 [d1], [a2], %3, [e1], %4, t;\n\t")
+      SP_MMA(".sp.cta_group::1.kind::f16 [%0], [a3], b3, [e1], %6, t;\n\t")
+      SP_MMA(".sp.cta_group::1.kind::f16 [d1], [a3], b2, [e1], %4, t;\n\t")
+      "@q tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%7];}" ::"r"(d),
+      "r"(a), "r"(e), "l"(br), "r"(idesc), "r"(accum), "r"(idesc | (1u << 13)), "r"(su32(bar))
+      : "memory");
+  }
+#undef SP_MMA
+}
+// commit to `bar` from one elected lane, branch-free
+__device__ __forceinline__ void tc_commit_elect(uint64_t* bar) {
+  asm volatile(
+      "{.reg .pred q;\n\telect.sync _|q, 0xffffffff;\n\t"
+      "@q tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];}" ::"r"(su32(bar))
+      : "memory");
 }
 
 // Byte offset of (row, level) in the K-major no-swizzle 128 x 64 fp16 round
@@ -353,6 +475,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_sp_score(SpArgs a) {
     const float sc = 0.08838834764831845f;  // 1 / sqrt(128)
     float2 ph = make_float2(1.f, 0.f);
     float2 qv[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+#ifdef SP_R2_EREG
+    // this lane's phase factors e^{+i lane theta_j} for the warp's 16
+    // subspaces, held in registers for the whole kernel (no smem reads in
+    // the per-tile loop: the MMAs' B operand reads use all the smem bandwidth)
+    float2 ereg[16];
+#pragma unroll
+    for (int jj = 0; jj < 16; ++jj) ereg[jj] = etab[(eslot * 16 + jj) * 32 + lane];
+#endif
     SpIter<PAIR> it;
     int k = 0;
     for (bool ok = it.first(a); ok; ok = it.next(a), ++k) {
@@ -386,7 +516,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_sp_score(SpArgs a) {
         }
       }
       __syncwarp();
+      if (TRK(k)) SPTR(1024 + warp * 16 + 0 + (k - kTrK0));
       mbar_wait_sleep(dfull + db, (k >> 1) & 1);
+      if (TRK(k)) SPTR(1024 + warp * 16 + 4 + (k - kTrK0));
       tc_fence_after();
       uint32_t re[16], im[16];
       tmem_ld16(tmem + lane_base + db * 128 + eslot * 16, re);
@@ -398,13 +530,18 @@ __global__ void __launch_bounds__(kThreads, 1) k_sp_score(SpArgs a) {
         if constexpr (PAIR) mbar_arrive_cluster(dempty + db, 0);
         else mbar_arrive(dempty + db);
       }
+      if (TRK(k)) SPTR(1024 + warp * 16 + 8 + (k - kTrK0));
       const float2* E = etab + eslot * 16 * 32 + lane;
       float* rb = red + (size_t)((db * 4 + quarter) * 4) * 32 * G;  // [e][lane][G]
       if constexpr (G == 4) {
         float2 acc01 = make_float2(0.f, 0.f), acc23 = make_float2(0.f, 0.f);
 #pragma unroll
         for (int jj = 0; jj < 16; ++jj) {
+#ifdef SP_R2_EREG
+          const float2 ej = ereg[jj];
+#else
           const float2 ej = E[jj * 32];
+#endif
           const float kr = __uint_as_float(re[jj]), ki = __uint_as_float(im[jj]);
           const float zx = ej.x * kr - ej.y * ki;
           const float zy = ej.x * ki + ej.y * kr;
@@ -437,6 +574,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_sp_score(SpArgs a) {
         for (int e2 = 0; e2 < 4; ++e2) v += rb[(e2 * 32 + lane) * G + eslot];
         a.ps[(((size_t)it.s * a.js + it.part) * a.n + it.base() + tok) * G + eslot] = v;
       }
+      if (TRK(k)) SPTR(1024 + warp * 16 + 12 + (k - kTrK0));
     }
   } else if (warp < kEpiWarps + kProdWarps) {
     // ============ one-hot producers: thread = token 32 quarter + lane; warp
@@ -463,6 +601,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_sp_score(SpArgs a) {
     bool ok = it.first(a);
     if (ok) load_raw(it, raw, off);
     const int src = (lane & 7) | (lane & 16);
+    int kk = 0;
     while (ok) {
       uint64_t w[NW];  // token record at bit 0
 #pragma unroll
@@ -474,9 +613,16 @@ __global__ void __launch_bounds__(kThreads, 1) k_sp_score(SpArgs a) {
       // this warp's rounds r = sub, sub + 2, ...: their 12-bit (a, b) fields
       // packed back to back into (pk0, pk1)
       uint64_t pk0 = 0, pk1 = 0;
+#ifdef SP_R2_GROT
+      // rounds by GLOBAL round index: this warp takes g = gbase + r with
+      // g % 2 == sub, so its rounds are exactly 2 apart across tiles too
+      const int rfirst = (int)((uint32_t)(sub + 2 - (int)(gbase & 1u)) & 1u);
+#else
+      const int rfirst = sub;
+#endif
 #pragma unroll
       for (int r = 0, i = 0; r < R; ++r) {
-        if ((r & 1) != sub) continue;
+        if ((r & 1) != rfirst) continue;
         const int b0 = 12 * r, wi = b0 >> 6, sh = b0 & 63;
         const uint64_t f = ((w[wi] >> sh) | (sh > 52 ? w[wi + 1] << (64 - sh) : 0ull)) & 0xFFFull;
         if (i < 5) pk0 |= f << (12 * i);
@@ -484,14 +630,16 @@ __global__ void __launch_bounds__(kThreads, 1) k_sp_score(SpArgs a) {
         ++i;
       }
 #pragma unroll 1
-      for (int r = sub; r < it.nr; r += 2) {
+      for (int r = rfirst; r < it.nr; r += 2) {
         const uint32_t fld = (uint32_t)pk0 & 0xFFFu;
         pk0 = (pk0 >> 12) | (pk1 << 48);
         pk1 >>= 12;
         // round stage of this CTA's global round g
         const uint32_t g = gbase + (uint32_t)r, st = g % kAStages, use = g / kAStages;
         if (use > 0) {
+          if (TRK(kk)) SPTR(256 + quarter * 64 + (kk - kTrK0) * 16 + r);
           mbar_wait_sleep(aempty + st, (use - 1) & 1u);  // back off: spinning takes issue slots from the MMA warp
+          if (TRK(kk)) SPTR(512 + quarter * 64 + (kk - kTrK0) * 16 + r);
           tc_fence_after();
         }
 #pragma unroll
@@ -521,11 +669,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_sp_score(SpArgs a) {
           if constexpr (PAIR) mbar_arrive_cluster(afull + st, 0);
           else mbar_arrive(afull + st);
         }
+        if (TRK(kk)) SPTR(768 + quarter * 64 + (kk - kTrK0) * 16 + r);
       }
 #pragma unroll
       for (int i = 0; i < NW; ++i) raw[i] = nraw[i];
       off = noff;
       gbase += (uint32_t)it.nr;
+      ++kk;
       it = nx;
       ok = okn;
     }
@@ -580,10 +730,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_sp_score(SpArgs a) {
       }
       if constexpr (PAIR) {
         if (rank != 0) continue;  // the peer CTA only loads its codebook half
+        if (TRK(k)) SPTR(128 + (k - kTrK0));
         if (k >= 2) {  // D buffer db was read by both CTAs' epilogues of tile k-2
           mbar_wait(dempty + db, ((k - 2) >> 1) & 1);
           tc_fence_after();
         }
+        if (TRK(k)) SPTR(136 + (k - kTrK0));
         // M = 256 (both CTAs' tokens), N = 128: side a = [X ; Y] (P halves),
         // side b = -[Y ; -X] (Q halves, negate-A) -> [Re | Im] of every token
         constexpr uint32_t idesc2 = (1u << 2) | (1u << 4) | ((128u >> 3) << 17) | (16u << 24);
@@ -598,8 +750,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_sp_score(SpArgs a) {
             st1 = 0;
             ph1 ^= 1u;
           }
+          if (TRK(k)) SPTR(0 + (k - kTrK0) * 16 + r);
           mbar_wait(afull + st0, ph0);
+          if (TRK(k)) SPTR(64 + (k - kTrK0) * 16 + r);
           if (two) mbar_wait(afull + st1, ph1);
+          if (TRK(k) && two) SPTR(64 + (k - kTrK0) * 16 + r + 1);
           tc_fence_after();
           if (elect_one()) {
 #pragma unroll
@@ -630,13 +785,70 @@ __global__ void __launch_bounds__(kThreads, 1) k_sp_score(SpArgs a) {
         }
         if (elect_one()) tc_commit_pair(dfull + db);
         __syncwarp();
+        if (TRK(k)) SPTR(144 + (k - kTrK0));
         continue;
       }
+      if (TRK(k)) SPTR(128 + (k - kTrK0));
       if (k >= 2) {  // D buffer db was read by the epilogue of tile k-2
-        mbar_wait(dempty + db, ((k - 2) >> 1) & 1);
+        mbar_wait_iss(dempty + db, ((k - 2) >> 1) & 1);
         tc_fence_after();
       }
+      if (TRK(k)) SPTR(136 + (k - kTrK0));
       const uint32_t dcol = tmem + (uint32_t)db * 128u;
+#ifdef SP_R2_PRED
+#ifndef SP_R2_WS
+#define SP_R2_WS false
+#endif
+      uint64_t br = bdesc0;
+#ifdef SP_R2_PAIRWAIT
+#pragma unroll 1
+      for (int r = 0; r < it.nr; r += 2) {
+        const bool two = r + 1 < it.nr;
+        uint32_t st1 = gst + 1, ph1 = gph;
+        if (st1 == kAStages) {
+          st1 = 0;
+          ph1 ^= 1u;
+        }
+        mbar_wait(afull + gst, gph);
+        if (two) mbar_wait(afull + st1, ph1);
+        tc_fence_after();
+        sp_issue_round<SP_R2_WS>(dcol, tmem + kACol0 + 32 * gst, tmem + kMetaCol0 + 4 * gst, br, idesc,
+                                 r > 0 ? 1u : 0u, aempty + gst);
+        if (two)
+          sp_issue_round<SP_R2_WS>(dcol, tmem + kACol0 + 32 * st1, tmem + kMetaCol0 + 4 * st1,
+                                   br + (uint64_t)(kRoundBytes >> 4), idesc, 1u, aempty + st1);
+        br += (uint64_t)((2 * kRoundBytes) >> 4);
+        gst = two ? st1 + 1 : st1;
+        gph = ph1;
+        if (gst == kAStages) {
+          gst = 0;
+          gph ^= 1u;
+        }
+      }
+#else
+      // one round per issue block: wait its stage, fence, 8 predicated MMAs
+      // and the stage's commit (sp_issue_round)
+#pragma unroll 1
+      for (int r = 0; r < it.nr; ++r) {
+        if (TRK(k)) SPTR(0 + (k - kTrK0) * 16 + r);
+        mbar_wait_iss(afull + gst, gph);
+        if (TRK(k)) SPTR(64 + (k - kTrK0) * 16 + r);
+        tc_fence_after();
+        sp_issue_round<SP_R2_WS>(dcol, tmem + kACol0 + 32 * gst, tmem + kMetaCol0 + 4 * gst, br, idesc,
+                                 r > 0 ? 1u : 0u, aempty + gst);
+        br += (uint64_t)(kRoundBytes >> 4);
+        if (++gst == kAStages) {
+          gst = 0;
+          gph ^= 1u;
+        }
+      }
+#endif
+      tc_commit_elect(dfull + db);
+      if (TRK(k)) SPTR(144 + (k - kTrK0));
+    }
+  }
+  tc_fence_before();
+#else
       // rounds in pairs: one elected issue region of 16 MMAs (2 rounds x 2
       // sides x 2 K-halves x Re/Im) per pair, so the per-region overhead
       // (barrier waits, elect, reconvergence) is paid every 16 MMAs; each
@@ -651,8 +863,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_sp_score(SpArgs a) {
           st1 = 0;
           ph1 ^= 1u;
         }
-        mbar_wait(afull + st0, ph0);
-        if (two) mbar_wait(afull + st1, ph1);
+        if (TRK(k)) SPTR(0 + (k - kTrK0) * 16 + r);
+        mbar_wait_iss(afull + st0, ph0);
+        if (TRK(k)) SPTR(64 + (k - kTrK0) * 16 + r);
+        if (two) mbar_wait_iss(afull + st1, ph1);
+        if (TRK(k) && two) SPTR(64 + (k - kTrK0) * 16 + r + 1);
         tc_fence_after();
         if (elect_one()) {
 #pragma unroll
@@ -690,9 +905,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_sp_score(SpArgs a) {
       }
       if (elect_one()) tc_commit(dfull + db);
       __syncwarp();
+      if (TRK(k)) SPTR(144 + (k - kTrK0));
     }
   }
   tc_fence_before();
+#endif
   if constexpr (PAIR) cluster_sync_all();  // the leader's MMAs into this CTA's TMEM are done
   else __syncthreads();
   tc_fence_after();
@@ -747,6 +964,13 @@ cudaError_t launch_sp(const SpArgs& a, cudaStream_t st) {
 
 }  // namespace
 
+#ifdef SP_TRACE
+}  // namespace cvq
+extern "C" __attribute__((visibility("default"))) int cvq_debug_sp_trace(long long* host, int n) {
+  return (int)cudaMemcpyFromSymbol(host, cvq::g_sptr, sizeof(long long) * (size_t)n);
+}
+namespace cvq {
+#endif
 bool sp_supported(int R) { return R == 11 || R == 21; }
 
 int sp_parts(int R) { return (R + kRPart - 1) / kRPart; }
