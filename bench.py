@@ -166,6 +166,8 @@ def main():
     ap.add_argument("--keys", default="tc", choices=["fp32", "fp16", "tc"],
                     help="score kernel: tc = tcgen05 one-hot MMA (fp16 codebook), fp16 / fp32 = "
                          "CUDA-core gather with that codebook precision; fp32 accumulation always")
+    ap.add_argument("--tc-variant", default="sparse", choices=["sparse", "dense", "pair"],
+                    help="tcgen05 score kernel: 2:4-sparse (default), dense one-hot, or CTA-pair")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
     if args.impl == "reference":
@@ -204,6 +206,8 @@ def main():
     cache = G.QuantizedKVCache(kq, nc, n_seqs=B, n_layers=layers, n_kv_heads=H, q_per_kv=Gq,
                                capacity=n_local + extra, hidden=2 * nc, position_offset=lo, ctx=ctx,
                                keys=args.keys)
+    if args.tc_variant != "sparse":
+        cache.set_variant({"dense": "tc_dense", "pair": "tc_pair"}[args.tc_variant])
     rs = np.random.default_rng(1234)
     for layer in range(layers):
         for h in range(H):
@@ -316,7 +320,7 @@ def main():
         ach_tf = flops / (avg_main_ms / 1e3) / 1e12
         # R = 11: the one-hot is a 2:4-sparse A operand (tcgen05.mma.sp,
         # attn_sp.cu) -- the ceiling is the sparse fp16 rate, twice the dense
-        sparse = R in (11, 21) and os.environ.get("CVQ_TC_DENSE", "0") != "1"
+        sparse = R in (11, 21) and args.tc_variant != "dense"
         peak_tf = TENSOR_NOMINAL_TFLOPS * (2 if sparse else 1)
         roof = {"bound": "tensor", "achieved": ach_tf, "peak": peak_tf,
                 "unit": "TFLOP/s", "frac": ach_tf / peak_tf,

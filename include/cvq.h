@@ -92,6 +92,8 @@ CVQ_API cvq_status cvq_context_create(int device, void* cuda_stream,
                                       cvq_context** out);
 CVQ_API cvq_status cvq_context_destroy(cvq_context* ctx);
 CVQ_API cvq_status cvq_context_synchronize(cvq_context* ctx);
+/* The context's cudaStream_t (callers order their own streams against it). */
+CVQ_API cvq_status cvq_context_stream(cvq_context* ctx, void** stream);
 /* Live timing of the dominant attention kernel: when enabled, every
  * attention call brackets its main (score/decode) kernel with CUDA events on
  * the context stream; _read synchronises, returns the summed milliseconds
@@ -233,7 +235,7 @@ typedef struct cvq_cache_desc {
   uint32_t n_layers;
   uint32_t n_kv_heads;
   uint32_t q_per_kv;   /* query heads per KV stream (GQA)   */
-  uint64_t capacity;   /* max tokens per stream             */
+  uint64_t capacity;   /* initial reservation (tokens/stream) */
   uint64_t position_offset;
   double rope_base;    /* RopeParams::base (rope.hpp:17)    */
   uint32_t flags;      /* CVQ_CACHE_* below                 */
@@ -246,17 +248,48 @@ typedef struct cvq_cache_desc {
 #define CVQ_CACHE_KEYS_FP16 1u
 /* Score with the tcgen05 tensor-core kernel: the key decode as a one-hot
  * GEMM (fp16 codebook operand, fp32 accumulators in TMEM); the fastest mode
- * on B200 (bench.py default).  Same precision class as CVQ_CACHE_KEYS_FP16.
- * Head presets (d=128, g=64, L=64, R in {11, 21}, 1 or 4 query heads per KV
- * head); other shapes run the CUDA-core kernels.  Both presets use the
- * 2:4-sparse variant (one-hot as the sparse operand); the environment
- * variable CVQ_TC_DENSE=1 selects the dense kernel instead. */
+ * on B200 (bench.py default).  Same precision class as CVQ_CACHE_KEYS_FP16,
+ * guarded per codebook (cvq_cache_key_mode).  Head presets (d=128, g=64,
+ * L=64, R in {11, 21}, 1 or 4 query heads per KV head); other shapes run the
+ * CUDA-core kernels.  Both presets use the 2:4-sparse kernel (one-hot as the
+ * sparse operand); CVQ_VARIANT_TC_DENSE selects the dense kernel instead. */
 #define CVQ_CACHE_KEYS_TC 2u
+
+/* Kernel variants (cvq_cache_set_variant): cross-check and experimental
+ * kernels next to the defaults.  Selected per cache by the caller (never by
+ * the environment); 0 = the defaults the bench runs. */
+#define CVQ_VARIANT_GENERIC 1u  /* generic kernels for every shape (no specialisation) */
+#define CVQ_VARIANT_TC_DENSE 2u /* tcgen05: dense one-hot MMA instead of 2:4 sparse   */
+#define CVQ_VARIANT_TC_PAIR 4u  /* tcgen05: CTA-pair (cta_group::2) sparse kernel     */
+#define CVQ_VARIANT_FUSED 8u    /* fp16 codebook: one fused score+value kernel        */
 
 CVQ_API cvq_status cvq_cache_create(cvq_context* ctx, const cvq_cache_desc* d,
                                     cvq_cache** out);
 CVQ_API cvq_status cvq_cache_destroy(cvq_cache* c);
+/* Tokens per stream (QuantizedKVCache::size, cache.hpp:83).  Synchronises when
+ * appends are unchecked, so deferred encoder errors surface here. */
 CVQ_API cvq_status cvq_cache_length(const cvq_cache* c, uint64_t* n_tokens);
+/* desc.capacity is an initial reservation, not a limit: appends, imports and
+ * set_length grow the pools (x1.5, whole 128-token tiles) like the reference
+ * cache grows its vectors (cache.cpp:256-285).  Growth moves the pools
+ * (cvq_cache_pools pointers are invalidated). */
+CVQ_API cvq_status cvq_cache_reserve(cvq_cache* c, uint64_t n_tokens);
+CVQ_API cvq_status cvq_cache_capacity(const cvq_cache* c, uint64_t* n_tokens);
+/* Appends never wait for the device: an encoder failure (non-finite logits,
+ * valquant.cpp:86-87) is recorded on the device, later appends are skipped,
+ * and the next synchronising call on the cache (this one, cvq_cache_length,
+ * export, any host-buffer attention / decode step) returns CVQ_ETRAINING
+ * with the length rolled back to the failed append -- the state the
+ * reference's throwing append leaves.  Prefill checks before returning. */
+CVQ_API cvq_status cvq_cache_synchronize(cvq_cache* c);
+/* CVQ_VARIANT_* bits; takes effect from the next attention call. */
+CVQ_API cvq_status cvq_cache_set_variant(cvq_cache* c, uint32_t variant);
+/* Effective key-codebook mode (CVQ_CACHE_KEYS_* bits actually in use).  A
+ * CVQ_CACHE_KEYS_TC cache whose key codebook fails the fp16 guard (an atom
+ * outside the fp16 range, or sum_r max|U| > 96: the output error of the
+ * fp16 operand approaches the 1e-3 bar) runs the fp32 CUDA-core kernels and
+ * reports the bit cleared. */
+CVQ_API cvq_status cvq_cache_key_mode(const cvq_cache* c, uint32_t* flags);
 
 /* Codebooks for slot (layer, head); host fp64 in reference order.
  * key: R*(d/2)*L*2 doubles.  value quantizer: w1[d][hidden], b1[hidden],
@@ -342,7 +375,8 @@ CVQ_API cvq_status cvq_cache_export_stream(const cvq_cache* c, uint32_t seq,
 
 /* Raw device pools (stream-major, fixed stride in words) and length setter,
  * for callers that fill codes on the device (synthetic benchmarks, CVQC
- * bulk loads).  Streams are ordered (seq, layer, kv_head). */
+ * bulk loads).  Streams are ordered (seq, layer, kv_head).  set_length grows
+ * the pools when needed (then re-query the pointers). */
 CVQ_API cvq_status cvq_cache_pools(cvq_cache* c, uint64_t** key_words,
                                    uint64_t* key_stride_words,
                                    uint64_t** value_words,

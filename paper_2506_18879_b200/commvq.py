@@ -91,6 +91,8 @@ class _Desc(C.Structure):
 
 CVQ_CACHE_KEYS_FP16 = 1
 CVQ_CACHE_KEYS_TC = 2
+# kernel variants (cvq.h CVQ_VARIANT_*), QuantizedKVCache.set_variant
+VARIANTS = {"generic": 1, "tc_dense": 2, "tc_pair": 4, "fused": 8}
 
 
 @dataclass(frozen=True)
@@ -155,12 +157,18 @@ def _ptr(x):
 
 
 class Context:
-    """cvq_context: one device, one CUDA stream (cudaStream_t or None)."""
+    """cvq_context: one device, one CUDA stream (cudaStream_t or None = a
+    private stream).  Wrappers given CUDA torch tensors order the context's
+    stream after torch's current stream on entry and torch's after the
+    context's on return (no-op when they are the same stream)."""
 
     def __init__(self, device: int = 0, stream: int | None = None):
         h = _p()
         _check(_lib.cvq_context_create(_i(device), _p(stream) if stream else None, C.byref(h)))
         self.h = h
+        sp = _p()
+        _check(_lib.cvq_context_stream(h, C.byref(sp)))
+        self.stream_ptr = sp.value or 0
 
     def close(self):
         if getattr(self, "h", None):
@@ -175,6 +183,31 @@ class Context:
 
     def synchronize(self):
         _check(_lib.cvq_context_synchronize(self.h))
+
+
+class _TorchOrder:
+    """Stream ordering between torch's current stream and a context's stream
+    around one library call on CUDA tensors (the library queues
+    work on the context stream; torch writes inputs / reads outputs on its
+    current stream)."""
+
+    def __init__(self, ctx, *xs):
+        self.ctx, self.xs, self.ext = ctx, xs, None
+
+    def __enter__(self):
+        if any(getattr(x, "is_cuda", False) for x in self.xs):
+            import torch
+            cur = torch.cuda.current_stream()
+            if cur.cuda_stream != self.ctx.stream_ptr:
+                self.cur = cur
+                self.ext = torch.cuda.ExternalStream(self.ctx.stream_ptr)
+                self.ext.wait_stream(cur)
+        return self
+
+    def __exit__(self, *exc):
+        if self.ext is not None:
+            self.cur.wait_stream(self.ext)
+        return False
 
 
 _default_ctx = None
@@ -532,14 +565,45 @@ class QuantizedKVCache:
         vp, _, vk = _buf(V)
         dt = CVQ_F64 if str(kk.dtype).endswith("float64") else CVQ_F32
         n = kk.shape[-2]
-        _check(_lib.cvq_cache_prefill(self.h, kp, vp, _u64(n), _i(dt), _i(where)))
+        with _TorchOrder(self.ctx, kk, vk):
+            _check(_lib.cvq_cache_prefill(self.h, kp, vp, _u64(n), _i(dt), _i(where)))
 
     def append(self, k, v):
-        """k, v: [n_seqs][n_layers][n_kv_heads][d] (cache.cpp:256-285)."""
+        """k, v: [n_seqs][n_layers][n_kv_heads][d] (cache.cpp:256-285).  Does
+        not wait for the device: an encoder error surfaces at the next
+        synchronising call (synchronize(), size(), host-buffer attention)."""
         kp, where, kk = _buf(k)
         vp, _, vk = _buf(v)
         dt = CVQ_F64 if str(kk.dtype).endswith("float64") else CVQ_F32
-        _check(_lib.cvq_cache_append(self.h, kp, vp, _i(dt), _i(where)))
+        with _TorchOrder(self.ctx, kk, vk):
+            _check(_lib.cvq_cache_append(self.h, kp, vp, _i(dt), _i(where)))
+
+    def synchronize(self):
+        _check(_lib.cvq_cache_synchronize(self.h))
+
+    def reserve(self, n):
+        _check(_lib.cvq_cache_reserve(self.h, _u64(n)))
+
+    def capacity_tokens(self):
+        n = _u64()
+        _check(_lib.cvq_cache_capacity(self.h, C.byref(n)))
+        return n.value
+
+    def set_variant(self, variant=0):
+        """CVQ_VARIANT_* bits (or names: "generic", "tc_dense", "tc_pair",
+        "fused") -- cross-check / experimental kernels; 0 = defaults."""
+        if isinstance(variant, str):
+            variant = [variant]
+        if not isinstance(variant, int):
+            variant = sum(VARIANTS[v] for v in variant)
+        _check(_lib.cvq_cache_set_variant(self.h, _u32(variant)))
+
+    def key_mode(self):
+        """Effective key-codebook mode: "tc", "fp16" or "fp32" ("tc" caches
+        whose codebook fails the fp16 guard report "fp32")."""
+        f = _u32()
+        _check(_lib.cvq_cache_key_mode(self.h, C.byref(f)))
+        return "tc" if f.value & CVQ_CACHE_KEYS_TC else "fp16" if f.value & CVQ_CACHE_KEYS_FP16 else "fp32"
 
     def attention(self, q, t=None, out=None):
         """q: [n_seqs][n_layers][Hq][d] float32 -> out of the same shape."""
@@ -552,14 +616,16 @@ class QuantizedKVCache:
             else:
                 out = qk.new_empty(qk.shape)
         op, _, ok = _buf(out)
-        _check(_lib.cvq_cache_attention(self.h, qp, _u64(t), op, _i(where)))
+        with _TorchOrder(self.ctx, qk, ok):
+            _check(_lib.cvq_cache_attention(self.h, qp, _u64(t), op, _i(where)))
         return out
 
     def attention_partial(self, q, m, l, o, t):
         """Device tensors: m, l [rows], o [rows][d] (split-K partial)."""
-        _check(_lib.cvq_cache_attention_partial(self.h, _p(q.data_ptr()), _u64(t),
-                                                _p(m.data_ptr()), _p(l.data_ptr()),
-                                                _p(o.data_ptr())))
+        with _TorchOrder(self.ctx, q, m, l, o):
+            _check(_lib.cvq_cache_attention_partial(self.h, _p(q.data_ptr()), _u64(t),
+                                                    _p(m.data_ptr()), _p(l.data_ptr()),
+                                                    _p(o.data_ptr())))
 
     def decode_step(self, k, v, q, out=None):
         """cache.cpp:287-296: append (k, v) then attend q at the new last position."""
@@ -570,7 +636,8 @@ class QuantizedKVCache:
         if out is None:
             out = np.zeros(qk.shape, np.float32) if where == CVQ_HOST else qk.new_empty(qk.shape)
         op, _, ok = _buf(out)
-        _check(_lib.cvq_cache_decode_step(self.h, kp, vp, _i(dt), qp, op, _i(where)))
+        with _TorchOrder(self.ctx, kk, vk, qk, ok):
+            _check(_lib.cvq_cache_decode_step(self.h, kp, vp, _i(dt), qp, op, _i(where)))
         return out
 
     def import_stream(self, seq, layer, head, key_words, value_words, n_tokens):
@@ -604,8 +671,9 @@ def lse_combine_packed(parts, rows, d, out, ctx=None):
     P = parts.shape[0]
     if parts.numel() != P * rows * (d + 2):
         raise ValueError("lse_combine_packed: parts must be [P][rows*(d+2)]")
-    _check(_lib.cvq_lse_combine_packed(ctx.h, _p(parts.data_ptr()), _u32(P), _u64(rows), _u32(d),
-                                       _p(out.data_ptr())))
+    with _TorchOrder(ctx, parts, out):
+        _check(_lib.cvq_lse_combine_packed(ctx.h, _p(parts.data_ptr()), _u32(P), _u64(rows),
+                                           _u32(d), _p(out.data_ptr())))
 
 
 def lse_combine_ptrs(ptrs_dev, offset, n_parts, rows, d, out, ctx=None):
@@ -614,8 +682,9 @@ def lse_combine_ptrs(ptrs_dev, offset, n_parts, rows, d, out, ctx=None):
     block starts at ptrs[p] + offset floats -> out [rows][d]."""
     ctx = ctx or default_context()
     addr = ptrs_dev if isinstance(ptrs_dev, int) else ptrs_dev.data_ptr()
-    _check(_lib.cvq_lse_combine_ptrs(ctx.h, _p(addr), _u64(offset), _u32(n_parts), _u64(rows),
-                                     _u32(d), _p(out.data_ptr())))
+    with _TorchOrder(ctx, out):
+        _check(_lib.cvq_lse_combine_ptrs(ctx.h, _p(addr), _u64(offset), _u32(n_parts), _u64(rows),
+                                         _u32(d), _p(out.data_ptr())))
 
 
 def lse_combine(m, l, o, out, ctx=None):
@@ -623,5 +692,6 @@ def lse_combine(m, l, o, out, ctx=None):
     ctx = ctx or default_context()
     P, rows = m.shape
     d = o.shape[-1]
-    _check(_lib.cvq_lse_combine(ctx.h, _p(m.data_ptr()), _p(l.data_ptr()), _p(o.data_ptr()),
-                                _u32(P), _u64(rows), _u32(d), _p(out.data_ptr())))
+    with _TorchOrder(ctx, m, l, o, out):
+        _check(_lib.cvq_lse_combine(ctx.h, _p(m.data_ptr()), _p(l.data_ptr()), _p(o.data_ptr()),
+                                    _u32(P), _u64(rows), _u32(d), _p(out.data_ptr())))

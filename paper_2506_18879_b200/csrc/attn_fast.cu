@@ -782,7 +782,7 @@ __global__ void __launch_bounds__(kThreads) k_fast_value(FastArgs a) {
 
 // subspace split (CTAs per stream) so the codebook slice fits in smem
 int js_for(const AttnJob& job) {
-  if (job.cb_key_tc) return tc_blocks(job.geo.R);    // tcgen05: round blocks of 11
+  if (job.cb_key_tc) return tc_blocks(job);          // tcgen05: round blocks of 11
   if (job.cb_key16) return job.geo.R <= 13 ? 1 : 2;  // fp16: 16 KiB per round
   return job.geo.R <= 12 ? 2 : 4;                    // fp32: 32 KiB per round
 }
@@ -937,7 +937,7 @@ cudaError_t run_fast_combine(const AttnJob& job, const float* pm, const float* p
 
 bool fast_path_applies(const AttnJob& job) {
   const Geom& g = job.geo;
-  if (getenv("CVQ_DISABLE_FAST")) return false;
+  if (job.variant & kVarGeneric) return false;
   return g.d == 128 && g.groups == 1 && g.L == 64 && (g.R == 11 || g.R == 21) &&
          (g.n_codes == 128 || g.n_codes == 256) && (g.G == 1 || g.G == 4) && job.n > 0;
 }
@@ -949,7 +949,7 @@ bool fused_applies(const AttnJob& job) {
   // score loop is issue-bound, so in-loop value work costs more than the
   // separate kernel); opt-in only.
   return job.cb_key16 && !job.cb_key_tc && g.R == 11 && g.G == 4 && g.n_codes == 128 &&
-         getenv("CVQ_ENABLE_FUSED");
+         (job.variant & kVarFused);
 }
 
 size_t fast_scratch_bytes(const AttnJob& job, int* n_chunks) {

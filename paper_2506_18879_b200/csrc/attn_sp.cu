@@ -33,7 +33,7 @@
 //   theta_j} / sqrt(d) is per warp (fp64-based at a work item's first tile,
 //   advanced by e^{+i 128 theta_j} per tile); a 4-warp smem sum per quarter.
 //
-// * CTA pairs (CVQ_TC_PAIR=1, experimental, off by default): clusters of 2
+// * CTA pairs (CVQ_VARIANT_TC_PAIR, experimental, off by default): clusters of 2
 //   with tcgen05 cta_group::2 -- one MMA covers 256 tokens x N = 128. Each
 //   CTA keeps half of B: rank 0 P = X, Q = Y; rank 1 P = Y, Q = -X, so side a
 //   is [X ; Y] over the P halves and side b is -[Y ; -X] over the Q halves
@@ -1009,15 +1009,11 @@ void sp_build_codebook(int R, const double* xy, uint16_t* out, uint16_t (*to_hal
   }
 }
 
-bool sp_pair_enabled() {
-  const char* e = getenv("CVQ_TC_PAIR");
-  return e && e[0] == '1';
-}
 
 cudaError_t run_sp_score(const AttnJob& job, const uint16_t* cb, size_t slot_elems,
                          const float* q, float* ps, int chunk, cudaStream_t st) {
   // cb: slot 0's single-CTA layout; the pair layout follows it (sp_build_codebook)
-  const bool pair = sp_pair_enabled();
+  const bool pair = (job.variant & kVarTcPair) != 0;
   const Geom& g = job.geo;
   if (!cb || g.d != 128 || g.L != 64 || g.subs != 64 || !sp_supported(g.R))
     return cudaErrorInvalidValue;

@@ -566,15 +566,15 @@ size_t tc_smem_bytes(int G, int R) {
          (2 * kStages + 4) * 8 + 16;
 }
 
-// the 2:4-sparse kernel is used where it applies unless CVQ_TC_DENSE=1
-bool tc_use_sparse(int R) {
-  const char* fd = getenv("CVQ_TC_DENSE");
-  return sp_supported(R) && !(fd && fd[0] == '1');
+// the 2:4-sparse kernel is used where it applies unless the cache selected
+// the dense one (CVQ_VARIANT_TC_DENSE)
+static bool tc_use_sparse(const AttnJob& job) {
+  return sp_supported(job.geo.R) && !(job.variant & kVarTcDense);
 }
 
 // partial-score slices per stream written by the tcgen05 score kernel (the
 // sparse kernel keeps <= 11 rounds resident, so R = 21 runs as 2 parts)
-int tc_blocks(int R) { return tc_use_sparse(R) ? sp_parts(R) : 1; }
+int tc_blocks(const AttnJob& job) { return tc_use_sparse(job) ? sp_parts(job.geo.R) : 1; }
 
 // per slot: the dense layout [R][2][8192], then (R = 11) the sparse kernel's
 // [R][X | Y][64] blocks (attn_sp.cu)
@@ -602,8 +602,8 @@ cudaError_t run_tc_score(const AttnJob& job, const float* q, float* ps, int chun
   const Geom& g = job.geo;
   if (!job.cb_key_tc || g.d != 128 || g.L != 64 || g.subs != 64) return cudaErrorInvalidValue;
   const size_t slot_elems = tc_codebook_elems(g.R);
-  // 2:4-sparse kernel where it applies (CVQ_TC_DENSE=1 keeps the dense one)
-  if (tc_use_sparse(g.R))
+  // 2:4-sparse kernel where it applies (CVQ_VARIANT_TC_DENSE keeps the dense one)
+  if (tc_use_sparse(job))
     return run_sp_score(job, job.cb_key_tc + (size_t)g.R * 2 * (kABytes / 2), slot_elems, q, ps,
                         chunk, st);
   TcArgs a{};

@@ -128,6 +128,15 @@ Geom make_geom(const cvq_key_config* kc, uint32_t n_codes, uint32_t hidden, uint
 
 uint64_t words_for_bits(uint64_t bits) { return (bits + 63) / 64; }
 
+// Per-stream pool strides (64-bit words) for `capacity` tokens: whole
+// 128-token tiles, rounded to 32 B so tiles stay 32-B aligned, plus slack for
+// the score kernels' window over-reads.
+void pool_strides(const Geom& g, uint64_t capacity, uint64_t* ks, uint64_t* vs) {
+  const uint64_t cap128 = (capacity + 127) / 128 * 128;
+  *ks = (words_for_bits(cap128 * (uint64_t)g.bpt) + 8 + 3) / 4 * 4;
+  *vs = (words_for_bits(cap128 * (uint64_t)g.n_codes) + 4 + 3) / 4 * 4;
+}
+
 std::vector<double> make_thetas(int d, double base) {  // rope.cpp:8-25
   std::vector<double> th(d / 2);
   for (int j = 0; j < d / 2; ++j) th[j] = std::pow(base, -2.0 * (double)j / (double)d);
@@ -156,7 +165,7 @@ struct cvq_context {
   int device = 0;
   cudaStream_t stream = nullptr;
   bool own_stream = false;
-  int* d_err = nullptr;
+  unsigned long long* d_err = nullptr;  // single-stream encoder failure flag
   DevBuf scratch;
   // live timing of the dominant attention kernel (cvq_context_profile)
   bool prof = false;
@@ -193,7 +202,12 @@ struct cvq_cache {
   double *w1 = nullptr, *b1 = nullptr, *w2 = nullptr, *b2 = nullptr;
   double* thetas = nullptr;
   std::vector<char> key_set, val_set, enc_set;
-  DevBuf attn_scratch, enc_scratch, stage_in, stage_out;
+  DevBuf attn_scratch, enc_scratch, stage_in, stage_out, stage_kv;
+  uint32_t variant = 0;                   // CVQ_VARIANT_* kernel selection
+  bool tc_demoted = false;                // a key codebook failed the fp16 guard
+  unsigned long long* d_errpos = nullptr; // first failed append position (~0 = none)
+  unsigned long long* h_errpos = nullptr; // pinned mirror, read at sync points
+  bool pending = false;                   // appends not yet checked for errors
 };
 
 namespace {
@@ -202,6 +216,91 @@ cvq_status ctx_check(cvq_context* ctx) {
   if (!ctx) return fail(CVQ_EINVAL, "null context");
   CU(cudaSetDevice(ctx->device));
   return CVQ_OK;
+}
+
+// fp16 guard of the tcgen05 path (fp16 codebook operand, fp32 accumulate):
+// the key decode K_j = sum_r U[r,j,a] + i U[r,j,b] is exact in fp32 but each
+// atom is rounded once to fp16 (relative 2^-11).  The absolute error of K_j
+// grows with kappa = sum_r max_{j,l} |U|, and sharp softmaxes turn it into
+// output error.  Measured (tests/test_tc_precision.py): kappa ~ 82 (R = 21,
+// atoms N(0, 1)) gives 7.7e-4 relative output error against the 1e-3 bar, so
+// codebooks beyond kappa = 96, or with an atom outside the fp16 range, demote
+// the cache to the fp32-codebook CUDA-core kernels (exact to ~1e-6).
+constexpr double kTcKappaMax = 96.0;
+bool tc_codebook_ok(const Geom& g, const double* xy) {
+  double kappa = 0.0;
+  for (int r = 0; r < g.R; ++r) {
+    double mx = 0.0;
+    const size_t n = (size_t)g.subs * g.L * 2;
+    for (size_t i = 0; i < n; ++i) mx = std::max(mx, std::fabs(xy[(size_t)r * n + i]));
+    if (mx > 60000.0) return false;
+    kappa += mx;
+  }
+  return kappa <= kTcKappaMax;
+}
+
+// Grows the packed pools so `need` tokens fit (amortised: x1.5, whole
+// 128-token tiles).  The reference cache grows without bound on append
+// (cache.cpp:256-285); pool pointers from cvq_cache_pools are invalidated.
+cvq_status ensure_capacity(cvq_cache* c, uint64_t need) {
+  if (need <= c->desc.capacity) return CVQ_OK;
+  uint64_t cap = std::max<uint64_t>(need, c->desc.capacity + c->desc.capacity / 2);
+  cap = (cap + 127) / 128 * 128;
+  uint64_t ks = 0, vs = 0;
+  pool_strides(c->geo, cap, &ks, &vs);
+  cudaStream_t st = c->ctx->stream;
+  uint64_t *kp = nullptr, *vp = nullptr;
+  cudaError_t e = cudaMalloc(&kp, (size_t)c->S * ks * 8);
+  if (e == cudaSuccess) e = cudaMalloc(&vp, (size_t)c->S * vs * 8);
+  if (e == cudaSuccess) e = cudaMemsetAsync(kp, 0, (size_t)c->S * ks * 8, st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(vp, 0, (size_t)c->S * vs * 8, st);
+  if (e == cudaSuccess)
+    e = cudaMemcpy2DAsync(kp, ks * 8, c->kpool, c->kstride * 8, c->kstride * 8, c->S,
+                          cudaMemcpyDeviceToDevice, st);
+  if (e == cudaSuccess)
+    e = cudaMemcpy2DAsync(vp, vs * 8, c->vpool, c->vstride * 8, c->vstride * 8, c->S,
+                          cudaMemcpyDeviceToDevice, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) {
+    if (kp) cudaFree(kp);
+    if (vp) cudaFree(vp);
+    return fail(e == cudaErrorMemoryAllocation ? CVQ_ENOMEM : CVQ_ECUDA,
+                std::string("cache grow: ") + cudaGetErrorString(e));
+  }
+  cudaFree(c->kpool);
+  cudaFree(c->vpool);
+  c->kpool = kp;
+  c->vpool = vp;
+  c->kstride = ks;
+  c->vstride = vs;
+  c->desc.capacity = cap;
+  return CVQ_OK;
+}
+
+// Appends run without a host round trip: the value encoder records the first
+// failed append position on the device (d_errpos) and the pack kernels skip
+// that batch and every later one.  At the next synchronising call the error
+// surfaces as CVQ_ETRAINING and the length rolls back to the failed append,
+// as if it had thrown (valquant.cpp:86-87, cache.cpp:256-285).
+cvq_status take_errors(cvq_cache* c) {
+  if (!c->pending) return CVQ_OK;
+  c->pending = false;
+  const unsigned long long pos = *c->h_errpos;
+  if (pos == ~0ull) return CVQ_OK;
+  if (pos < c->length) c->length = pos;
+  CU(cudaMemsetAsync(c->d_errpos, 0xFF, sizeof(unsigned long long), c->ctx->stream));
+  return fail(CVQ_ETRAINING, "encoder_forward: non-finite activations");
+}
+cvq_status enqueue_error_read(cvq_cache* c) {
+  if (c->pending)
+    CU(cudaMemcpyAsync(c->h_errpos, c->d_errpos, sizeof(unsigned long long),
+                       cudaMemcpyDeviceToHost, c->ctx->stream));
+  return CVQ_OK;
+}
+cvq_status sync_check(cvq_cache* c) {
+  TRY(enqueue_error_read(c));
+  CU(cudaStreamSynchronize(c->ctx->stream));
+  return take_errors(c);
 }
 
 void free_cache(cvq_cache* c) {
@@ -213,6 +312,9 @@ void free_cache(cvq_cache* c) {
   c->enc_scratch.release();
   c->stage_in.release();
   c->stage_out.release();
+  c->stage_kv.release();
+  if (c->d_errpos) cudaFree(c->d_errpos);
+  if (c->h_errpos) cudaFreeHost(c->h_errpos);
 }
 
 AttnJob make_job(const cvq_cache* c) {
@@ -226,7 +328,8 @@ AttnJob make_job(const cvq_cache* c) {
   j.n_slots = c->n_slots;
   j.cb_key = c->cbk;
   j.cb_key16 = c->cbk16;
-  j.cb_key_tc = c->cbtc;
+  j.cb_key_tc = c->tc_demoted ? nullptr : c->cbtc;  // demoted: fp32 CUDA-core path
+  j.variant = c->variant;
   j.cb_val = c->cbv;
   j.thetas = c->thetas;
   j.n = (long long)c->length;
@@ -287,7 +390,7 @@ CVQ_API cvq_status cvq_context_create(int device, void* stream, cvq_context** ou
     }
     c->own_stream = true;
   }
-  cudaError_t e = cudaMalloc(&c->d_err, sizeof(int));
+  cudaError_t e = cudaMalloc(&c->d_err, sizeof(unsigned long long));
   if (e != cudaSuccess) {
     delete c;
     return fail(CVQ_ECUDA, cudaGetErrorString(e));
@@ -328,6 +431,12 @@ CVQ_API cvq_status cvq_context_destroy(cvq_context* ctx) {
   if (ctx->d_err) cudaFree(ctx->d_err);
   if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
+  return CVQ_OK;
+}
+
+CVQ_API cvq_status cvq_context_stream(cvq_context* ctx, void** stream) {
+  if (!ctx || !stream) return fail(CVQ_EINVAL, "null argument");
+  *stream = ctx->stream;
   return CVQ_OK;
 }
 
@@ -377,10 +486,7 @@ CVQ_API cvq_status cvq_cache_create(cvq_context* ctx, const cvq_cache_desc* d, c
   c->S = (int)(d->n_seqs * d->n_layers * d->n_kv_heads);
   c->n_slots = (int)(d->n_layers * d->n_kv_heads);
   const Geom& g = c->geo;
-  // stream strides rounded to 32 B so 128-token tiles stay 32-B aligned
-  const uint64_t cap128 = (d->capacity + 127) / 128 * 128;  // whole 128-token tiles
-  c->kstride = (words_for_bits(cap128 * (uint64_t)g.bpt) + 8 + 3) / 4 * 4;  // slack for window over-reads
-  c->vstride = (words_for_bits(cap128 * (uint64_t)g.n_codes) + 4 + 3) / 4 * 4;
+  pool_strides(g, d->capacity, &c->kstride, &c->vstride);
   c->key_set.assign(c->n_slots, 0);
   c->val_set.assign(c->n_slots, 0);
   c->enc_set.assign(c->n_slots, 0);
@@ -390,7 +496,9 @@ CVQ_API cvq_status cvq_cache_create(cvq_context* ctx, const cvq_cache_desc* d, c
     if (e == cudaSuccess) e = cudaMemsetAsync(*p, 0, bytes ? bytes : 8, ctx->stream);
     return e;
   };
-  cudaError_t e = cudaSuccess;
+  cudaError_t e = cudaMalloc(&c->d_errpos, sizeof(unsigned long long));
+  if (e == cudaSuccess) e = cudaMemsetAsync(c->d_errpos, 0xFF, sizeof(unsigned long long), ctx->stream);
+  if (e == cudaSuccess) e = cudaMallocHost(&c->h_errpos, sizeof(unsigned long long));
   if (e == cudaSuccess) e = alloc((void**)&c->kpool, (size_t)c->S * c->kstride * 8);
   if (e == cudaSuccess) e = alloc((void**)&c->vpool, (size_t)c->S * c->vstride * 8);
   if (e == cudaSuccess) e = alloc((void**)&c->atoms64, na * 2 * sizeof(double));
@@ -442,6 +550,10 @@ CVQ_API cvq_status cvq_cache_destroy(cvq_cache* c) {
 
 CVQ_API cvq_status cvq_cache_length(const cvq_cache* c, uint64_t* n) {
   if (!c || !n) return fail(CVQ_EINVAL, "null argument");
+  if (c->pending) {  // surface deferred append errors (and their rollback)
+    TRY(ctx_check(c->ctx));
+    TRY(sync_check(const_cast<cvq_cache*>(c)));
+  }
   *n = c->length;
   return CVQ_OK;
 }
@@ -479,6 +591,7 @@ CVQ_API cvq_status cvq_cache_set_key_codebook(cvq_cache* c, uint32_t layer, uint
                        st));
   }
   std::vector<uint16_t> dt;
+  if (c->cbtc && !tc_codebook_ok(g, xy)) c->tc_demoted = true;
   if (c->cbtc) {  // canonical K-major A operand of the one-hot MMA
     dt.assign(tc_codebook_elems(g.R), 0);
     tc_build_codebook(g.R, xy, dt.data(),
@@ -532,9 +645,10 @@ CVQ_API cvq_status cvq_cache_set_value_quantizer(cvq_cache* c, uint32_t layer, u
 namespace {
 
 // Encode + pack n tokens per stream (device K/V, element (s,i,k) at
-// s*s_stride + i*d + k), appended at the current length.
+// s*s_stride + i*d + k), appended at the current length.  err_at: the
+// position a failure rolls back to (the start of the enclosing prefill).
 cvq_status encode_append(cvq_cache* c, const void* K, const void* V, int dtype,
-                         long long s_stride, long long n) {
+                         long long s_stride, long long n, uint64_t err_at) {
   const Geom& g = c->geo;
   cudaStream_t st = c->ctx->stream;
   const size_t per_tok = (size_t)c->S * (2 * sizeof(uint16_t) * g.R * g.groups + g.n_codes);
@@ -544,34 +658,33 @@ cvq_status encode_append(cvq_cache* c, const void* K, const void* V, int dtype,
   uint8_t* bits = reinterpret_cast<uint8_t*>(b + (size_t)c->S * n * g.R * g.groups);
   KeyEncTables tab{c->atoms64, c->base, c->maxnorm};
   CU(run_encode_keys(g, c->S, c->n_slots, tab, K, dtype, s_stride, n, a, b, st));
-  CU(cudaMemsetAsync(c->ctx->d_err, 0, sizeof(int), st));
   ValEncWeights w{c->w1, c->b1, c->w2, c->b2};
-  CU(run_encode_values(g, c->S, c->n_slots, w, V, dtype, s_stride, n, bits, nullptr,
-                       c->ctx->d_err, st));
-  int herr = 0;
-  CU(cudaMemcpyAsync(&herr, c->ctx->d_err, sizeof(int), cudaMemcpyDeviceToHost, st));
-  CU(cudaStreamSynchronize(st));
-  if (herr) return fail(CVQ_ETRAINING, "encoder_forward: non-finite activations");
-  CU(run_pack_keys(g, c->S, a, b, n, (long long)c->length, c->kpool, c->kstride, st));
-  CU(run_pack_values(g, c->S, bits, n, (long long)c->length, c->vpool, c->vstride, st));
+  CU(run_encode_values(g, c->S, c->n_slots, w, V, dtype, s_stride, n, bits, nullptr, c->d_errpos,
+                       err_at, st));
+  CU(run_pack_keys(g, c->S, a, b, n, (long long)c->length, c->kpool, c->kstride, st, c->d_errpos));
+  CU(run_pack_values(g, c->S, bits, n, (long long)c->length, c->vpool, c->vstride, st,
+                     c->d_errpos));
   c->length += (uint64_t)n;
+  c->pending = true;
   return CVQ_OK;
 }
 
-}  // namespace
-
-CVQ_API cvq_status cvq_cache_prefill(cvq_cache* c, const void* K, const void* V,
-                                     uint64_t n_tokens, int dtype, int where) {
+// QuantizedKVCache::prefill / append: n tokens for every stream; `check`
+// synchronises and surfaces encoder errors before returning (prefill); the
+// decode-step append leaves that to the step's own sync.
+cvq_status append_tokens(cvq_cache* c, const void* K, const void* V, uint64_t n_tokens,
+                         int dtype, int where, bool check) {
   if (!c) return fail(CVQ_EINVAL, "null cache");
   TRY(ctx_check(c->ctx));
   if (n_tokens == 0) return CVQ_OK;  // cache.cpp:225
   if (!K || !V) return fail(CVQ_EINVAL, "prefill: null input");
   if (dtype != CVQ_F32 && dtype != CVQ_F64) return fail(CVQ_EINVAL, "prefill: bad dtype");
-  if (c->length + n_tokens > c->desc.capacity) return fail(CVQ_ERANGE, "cache: capacity exceeded");
   TRY(require_codebooks(c, true, true, true));
+  TRY(ensure_capacity(c, c->length + n_tokens));
   const Geom& g = c->geo;
   const size_t es = dtype == CVQ_F32 ? 4 : 8;
   const long long s_stride = (long long)n_tokens * g.d;
+  const uint64_t err_at = c->length;
   // chunk tokens so scratch stays bounded (~256 MB of inputs per chunk)
   const long long per_tok_bytes = (long long)c->S * g.d * (long long)es * 2;
   long long chunk = (256ll << 20) / (per_tok_bytes > 0 ? per_tok_bytes : 1);
@@ -584,15 +697,21 @@ CVQ_API cvq_status cvq_cache_prefill(cvq_cache* c, const void* K, const void* V,
     long long stride = s_stride;
     if (where == CVQ_HOST) {
       const size_t row = (size_t)nn * g.d * es;
-      CU(c->stage_in.ensure(2 * row * c->S));
-      char* kd = static_cast<char*>(c->stage_in.p);
+      if (c0 > 0) CU(cudaStreamSynchronize(c->ctx->stream));  // staging buffer reuse
+      CU(c->stage_kv.ensure(2 * row * c->S));
+      char* kd = static_cast<char*>(c->stage_kv.p);
       char* vd = kd + row * c->S;
-      CU(cudaMemcpy2DAsync(kd, row, static_cast<const char*>(K) + (size_t)c0 * g.d * es,
-                           (size_t)s_stride * es, row, c->S, cudaMemcpyHostToDevice,
-                           c->ctx->stream));
-      CU(cudaMemcpy2DAsync(vd, row, static_cast<const char*>(V) + (size_t)c0 * g.d * es,
-                           (size_t)s_stride * es, row, c->S, cudaMemcpyHostToDevice,
-                           c->ctx->stream));
+      if (nn == (long long)n_tokens) {  // one contiguous block per tensor
+        CU(cudaMemcpyAsync(kd, K, row * c->S, cudaMemcpyHostToDevice, c->ctx->stream));
+        CU(cudaMemcpyAsync(vd, V, row * c->S, cudaMemcpyHostToDevice, c->ctx->stream));
+      } else {
+        CU(cudaMemcpy2DAsync(kd, row, static_cast<const char*>(K) + (size_t)c0 * g.d * es,
+                             (size_t)s_stride * es, row, c->S, cudaMemcpyHostToDevice,
+                             c->ctx->stream));
+        CU(cudaMemcpy2DAsync(vd, row, static_cast<const char*>(V) + (size_t)c0 * g.d * es,
+                             (size_t)s_stride * es, row, c->S, cudaMemcpyHostToDevice,
+                             c->ctx->stream));
+      }
       Kd = kd;
       Vd = vd;
       stride = nn * g.d;
@@ -600,14 +719,23 @@ CVQ_API cvq_status cvq_cache_prefill(cvq_cache* c, const void* K, const void* V,
       Kd = static_cast<const char*>(K) + (size_t)c0 * g.d * es;
       Vd = static_cast<const char*>(V) + (size_t)c0 * g.d * es;
     }
-    TRY(encode_append(c, Kd, Vd, dtype, stride, nn));
+    TRY(encode_append(c, Kd, Vd, dtype, stride, nn, err_at));
   }
-  return CVQ_OK;
+  return check ? sync_check(c) : CVQ_OK;
+}
+
+}  // namespace
+
+CVQ_API cvq_status cvq_cache_prefill(cvq_cache* c, const void* K, const void* V,
+                                     uint64_t n_tokens, int dtype, int where) {
+  return append_tokens(c, K, V, n_tokens, dtype, where, true);
 }
 
 CVQ_API cvq_status cvq_cache_append(cvq_cache* c, const void* k, const void* v, int dtype,
                                     int where) {
-  return cvq_cache_prefill(c, k, v, 1, dtype, where);
+  // no host round trip: encoder errors surface at the next synchronising
+  // call (cvq_cache_synchronize, cvq_cache_length, host-buffer attention)
+  return append_tokens(c, k, v, 1, dtype, where, false);
 }
 
 namespace {
@@ -636,9 +764,11 @@ cvq_status attention_common(cvq_cache* c, const float* q, uint64_t t, float* out
   }
   CU(run_attention(job, static_cast<const float*>(qd), od, m, l, o, nullptr, c->attn_scratch.p,
                    c->attn_scratch.n, c->ctx->stream, c->ctx->next_prof_pair()));
-  if (out && where == CVQ_HOST) {
+  if (out && where == CVQ_HOST) {  // the step's one sync also checks the appends
     CU(cudaMemcpyAsync(out, od, qbytes, cudaMemcpyDeviceToHost, c->ctx->stream));
+    TRY(enqueue_error_read(c));
     CU(cudaStreamSynchronize(c->ctx->stream));
+    return take_errors(c);
   }
   return CVQ_OK;
 }
@@ -702,7 +832,7 @@ CVQ_API cvq_status cvq_cache_import_stream(cvq_cache* c, uint32_t seq, uint32_t 
   TRY(ctx_check(c->ctx));
   if (seq >= c->desc.n_seqs || layer >= c->desc.n_layers || head >= c->desc.n_kv_heads)
     return fail(CVQ_EINVAL, "cache: stream out of range");
-  if (n > c->desc.capacity) return fail(CVQ_ERANGE, "cache: capacity exceeded");
+  TRY(ensure_capacity(c, n));
   const Geom& g = c->geo;
   const size_t s = ((size_t)seq * c->desc.n_layers + layer) * c->desc.n_kv_heads + head;
   const uint64_t nk = words_for_bits(n * (uint64_t)g.bpt), nv = words_for_bits(n * (uint64_t)g.n_codes);
@@ -723,6 +853,7 @@ CVQ_API cvq_status cvq_cache_export_stream(const cvq_cache* c, uint32_t seq, uin
   CU(cudaSetDevice(c->ctx->device));
   if (seq >= c->desc.n_seqs || layer >= c->desc.n_layers || head >= c->desc.n_kv_heads)
     return fail(CVQ_EINVAL, "cache: stream out of range");
+  TRY(sync_check(const_cast<cvq_cache*>(c)));
   const Geom& g = c->geo;
   const size_t s = ((size_t)seq * c->desc.n_layers + layer) * c->desc.n_kv_heads + head;
   const uint64_t nk = words_for_bits(c->length * (uint64_t)g.bpt);
@@ -746,8 +877,44 @@ CVQ_API cvq_status cvq_cache_pools(cvq_cache* c, uint64_t** kw, uint64_t* ks, ui
 
 CVQ_API cvq_status cvq_cache_set_length(cvq_cache* c, uint64_t n) {
   if (!c) return fail(CVQ_EINVAL, "null cache");
-  if (n > c->desc.capacity) return fail(CVQ_ERANGE, "cache: capacity exceeded");
+  TRY(ctx_check(c->ctx));
+  TRY(ensure_capacity(c, n));
   c->length = n;
+  return CVQ_OK;
+}
+
+CVQ_API cvq_status cvq_cache_reserve(cvq_cache* c, uint64_t n_tokens) {
+  if (!c) return fail(CVQ_EINVAL, "null cache");
+  TRY(ctx_check(c->ctx));
+  return ensure_capacity(c, n_tokens);
+}
+
+CVQ_API cvq_status cvq_cache_capacity(const cvq_cache* c, uint64_t* n_tokens) {
+  if (!c || !n_tokens) return fail(CVQ_EINVAL, "null argument");
+  *n_tokens = c->desc.capacity;
+  return CVQ_OK;
+}
+
+CVQ_API cvq_status cvq_cache_synchronize(cvq_cache* c) {
+  if (!c) return fail(CVQ_EINVAL, "null cache");
+  TRY(ctx_check(c->ctx));
+  return sync_check(c);
+}
+
+CVQ_API cvq_status cvq_cache_set_variant(cvq_cache* c, uint32_t variant) {
+  if (!c) return fail(CVQ_EINVAL, "null cache");
+  if (variant & ~(uint32_t)(CVQ_VARIANT_GENERIC | CVQ_VARIANT_TC_DENSE | CVQ_VARIANT_TC_PAIR |
+                            CVQ_VARIANT_FUSED))
+    return fail(CVQ_EINVAL, "cache: unknown kernel variant");
+  c->variant = variant;
+  return CVQ_OK;
+}
+
+CVQ_API cvq_status cvq_cache_key_mode(const cvq_cache* c, uint32_t* flags) {
+  if (!c || !flags) return fail(CVQ_EINVAL, "null argument");
+  uint32_t f = c->desc.flags & (CVQ_CACHE_KEYS_FP16 | CVQ_CACHE_KEYS_TC);
+  if (!c->cbtc || c->tc_demoted) f &= ~CVQ_CACHE_KEYS_TC;
+  *flags = f;
   return CVQ_OK;
 }
 
@@ -1009,15 +1176,15 @@ CVQ_API cvq_status cvq_encoder_forward_infer(cvq_context* ctx, uint32_t d, uint3
   CU(cudaMemcpyAsync(dw2, w2, (size_t)hidden * n_codes * 8, cudaMemcpyHostToDevice, st));
   CU(cudaMemcpyAsync(db2, b2, (size_t)n_codes * 8, cudaMemcpyHostToDevice, st));
   CU(cudaMemcpyAsync(dv, values, (size_t)n * d * 8, cudaMemcpyHostToDevice, st));
-  CU(cudaMemsetAsync(ctx->d_err, 0, sizeof(int), st));
+  CU(cudaMemsetAsync(ctx->d_err, 0xFF, sizeof(unsigned long long), st));
   ValEncWeights w{dw1, db1, dw2, db2};
-  CU(run_encode_values(g, 1, 1, w, dv, CVQ_F64, 0, (long long)n, dbits, dl, ctx->d_err, st));
-  int herr = 0;
-  CU(cudaMemcpyAsync(&herr, ctx->d_err, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CU(run_encode_values(g, 1, 1, w, dv, CVQ_F64, 0, (long long)n, dbits, dl, ctx->d_err, 0, st));
+  unsigned long long herr = ~0ull;
+  CU(cudaMemcpyAsync(&herr, ctx->d_err, sizeof(herr), cudaMemcpyDeviceToHost, st));
   CU(cudaMemcpyAsync(bits, dbits, (size_t)n * n_codes, cudaMemcpyDeviceToHost, st));
   if (logits) CU(cudaMemcpyAsync(logits, dl, (size_t)n * n_codes * 8, cudaMemcpyDeviceToHost, st));
   CU(cudaStreamSynchronize(st));
-  if (herr) return fail(CVQ_ETRAINING, "encoder_forward: non-finite activations");
+  if (herr != ~0ull) return fail(CVQ_ETRAINING, "encoder_forward: non-finite activations");
   return CVQ_OK;
 }
 

@@ -41,7 +41,16 @@ struct AttnJob {
   long long n;                // tokens per stream
   long long pos0;             // global position of token 0
   long long t;                // query position
+  uint32_t variant;           // kVar* kernel-variant bits (cvq_cache_set_variant)
 };
+
+// Kernel variants selectable per cache (cvq.h CVQ_VARIANT_*): cross-check /
+// experimental kernels next to the defaults, chosen by the caller, never by
+// the environment.
+constexpr uint32_t kVarGeneric = 1u;  // generic kernels for every shape
+constexpr uint32_t kVarTcDense = 2u;  // dense one-hot tcgen05 kernel (attn_tc.cu)
+constexpr uint32_t kVarTcPair = 4u;   // CTA-pair (cta_group::2) sparse kernel
+constexpr uint32_t kVarFused = 8u;    // single fused CUDA-core kernel (fp16 codebook)
 
 // Scratch handed to run_attention (sized by attn_scratch_bytes).
 size_t attn_scratch_bytes(const AttnJob& job, int* n_chunks_out);
@@ -58,7 +67,7 @@ cudaError_t run_attention(const AttnJob& job, const float* q, float* out,
 
 // tcgen05 one-hot-MMA score kernel (attn_tc.cu).
 size_t tc_smem_bytes(int G, int R);
-int tc_blocks(int R);
+int tc_blocks(const AttnJob& job);
 // A operand of the one-hot MMA for one slot: [R][side][16 KiB core-matrix
 // layout]; side b holds the rotated codebook (x <- -y, y <- x).
 void tc_build_codebook(int R, const double* xy, uint16_t* out, uint16_t (*to_half)(double));
@@ -135,7 +144,8 @@ struct ValEncWeights {
 cudaError_t run_encode_values(const Geom& g, int S, int n_slots,
                               const ValEncWeights& w, const void* vals,
                               int dtype, long long s_stride, long long n,
-                              uint8_t* bits, double* logits, int* err_flag,
+                              uint8_t* bits, double* logits,
+                              unsigned long long* errpos, unsigned long long tok0,
                               cudaStream_t st);
 
 // ---- key-codebook training (train.cu) -------------------------------------
@@ -175,12 +185,17 @@ int train_value_quantizer_gpu(const double* calib, long long n, int d, int n_cod
 // ---- packing (pack.cu) -----------------------------------------------------
 // Writes n tokens' key codes (a/b [s][n][R*groups]) into stream words at
 // token offset tok0 (read-modify-write of boundary words).
+// errpos (optional): the cache's first-failed-append position; a batch at
+// tok0 >= *errpos is not written (a failed append leaves the words as they
+// were, cache.cpp:256-285 throws before mutating).
 cudaError_t run_pack_keys(const Geom& g, int S, const uint16_t* a,
                           const uint16_t* b, long long n, long long tok0,
-                          uint64_t* kpool, uint64_t kstride, cudaStream_t st);
+                          uint64_t* kpool, uint64_t kstride, cudaStream_t st,
+                          const unsigned long long* errpos = nullptr);
 cudaError_t run_pack_values(const Geom& g, int S, const uint8_t* bits,
                             long long n, long long tok0, uint64_t* vpool,
-                            uint64_t vstride, cudaStream_t st);
+                            uint64_t vstride, cudaStream_t st,
+                            const unsigned long long* errpos = nullptr);
 cudaError_t run_unpack_keys(const Geom& g, const uint64_t* words, long long n,
                             uint16_t* a, uint16_t* b, cudaStream_t st);
 cudaError_t run_unpack_values(const Geom& g, const uint64_t* words,

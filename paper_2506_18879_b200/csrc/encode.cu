@@ -543,7 +543,8 @@ template <int TV>
 __global__ void k_encode_values(Geom g, int n_slots, ValEncWeights w,
                                 const void* __restrict__ vals, int dtype, long long s_stride,
                                 long long n, uint8_t* __restrict__ bits,
-                                double* __restrict__ logits, int* __restrict__ err) {
+                                double* __restrict__ logits,
+                                unsigned long long* __restrict__ errpos, unsigned long long tok0) {
   extern __shared__ double sm[];
   double* T = sm;                          // [TV][d]
   double* H = T + (size_t)TV * g.d;        // [TV][hidden]
@@ -596,7 +597,7 @@ __global__ void k_encode_values(Geom g, int n_slots, ValEncWeights w,
     const double bc = b2[c];
     for (int k = 0; k < nt; ++k) {
       const double v = __dadd_rn(lg[k], bc);
-      if (!isfinite(v)) atomicExch(err, 1);
+      if (!isfinite(v)) atomicMin(errpos, tok0);  // valquant.cpp:86-87 (TrainingError)
       const size_t o = ((size_t)s * n + i0 + k) * g.n_codes + c;
       bits[o] = v > 0.0 ? 1 : 0;
       if (logits) logits[o] = v;
@@ -607,7 +608,8 @@ __global__ void k_encode_values(Geom g, int n_slots, ValEncWeights w,
 template <int TV>
 static cudaError_t launch_values(const Geom& g, int S, int n_slots, const ValEncWeights& w,
                                  const void* vals, int dtype, long long s_stride, long long n,
-                                 uint8_t* bits, double* logits, int* err_flag, cudaStream_t st) {
+                                 uint8_t* bits, double* logits, unsigned long long* errpos,
+                                 unsigned long long tok0, cudaStream_t st) {
   int threads = ((g.hidden > g.n_codes ? g.hidden : g.n_codes) + 31) / 32 * 32;
   if (threads > 1024) threads = 1024;
   if (threads < 64) threads = 64;
@@ -619,18 +621,21 @@ static cudaError_t launch_values(const Geom& g, int S, int n_slots, const ValEnc
   }
   dim3 grid((unsigned)((n + TV - 1) / TV), S);
   k_encode_values<TV><<<grid, threads, sm, st>>>(g, n_slots, w, vals, dtype, s_stride, n, bits,
-                                                 logits, err_flag);
+                                                 logits, errpos, tok0);
   count_launch();
   return cudaGetLastError();
 }
 
 cudaError_t run_encode_values(const Geom& g, int S, int n_slots, const ValEncWeights& w,
                               const void* vals, int dtype, long long s_stride, long long n,
-                              uint8_t* bits, double* logits, int* err_flag, cudaStream_t st) {
+                              uint8_t* bits, double* logits, unsigned long long* errpos,
+                              unsigned long long tok0, cudaStream_t st) {
   if (n <= 0 || S <= 0) return cudaSuccess;
   if (n < 16)  // decode-step appends: one token per CTA, no wasted lanes
-    return launch_values<1>(g, S, n_slots, w, vals, dtype, s_stride, n, bits, logits, err_flag, st);
-  return launch_values<16>(g, S, n_slots, w, vals, dtype, s_stride, n, bits, logits, err_flag, st);
+    return launch_values<1>(g, S, n_slots, w, vals, dtype, s_stride, n, bits, logits, errpos, tok0,
+                            st);
+  return launch_values<16>(g, S, n_slots, w, vals, dtype, s_stride, n, bits, logits, errpos, tok0,
+                           st);
 }
 
 }  // namespace cvq

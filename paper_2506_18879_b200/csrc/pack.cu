@@ -34,7 +34,9 @@ struct BitFieldSrc {
 // Writes batch fields [0, nf) of stream s at stream field offset f0.
 template <class Src>
 __global__ void k_pack(Src src, int lb, unsigned long long f0, unsigned long long nf,
-                       uint64_t* __restrict__ pool, uint64_t stride) {
+                       uint64_t* __restrict__ pool, uint64_t stride,
+                       const unsigned long long* __restrict__ errpos, unsigned long long tok0) {
+  if (errpos && *errpos <= tok0) return;  // this append (or an earlier one) failed
   const int s = blockIdx.y;
   const unsigned long long bit0 = f0 * lb, bit1 = (f0 + nf) * lb;  // [bit0, bit1)
   const unsigned long long w0 = bit0 >> 6, w1 = (bit1 + 63) >> 6;
@@ -61,29 +63,35 @@ __global__ void k_pack(Src src, int lb, unsigned long long f0, unsigned long lon
 template <class Src>
 static cudaError_t launch_pack(Src src, int S, int lb, unsigned long long f0,
                                unsigned long long nf, uint64_t* pool, uint64_t stride,
-                               cudaStream_t st) {
-  if (nf == 0 || S == 0) return cudaSuccess;
+                               cudaStream_t st, const unsigned long long* errpos,
+                               unsigned long long tok0) {
+  // lb = 0 (n_levels = 1): zero-width fields, nothing to write (BitBuffer
+  // appends of 0 bits, cache.cpp:60-75)
+  if (nf == 0 || S == 0 || lb == 0) return cudaSuccess;
   const unsigned long long w0 = (f0 * lb) >> 6, w1 = ((f0 + nf) * lb + 63) >> 6;
   const unsigned long long nw = w1 - w0;
   dim3 grid((unsigned)((nw + 255) / 256), S);
-  k_pack<Src><<<grid, 256, 0, st>>>(src, lb, f0, nf, pool, stride);
+  k_pack<Src><<<grid, 256, 0, st>>>(src, lb, f0, nf, pool, stride, errpos, tok0);
   count_launch();
   return cudaGetLastError();
 }
 
 cudaError_t run_pack_keys(const Geom& g, int S, const uint16_t* a, const uint16_t* b,
                           long long n, long long tok0, uint64_t* kpool, uint64_t kstride,
-                          cudaStream_t st) {
+                          cudaStream_t st, const unsigned long long* errpos) {
   KeyFieldSrc src{a, b, (unsigned long long)n * g.fpt};
   return launch_pack(src, S, g.lb, (unsigned long long)tok0 * g.fpt,
-                     (unsigned long long)n * g.fpt, kpool, kstride, st);
+                     (unsigned long long)n * g.fpt, kpool, kstride, st, errpos,
+                     (unsigned long long)tok0);
 }
 
 cudaError_t run_pack_values(const Geom& g, int S, const uint8_t* bits, long long n,
-                            long long tok0, uint64_t* vpool, uint64_t vstride, cudaStream_t st) {
+                            long long tok0, uint64_t* vpool, uint64_t vstride, cudaStream_t st,
+                            const unsigned long long* errpos) {
   BitFieldSrc src{bits, (unsigned long long)n * g.n_codes};
   return launch_pack(src, S, 1, (unsigned long long)tok0 * g.n_codes,
-                     (unsigned long long)n * g.n_codes, vpool, vstride, st);
+                     (unsigned long long)n * g.n_codes, vpool, vstride, st, errpos,
+                     (unsigned long long)tok0);
 }
 
 // ---- unpack (cache.cpp:108-135, 145-155): one thread per field ----------
@@ -109,6 +117,11 @@ cudaError_t run_unpack_keys(const Geom& g, const uint64_t* words, long long n, u
                             uint16_t* b, cudaStream_t st) {
   const unsigned long long nf = (unsigned long long)n * g.fpt;
   if (nf == 0) return cudaSuccess;
+  if (g.lb == 0) {  // n_levels = 1: every code is 0 (cache.cpp:108-135)
+    cudaError_t e = cudaMemsetAsync(a, 0, (nf / 2) * sizeof(uint16_t), st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(b, 0, (nf / 2) * sizeof(uint16_t), st);
+    return e;
+  }
   k_unpack_keys<<<(unsigned)((nf + 255) / 256), 256, 0, st>>>(words, g.lb, nf, a, b);
   count_launch();
   return cudaGetLastError();

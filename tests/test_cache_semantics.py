@@ -1,0 +1,145 @@
+"""Device-resident cache semantics the reference's QuantizedKVCache has
+(cache.hpp:62-113, cache.cpp:188-373) and round 1 lacked:
+
+* no fixed capacity: appends / prefill / imports past the initial
+  reservation grow the pools (the reference's vectors grow,
+  cache.cpp:256-285), with words identical to the reference packing;
+* an append whose value encoder yields non-finite logits throws
+  TrainingError and leaves the cache unchanged (valquant.cpp:86-87) -- here
+  the error is deferred to the next synchronising call (appends never wait
+  for the device) but the observable state is the same;
+* the tcgen05 fp16-operand guard: a key codebook whose atoms make the fp16
+  operand too coarse demotes the cache to the fp32 kernels (key_mode()).
+"""
+import numpy as np
+import pytest
+
+from oracle.oracle import KQ, Oracle
+from tests import fixtures as fx
+
+pytestmark = pytest.mark.gpu
+
+P = Oracle("port")
+
+
+@pytest.fixture(scope="module")
+def G():
+    from paper_2506_18879_b200 import commvq
+    return commvq
+
+
+def _cache(G, f, capacity, keys="fp32"):
+    c = G.QuantizedKVCache(f.kq, 8, capacity=capacity, hidden=16, keys=keys)
+    c.set_key_codebook(0, 0, f.atoms)
+    c.set_value_quantizer(0, 0, f.vrows, f.w1, f.b1, f.w2, f.b2)
+    return c
+
+
+def test_appends_grow_past_initial_capacity(G):
+    """test_cache.cpp:155-180 (prefill == appends, word-exact) with the
+    device cache created for 16 tokens and filled with 700 (prefill 300, then
+    400 single appends): words equal the oracle cache's; capacity grew."""
+    f = fx.CacheFixture()
+    K = P.gen_synth(700, 8, 8, 3)
+    V = P.gen_synth(700, 8, 8, 4)
+    c = _cache(G, f, 16)
+    c.prefill(K[None, None, None, :300], V[None, None, None, :300])
+    for i in range(300, 700):
+        c.append(K[None, None, None, i], V[None, None, None, i])
+    assert c.size() == 700 and c.capacity_tokens() >= 700
+    kw, vw = c.export_stream(0, 0, 0)
+    a, b = P.encode_keys(f.kq, f.atoms, K)
+    bits, _ = P.encoder_forward_infer(f.w1, f.b1, f.w2, f.b2, V)
+    assert (kw == P.pack_key_codes(f.kq, a, b)).all() and (vw == P.pack_value_codes(bits)).all()
+    q = P.rng(9).normal(8)
+    out = c.attention(q.reshape(1, 1, 1, 8).astype(np.float32), 699)
+    want, _, _ = P.fused_attention(f.kq, f.atoms, a, b, bits, f.vrows, q, 699)
+    assert fx.rel_err(out.reshape(-1), want) <= 1e-5
+
+
+def test_import_and_set_length_grow(G):
+    kq = KQ(128, 64, 64, 11)
+    c = G.QuantizedKVCache(kq, 128, capacity=128, keys="tc")
+    rng = P.rng(3)
+    atoms = rng.normal(2 * kq.n_atoms, 0.3)
+    vrows = rng.normal(128 * 128, 1 / 16).reshape(128, 128)
+    c.set_key_codebook(0, 0, atoms)
+    c.set_value_quantizer(0, 0, vrows)
+    n = 5000
+    a, b = fx.random_key_codes(kq, n, rng=rng)
+    bits = fx.random_value_codes(128, n, rng=rng)
+    c.import_stream(0, 0, 0, P.pack_key_codes(kq, a, b), P.pack_value_codes(bits), n)
+    assert c.capacity_tokens() >= n
+    q = rng.normal(128)
+    out = c.attention(q.reshape(1, 1, 1, 128).astype(np.float32), n - 1)
+    want, _, _ = P.fused_attention(kq, atoms, a, b, bits, vrows, q, n - 1)
+    assert fx.rel_err(out.reshape(-1), want) <= 1e-3
+    c.set_length(9000)
+    assert c.size() == 9000 and c.capacity_tokens() >= 9000
+
+
+def test_nonfinite_append_rolls_back(G):
+    """A value row with an inf makes the logits non-finite: the append is
+    dropped and TrainingError surfaces at the next synchronising call; the
+    tokens before it are intact and later appends work again."""
+    f = fx.CacheFixture()
+    K = P.gen_synth(40, 8, 8, 5)
+    V = P.gen_synth(40, 8, 8, 6)
+    c = _cache(G, f, 64)
+    c.prefill(K[None, None, None, :20], V[None, None, None, :20])
+    bad = V[20].copy()
+    bad[0] = np.inf
+    c.append(K[None, None, None, 20], bad[None, None, None])  # returns at once
+    c.append(K[None, None, None, 21], V[None, None, None, 21])  # skipped on the device
+    with pytest.raises(G.TrainingError):
+        c.synchronize()
+    assert c.size() == 20
+    for i in range(20, 40):
+        c.append(K[None, None, None, i], V[None, None, None, i])
+    assert c.size() == 40
+    kw, vw = c.export_stream(0, 0, 0)
+    a, b = P.encode_keys(f.kq, f.atoms, K)
+    bits, _ = P.encoder_forward_infer(f.w1, f.b1, f.w2, f.b2, V)
+    assert (kw == P.pack_key_codes(f.kq, a, b)).all() and (vw == P.pack_value_codes(bits)).all()
+    # a failing prefill leaves the cache unchanged
+    with pytest.raises(G.TrainingError):
+        Vb = V[None, None, None, :10].copy()
+        Vb[0, 0, 0, 7, 1] = np.nan
+        c.prefill(K[None, None, None, :10], Vb)
+    assert c.size() == 40
+
+
+def test_decode_step_host_buffers_reports_encoder_error(G):
+    f = fx.CacheFixture()
+    K = P.gen_synth(10, 8, 8, 7)
+    V = P.gen_synth(10, 8, 8, 8)
+    c = _cache(G, f, 16)
+    c.prefill(K[None, None, None, :9], V[None, None, None, :9])
+    bad = V[9].copy()
+    bad[3] = -np.inf
+    q = np.ones((1, 1, 1, 8), np.float32)
+    with pytest.raises(G.TrainingError):
+        c.decode_step(K[None, None, None, 9], bad[None, None, None], q)
+    assert c.size() == 9
+
+
+@pytest.mark.parametrize("scale,want_mode", [(0.3, "tc"), (1.0, "tc"), (3.0, "fp32")])
+def test_tc_fp16_guard(G, scale, want_mode):
+    """sum_r max|U| <= 96 keeps the tcgen05 path (R = 11 at sigma 1.0: ~43);
+    sigma 3.0 (~130) demotes to the fp32 kernels, which then meet 1e-4."""
+    kq = KQ(128, 64, 64, 11)
+    nc, n = 128, 3000
+    rng = P.rng(int(scale * 100))
+    atoms = rng.normal(2 * kq.n_atoms, scale)
+    vrows = rng.normal(nc * 128, 1 / 16).reshape(nc, 128)
+    c = G.QuantizedKVCache(kq, nc, capacity=n, keys="tc")
+    c.set_key_codebook(0, 0, atoms)
+    c.set_value_quantizer(0, 0, vrows)
+    assert c.key_mode() == want_mode
+    a, b = fx.random_key_codes(kq, n, rng=rng)
+    bits = fx.random_value_codes(nc, n, rng=rng)
+    c.import_stream(0, 0, 0, P.pack_key_codes(kq, a, b), P.pack_value_codes(bits), n)
+    q = rng.normal(128)
+    out = c.attention(q.reshape(1, 1, 1, 128).astype(np.float32), n - 1)
+    want, _, _ = P.fused_attention(kq, atoms, a, b, bits, vrows, q, n - 1)
+    assert fx.rel_err(out.reshape(-1), want) <= (1e-3 if want_mode == "tc" else 1e-4)

@@ -340,7 +340,7 @@ def test_cache_2bit_encode_decode_sample(G):
 @pytest.mark.parametrize("keys", ["fp32", "fp16", "tc"])
 @pytest.mark.parametrize("preset,n", [("1bit", 1), ("1bit", 127), ("1bit", 129), ("1bit", 3001),
                                       ("2bit", 5), ("2bit", 1000), ("2bit", 2177)])
-def test_fast_path_tiles_vs_oracle_and_generic(G, preset, n, keys, monkeypatch):
+def test_fast_path_tiles_vs_oracle_and_generic(G, preset, n, keys):
     """The specialised kernels (attn_fast.cu) on partial tiles / chunks, GQA=4,
     two sequences x two layers; each q head vs the oracle, and fast == generic.
     Tolerance (north_star): outputs within 1e-3 relative; the fp32-codebook
@@ -371,9 +371,9 @@ def test_fast_path_tiles_vs_oracle_and_generic(G, preset, n, keys, monkeypatch):
     q = rng.normal(B * Ly * H * Gq * 128).reshape(B, Ly, H * Gq, 128).astype(np.float32)
     t = n - 1 + 777
     out = c.attention(q, t)
-    monkeypatch.setenv("CVQ_DISABLE_FAST", "1")
+    c.set_variant("generic")
     out_generic = c.attention(q, t)
-    monkeypatch.delenv("CVQ_DISABLE_FAST")
+    c.set_variant(0)
     assert fx.rel_err(out, out_generic) <= (1e-5 if keys == "fp32" else tol)
     worst = 0.0
     for sq in range(B):
@@ -442,7 +442,7 @@ def test_encode_keys_small_batches_bit_exact(G, shape):
 
 
 @pytest.mark.parametrize("n", [1, 200, 5000])
-def test_fused_kernel_matches_split_kernels(G, n, monkeypatch):
+def test_fused_kernel_matches_split_kernels(G, n):
     """k_fast_attn_h (opt-in single-kernel path) == score + value kernels."""
     kq = KQ(128, 64, 64, 11)
     nc, H, Gq = 128, 2, 4
@@ -457,7 +457,7 @@ def test_fused_kernel_matches_split_kernels(G, n, monkeypatch):
             c.import_stream(0, layer, h, P.pack_key_codes(kq, a, b), P.pack_value_codes(bits), n)
     q = rng.normal(2 * H * Gq * 128).reshape(1, 2, H * Gq, 128).astype(np.float32)
     split = c.attention(q)
-    monkeypatch.setenv("CVQ_ENABLE_FUSED", "1")
+    c.set_variant("fused")
     fused = c.attention(q)
     assert fx.rel_err(fused, split) <= 1e-5
 
@@ -555,9 +555,9 @@ def test_mha_one_query_head_per_stream(G, preset, n, keys):
 @pytest.mark.parametrize("R,Gq,n", [(11, 4, 1), (11, 4, 127), (11, 4, 129), (11, 4, 8197),
                                     (11, 1, 300), (11, 1, 20000), (21, 4, 1000), (21, 4, 9001),
                                     (21, 1, 4099)])
-def test_sparse_tc_matches_dense_tc(G, R, Gq, n, monkeypatch):
+def test_sparse_tc_matches_dense_tc(G, R, Gq, n):
     """The 2:4-sparse tcgen05 kernel (attn_sp.cu) against the dense one-hot
-    tcgen05 kernel (CVQ_TC_DENSE=1) on the same cache: same fp16 codebook,
+    tcgen05 kernel (variant "tc_dense") on the same cache: same fp16 codebook,
     fp32 accumulation in another order, so outputs agree to 1e-5 relative.
     3 layers x 2 KV heads exercise codebook-slot reloads; the 2-bit preset
     (R = 21) runs as two round parts of 11 and 10 resident rounds whose
@@ -576,9 +576,9 @@ def test_sparse_tc_matches_dense_tc(G, R, Gq, n, monkeypatch):
     q = rng.normal(Ly * H * Gq * 128).reshape(1, Ly, H * Gq, 128).astype(np.float32)
     t = n + 4000
     out_sp = c.attention(q, t)
-    monkeypatch.setenv("CVQ_TC_DENSE", "1")
+    c.set_variant("tc_dense")
     out_dense = c.attention(q, t)
-    monkeypatch.delenv("CVQ_TC_DENSE")
+    c.set_variant(0)
     assert np.isfinite(out_sp).all()
     assert fx.rel_err(out_sp, out_dense) <= 1e-5
 
@@ -610,9 +610,9 @@ def test_sparse_tc_tile_boundaries_vs_oracle(G, n):
 
 
 @pytest.mark.parametrize("R,Gq,n", [(11, 4, 8197), (11, 1, 300), (21, 4, 1000), (11, 4, 129)])
-def test_pair_tc_matches_dense_tc(G, R, Gq, n, monkeypatch):
+def test_pair_tc_matches_dense_tc(G, R, Gq, n):
     """The CTA-pair (tcgen05 cta_group::2) variant of the sparse kernel
-    (CVQ_TC_PAIR=1): each CTA of an SM pair holds half of the codebook rows
+    (variant "tc_pair"): each CTA of an SM pair holds half of the codebook rows
     and 128 of the 256 tokens of a pair tile; ragged tiles leave the second
     CTA empty.  Same cache, outputs vs the dense kernel within 1e-5."""
     kq = KQ(128, 64, 64, R)
@@ -628,24 +628,21 @@ def test_pair_tc_matches_dense_tc(G, R, Gq, n, monkeypatch):
             c.import_stream(0, layer, h, P.pack_key_codes(kq, a, b), P.pack_value_codes(bits), n)
     q = rng.normal(Ly * H * Gq * 128).reshape(1, Ly, H * Gq, 128).astype(np.float32)
     t = n + 99
-    monkeypatch.setenv("CVQ_TC_PAIR", "1")
+    c.set_variant("tc_pair")
     out_pair = c.attention(q, t)
-    monkeypatch.delenv("CVQ_TC_PAIR")
-    monkeypatch.setenv("CVQ_TC_DENSE", "1")
+    c.set_variant("tc_dense")
     out_dense = c.attention(q, t)
     assert np.isfinite(out_pair).all()
     assert fx.rel_err(out_pair, out_dense) <= 1e-5
 
 
 @pytest.mark.parametrize("dense", [False, True])
-def test_tc_long_context_phases_vs_oracle(G, dense, monkeypatch):
+def test_tc_long_context_phases_vs_oracle(G, dense):
     """Both tcgen05 score kernels far from the query (Delta ~ 1e6) and past
     two 8192-token work items: the sparse kernel advances each warp's phases
     by e^{i 128 theta} per tile from an fp64-reduced base per item, the dense
     one per token from an fp64 base per tile.  Outputs vs the oracle within
     the 1e-3 bar, with a non-zero position_offset and a ragged last tile."""
-    if dense:
-        monkeypatch.setenv("CVQ_TC_DENSE", "1")
     kq = KQ(128, 64, 64, 11)
     nc, n, Gq, off = 128, 16384 + 77, 4, 5
     rng = P.rng(2024)
@@ -655,6 +652,8 @@ def test_tc_long_context_phases_vs_oracle(G, dense, monkeypatch):
     bits = fx.random_value_codes(nc, n, rng=rng)
     c = G.QuantizedKVCache(kq, nc, n_kv_heads=1, q_per_kv=Gq, capacity=n, keys="tc",
                            position_offset=off)
+    if dense:
+        c.set_variant("tc_dense")
     c.set_key_codebook(0, 0, atoms)
     c.set_value_quantizer(0, 0, vrows)
     c.import_stream(0, 0, 0, P.pack_key_codes(kq, a, b), P.pack_value_codes(bits), n)

@@ -60,7 +60,7 @@ c.import_stream(0, 0, 0, P.pack_key_codes(kq, a, b), P.pack_value_codes(bits), n
 q = rng.normal(Gq * 128).reshape(1, 1, Gq, 128).astype(np.float32)
 t = n - 1
 out_sp = c.attention(q, t)[0, 0]
-os.environ["CVQ_TC_DENSE"] = "1"
+c.set_variant("tc_dense")
 out_d = c.attention(q, t)[0, 0]
 np.set_printoptions(precision=3, suppress=True, linewidth=200)
 for h in range(Gq):
