@@ -24,6 +24,7 @@
 #include <memory>
 #include <stdexcept>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "commvq/attn.hpp"
@@ -134,19 +135,22 @@ inline AttnResult naive_quantized_attention(const AttnInput& in, RopeTable& tabl
   return attend(in, table, true);
 }
 
-// keyquant.hpp:135-136 / keyquant.cpp:705-739.  Codes are those of the
-// reference brute-force search for either AssignSearch value (the
-// reference's two searches agree, test_keyquant.cpp:159-177).
+// keyquant.hpp:135-136 / keyquant.cpp:705-739.  Each AssignSearch value
+// reproduces the reference's own search bit for bit: brute_force the exact
+// sequential distances (180-200), factorized the base - 2 pu - 2 pv ranking
+// (204-224) -- they can pick differently on fp64 near-ties, as the
+// reference's do.
 inline KeyCodes encode_keys(const Mat& keys, const KeyCodebook& cb,
-                            AssignSearch = AssignSearch::brute_force) {
+                            AssignSearch search = AssignSearch::brute_force) {
   cb.config.validate();
   if (keys.cols != cb.config.d) throw std::invalid_argument("encode_keys: keys width != d");
   KeyCodes codes = KeyCodes::empty(cb.config, keys.rows);
   if (keys.rows == 0) return codes;
   const cvq_key_config ck = key_config(cb.config);
   const std::vector<double> xy = atoms_xy(cb);
-  check(cvq_encode_keys(context(), &ck, xy.data(), keys.data.data(), keys.rows,
-                        codes.a.data(), codes.b.data()));
+  check(cvq_encode_keys_search(context(), &ck, xy.data(), keys.data.data(), keys.rows,
+                               search == AssignSearch::factorized ? 1 : 0, codes.a.data(),
+                               codes.b.data()));
   return codes;
 }
 
@@ -277,15 +281,54 @@ inline ValueCodes unpack_value_codes(const std::vector<uint64_t>& words, size_t 
   return codes;
 }
 
-// QuantizedKVCache (cache.hpp:63-113), single stream like the reference,
-// with the packed words resident in HBM.  save/load write and read the CVQC
-// format of cache.cpp:310-373, so caches move freely between the two.
+// CacheStats / compute_cache_stats (cache.hpp:43-58, cache.cpp:157-186):
+// closed-form bookkeeping, restated so the gpu namespace is complete.
+inline CacheStats compute_cache_stats(const KeyQuantConfig& key_config, size_t n_codes,
+                                      size_t tokens) {
+  key_config.validate();
+  if (n_codes == 0) throw std::invalid_argument("cache stats: n_codes must be positive");
+  CacheStats s;
+  if (tokens == 0) return s;
+  const size_t d = key_config.d;
+  const uint64_t key_bits = static_cast<uint64_t>(tokens) * key_config.bits_per_token();
+  const uint64_t value_bits = static_cast<uint64_t>(tokens) * n_codes;
+  s.tokens = tokens;
+  s.fp16_equivalent_bytes = static_cast<uint64_t>(tokens) * d * 2 * 2;
+  s.quantized_payload_bits = key_bits + value_bits;
+  s.quantized_payload_bytes = static_cast<double>(s.quantized_payload_bits) / 8.0;
+  s.codebook_bytes = key_codebook_bytes(key_config) + value_codebook_bytes(n_codes, d);
+  const double scalars = static_cast<double>(tokens) * d * 2;
+  s.avg_bit_effective = static_cast<double>(s.quantized_payload_bits) / scalars;
+  s.avg_bit_amortized = (static_cast<double>(s.quantized_payload_bits) +
+                         8.0 * static_cast<double>(s.codebook_bytes)) / scalars;
+  s.avg_bit_key_side = static_cast<double>(key_bits) / (static_cast<double>(tokens) * d);
+  s.avg_bit_value_side = static_cast<double>(value_bits) / (static_cast<double>(tokens) * d);
+  return s;
+}
+
+// Device options of the GPU cache (not in the reference API: defaulted, so
+// reference call sites compile unchanged).
+struct CacheOptions {
+  size_t reserve = 1024;       // initial device reservation in tokens; grows on demand
+  bool tensor_cores = false;   // CVQ_CACHE_KEYS_TC: tcgen05 score kernel, fp16 codebook
+                               // operand (guarded, cvq_cache_key_mode), fp32 accumulate
+};
+
+// QuantizedKVCache (cache.hpp:62-113): same constructors, by-value
+// prefill / load, accessors and save format as the reference; the packed
+// words live in HBM (one stream) and the pools grow like the reference's
+// vectors.  Accessors that return references (key_codes, value_codes,
+// packed_keys, packed_values) materialise host mirrors from the device words
+// on first use after a change, so the decode loop itself never copies back.
+// Copyable (deep copy on the device) and movable.
 class QuantizedKVCache {
  public:
   QuantizedKVCache(std::shared_ptr<const KeyCodebook> key_codebook,
                    std::shared_ptr<const ValueCodebook> value_codebook,
-                   std::shared_ptr<const ValueEncoder> encoder, size_t capacity = 1 << 16)
-      : kcb_(std::move(key_codebook)), vcb_(std::move(value_codebook)), enc_(std::move(encoder)) {
+                   std::shared_ptr<const ValueEncoder> encoder, CacheOptions opt = {})
+      : kcb_(std::move(key_codebook)), vcb_(std::move(value_codebook)), enc_(std::move(encoder)),
+        opt_(opt) {
+    // cache.cpp:189-212 (rope_for throws first on a null key codebook)
     if (!kcb_) throw std::invalid_argument("cache: key codebook is null");
     if (!vcb_) throw std::invalid_argument("cache: value codebook is null");
     if (!enc_) throw std::invalid_argument("cache: encoder is null");
@@ -293,37 +336,48 @@ class QuantizedKVCache {
     if (vcb_->d != kcb_->config.d) throw std::invalid_argument("cache: key/value dimension mismatch");
     if (enc_->d != kcb_->config.d || enc_->n_codes != vcb_->n_codes)
       throw std::invalid_argument("cache: encoder does not match value codebook");
-    cvq_cache_desc d{};
-    d.key = key_config(kcb_->config);
-    d.n_codes = static_cast<uint32_t>(vcb_->n_codes);
-    d.hidden = static_cast<uint32_t>(enc_->hidden);
-    d.n_seqs = d.n_layers = d.n_kv_heads = d.q_per_kv = 1;
-    d.capacity = capacity;
-    d.rope_base = 10000.0;  // cache.cpp:47-50 uses the default base
-    check(cvq_cache_create(context(), &d, &c_));
-    const std::vector<double> xy = atoms_xy(*kcb_);
-    check(cvq_cache_set_key_codebook(c_, 0, 0, xy.data()));
-    check(cvq_cache_set_value_quantizer(c_, 0, 0, enc_->w1.data.data(), enc_->b1.data(),
-                                        enc_->w2.data.data(), enc_->b2.data(),
-                                        vcb_->rows.data.data()));
+    create();
   }
-  ~QuantizedKVCache() { cvq_cache_destroy(c_); }
-  QuantizedKVCache(const QuantizedKVCache&) = delete;
-  QuantizedKVCache& operator=(const QuantizedKVCache&) = delete;
+  ~QuantizedKVCache() {
+    if (c_) cvq_cache_destroy(c_);
+  }
+  QuantizedKVCache(const QuantizedKVCache& o)
+      : kcb_(o.kcb_), vcb_(o.vcb_), enc_(o.enc_), opt_(o.opt_) {
+    create();
+    const size_t n = o.size();
+    if (n) {
+      auto [kw, vw] = o.export_words();
+      check(cvq_cache_import_stream(c_, 0, 0, 0, kw.data(), vw.data(), n, CVQ_HOST));
+    }
+  }
+  QuantizedKVCache& operator=(const QuantizedKVCache& o) {
+    if (this != &o) {
+      QuantizedKVCache tmp(o);
+      swap(tmp);
+    }
+    return *this;
+  }
+  QuantizedKVCache(QuantizedKVCache&& o) noexcept { swap(o); }
+  QuantizedKVCache& operator=(QuantizedKVCache&& o) noexcept {
+    swap(o);
+    return *this;
+  }
 
-  static std::unique_ptr<QuantizedKVCache> prefill(
-      const Mat& keys, const Mat& values, std::shared_ptr<const KeyCodebook> kcb,
-      std::shared_ptr<const ValueCodebook> vcb, std::shared_ptr<const ValueEncoder> enc,
-      size_t capacity = 0) {
+  // cache.cpp:213-254.
+  static QuantizedKVCache prefill(const Mat& keys, const Mat& values,
+                                  std::shared_ptr<const KeyCodebook> key_codebook,
+                                  std::shared_ptr<const ValueCodebook> value_codebook,
+                                  std::shared_ptr<const ValueEncoder> encoder,
+                                  CacheOptions opt = {}) {
+    if (keys.rows > opt.reserve) opt.reserve = keys.rows;
+    QuantizedKVCache c(std::move(key_codebook), std::move(value_codebook), std::move(encoder), opt);
     if (keys.rows != values.rows)
       throw std::invalid_argument("prefill: key/value token count mismatch");
-    auto c = std::make_unique<QuantizedKVCache>(kcb, vcb, enc,
-                                                capacity ? capacity : keys.rows + 4096);
-    const size_t d = c->kcb_->config.d;
+    const size_t d = c.kcb_->config.d;
     if (keys.rows > 0 && (keys.cols != d || values.cols != d))
       throw std::invalid_argument("prefill: wrong dimension");
     if (keys.rows)
-      check(cvq_cache_prefill(c->c_, keys.data.data(), values.data.data(), keys.rows, CVQ_F64,
+      check(cvq_cache_prefill(c.c_, keys.data.data(), values.data.data(), keys.rows, CVQ_F64,
                               CVQ_HOST));
     return c;
   }
@@ -334,40 +388,86 @@ class QuantizedKVCache {
     return n;
   }
 
+  // cache.cpp:256-285 (an encoder failure throws TrainingError at the next
+  // synchronising call -- size(), decode_step, accessors -- with the cache
+  // rolled back to the failed append).
   void append(const Vec& key, const Vec& value) {
     const size_t d = kcb_->config.d;
     if (key.size() != d || value.size() != d) throw std::invalid_argument("append: wrong dimension");
     check(cvq_cache_append(c_, key.data(), value.data(), CVQ_F64, CVQ_HOST));
+    ++version_;
   }
 
+  // cache.cpp:287-296.
   Vec decode_step(const Vec& key, const Vec& value, const Vec& q, FlopReport* flops = nullptr) {
     const size_t d = kcb_->config.d;
     if (q.size() != d) throw std::invalid_argument("attention: dimension mismatch");
     append(key, value);
+    const size_t n = size();  // surfaces an append error before attending
     std::vector<float> qf(q.begin(), q.end()), of(d);
-    check(cvq_cache_attention(c_, qf.data(), size() - 1, of.data(), CVQ_HOST));
-    if (flops) {
+    check(cvq_cache_attention(c_, qf.data(), n - 1, of.data(), CVQ_HOST));
+    if (flops) {  // FlopReport of the fused pathway (attn.cpp:176-178, 258-261)
       const KeyQuantConfig& kc = kcb_->config;
       flops->pathway = "fused";
-      flops->tokens = size();
+      flops->tokens = n;
       flops->d = d;
       flops->n_codes = vcb_->n_codes;
       flops->rounds = kc.rounds;
       flops->n_levels = kc.n_levels;
-      flops->predicted_mults = predicted_flops_fused(size(), d, vcb_->n_codes, kc.rounds, kc.n_levels);
+      flops->predicted_mults = predicted_flops_fused(n, d, vcb_->n_codes, kc.rounds, kc.n_levels);
       flops->measured_mults = 2 * d + 2 * d * kc.rounds * kc.n_levels +
-                              size() * (kc.rounds * d + 1) + vcb_->n_codes * d;
+                              n * (kc.rounds * d + 1) + vcb_->n_codes * d;
     }
     return Vec(of.begin(), of.end());
   }
 
+  // cache.hpp:84-89.
+  const KeyCodes& key_codes() const {
+    refresh();
+    return key_codes_;
+  }
+  const ValueCodes& value_codes() const {
+    refresh();
+    return value_codes_;
+  }
+  const BitBuffer& packed_keys() const {
+    refresh();
+    return key_bits_;
+  }
+  const BitBuffer& packed_values() const {
+    refresh();
+    return value_bits_;
+  }
+  const KeyCodebook& key_codebook() const { return *kcb_; }
+  const ValueCodebook& value_codebook() const { return *vcb_; }
+
+  // cache.cpp:298-308.
+  CacheStats stats() const {
+    const size_t n = size();
+    CacheStats s = gpu::compute_cache_stats(kcb_->config, vcb_->n_codes, n);
+    if (n > 0) {
+      const uint64_t actual = packed_keys().bit_size() + packed_values().bit_size();
+      if (actual != s.quantized_payload_bits)
+        throw std::logic_error("cache stats: payload size drifted from formula");
+    }
+    return s;
+  }
+
+  // GPU extras: the device words, the C handle, the effective key mode.
   std::vector<uint64_t> packed_key_words() const { return export_words().first; }
   std::vector<uint64_t> packed_value_words() const { return export_words().second; }
+  cvq_cache* handle() const { return c_; }
+  bool uses_tensor_cores() const {
+    uint32_t f = 0;
+    check(cvq_cache_key_mode(c_, &f));
+    return (f & CVQ_CACHE_KEYS_TC) != 0;
+  }
 
   // CVQC v1 (cache.cpp:310-327): magic, version, d, g, L, R, N_c, tokens,
   // key words, value words, all little-endian.
   void save(const std::string& path) const {
     auto [kw, vw] = export_words();
+    const size_t n = size();
     std::ofstream os(path, std::ios::binary | std::ios::trunc);
     if (!os) throw IoError("cannot open for write: " + path);
     const KeyQuantConfig& c = kcb_->config;
@@ -378,7 +478,7 @@ class QuantizedKVCache {
     put32(os, static_cast<uint32_t>(c.n_levels));
     put32(os, static_cast<uint32_t>(c.rounds));
     put32(os, static_cast<uint32_t>(vcb_->n_codes));
-    put64(os, size());
+    put64(os, n);
     put64(os, kw.size());
     for (uint64_t w : kw) put64(os, w);
     put64(os, vw.size());
@@ -387,20 +487,18 @@ class QuantizedKVCache {
   }
 
   // cache.cpp:329-373.
-  static std::unique_ptr<QuantizedKVCache> load(const std::string& path,
-                                                std::shared_ptr<const KeyCodebook> kcb,
-                                                std::shared_ptr<const ValueCodebook> vcb,
-                                                std::shared_ptr<const ValueEncoder> enc,
-                                                size_t extra_capacity = 4096) {
+  static QuantizedKVCache load(const std::string& path, std::shared_ptr<const KeyCodebook> kcb,
+                               std::shared_ptr<const ValueCodebook> vcb,
+                               std::shared_ptr<const ValueEncoder> enc, CacheOptions opt = {}) {
     std::ifstream is(path, std::ios::binary);
     if (!is) throw IoError("cannot open: " + path);
     if (get32(is) != 0x43515643u) throw IoError("not a cache file: " + path);
     if (get32(is) != 1) throw IoError("unsupported cache version: " + path);
+    QuantizedKVCache c(std::move(kcb), std::move(vcb), std::move(enc), opt);
+    const KeyQuantConfig& cfg = c.kcb_->config;
     const uint32_t d = get32(is), g = get32(is), L = get32(is), r = get32(is), nc = get32(is);
-    if (!kcb || !vcb) throw std::invalid_argument("cache: codebook is null");
-    const KeyQuantConfig& cfg = kcb->config;
     if (d != cfg.d || g != cfg.group_size || L != cfg.n_levels || r != cfg.rounds ||
-        nc != vcb->n_codes)
+        nc != c.vcb_->n_codes)
       throw IoError("cache config does not match provided codebooks: " + path);
     const uint64_t tokens = get64(is);
     const uint64_t nkw = get64(is);
@@ -420,12 +518,54 @@ class QuantizedKVCache {
     } catch (const std::invalid_argument& e) {
       throw IoError(std::string("corrupt cache payload: ") + e.what());
     }
-    auto c = std::make_unique<QuantizedKVCache>(kcb, vcb, enc, tokens + extra_capacity);
-    check(cvq_cache_import_stream(c->c_, 0, 0, 0, kw.data(), vw.data(), tokens, CVQ_HOST));
+    if (tokens) check(cvq_cache_import_stream(c.c_, 0, 0, 0, kw.data(), vw.data(), tokens, CVQ_HOST));
     return c;
   }
 
  private:
+  void create() {
+    cvq_cache_desc d{};
+    d.key = key_config(kcb_->config);
+    d.n_codes = static_cast<uint32_t>(vcb_->n_codes);
+    d.hidden = static_cast<uint32_t>(enc_->hidden);
+    d.n_seqs = d.n_layers = d.n_kv_heads = d.q_per_kv = 1;
+    d.capacity = opt_.reserve ? opt_.reserve : 1;
+    d.rope_base = 10000.0;  // RopeParams::make default base (cache.cpp:47-50)
+    d.flags = opt_.tensor_cores ? CVQ_CACHE_KEYS_TC : 0u;
+    check(cvq_cache_create(context(), &d, &c_));
+    const std::vector<double> xy = atoms_xy(*kcb_);
+    check(cvq_cache_set_key_codebook(c_, 0, 0, xy.data()));
+    check(cvq_cache_set_value_quantizer(c_, 0, 0, enc_->w1.data.data(), enc_->b1.data(),
+                                        enc_->w2.data.data(), enc_->b2.data(),
+                                        vcb_->rows.data.data()));
+  }
+  void swap(QuantizedKVCache& o) noexcept {
+    std::swap(kcb_, o.kcb_);
+    std::swap(vcb_, o.vcb_);
+    std::swap(enc_, o.enc_);
+    std::swap(opt_, o.opt_);
+    std::swap(c_, o.c_);
+    std::swap(version_, o.version_);
+    std::swap(mirror_version_, o.mirror_version_);
+    std::swap(n_mirrored_, o.n_mirrored_);
+    std::swap(key_codes_, o.key_codes_);
+    std::swap(value_codes_, o.value_codes_);
+    std::swap(key_bits_, o.key_bits_);
+    std::swap(value_bits_, o.value_bits_);
+  }
+  // host mirrors (cache.hpp:107-112) rebuilt from the device words when stale
+  void refresh() const {
+    const size_t n = size();
+    if (mirror_version_ == version_ && key_codes_.tokens == n && n_mirrored_ == n) return;
+    auto [kw, vw] = export_words();
+    const KeyQuantConfig& cfg = kcb_->config;
+    key_codes_ = gpu::unpack_key_codes(kw, n, cfg);
+    value_codes_ = gpu::unpack_value_codes(vw, n, vcb_->n_codes);
+    key_bits_ = BitBuffer::from_words(std::move(kw), n * cfg.bits_per_token());
+    value_bits_ = BitBuffer::from_words(std::move(vw), n * vcb_->n_codes);
+    mirror_version_ = version_;
+    n_mirrored_ = n;
+  }
   std::pair<std::vector<uint64_t>, std::vector<uint64_t>> export_words() const {
     const size_t n = size();
     std::vector<uint64_t> kw((n * kcb_->config.bits_per_token() + 63) / 64);
@@ -456,7 +596,15 @@ class QuantizedKVCache {
   std::shared_ptr<const KeyCodebook> kcb_;
   std::shared_ptr<const ValueCodebook> vcb_;
   std::shared_ptr<const ValueEncoder> enc_;
+  CacheOptions opt_;
   cvq_cache* c_ = nullptr;
+  uint64_t version_ = 0;
+  mutable uint64_t mirror_version_ = ~0ull;
+  mutable size_t n_mirrored_ = ~size_t(0);
+  mutable KeyCodes key_codes_;
+  mutable ValueCodes value_codes_;
+  mutable BitBuffer key_bits_;
+  mutable BitBuffer value_bits_;
 };
 
 }  // namespace gpu

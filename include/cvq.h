@@ -140,6 +140,16 @@ CVQ_API cvq_status cvq_encode_keys(cvq_context* ctx, const cvq_key_config* kc,
                                    const double* keys, uint64_t n_tokens,
                                    uint16_t* a, uint16_t* b);
 
+/* encode_keys with the AssignSearch argument (keyquant.hpp:135-136):
+ * search 0 = brute_force (as cvq_encode_keys), 1 = factorized -- the
+ * reference's assign_factorized ranking base - 2 pu - 2 pv (keyquant.cpp:
+ * 204-224) in its fp64 operation order, so codes equal the reference's for
+ * that search, near-ties included (the two searches may differ there). */
+CVQ_API cvq_status cvq_encode_keys_search(cvq_context* ctx, const cvq_key_config* kc,
+                                          const double* key_atoms_xy, const double* keys,
+                                          uint64_t n_tokens, int32_t search, uint16_t* a,
+                                          uint16_t* b);
+
 /* EmConfig (keyquant.hpp:71-80).  search: 0 = brute_force (default),
  * 1 = factorized. */
 typedef struct cvq_em_config {

@@ -280,8 +280,12 @@ def naive_attention(kq, atoms, a, b, bits, vrows, q, t, base=10000.0, ctx=None):
     return _attn("naive", kq, atoms, a, b, bits, vrows, q, t, base, ctx)
 
 
-def encode_keys(kq, atoms, keys, ctx=None):
-    """keyquant.cpp:705-739 (brute-force semantics) -> (a, b) uint16."""
+def encode_keys(kq, atoms, keys, ctx=None, search="brute_force"):
+    """keyquant.cpp:705-739 with the reference's AssignSearch ("brute_force"
+    or "factorized", each bit-exact to the reference's own search) -> (a, b)
+    uint16 in KeyCodes::idx order."""
+    if search not in ("brute_force", "factorized"):
+        raise ValueError("encode_keys: unknown search")
     kq = _kc(kq)
     ctx = ctx or default_context()
     atoms = _a(atoms, np.float64)
@@ -293,8 +297,9 @@ def encode_keys(kq, atoms, keys, ctx=None):
     a = np.zeros(max(m, 1), np.uint16)
     b = np.zeros(max(m, 1), np.uint16)
     kc = kq._c()
-    _check(_lib.cvq_encode_keys(ctx.h, C.byref(kc), _ptr(atoms), _ptr(keys), _u64(n), _ptr(a),
-                                _ptr(b)))
+    _check(_lib.cvq_encode_keys_search(ctx.h, C.byref(kc), _ptr(atoms), _ptr(keys), _u64(n),
+                                       C.c_int32(1 if search == "factorized" else 0), _ptr(a),
+                                       _ptr(b)))
     return a[:m], b[:m]
 
 

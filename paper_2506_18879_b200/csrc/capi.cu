@@ -161,7 +161,10 @@ std::vector<float> atoms_to_decode_layout(const Geom& g, const double* xy) {
 }  // namespace
 
 // ------------------------------------------------------------- structs
+struct cvq_mirror;
+void destroy_mirror(cvq_mirror* m);  // after its definition (mirrors section)
 struct cvq_context {
+  cvq_mirror* mirror = nullptr;  // single-stream mirrors' device cache (capi.cu)
   int device = 0;
   cudaStream_t stream = nullptr;
   bool own_stream = false;
@@ -427,6 +430,7 @@ CVQ_API cvq_status cvq_context_destroy(cvq_context* ctx) {
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
   for (cudaEvent_t e : ctx->prof_ev) cudaEventDestroy(e);
+  destroy_mirror(ctx->mirror);
   ctx->scratch.release();
   if (ctx->d_err) cudaFree(ctx->d_err);
   if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
@@ -921,40 +925,125 @@ CVQ_API cvq_status cvq_cache_key_mode(const cvq_cache* c, uint32_t* flags) {
 // ===================================================== single-stream mirrors
 namespace {
 
-// A one-stream cache holding the caller's unpacked codes, packed on device.
-struct OneStream {
+// The single-stream mirrors keep one device cache per context, reused across
+// calls by identity (SURVEY 8b "Ownership": upload once, cache by identity):
+// the key / value codebooks are re-uploaded only when their pointer or
+// content hash changes, and the codes are treated as the reference's
+// append-only vectors -- same buffers and n >= the cached n with the sampled
+// earlier codes unchanged -> only the new tail tokens are uploaded and packed
+// (a decode loop calling fused_attention per step re-sends one token, not N).
+uint64_t fnv(const void* p, size_t bytes, uint64_t h = 1469598103934665603ull) {
+  const unsigned char* c = static_cast<const unsigned char*>(p);
+  for (size_t i = 0; i < bytes; ++i) h = (h ^ c[i]) * 1099511628211ull;
+  return h;
+}
+// hash of up to 64 sampled tokens of [0, n) plus the last one
+uint64_t sample_hash(const uint16_t* a, const uint16_t* b, const uint8_t* bits, uint64_t n,
+                     size_t per_tok, uint32_t n_codes) {
+  uint64_t h = fnv(&n, sizeof(n));
+  if (n == 0) return h;
+  const uint64_t step = n > 64 ? n / 64 : 1;
+  for (uint64_t t = 0; t < n; t += step) {
+    h = fnv(a + t * per_tok, per_tok * 2, h);
+    h = fnv(b + t * per_tok, per_tok * 2, h);
+    h = fnv(bits + t * n_codes, n_codes, h);
+  }
+  h = fnv(a + (n - 1) * per_tok, per_tok * 2, h);
+  h = fnv(b + (n - 1) * per_tok, per_tok * 2, h);
+  return fnv(bits + (n - 1) * n_codes, n_codes, h);
+}
+
+}  // namespace
+
+struct cvq_mirror {
   cvq_cache* c = nullptr;
-  ~OneStream() { cvq_cache_destroy(c); }
+  cvq_key_config kc{};
+  uint32_t n_codes = 0;
+  double base = 0.0;
+  const double* atoms = nullptr;
+  uint64_t atoms_hash = 0;
+  const double* vrows = nullptr;
+  uint64_t vrows_hash = 0;
+  const uint16_t* a = nullptr;
+  const uint16_t* b = nullptr;
+  const uint8_t* bits = nullptr;
+  uint64_t n = 0, codes_hash = 0;
+  ~cvq_mirror() {
+    if (c) cvq_cache_destroy(c);
+  }
 };
 
-cvq_status make_one_stream(cvq_context* ctx, const cvq_key_config* kc, uint32_t n_codes,
-                           const double* atoms, const uint16_t* a, const uint16_t* b, uint64_t n,
-                           const uint8_t* bits, const double* vrows, double base, OneStream& os) {
-  cvq_cache_desc d{};
-  d.key = *kc;
-  d.n_codes = n_codes;
-  d.hidden = 0;
-  d.n_seqs = d.n_layers = d.n_kv_heads = d.q_per_kv = 1;
-  d.capacity = n;
-  d.position_offset = 0;
-  d.rope_base = base;
-  TRY(cvq_cache_create(ctx, &d, &os.c));
-  TRY(cvq_cache_set_key_codebook(os.c, 0, 0, atoms));
-  TRY(cvq_cache_set_value_quantizer(os.c, 0, 0, nullptr, nullptr, nullptr, nullptr, vrows));
-  cvq_cache* c = os.c;
-  const Geom& g = c->geo;
-  const size_t np = (size_t)n * g.R * g.groups;
-  CU(c->enc_scratch.ensure(np * 4 + (size_t)n * n_codes + 64));
-  uint16_t* da = static_cast<uint16_t*>(c->enc_scratch.p);
-  uint16_t* db = da + np;
-  uint8_t* dbits = reinterpret_cast<uint8_t*>(db + np);
-  cudaStream_t st = ctx->stream;
-  CU(cudaMemcpyAsync(da, a, np * 2, cudaMemcpyHostToDevice, st));
-  CU(cudaMemcpyAsync(db, b, np * 2, cudaMemcpyHostToDevice, st));
-  CU(cudaMemcpyAsync(dbits, bits, (size_t)n * n_codes, cudaMemcpyHostToDevice, st));
-  CU(run_pack_keys(g, 1, da, db, (long long)n, 0, c->kpool, c->kstride, st));
-  CU(run_pack_values(g, 1, dbits, (long long)n, 0, c->vpool, c->vstride, st));
+void destroy_mirror(cvq_mirror* m) { delete m; }
+
+namespace {
+
+cvq_status mirror_cache(cvq_context* ctx, const cvq_key_config* kc, uint32_t n_codes,
+                        const double* atoms, const uint16_t* a, const uint16_t* b, uint64_t n,
+                        const uint8_t* bits, const double* vrows, double base, cvq_cache** out) {
+  if (!ctx->mirror) ctx->mirror = new cvq_mirror;
+  cvq_mirror& m = *ctx->mirror;
+  const Geom g = make_geom(kc, n_codes, 0, 1);
+  const size_t na = (size_t)g.R * g.subs * g.L;
+  const bool same_geom = m.c && m.kc.d == kc->d && m.kc.group_size == kc->group_size &&
+                         m.kc.n_levels == kc->n_levels && m.kc.rounds == kc->rounds &&
+                         m.n_codes == n_codes && m.base == base;
+  if (!same_geom) {
+    if (m.c) cvq_cache_destroy(m.c);
+    m = cvq_mirror{};
+    cvq_cache_desc d{};
+    d.key = *kc;
+    d.n_codes = n_codes;
+    d.hidden = 0;
+    d.n_seqs = d.n_layers = d.n_kv_heads = d.q_per_kv = 1;
+    d.capacity = n;
+    d.position_offset = 0;
+    d.rope_base = base;
+    TRY(cvq_cache_create(ctx, &d, &m.c));
+    m.kc = *kc;
+    m.n_codes = n_codes;
+    m.base = base;
+  }
+  cvq_cache* c = m.c;
+  const uint64_t ah = fnv(atoms, na * 2 * sizeof(double));
+  if (m.atoms != atoms || m.atoms_hash != ah) {
+    TRY(cvq_cache_set_key_codebook(c, 0, 0, atoms));
+    m.atoms = atoms;
+    m.atoms_hash = ah;
+  }
+  const uint64_t vh = fnv(vrows, (size_t)n_codes * g.d * sizeof(double));
+  if (m.vrows != vrows || m.vrows_hash != vh) {
+    TRY(cvq_cache_set_value_quantizer(c, 0, 0, nullptr, nullptr, nullptr, nullptr, vrows));
+    m.vrows = vrows;
+    m.vrows_hash = vh;
+  }
+  const size_t per_tok = (size_t)g.R * g.groups;
+  uint64_t from = 0;  // first token to (re)upload
+  if (m.a == a && m.b == b && m.bits == bits && n >= m.n &&
+      sample_hash(a, b, bits, m.n, per_tok, n_codes) == m.codes_hash)
+    from = m.n;
+  TRY(ensure_capacity(c, n));
+  const uint64_t nn = n - from;
+  if (nn > 0) {
+    const size_t np = (size_t)nn * per_tok;
+    CU(c->enc_scratch.ensure(np * 4 + (size_t)nn * n_codes + 64));
+    uint16_t* da = static_cast<uint16_t*>(c->enc_scratch.p);
+    uint16_t* db = da + np;
+    uint8_t* dbits = reinterpret_cast<uint8_t*>(db + np);
+    cudaStream_t st = ctx->stream;
+    CU(cudaMemcpyAsync(da, a + from * per_tok, np * 2, cudaMemcpyHostToDevice, st));
+    CU(cudaMemcpyAsync(db, b + from * per_tok, np * 2, cudaMemcpyHostToDevice, st));
+    CU(cudaMemcpyAsync(dbits, bits + from * n_codes, (size_t)nn * n_codes, cudaMemcpyHostToDevice,
+                       st));
+    CU(run_pack_keys(g, 1, da, db, (long long)nn, (long long)from, c->kpool, c->kstride, st));
+    CU(run_pack_values(g, 1, dbits, (long long)nn, (long long)from, c->vpool, c->vstride, st));
+  }
   c->length = n;
+  m.a = a;
+  m.b = b;
+  m.bits = bits;
+  m.n = n;
+  m.codes_hash = sample_hash(a, b, bits, n, per_tok, n_codes);
+  *out = c;
   return CVQ_OK;
 }
 
@@ -999,9 +1088,8 @@ CVQ_API cvq_status cvq_fused_attention(cvq_context* ctx, const cvq_key_config* k
   if (!kc || !atoms || !q || !out || !vrows || (n && (!a || !b || !bits)))
     return fail(CVQ_EINVAL, "null argument");
   TRY(validate_attn(kc, n_codes, a, b, n, t));
-  OneStream os;
-  TRY(make_one_stream(ctx, kc, n_codes, atoms, a, b, n, bits, vrows, base, os));
-  cvq_cache* c = os.c;
+  cvq_cache* c = nullptr;
+  TRY(mirror_cache(ctx, kc, n_codes, atoms, a, b, n, bits, vrows, base, &c));
   const Geom& g = c->geo;
   AttnJob job = make_job(c);
   job.t = (long long)t;
@@ -1037,9 +1125,8 @@ CVQ_API cvq_status cvq_naive_attention(cvq_context* ctx, const cvq_key_config* k
   if (!kc || !atoms || !q || !out || !vrows || (n && (!a || !b || !bits)))
     return fail(CVQ_EINVAL, "null argument");
   TRY(validate_attn(kc, n_codes, a, b, n, t));
-  OneStream os;
-  TRY(make_one_stream(ctx, kc, n_codes, atoms, a, b, n, bits, vrows, base, os));
-  cvq_cache* c = os.c;
+  cvq_cache* c = nullptr;
+  TRY(mirror_cache(ctx, kc, n_codes, atoms, a, b, n, bits, vrows, base, &c));
   const Geom& g = c->geo;
   AttnJob job = make_job(c);
   job.t = (long long)t;
@@ -1084,6 +1171,33 @@ CVQ_API cvq_status cvq_encode_keys(cvq_context* ctx, const cvq_key_config* kc, c
   if (tables) CU(build_key_enc_tables(g, 1, d_atoms, d_base, d_max, st));
   KeyEncTables tab{d_atoms, tables ? d_base : nullptr, d_max};
   CU(run_encode_keys(g, 1, 1, tab, d_keys, CVQ_F64, 0, (long long)n, da, db, st));
+  CU(cudaMemcpyAsync(a, da, np * 2, cudaMemcpyDeviceToHost, st));
+  CU(cudaMemcpyAsync(b, db, np * 2, cudaMemcpyDeviceToHost, st));
+  CU(cudaStreamSynchronize(st));
+  return CVQ_OK;
+}
+
+CVQ_API cvq_status cvq_encode_keys_search(cvq_context* ctx, const cvq_key_config* kc,
+                                          const double* atoms, const double* keys, uint64_t n,
+                                          int32_t search, uint16_t* a, uint16_t* b) {
+  if (search == 0) return cvq_encode_keys(ctx, kc, atoms, keys, n, a, b);
+  TRY(ctx_check(ctx));
+  TRY(validate_kc(kc));
+  if (search != 1) return fail(CVQ_EINVAL, "encode_keys: unknown AssignSearch");
+  if (!atoms || (n && (!keys || !a || !b))) return fail(CVQ_EINVAL, "null argument");
+  if (n == 0) return CVQ_OK;
+  Geom g = make_geom(kc, 1, 0, 1);
+  const size_t na = (size_t)g.R * g.subs * g.L;
+  const size_t np = (size_t)n * g.R * g.groups;
+  CU(ctx->scratch.ensure((na * 2 + (size_t)n * g.d) * 8 + np * 4 + 256));
+  double* d_atoms = static_cast<double*>(ctx->scratch.p);
+  double* d_keys = d_atoms + na * 2;
+  uint16_t* da = reinterpret_cast<uint16_t*>(d_keys + (size_t)n * g.d);
+  uint16_t* db = da + np;
+  cudaStream_t st = ctx->stream;
+  CU(cudaMemcpyAsync(d_atoms, atoms, na * 16, cudaMemcpyHostToDevice, st));
+  CU(cudaMemcpyAsync(d_keys, keys, (size_t)n * g.d * 8, cudaMemcpyHostToDevice, st));
+  CU(encode_keys_factorized_gpu(g, d_atoms, d_keys, (long long)n, da, db, st));
   CU(cudaMemcpyAsync(a, da, np * 2, cudaMemcpyDeviceToHost, st));
   CU(cudaMemcpyAsync(b, db, np * 2, cudaMemcpyDeviceToHost, st));
   CU(cudaStreamSynchronize(st));

@@ -160,6 +160,8 @@ struct TrainConfig {  // EmConfig, keyquant.hpp:71-80
 // atoms_out [R][d/2][L][2]; traces: hard objective per (round, group);
 // mse: reconstruction MSE per round.  Returns 0, or 1 (invalid argument),
 // 2 (training error), 3 (CUDA error) with *err set.
+cudaError_t encode_keys_factorized_gpu(const Geom& g, const double* atoms, const double* keys,
+                                       long long n, uint16_t* a, uint16_t* b, cudaStream_t st);
 int train_key_codebook_gpu(const Geom& g, const double* calib, long long n, const TrainConfig& em,
                            double* atoms_out, std::vector<std::vector<double>>* traces,
                            std::vector<double>* mse, std::string* err, cudaStream_t st);

@@ -425,7 +425,7 @@ __global__ void k_em_assign_factorized(const double* __restrict__ pu, const doub
                                        const double* __restrict__ pnorm,
                                        const double* __restrict__ base, int L, long long n,
                                        uint16_t* __restrict__ a_out, uint16_t* __restrict__ b_out,
-                                       double* __restrict__ d2) {
+                                       double* __restrict__ d2, int ostride = 1) {
   const long long p = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (p >= n) return;
@@ -450,22 +450,22 @@ __global__ void k_em_assign_factorized(const double* __restrict__ pu, const doub
   }
   if (lane == 0) {
     if (bc == 0x7fffffff) bc = 0;
-    a_out[p] = (uint16_t)(bc / L);
-    b_out[p] = (uint16_t)(bc % L);
-    d2[p] = best + pnorm[p];
+    a_out[p * ostride] = (uint16_t)(bc / L);
+    b_out[p * ostride] = (uint16_t)(bc % L);
+    if (d2) d2[p] = best + pnorm[p];
   }
 }
 
 // Residual update after a group (keyquant.cpp:686-694).
 __global__ void k_em_residual(double* __restrict__ R, int d, int col0, int g, int L, long long n,
                               const double* __restrict__ atoms, const uint16_t* __restrict__ a,
-                              const uint16_t* __restrict__ b) {
+                              const uint16_t* __restrict__ b, int cstride = 1) {
   const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= n * g) return;
   const long long p = e / g;
   const int s = (int)(e % g);
-  const double* ua = atoms + ((size_t)s * L + a[p]) * 2;
-  const double* ub = atoms + ((size_t)s * L + b[p]) * 2;
+  const double* ua = atoms + ((size_t)s * L + a[p * cstride]) * 2;
+  const double* ub = atoms + ((size_t)s * L + b[p * cstride]) * 2;
   double* row = R + p * d + col0;
   row[2 * s] = __dsub_rn(row[2 * s], __dsub_rn(ua[0], ub[1]));
   row[2 * s + 1] = __dsub_rn(row[2 * s + 1], __dadd_rn(ua[1], ub[0]));
@@ -829,6 +829,53 @@ int train_key_codebook_gpu(const Geom& g, const double* calib, long long n, cons
   } catch (const TrainFail& f) {
     *err = f.msg;
     return f.code;
+  }
+}
+
+// encode_keys with AssignSearch::factorized (keyquant.cpp:705-739 with
+// assign_factorized 204-224): per (round, group) the CenterCache tables, the
+// sequential projections and |p|^2, the base - 2 pu - 2 pv argmin (strict
+// '<' in a*L+b order), then the exact residual update -- the same kernels
+// (and therefore the same fp64 operation order) as the factorized EM E-step.
+// keys: device fp64 [n][d]; a, b: device, KeyCodes::idx order.
+cudaError_t encode_keys_factorized_gpu(const Geom& g, const double* atoms, const double* keys,
+                                       long long n, uint16_t* a, uint16_t* b, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  try {
+  const int w = 2 * g.g, L = g.L;
+  DevBufs buf;
+  double* res = buf.get<double>((size_t)n * g.d);
+  double* uT = buf.get<double>((size_t)w * L);
+  double* vT = buf.get<double>((size_t)w * L);
+  double* un = buf.get<double>((size_t)L);
+  double* vn = buf.get<double>((size_t)L);
+  double* base = buf.get<double>((size_t)L * L);
+  double* pu = buf.get<double>((size_t)n * L);
+  double* pv = buf.get<double>((size_t)n * L);
+  double* pn = buf.get<double>((size_t)n);
+  cudaError_t e = cudaMemcpyAsync(res, keys, (size_t)n * g.d * 8, cudaMemcpyDeviceToDevice, st);
+  if (e != cudaSuccess) return e;
+  const int cs = g.R * g.groups;  // codes per token
+  for (int r = 0; r < g.R; ++r)
+    for (int grp = 0; grp < g.groups; ++grp) {
+      const double* slice = atoms + ((size_t)r * g.subs + (size_t)grp * g.g) * L * 2;
+      k_em_tables<<<nblk((long long)w * L, 256), 256, 0, st>>>(slice, g.g, L, uT, vT, un, vn, base, 0);
+      k_em_tables<<<nblk((long long)L * L, 256), 256, 0, st>>>(slice, g.g, L, uT, vT, un, vn, base, 1);
+      double* P = res + (size_t)grp * w;
+      k_em_pnorm<<<nblk(n, 256), 256, 0, st>>>(P, g.d, w, n, pn);
+      k_em_project<<<nblk(n, kProjPts), 128, (size_t)kProjPts * w * 8, st>>>(P, g.d, w, n, uT, vT,
+                                                                          L, pu, pv);
+      const int off = r * g.groups + grp;
+      k_em_assign_factorized<<<nblk(n, 8), 256, 0, st>>>(pu, pv, pn, base, L, n, a + off, b + off,
+                                                         nullptr, cs);
+      k_em_residual<<<nblk(n * g.g, 256), 256, 0, st>>>(res, g.d, grp * w, g.g, L, n, slice, a + off,
+                                                        b + off, cs);
+      count_launch(6);
+      if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    }
+  return cudaStreamSynchronize(st);  // DevBufs frees on return
+  } catch (const TrainFail&) {
+    return cudaErrorMemoryAllocation;
   }
 }
 

@@ -42,6 +42,100 @@ static KeyCodebook rand_kcb(const KeyQuantConfig& c, Rng& r, double s = 1.0) {
   return cb;
 }
 
+struct CacheFixture {  // test_cache.cpp:18-36
+  KeyQuantConfig cfg{8, 2, 4, 2};
+  std::shared_ptr<KeyCodebook> kcb;
+  std::shared_ptr<ValueCodebook> vcb;
+  std::shared_ptr<ValueEncoder> enc;
+  explicit CacheFixture(uint64_t seed = 51) {
+    kcb = std::make_shared<KeyCodebook>(KeyCodebook::zeros(cfg));
+    Rng rng(seed);
+    for (CommMat& m : kcb->atoms) m = comm_mat(rng.normal(), rng.normal());
+    vcb = std::make_shared<ValueCodebook>(ValueCodebook::zeros(8, 8));
+    for (double& v : vcb->rows.data) v = 0.5 * rng.normal();
+    enc = std::make_shared<ValueEncoder>(ValueEncoder::zeros(8, 16, 8));
+    for (double& v : enc->w1.data) v = 0.4 * rng.normal();
+    for (double& v : enc->b1) v = 0.1 * rng.normal();
+    for (double& v : enc->w2.data) v = 0.4 * rng.normal();
+    for (double& v : enc->b2) v = 0.1 * rng.normal();
+  }
+};
+
+static Mat rmat(size_t r, size_t c, uint64_t seed) {  // oracles.hpp random_mat
+  Mat m(r, c);
+  Rng rng(seed);
+  for (double& v : m.data) v = rng.normal();
+  return m;
+}
+
+struct CacheRun {
+  std::vector<uint64_t> kw_pre, vw_pre, kw_inc, kw_loaded, kw_long, vw_long;
+  std::vector<uint16_t> a, b, a_loaded;
+  std::vector<uint8_t> bits;
+  std::vector<Vec> outs;
+  Vec out_long;
+  CacheStats stats;
+  size_t n_loaded = 0, n_long = 0;
+  bool threw_dim = false, flop_tokens_ok = true, copy_ok = false;
+};
+
+// One body, any cache type with the reference's API (cache.hpp:62-113).
+template <class Cache>
+static CacheRun run_cache_body(const CacheFixture& fx, const std::string& tag) {
+  CacheRun r;
+  Mat keys = rmat(24, 8, 81), values = rmat(24, 8, 82);
+  Cache pre = Cache::prefill(keys, values, fx.kcb, fx.vcb, fx.enc);
+  Cache inc(fx.kcb, fx.vcb, fx.enc);
+  for (size_t t = 0; t < 24; ++t)
+    inc.append(Vec(keys.row(t).begin(), keys.row(t).end()),
+               Vec(values.row(t).begin(), values.row(t).end()));
+  r.kw_pre = pre.packed_keys().words();
+  r.vw_pre = pre.packed_values().words();
+  r.kw_inc = inc.packed_keys().words();
+  r.a = pre.key_codes().a;
+  r.b = pre.key_codes().b;
+  r.bits = pre.value_codes().bits;
+  try {
+    inc.append(Vec(7), Vec(8));
+  } catch (const std::invalid_argument&) {
+    r.threw_dim = true;
+  }
+  Mat qk = rmat(16, 8, 91), qv = rmat(16, 8, 92), qq = rmat(16, 8, 93);
+  Cache dec(fx.kcb, fx.vcb, fx.enc);
+  for (size_t t = 0; t < 16; ++t) {
+    FlopReport fl;
+    r.outs.push_back(dec.decode_step(Vec(qk.row(t).begin(), qk.row(t).end()),
+                                     Vec(qv.row(t).begin(), qv.row(t).end()),
+                                     Vec(qq.row(t).begin(), qq.row(t).end()), &fl));
+    r.flop_tokens_ok = r.flop_tokens_ok && fl.tokens == t + 1 && dec.size() == t + 1;
+  }
+  Mat sk = rmat(10, 8, 95), sv = rmat(10, 8, 96);
+  r.stats = Cache::prefill(sk, sv, fx.kcb, fx.vcb, fx.enc).stats();
+  const std::string path =
+      (std::filesystem::temp_directory_path() / ("parity_" + tag + ".cvqc")).string();
+  pre.save(path);
+  Cache back = Cache::load(path, fx.kcb, fx.vcb, fx.enc);
+  r.kw_loaded = back.packed_keys().words();
+  r.a_loaded = back.key_codes().a;
+  r.n_loaded = back.size();
+  std::filesystem::remove(path);
+  // copy is deep, move keeps the contents
+  Cache cp = pre;
+  cp.append(Vec(8, 0.25), Vec(8, -0.5));
+  Cache mv = std::move(cp);
+  r.copy_ok = pre.size() == 24 && mv.size() == 25 && mv.packed_keys().words().size() >= r.kw_pre.size();
+  // 70,000 appends (past any initial device reservation), then one decode step
+  Mat lk = rmat(70000, 8, 201), lv = rmat(70000, 8, 202);
+  Cache lng(fx.kcb, fx.vcb, fx.enc);
+  for (size_t t = 0; t < 70000; ++t)
+    lng.append(Vec(lk.row(t).begin(), lk.row(t).end()), Vec(lv.row(t).begin(), lv.row(t).end()));
+  r.n_long = lng.size();
+  r.kw_long = lng.packed_keys().words();
+  r.vw_long = lng.packed_values().words();
+  r.out_long = lng.decode_step(Vec(8, 0.3), Vec(8, -0.2), Vec(qq.row(0).begin(), qq.row(0).end()));
+  return r;
+}
+
 int main() {
   // 1. fused attention: reference vs GPU, incl. preset head shapes
   {
@@ -114,7 +208,7 @@ int main() {
     for (double& v : values.data) v = rng.normal();
     for (double& v : qs.data) v = rng.normal();
     QuantizedKVCache ref(kcb, vcb, enc);
-    gpu::QuantizedKVCache gc(kcb, vcb, enc, n + 8);
+    gpu::QuantizedKVCache gc(kcb, vcb, enc);
     double worst = 0;
     for (size_t t = 0; t < n; ++t) {
       Vec k(keys.row(t).begin(), keys.row(t).end()), v(values.row(t).begin(), values.row(t).end());
@@ -127,16 +221,16 @@ int main() {
     report(gc.packed_key_words() == ref.packed_keys().words() &&
                gc.packed_value_words() == ref.packed_values().words(),
            "incremental packed words identical");
-    auto pre = gpu::QuantizedKVCache::prefill(keys, values, kcb, vcb, enc);
-    report(pre->packed_key_words() == ref.packed_keys().words(), "gpu prefill == reference appends");
+    gpu::QuantizedKVCache pre = gpu::QuantizedKVCache::prefill(keys, values, kcb, vcb, enc);
+    report(pre.packed_key_words() == ref.packed_keys().words(), "gpu prefill == reference appends");
     const auto dir = std::filesystem::temp_directory_path();
     const std::string p1 = (dir / "cvq_gpu.cvqc").string(), p2 = (dir / "cvq_ref.cvqc").string();
     gc.save(p1);
     QuantizedKVCache back = QuantizedKVCache::load(p1, kcb, vcb, enc);
     report(back.packed_keys().words() == ref.packed_keys().words(), "reference loads GPU CVQC");
     ref.save(p2);
-    auto gback = gpu::QuantizedKVCache::load(p2, kcb, vcb, enc);
-    report(gback->packed_key_words() == ref.packed_keys().words() && gback->size() == n,
+    gpu::QuantizedKVCache gback = gpu::QuantizedKVCache::load(p2, kcb, vcb, enc);
+    report(gback.packed_key_words() == ref.packed_keys().words() && gback.size() == n,
            "GPU loads reference CVQC");
     bool threw = false;
     try {
@@ -221,6 +315,77 @@ int main() {
                       ref.loss_curve.size() == dev.loss_curve.size();
     report(same && worst <= 1e-9 * scale, "train_value_quantizer",
            "max |d param| / max |param| = " + std::to_string(worst / scale));
+  }
+  // 7. the reference's cache test bodies (test_cache.cpp:155-276) written
+  // once against a Cache type and instantiated with commvq::QuantizedKVCache
+  // and commvq::gpu::QuantizedKVCache -- only the namespace differs
+  {
+    CacheFixture fx;
+    const CacheRun ref = run_cache_body<QuantizedKVCache>(fx, "ref");
+    const CacheRun dev = run_cache_body<gpu::QuantizedKVCache>(fx, "gpu");
+    report(dev.kw_pre == ref.kw_pre && dev.vw_pre == ref.vw_pre && dev.kw_inc == ref.kw_inc,
+           "cache body: prefill / appends words (by-value prefill)");
+    report(dev.a == ref.a && dev.b == ref.b && dev.bits == ref.bits,
+           "cache body: key_codes() / value_codes() accessors");
+    report(dev.threw_dim && ref.threw_dim, "cache body: append(Vec(7), Vec(8)) -> invalid_argument");
+    double worst = 0;
+    for (size_t i = 0; i < ref.outs.size(); ++i) worst = std::max(worst, rel_err(dev.outs[i], ref.outs[i]));
+    report(worst <= 1e-5 && dev.flop_tokens_ok && ref.flop_tokens_ok,
+           "cache body: decode_step + FlopReport", std::to_string(worst));
+    report(dev.stats.tokens == ref.stats.tokens &&
+               dev.stats.quantized_payload_bits == ref.stats.quantized_payload_bits &&
+               dev.stats.fp16_equivalent_bytes == ref.stats.fp16_equivalent_bytes &&
+               dev.stats.codebook_bytes == ref.stats.codebook_bytes &&
+               dev.stats.avg_bit_effective == ref.stats.avg_bit_effective &&
+               dev.stats.avg_bit_amortized == ref.stats.avg_bit_amortized,
+           "cache body: stats() == compute_cache_stats");
+    const CacheStats z1 = compute_cache_stats(fx.cfg, 8, 131072),
+                     z2 = gpu::compute_cache_stats(fx.cfg, 8, 131072);
+    report(z1.quantized_payload_bits == z2.quantized_payload_bits &&
+               z1.avg_bit_amortized == z2.avg_bit_amortized,
+           "compute_cache_stats closed form");
+    report(dev.kw_loaded == ref.kw_loaded && dev.n_loaded == ref.n_loaded &&
+               dev.a_loaded == ref.a_loaded,
+           "cache body: save / load by value");
+    report(dev.kw_long == ref.kw_long && dev.vw_long == ref.vw_long && dev.n_long == 70000 &&
+               ref.n_long == 70000,
+           "cache body: 70,000 appends past the initial reservation (words identical)");
+    report(rel_err(dev.out_long, ref.out_long) <= 1e-5, "decode_step at 70,001 tokens",
+           std::to_string(rel_err(dev.out_long, ref.out_long)));
+    report(dev.copy_ok && ref.copy_ok, "cache body: copy is deep, move keeps contents");
+  }
+  // 8. encode_keys honours AssignSearch (keyquant.cpp:724-730): both searches
+  // bit-exact against the reference's, on constructed near-ties where the two
+  // searches may disagree
+  {
+    KeyQuantConfig cfg{16, 4, 16, 3};
+    Rng rng(99);
+    KeyCodebook kcb = rand_kcb(cfg, rng);
+    Mat keys(300, 16);
+    for (double& v : keys.data) v = rng.normal();
+    for (size_t p = 0; p < 60; ++p) {  // midpoints of two centers of round 0, group 0..3
+      const size_t a1 = rng.index(16), b1 = rng.index(16), a2 = rng.index(16), b2 = rng.index(16);
+      for (size_t j = 0; j < 8; ++j) {
+        const CommMat& u1 = kcb.atoms[kcb.atom_index(0, j, a1)];
+        const CommMat& v1 = kcb.atoms[kcb.atom_index(0, j, b1)];
+        const CommMat& u2 = kcb.atoms[kcb.atom_index(0, j, a2)];
+        const CommMat& v2 = kcb.atoms[kcb.atom_index(0, j, b2)];
+        keys(p, 2 * j) = 0.5 * ((u1.x - v1.y) + (u2.x - v2.y));
+        keys(p, 2 * j + 1) = 0.5 * ((u1.y + v1.x) + (u2.y + v2.x));
+      }
+    }
+    bool ok = true;
+    size_t differ = 0;
+    for (AssignSearch sch : {AssignSearch::brute_force, AssignSearch::factorized}) {
+      KeyCodes r = commvq::encode_keys(keys, kcb, sch);
+      KeyCodes g2 = gpu::encode_keys(keys, kcb, sch);
+      ok = ok && r.a == g2.a && r.b == g2.b;
+    }
+    KeyCodes rb = commvq::encode_keys(keys, kcb, AssignSearch::brute_force);
+    KeyCodes rf = commvq::encode_keys(keys, kcb, AssignSearch::factorized);
+    for (size_t i = 0; i < rb.a.size(); ++i) differ += rb.a[i] != rf.a[i] || rb.b[i] != rf.b[i];
+    report(ok, "encode_keys brute_force and factorized bit-exact",
+           "(reference searches differ on " + std::to_string(differ) + " codes)");
   }
   std::printf("%d failure(s)\n", g_fail);
   return g_fail;

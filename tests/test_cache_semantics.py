@@ -143,3 +143,53 @@ def test_tc_fp16_guard(G, scale, want_mode):
     out = c.attention(q.reshape(1, 1, 1, 128).astype(np.float32), n - 1)
     want, _, _ = P.fused_attention(kq, atoms, a, b, bits, vrows, q, n - 1)
     assert fx.rel_err(out.reshape(-1), want) <= (1e-3 if want_mode == "tc" else 1e-4)
+
+
+@pytest.mark.parametrize("shape", [(16, 4, 16, 3), (128, 64, 64, 11), (8, 2, 4, 2)])
+def test_encode_keys_factorized_bit_exact(G, shape):
+    """AssignSearch::factorized (keyquant.cpp:204-224, 724-730) on the
+    device vs the oracle's factorized search, with constructed midpoints
+    between two centers where brute force and factorized may disagree."""
+    kq = KQ(*shape)
+    rng = P.rng(sum(shape) + 5)
+    atoms = rng.normal(2 * kq.n_atoms, 0.3 if kq.d == 128 else 1.0)
+    keys = P.gen_synth(257, kq.d, min(kq.d, 32), 17)
+    xy = atoms.reshape(kq.rounds, kq.subspaces, kq.n_levels, 2)
+    for p in range(40):
+        a1, b1, a2, b2 = rng.index(4, kq.n_levels).tolist()
+        for j in range(kq.group_size):
+            keys[p, 2 * j] = 0.5 * (xy[0, j, a1, 0] - xy[0, j, b1, 1] + xy[0, j, a2, 0] - xy[0, j, b2, 1])
+            keys[p, 2 * j + 1] = 0.5 * (xy[0, j, a1, 1] + xy[0, j, b1, 0] + xy[0, j, a2, 1] + xy[0, j, b2, 0])
+    for search in ("brute_force", "factorized"):
+        ga, gb = G.encode_keys(kq, atoms, keys, search=search)
+        oa, ob = P.encode_keys(kq, atoms, keys, factorized=(search == "factorized"))
+        assert (ga == oa).all() and (gb == ob).all(), search
+
+
+def test_single_stream_mirror_reuses_device_copies(G):
+    """fused_attention called as a decode loop over growing, append-only
+    arrays (the reference cache's key_codes_/value_codes_ vectors): every
+    step equals the oracle; the device cache is reused (only the tail is
+    uploaded) and an in-place change of earlier codes is detected."""
+    kq = KQ(16, 4, 16, 3)
+    nc, n_max = 16, 400
+    rng = P.rng(77)
+    atoms = rng.normal(2 * kq.n_atoms)
+    vrows = rng.normal(nc * 16).reshape(nc, 16)
+    a_all, b_all = fx.random_key_codes(kq, n_max, rng=rng)
+    bits_all = fx.random_value_codes(nc, n_max, rng=rng)
+    per = kq.rounds * kq.groups
+    a = np.zeros(n_max * per, np.uint16)  # preallocated, filled in place
+    b = np.zeros(n_max * per, np.uint16)
+    bits = np.zeros((n_max, nc), np.uint8)
+    for n in (1, 2, 50, 51, 200, 399, 400):
+        a[:n * per], b[:n * per], bits[:n] = a_all[:n * per], b_all[:n * per], bits_all[:n]
+        q = rng.normal(16)
+        got, _ = G.fused_attention(kq, atoms, a[:n * per], b[:n * per], bits[:n], vrows, q, n - 1)
+        want, _, _ = P.fused_attention(kq, atoms, a[:n * per], b[:n * per], bits[:n], vrows, q, n - 1)
+        assert fx.rel_err(got, want) <= 1e-5, n
+    a[0] = (a[0] + 1) % kq.n_levels  # rewrite an early code in place
+    q = rng.normal(16)
+    got, _ = G.fused_attention(kq, atoms, a, b, bits, vrows, q, n_max - 1)
+    want, _, _ = P.fused_attention(kq, atoms, a, b, bits, vrows, q, n_max - 1)
+    assert fx.rel_err(got, want) <= 1e-5
