@@ -11,9 +11,11 @@ HBM.  metric = KV-tokens/s (one KV-token = one cached token of one
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
 
 Multi-GPU (torchrun): the context is sharded contiguously across ranks
-(position offsets kept global), each rank computes split-K partials
-(m, l, o) and one NCCL all-gather + LSE combine merges them
- -- strong scaling of the fixed C3 job.
+(cvq_shard_plan; position offsets kept global); each step runs the C-ABI
+shard group (cvq_mgpu_attention: partial on the local shard, one NCCL
+all-gather of the packed (m, l, o) blocks, LSE combine -- all inside
+libcvq_b200) -- strong scaling of the fixed C3 job.  e2e at
+N > 1 is cvq_mgpu_decode_step with host buffers (the last shard appends).
 """
 import argparse
 import json
@@ -161,8 +163,9 @@ def main():
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"])
     ap.add_argument("--no-prefill", action="store_true")
     ap.add_argument("--merge", default="nccl", choices=["nccl", "peer"],
-                    help="N>1 shard merge: one NCCL all-gather of packed partials + combine, or "
-                         "peer: symmetric-memory blocks read by the combine kernel over NVLink")
+                    help="N>1 shard merge: the C-ABI shard group (one NCCL all-gather of packed "
+                         "partials + combine inside libcvq_b200), or peer (experimental): "
+                         "symmetric-memory blocks read by the combine kernel over NVLink")
     ap.add_argument("--keys", default="tc", choices=["fp32", "fp16", "tc"],
                     help="score kernel: tc = tcgen05 one-hot MMA (fp16 codebook), fp16 / fp32 = "
                          "CUDA-core gather with that codebook precision; fp32 accumulation always")
@@ -194,7 +197,7 @@ def main():
     kq = G.KeyQuantConfig(d, g, L, R)
     S, rows = B * layers * H, B * layers * H * Gq
     # contiguous context shards, boundaries at multiples of 128 tokens
-    from paper_2506_18879_b200.dist import gather_packed, packed_views, shard_plan
+    from paper_2506_18879_b200.dist import shard_plan
     lo, hi = shard_plan(N, world)[rank]
     n_local = hi - lo
     extra = 2 * (args.steps + args.warmup) + 16  # room for the e2e decode steps' appends
@@ -238,25 +241,36 @@ def main():
     q = torch.randn(B, layers, H * Gq, d, device="cuda", generator=qgen)
     out = torch.empty_like(q)
     t_q = N - 1  # global query position (last cached token)
-    # this rank's partials (m, l, o) in one packed block -> one all-gather
-    pk = torch.empty(rows * (d + 2), device="cuda")
-    m_p, l_p, o_p = packed_views(pk, rows, d)
-    peer = None
+    peer = group = None
     if world > 1 and args.merge == "peer":
+        # experimental: symmetric-memory blocks read by the combine over NVLink
         from paper_2506_18879_b200.dist import PeerMerge
         peer = PeerMerge(rows, d)
+    elif world > 1 and args.dist_backend == "nccl":
+        # the C-ABI shard group (mgpu.cu): partial -> one ncclAllGather of the
+        # packed [m | l | o] blocks -> LSE combine, inside libcvq_b200
+        import torch.distributed as dist
+        uid = [G.ShardGroup.unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        group = G.ShardGroup(cache, rank, world, uid[0])
+    # gloo (several ranks sharing one GPU, host-staged exchange): the same
+    # packed blocks gathered through torch.distributed
+    from paper_2506_18879_b200.dist import gather_packed, packed_views
+    pk = torch.empty(rows * (d + 2), device="cuda")
+    m_p, l_p, o_p = packed_views(pk, rows, d)
 
     def step():
         if world == 1:
             cache.attention(q, t_q, out)
-        elif peer is not None:  # the combine kernel reads the peers' blocks over NVLink
+        elif peer is not None:
             m_v, l_v, o_v = peer.views()
             cache.attention_partial(q, m_v, l_v, o_v, t_q)
             peer.merge(out, G, ctx)
+        elif group is not None:
+            group.attention(q, t_q, out)
         else:
             cache.attention_partial(q, m_p, l_p, o_p, t_q)
-            parts = gather_packed(pk)  # NCCL all-gather, 520 B/row
-            G.lse_combine_packed(parts, rows, d, out, ctx)
+            G.lse_combine_packed(gather_packed(pk), rows, d, out, ctx)
 
     def barrier():
         if world > 1:
@@ -293,52 +307,90 @@ def main():
     value = kv_tokens / (ms / 1e3)
 
     # ---- roofline of the dominant kernel (live CUDA-event timing) ----
+    # the north-star roofline is HBM on compressed-cache bytes
+    # (32.5 B / 63.5 B per KV-head-token) against MEASURED_PEAKS; the binding
+    # resource of this algorithm is the tensor pipe (one-hot MMA), reported
+    # alongside against 2 x the measured bf16 burst (2:4 sparse doubles the
+    # dense rate) at the clock the run saw.
     hbm, tflops, src = peaks()
     kvht_per_launch = S * n_local
     bytes_per_launch = kvht_per_launch * BYTES_PER_KVHT[R]
     avg_main_ms = main_ms / max(main_n, 1)
     achieved = bytes_per_launch / (avg_main_ms / 1e3) / 1e9
-    # dram read+write bytes of the same kernel from the committed ncu capture
-    traffic = None
+    traffic = traffic_step = traffic_src = None
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
-            tr = json.load(f).get(f"{args.config}/{args.keys}")
+            tr = json.load(f).get(f"{args.config}/{args.keys}" +
+                                   ("" if args.tc_variant == "sparse" else "_" + args.tc_variant))
         if tr and world == 1:
             traffic = tr["dram_bytes_per_launch"]
+            traffic_step = tr.get("dram_bytes_per_step")
+            traffic_src = tr.get("source")
     except Exception:
         pass
-    common = {"traffic": traffic,
-              "traffic_note": "dram__bytes_read+write of the score kernel per launch "
-                              "(profiles/traffic.json); the value kernel reads the value words",
-              "kernel_ms": avg_main_ms, "kernel_share_of_step": avg_main_ms / ms,
-              "algorithmic_bytes_per_launch": bytes_per_launch,
-              "kv_head_tokens_per_s_kernel": kvht_per_launch / (avg_main_ms / 1e3)}
+    clk_sum = clk.summary()
+    kname = {"tc": {"sparse": "k_sp_score (2:4-sparse one-hot tcgen05 MMA)",
+                    "dense": "k_tc_score (dense one-hot tcgen05 MMA)",
+                    "pair": "k_sp_score CTA-pair"}[args.tc_variant],
+             "fp16": "k_fast_score_h (CUDA cores, fp16 codebook)",
+             "fp32": "k_fast_score (CUDA cores, fp32 codebook)"}[args.keys]
+    roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+            "frac": achieved / hbm, "traffic": traffic, "traffic_step": traffic_step,
+            "traffic_note": "dram__bytes_read+write per launch of the score kernel and per whole "
+                            "step (all kernels) from one ncu capture (%s)" % traffic_src,
+            "peak_source": "MEASURED_PEAKS.json hbm_gbs (%s)" % src, "kernel": kname,
+            "kernel_ms": avg_main_ms, "kernel_share_of_step": avg_main_ms / ms,
+            "algorithmic_bytes_per_launch": bytes_per_launch,
+            "bytes_per_kv_head_token": BYTES_PER_KVHT[R],
+            "kv_head_tokens_per_s_kernel": kvht_per_launch / (avg_main_ms / 1e3),
+            "step_hbm_achieved_gbs": bytes_per_launch / (ms / 1e3) / 1e9,
+            "step_frac": bytes_per_launch / (ms / 1e3) / 1e9 / hbm}
     if args.keys == "tc":
         # one-hot MMA: per KV-head-token 2 * 128 reals * (2 sides * 64 levels) * R
-        # = 4*R*L*d flops, executed on the tensor pipe
+        # = 4*R*L*d logical flops, executed on the tensor pipe
         flops = kvht_per_launch * 4.0 * R * L * d
         ach_tf = flops / (avg_main_ms / 1e3) / 1e12
-        # R = 11: the one-hot is a 2:4-sparse A operand (tcgen05.mma.sp,
-        # attn_sp.cu) -- the ceiling is the sparse fp16 rate, twice the dense
         sparse = R in (11, 21) and args.tc_variant != "dense"
-        peak_tf = TENSOR_NOMINAL_TFLOPS * (2 if sparse else 1)
-        roof = {"bound": "tensor", "achieved": ach_tf, "peak": peak_tf,
-                "unit": "TFLOP/s", "frac": ach_tf / peak_tf,
-                "kernel": "k_sp_score (2:4-sparse one-hot MMA)" if sparse else "k_tc_score (dense one-hot MMA)",
-                "peak_source": ("B200_PROFILING.md nominal fp16 %s (%.2f PFLOP/s, achieved counts the "
-                                "logical one-hot GEMM flops); MEASURED_PEAKS bf16 burst %.1f is a "
-                                "power-capped dense cuBLAS run at lower SM clocks"
-                                % ("2:4-sparse = 2 x dense" if sparse else "dense", peak_tf / 1e3, tflops)),
-                "frac_vs_dense_nominal": ach_tf / TENSOR_NOMINAL_TFLOPS,
-                "frac_vs_measured_bf16_burst": ach_tf / tflops,
-                "algorithmic_flops_per_launch": flops,
-                "hbm_achieved_gbs": achieved, "hbm_frac": achieved / hbm, **common}
-    else:
-        roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                "frac": achieved / hbm, "peak_source": src, **common}
+        peak_tf = tflops * (2 if sparse else 1)
+        roof["tensor"] = {
+            "achieved": ach_tf, "peak": peak_tf, "unit": "TFLOP/s", "frac": ach_tf / peak_tf,
+            "peak_source": "%s x MEASURED_PEAKS bf16_tflops burst (%.1f, cuBLAS dense)%s" % (
+                "2" if sparse else "1", tflops,
+                "; 2:4-sparse tcgen05 runs at twice the dense rate" if sparse else ""),
+            "sm_mhz_median": clk_sum.get("sm_mhz"),
+            "frac_vs_nominal": ach_tf / (TENSOR_NOMINAL_TFLOPS * (2 if sparse else 1)),
+            "algorithmic_flops_per_launch": flops}
 
     # ---- e2e through the C-ABI with host buffers (decode_step) ----
     e2e = None
+    if not args.no_e2e and world > 1 and group is not None:
+        # every rank passes its pinned host buffers; the last rank appends
+        kh = torch.from_numpy(np.random.default_rng(5).standard_normal((B, layers, H, d))
+                              .astype(np.float32)).pin_memory()
+        vh = torch.from_numpy(np.random.default_rng(6).standard_normal((B, layers, H, d))
+                              .astype(np.float32)).pin_memory()
+        qh = torch.from_numpy(np.random.default_rng(7).standard_normal((B, layers, H * Gq, d))
+                              .astype(np.float32)).pin_memory()
+        oh = torch.empty_like(qh).pin_memory()
+        n_e2e = min(args.steps, 8)
+        group.decode_step(kh, vh, qh, oh)
+        torch.cuda.synchronize()
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(n_e2e):
+            group.decode_step(kh, vh, qh, oh)
+        torch.cuda.synchronize()
+        e2e_ms = (time.perf_counter() - t0) * 1e3 / n_e2e
+        import torch.distributed as dist
+        tt = torch.tensor([e2e_ms], device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_ms = float(tt.item())
+        n_now = group.size()
+        e2e = {"value": B * layers * n_now / (e2e_ms / 1e3), "unit": "KV-tokens/s",
+               "h2d_bytes_per_step": int(kh.numel() * 4 * 2 + qh.numel() * 4),
+               "d2h_bytes_per_step": int(oh.numel() * 4), "ms_per_step": e2e_ms,
+               "path": "cvq_mgpu_decode_step (last shard appends k,v; partial + NCCL all-gather "
+                       "+ combine) with pinned host buffers on every rank, max over ranks"}
     if not args.no_e2e and world == 1:
         kh = np.random.default_rng(5).standard_normal((B, layers, H, d)).astype(np.float32)
         vh = np.random.default_rng(6).standard_normal((B, layers, H, d)).astype(np.float32)
@@ -432,7 +484,7 @@ def main():
                        "n_codes": nc, "parallelism": f"context-shard x{world}",
                        "merge": args.merge if world > 1 else None,
                        "l2": "inputs (packed cache) larger than L2"},
-            "kv_head_tokens_per_s": value * H, "roofline": roof, "clocks": clk.summary(),
+            "kv_head_tokens_per_s": value * H, "roofline": roof, "clocks": clk_sum,
             "gpu_launches": launches, "e2e": e2e, "cpu_baseline": cpu, "prefill": prefill,
         }
         print(json.dumps(line), flush=True)

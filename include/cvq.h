@@ -53,7 +53,8 @@ typedef enum cvq_status {
   CVQ_ERANGE = 3,    /* std::out_of_range                             */
   CVQ_EIO = 4,       /* commvq::IoError                               */
   CVQ_ECUDA = 5,     /* device / driver failure (no CPU fallback)     */
-  CVQ_ENOMEM = 6     /* device allocation failed                      */
+  CVQ_ENOMEM = 6,    /* device allocation failed                      */
+  CVQ_ENCCL = 7      /* NCCL missing or a collective failed (mgpu)    */
 } cvq_status;
 
 /* KeyQuantConfig (keyquant.hpp:16-28). */
@@ -368,6 +369,50 @@ CVQ_API cvq_status cvq_lse_combine_ptrs(cvq_context* ctx, const float* const* pa
 CVQ_API cvq_status cvq_cache_decode_step(cvq_cache* c, const void* k,
                                          const void* v, int kv_dtype,
                                          const float* q, float* out, int where);
+
+/* Shape of a cache (from its descriptor) and the context it runs on. */
+typedef struct cvq_cache_shape {
+  uint32_t n_seqs, n_layers, n_kv_heads, q_per_kv, d, n_codes;
+  uint64_t position_offset;
+} cvq_cache_shape;
+CVQ_API cvq_status cvq_cache_shape_of(const cvq_cache* c, cvq_cache_shape* out);
+CVQ_API cvq_context* cvq_cache_context(const cvq_cache* c);
+
+/* ----------------------------- context sharding across GPUs */
+/* Contiguous per-rank token ranges: bounds[2r], bounds[2r+1] = [lo, hi) of
+ * rank r, boundaries on `align`-token tiles (128 keeps packed tiles 32-B
+ * aligned); trailing ranks may be empty.  Host-only (no device needed). */
+CVQ_API cvq_status cvq_shard_plan(uint64_t n_tokens, uint32_t world, uint32_t align,
+                                  uint64_t* bounds);
+
+/* One rank of a context-sharded cache: `shard` holds this rank's tokens of
+ * every stream (position_offset = its first global position).  Attention =
+ * partial on the shard written as one packed [m | l | o] block (520 B per
+ * row at d = 128), ONE ncclAllGather of the blocks on the context stream,
+ * then the LSE combine kernel.  NCCL is loaded at run time (libnccl.so.2;
+ * in a torch process the copy torch loaded).  Errors: CVQ_ENCCL.
+ *   cvq_mgpu_init       an initialised ncclComm_t (passed as void*) that
+ *                       spans the ranks; the caller keeps ownership;
+ *   cvq_mgpu_init_rank  the library creates the communicator from a unique
+ *                       id (cvq_mgpu_unique_id on one rank, 128 bytes,
+ *                       broadcast by the caller's bootstrap). */
+typedef struct cvq_mgpu cvq_mgpu;
+CVQ_API cvq_status cvq_mgpu_unique_id(void* id_out /* 128 bytes */);
+CVQ_API cvq_status cvq_mgpu_init(cvq_cache* shard, void* nccl_comm, cvq_mgpu** out);
+CVQ_API cvq_status cvq_mgpu_init_rank(cvq_cache* shard, const void* unique_id, int rank,
+                                      int world, cvq_mgpu** out);
+CVQ_API cvq_status cvq_mgpu_destroy(cvq_mgpu* g);
+/* Global tokens per stream (the last shard's end). */
+CVQ_API cvq_status cvq_mgpu_length(const cvq_mgpu* g, uint64_t* n_tokens);
+/* Collective: every rank calls it with the same q and t; out gets the merged
+ * attention of all ranks' tokens.  q/out in `where` (host: one sync). */
+CVQ_API cvq_status cvq_mgpu_attention(cvq_mgpu* g, const float* q, uint64_t t, float* out,
+                                      int where);
+/* QuantizedKVCache::decode_step across the group (cache.cpp:287-296): the
+ * last rank appends (k, v) to its shard (other ranks ignore k, v, which may
+ * be NULL there), then every rank attends q at the new global position. */
+CVQ_API cvq_status cvq_mgpu_decode_step(cvq_mgpu* g, const void* k, const void* v, int kv_dtype,
+                                        const float* q, float* out, int where);
 
 /* Packed-word import/export of one stream (CVQC payload, cache.cpp:310-373).
  * Import sets the stream's words for tokens [0, n_tokens); all streams must

@@ -57,6 +57,10 @@ class CudaError(RuntimeError):
     """Device failure (no CPU fallback exists)."""
 
 
+class NcclError(RuntimeError):
+    """NCCL missing or a collective failed (shard groups)."""
+
+
 _lib.cvq_last_error.restype = C.c_char_p
 _lib.cvq_launch_count.restype = _u64
 _lib.cvq_abi_version.restype = _i
@@ -66,7 +70,8 @@ def _check(rc):
     if rc == 0:
         return
     msg = _lib.cvq_last_error().decode()
-    raise {1: ValueError, 2: TrainingError, 3: IndexError, 4: IoError}.get(rc, CudaError)(msg)
+    raise {1: ValueError, 2: TrainingError, 3: IndexError, 4: IoError,
+           7: NcclError}.get(rc, CudaError)(msg)
 
 
 def launch_count() -> int:
@@ -667,6 +672,64 @@ class QuantizedKVCache:
 
     def set_length(self, n):
         _check(_lib.cvq_cache_set_length(self.h, _u64(n)))
+
+
+class ShardGroup:
+    """One rank of a context-sharded cache (cvq_mgpu, mgpu.cu):
+    partial on the local shard -> one NCCL all-gather of the packed
+    [m | l | o] blocks -> LSE combine, all inside the library.  Every rank
+    builds its shard cache (position_offset = its first global token, from
+    shard_plan) and calls these collectively.
+
+    unique_id: 128 bytes from ShardGroup.unique_id() on one rank, broadcast
+    by the caller (e.g. torch.distributed.broadcast_object_list)."""
+
+    def __init__(self, shard, rank, world, unique_id):
+        self.shard = shard
+        uid = C.create_string_buffer(bytes(unique_id), 128)
+        h = _p()
+        _check(_lib.cvq_mgpu_init_rank(shard.h, uid, _i(rank), _i(world), C.byref(h)))
+        self.h = h
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = C.create_string_buffer(128)
+        _check(_lib.cvq_mgpu_unique_id(buf))
+        return buf.raw
+
+    def close(self):
+        if getattr(self, "h", None):
+            _lib.cvq_mgpu_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def size(self):
+        n = _u64()
+        _check(_lib.cvq_mgpu_length(self.h, C.byref(n)))
+        return n.value
+
+    def attention(self, q, t, out):
+        qp, where, qk = _buf(q, np.float32)
+        op, _, ok = _buf(out)
+        with _TorchOrder(self.shard.ctx, qk, ok):
+            _check(_lib.cvq_mgpu_attention(self.h, qp, _u64(t), op, _i(where)))
+        return out
+
+    def decode_step(self, k, v, q, out):
+        """The last rank appends (k, v); every rank attends q at the new end."""
+        kp, where, kk = _buf(k)
+        vp, _, vk = _buf(v)
+        dt = CVQ_F64 if str(kk.dtype).endswith("float64") else CVQ_F32
+        qp, _, qk = _buf(q, np.float32)
+        op, _, ok = _buf(out)
+        with _TorchOrder(self.shard.ctx, kk, vk, qk, ok):
+            _check(_lib.cvq_mgpu_decode_step(self.h, kp, vp, _i(dt), qp, op, _i(where)))
+        return out
 
 
 def lse_combine_packed(parts, rows, d, out, ctx=None):

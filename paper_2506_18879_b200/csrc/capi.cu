@@ -365,6 +365,10 @@ cvq_status to_device(cvq_cache* c, DevBuf& buf, const void* p, size_t bytes, int
 
 }  // namespace
 
+namespace cvq {
+cvq_status set_error(cvq_status s, const std::string& msg) { return fail(s, msg); }
+}  // namespace cvq
+
 // ================================================================ general
 CVQ_API const char* cvq_last_error(void) { return g_err.c_str(); }
 CVQ_API int cvq_abi_version(void) { return 1; }
@@ -886,6 +890,20 @@ CVQ_API cvq_status cvq_cache_set_length(cvq_cache* c, uint64_t n) {
   c->length = n;
   return CVQ_OK;
 }
+
+CVQ_API cvq_status cvq_cache_shape_of(const cvq_cache* c, cvq_cache_shape* out) {
+  if (!c || !out) return fail(CVQ_EINVAL, "null argument");
+  out->n_seqs = c->desc.n_seqs;
+  out->n_layers = c->desc.n_layers;
+  out->n_kv_heads = c->desc.n_kv_heads;
+  out->q_per_kv = c->desc.q_per_kv;
+  out->d = c->desc.key.d;
+  out->n_codes = c->desc.n_codes;
+  out->position_offset = c->desc.position_offset;
+  return CVQ_OK;
+}
+
+CVQ_API cvq_context* cvq_cache_context(const cvq_cache* c) { return c ? c->ctx : nullptr; }
 
 CVQ_API cvq_status cvq_cache_reserve(cvq_cache* c, uint64_t n_tokens) {
   if (!c) return fail(CVQ_EINVAL, "null cache");

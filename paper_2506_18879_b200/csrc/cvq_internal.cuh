@@ -6,6 +6,9 @@
 #include <cfloat>
 
 #include <cuda_runtime.h>
+#include <string>
+
+#include "../../include/cvq.h"
 #include <stdint.h>
 
 #include <atomic>
@@ -43,6 +46,9 @@ struct AttnJob {
   long long t;                // query position
   uint32_t variant;           // kVar* kernel-variant bits (cvq_cache_set_variant)
 };
+
+// Records the message returned by cvq_last_error() on this thread (capi.cu).
+cvq_status set_error(cvq_status s, const std::string& msg);
 
 // Kernel variants selectable per cache (cvq.h CVQ_VARIANT_*): cross-check /
 // experimental kernels next to the defaults, chosen by the caller, never by

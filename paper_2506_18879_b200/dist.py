@@ -11,17 +11,17 @@ TILE = 128
 
 
 def shard_plan(n_tokens: int, world: int, align: int = TILE):
-    """[(lo, hi)] per rank: contiguous, aligned, covering [0, n_tokens)."""
+    """[(lo, hi)] per rank: contiguous, aligned, covering [0, n_tokens) --
+    the library's host-side plan (cvq_shard_plan, mgpu.cu), the same one the
+    C-ABI shard group and bench.py use."""
+    import ctypes as C
+
+    from paper_2506_18879_b200 import commvq as G
     if world < 1:
         raise ValueError("world must be >= 1")
-    per = -(-n_tokens // world)
-    per = -(-per // align) * align
-    out = []
-    for r in range(world):
-        lo = min(n_tokens, r * per)
-        hi = min(n_tokens, (r + 1) * per)
-        out.append((lo, hi))
-    return out
+    b = (C.c_uint64 * (2 * world))()
+    G._check(G._lib.cvq_shard_plan(C.c_uint64(n_tokens), C.c_uint32(world), C.c_uint32(align), b))
+    return [(int(b[2 * r]), int(b[2 * r + 1])) for r in range(world)]
 
 
 def gather_partials(m, l, o, group=None):

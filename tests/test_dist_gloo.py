@@ -85,6 +85,41 @@ def _worker(rank, world, port, result_dir):
                 want, _, _ = P.fused_attention(kq, atoms, a, b, bits, vrows, q, t)
                 worst = max(worst, fx.rel_err(out[i], want))
             np.save(os.path.join(result_dir, "worst.npy"), np.array([worst]))
+        # decode steps (cvq_mgpu_decode_step): the new tokens go to the LAST
+        # shard only and every rank attends at the new global end; after k
+        # steps the merge equals the unsharded attention over n + k tokens
+        k_new = 3
+        n2 = n + k_new
+        lo2, hi2 = (lo, hi + k_new) if rank == world - 1 else (lo, hi)
+        pk2 = torch.zeros(len(rows) * (16 + 2))
+        mt2, lt2, ot2 = packed_views(pk2, len(rows), 16)
+        m2, l2, o2 = mt2.numpy(), lt2.numpy(), ot2.numpy()
+        ext = []
+        for s in range(streams):  # the first n tokens are the same draws
+            rng = P.rng(100 + s)
+            atoms = rng.normal(2 * kq.n_atoms, 0.5)
+            a, b = fx.random_key_codes(kq, n2, rng=P.rng(900 + s))
+            bits = fx.random_value_codes(nc, n2, rng=P.rng(950 + s))
+            vrows = P.rng(990 + s).normal(nc * 16).reshape(nc, 16)
+            for h in range(gq):
+                ext.append((atoms, a, b, bits, vrows, P.rng(10 * s + h).normal(16)))
+        for i, (atoms, a, b, bits, vrows, q) in enumerate(ext):
+            sc = P.fused_scores(kq, atoms, a, b, bits, vrows, q, n2 - 1)[lo2:hi2]
+            if hi2 > lo2:
+                m2[i] = sc.max()
+                p = np.exp(sc - m2[i])
+                l2[i] = p.sum()
+                o2[i] = ((p @ bits[lo2:hi2]) @ vrows) / l2[i]
+        parts2 = gather_packed(pk2).numpy().astype(np.float64)
+        R2 = len(ext)
+        out2 = lse_merge(parts2[:, :R2], parts2[:, R2:2 * R2],
+                         parts2[:, 2 * R2:].reshape(world, R2, 16))
+        if rank == 0:
+            worst2 = 0.0
+            for i, (atoms, a, b, bits, vrows, q) in enumerate(ext):
+                want, _, _ = P.fused_attention(kq, atoms, a, b, bits, vrows, q, n2 - 1)
+                worst2 = max(worst2, fx.rel_err(out2[i], want))
+            np.save(os.path.join(result_dir, "worst_decode.npy"), np.array([worst2]))
     finally:
         dist.destroy_process_group()
 
@@ -95,3 +130,5 @@ def test_sharded_decode_merges_to_unsharded(tmp_path, world):
     mp.spawn(_worker, args=(world, port, str(tmp_path)), nprocs=world, join=True)
     worst = float(np.load(tmp_path / "worst.npy")[0])
     assert worst <= 1e-5, worst
+    worst_decode = float(np.load(tmp_path / "worst_decode.npy")[0])
+    assert worst_decode <= 1e-5, worst_decode

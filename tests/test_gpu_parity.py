@@ -752,3 +752,40 @@ def test_peer_merge_world_one_roundtrip(G, tmp_path):
             assert torch.allclose(out, o, rtol=1e-6, atol=1e-6), step
     finally:
         dist.destroy_process_group()
+
+
+def test_mgpu_shard_group_world_one_nccl(G):
+    """The C-ABI shard group (cvq_mgpu, mgpu.cu) on a real NCCL communicator
+    of one rank: attention = partial + ncclAllGather + combine must equal the
+    cache's own attention; decode_step appends on the last (only) shard and
+    matches the cache's decode_step on a twin cache; host-buffer variants."""
+    kq = KQ(128, 64, 64, 11)
+    nc, n, H, Gq, hidden = 128, 3000, 2, 4, 256
+    rng = P.rng(4711)
+    caches = [G.QuantizedKVCache(kq, nc, n_kv_heads=H, q_per_kv=Gq, capacity=n, hidden=hidden,
+                                 keys="tc") for _ in range(2)]
+    for h in range(H):
+        atoms = rng.normal(2 * kq.n_atoms, 0.3)
+        vrows = rng.normal(nc * 128, 1 / 16).reshape(nc, 128)
+        w1 = rng.normal(128 * hidden, 0.1).reshape(128, hidden)
+        w2 = rng.normal(hidden * nc, 0.1).reshape(hidden, nc)
+        a, b = fx.random_key_codes(kq, n, rng=rng)
+        bits = fx.random_value_codes(nc, n, rng=rng)
+        for c in caches:
+            c.set_key_codebook(0, h, atoms)
+            c.set_value_quantizer(0, h, vrows, w1, np.zeros(hidden), w2, np.zeros(nc))
+            c.import_stream(0, 0, h, P.pack_key_codes(kq, a, b), P.pack_value_codes(bits), n)
+    grp = G.ShardGroup(caches[0], 0, 1, G.ShardGroup.unique_id())
+    assert grp.size() == n
+    q = rng.normal(H * Gq * 128).reshape(1, 1, H * Gq, 128).astype(np.float32)
+    want = caches[1].attention(q, n - 1)
+    got = grp.attention(q, n - 1, np.zeros_like(q))
+    assert fx.rel_err(got, want) <= 1e-6
+    for step in range(3):
+        k = rng.normal(H * 128).reshape(1, 1, H, 128).astype(np.float32)
+        v = rng.normal(H * 128).reshape(1, 1, H, 128).astype(np.float32)
+        got = grp.decode_step(k, v, q, np.zeros_like(q))
+        want = caches[1].decode_step(k, v, q)
+        assert fx.rel_err(got, want) <= 1e-6, step
+    assert grp.size() == n + 3 and caches[0].size() == n + 3
+    grp.close()
