@@ -22,24 +22,35 @@
 //   columns of fp16 pairs, group g = (c & 31) / 4 holds 1.0 in slot c & 1;
 //   the metadata column selects index pair (0,1) or (2,3) from bit 1 of c
 //   -- one column per (round, side); its lane L = m0 + 8 k1 + 16 m2 holds
-//   K-half k1 of rows m0 + 16 m2 (low 16 bits) and m0 + 8 + 16 m2 (high).  4
-//   producer warps (one per TMEM lane quarter, thread = token) write both
-//   with tcgen05.st; 6 round stages (both sides: 32 + 2 metadata columns);
-//   the MMA warp takes rounds in pairs (16 MMAs per elected region).
-// * D double-buffered (TMEM columns 0-255); epilogue = 16 warps, warp
-//   (quarter, slot) owns tokens [32 quarter, +32) x subspaces [16 slot, +16):
-//   z = E[lane][j] K_j with the per-lane phase table E = e^{+i lane theta_j},
-//   score_h += Re(w_hj z) where w_hj = conj(q_hj) e^{-i(t - p0 - 32 quarter)
-//   theta_j} / sqrt(d) is per warp (fp64-based at a work item's first tile,
-//   advanced by e^{+i 128 theta_j} per tile); a 4-warp smem sum per quarter.
+//   K-half k1 of rows m0 + 16 m2 (low 16 bits) and m0 + 8 + 16 m2 (high).
+//   16 producer warps, 4 per TMEM lane quarter (thread = token), take the
+//   rounds by global round index g = sub (mod 4); 6 round stages (both
+//   sides: 32 + 2 metadata columns).  A producer publishes a stage with a
+//   hardware named barrier (bar.arrive, ids 5-10), not an mbarrier: every
+//   shared-memory access of the issuer waits behind the tensor core's B
+//   reads (~100-200 clk), a named barrier does not.
+// * Two issuer warps take alternate global rounds (one's stage wait overlaps
+//   the other's MMAs).  Each round is ONE predicated asm block of 8 .ws.sp
+//   MMAs + the commit that frees its stage (sp_issue_round).  The round-0
+//   issuer of a tile zeroes D and releases the other through a named barrier.
+// * D double-buffered (TMEM columns 0-255); epilogue = 8 warps, warp
+//   (quarter, e2) owns tokens [32 quarter, +32) x subspaces [32 e2, +32) in
+//   two 16-subspace passes: z = E[lane][j] K_j with the per-lane phase table
+//   E = e^{+i lane theta_j}, score_h += Re(w_hj z) where w_hj = conj(q_hj)
+//   e^{-i(t - p0 - 32 quarter) theta_j} / sqrt(d) is per warp (fp64-based at a
+//   work item's first tile, advanced by e^{+i 128 theta_j} per tile); a
+//   2-warp smem sum per quarter.
+//   Round-2 measurements of these choices: DESIGN.md section 4 and
+//   profiles/r02_*.
 //
 // * CTA pairs (CVQ_VARIANT_TC_PAIR, experimental, off by default): clusters of 2
 //   with tcgen05 cta_group::2 -- one MMA covers 256 tokens x N = 128. Each
 //   CTA keeps half of B: rank 0 P = X, Q = Y; rank 1 P = Y, Q = -X, so side a
 //   is [X ; Y] over the P halves and side b is -[Y ; -X] over the Q halves
 //   (negate-A).  Producers of both CTAs arrive on the leader's stage
-//   barriers, the leader's commits multicast to both.  Exact (same parity
-//   tests), but 14.4 ms against 10.6 ms at C3.
+//   mbarriers, the leader's commits multicast to both; one issuer.  Exact
+//   (same parity tests), but slower than the single-CTA kernel at C3
+//   (DESIGN.md section 4).
 //
 // Codebook precision fp16 (as CVQ_CACHE_KEYS_FP16), accumulation fp32.
 #include <cuda_fp16.h>
@@ -69,10 +80,18 @@ constexpr int kTrK0 = 20;
 #define TRK(k) false
 #endif
 constexpr int kTok = 128;                 // tokens per tile (MMA M)
-constexpr int kEpiWarps = 16;
-constexpr int kProdWarps = 8;             // warp 16 + p: TMEM lane quarter p & 3, rounds r = p >> 2 (mod 2)
+constexpr int kEpiWarps = 8;              // warp (quarter, e2): subspaces [32 e2, +32) in 2 passes
+constexpr int kProdWarps = 16;            // 4 per lane quarter, global rounds g = sub (mod 4)
+constexpr int kProdPerQ = 4;
+constexpr int kEpiPerQ = kEpiWarps / 4;    // epilogue warps per lane quarter
+constexpr int kSubsPerEpi = 64 / kEpiPerQ; // subspaces per epilogue warp
 constexpr int kMmaWarp = kEpiWarps + kProdWarps;  // MMA issuer + codebook loader
-constexpr int kThreads = (kMmaWarp + 1) * 32;
+constexpr int kIssuers = 2;  // warps kMmaWarp, kMmaWarp + 1 issue alternate rounds
+constexpr int kThreads = (kMmaWarp + kIssuers) * 32;
+// named barriers (bar.sync ids): 1-4 the epilogue's per-quarter reduction,
+// 5-10 the A stages (producers arrive, the round's issuer syncs), 11-12 the
+// "D zeroed" handoff between the issuers per D buffer, 13 codebook reloaded
+constexpr int kBarStage0 = 5, kBarZero0 = 11, kBarCodebook = 13;
 constexpr int kAStages = 6;               // round stages: both sides of one round (32 + 4 metadata columns)
 constexpr uint32_t kACol0 = 256;          // round stage st: side s at columns 256 + 32 st + 16 s
 constexpr uint32_t kMetaCol0 = kACol0 + 32 * kAStages;  // its metadata: column kMetaCol0 + 4 st + 2 s
@@ -106,52 +125,12 @@ __device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t parity) {
       : "memory");
   return ok != 0;
 }
-__device__ __forceinline__ bool mbar_try_hint(uint64_t* bar, uint32_t parity);
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-#ifdef SP_R2_HINT_ALL
-  while (!mbar_try_hint(bar, parity)) {
-  }
-#else
   while (!mbar_try(bar, parity)) {
   }
-#endif
 }
-#if defined(SP_R2_HINT) || defined(SP_R2_HINT_ALL)
-// try_wait with a suspend-time hint: the warp sleeps in the barrier unit until
-// the phase completes (or ~the hint elapses) instead of re-issuing a poll loop
-__device__ __forceinline__ bool mbar_try_hint(uint64_t* bar, uint32_t parity) {
-  uint32_t ok;
-  asm volatile(
-      "{.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
-      "selp.u32 %0, 1, 0, p;}"
-      : "=r"(ok)
-      : "r"(su32(bar)), "r"(parity), "r"(0x989680u)
-      : "memory");
-  return ok != 0;
-}
-#endif
-#ifdef SP_R2_HINT
-__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
-  while (!mbar_try_hint(bar, parity)) {
-  }
-}
-#else
 __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
   while (!mbar_try(bar, parity)) __nanosleep(64);
-}
-#endif
-#ifndef SP_R2_ISS_SLEEP
-#define SP_R2_ISS_SLEEP 0
-#endif
-// the MMA warp's waits: with SP_R2_ISS_SLEEP > 0 it backs off between polls
-// (it shares SMSP 0 with lane quarter 0's producers)
-__device__ __forceinline__ void mbar_wait_iss(uint64_t* bar, uint32_t parity) {
-#ifdef SP_R2_HINT_ALL
-  mbar_wait(bar, parity);
-#else
-  while (!mbar_try(bar, parity))
-    if (SP_R2_ISS_SLEEP) __nanosleep(SP_R2_ISS_SLEEP);
-#endif
 }
 __device__ __forceinline__ bool elect_one() {
   uint32_t pred;
@@ -258,14 +237,15 @@ __device__ __forceinline__ float2 ffma2(float2 a, float b, float2 c) {
 // commit that frees the round's A stage.  No branch, so ptxas emits
 // @UP-predicated UTCHMMAs with no BSSY/BSYNC reconvergence (a BSYNC waits on
 // the UTCHMMA scoreboards, i.e. drains the MMA queue, ~200 clk per region;
-// tools/umma_pred_bench.cu, profiles/r02_umma_pred_bench.txt).
+// tools/umma_pred_bench.cu).  The MMAs are weight-stationary (.ws) with B
+// collector buffers: a round reads only 4 distinct B slices (X_h, Y_h per K
+// half h) and each is read from smem once (fill on side a, lastuse on side
+// b) instead of twice -- half of the smem bandwidth the B operand took
+// (bit-identical to plain .sp, tools/umma_ws_probe.cu).
 //   side a: Re += X (rows 0-63), Im += Y (rows 64-127)
 //   side b: Re -= Y (negate-A), Im += X;  K half h at +8 A columns, +4 x 2048 B
-template <bool WS>
 __device__ __forceinline__ void sp_issue_round(uint32_t d, uint32_t a, uint32_t e, uint64_t br,
                                                uint32_t idesc, uint32_t accum, uint64_t* bar) {
-#define SP_MMA(c) "@q tcgen05.mma" c
-  if constexpr (WS) {
   asm volatile(
       "{.reg .pred q, p, t;\n\t"
       ".reg .b32 a1, a2, a3, d1, e1;\n\t"
@@ -276,41 +256,17 @@ __device__ __forceinline__ void sp_issue_round(uint32_t d, uint32_t a, uint32_t 
       "add.u32 a1, %1, 8;\n\tadd.u32 a2, %1, 16;\n\tadd.u32 a3, %1, 24;\n\t"
       "add.u32 d1, %0, 64;\n\tadd.u32 e1, %2, 2;\n\t"
       "add.u64 b1, %3, 64;\n\tadd.u64 b2, %3, 512;\n\tadd.u64 b3, %3, 576;\n\t"
-      SP_MMA(".ws.sp.cta_group::1.kind::f16.collector::b0::fill [%0], [%1], %3, [%2], %4, p;\n\t")
-      SP_MMA(".ws.sp.cta_group::1.kind::f16.collector::b1::fill [d1], [%1], b1, [%2], %4, p;\n\t")
-      SP_MMA(".ws.sp.cta_group::1.kind::f16.collector::b2::fill [%0], [a1], b2, [%2], %4, t;\n\t")
-      SP_MMA(".ws.sp.cta_group::1.kind::f16.collector::b3::fill [d1], [a1], b3, [%2], %4, t;\n\t")
-      SP_MMA(".ws.sp.cta_group::1.kind::f16.collector::b1::lastuse [%0], [a2], b1, [e1], %6, t;\n\t")
-      SP_MMA(".ws.sp.cta_group::1.kind::f16.collector::b0::lastuse [d1], [a2], %3, [e1], %4, t;\n\t")
-      SP_MMA(".ws.sp.cta_group::1.kind::f16.collector::b3::lastuse [%0], [a3], b3, [e1], %6, t;\n\t")
-      SP_MMA(".ws.sp.cta_group::1.kind::f16.collector::b2::lastuse [d1], [a3], b2, [e1], %4, t;\n\t")
+      "@q tcgen05.mma.ws.sp.cta_group::1.kind::f16.collector::b0::fill [%0], [%1], %3, [%2], %4, p;\n\t"
+      "@q tcgen05.mma.ws.sp.cta_group::1.kind::f16.collector::b1::fill [d1], [%1], b1, [%2], %4, p;\n\t"
+      "@q tcgen05.mma.ws.sp.cta_group::1.kind::f16.collector::b2::fill [%0], [a1], b2, [%2], %4, t;\n\t"
+      "@q tcgen05.mma.ws.sp.cta_group::1.kind::f16.collector::b3::fill [d1], [a1], b3, [%2], %4, t;\n\t"
+      "@q tcgen05.mma.ws.sp.cta_group::1.kind::f16.collector::b1::lastuse [%0], [a2], b1, [e1], %6, t;\n\t"
+      "@q tcgen05.mma.ws.sp.cta_group::1.kind::f16.collector::b0::lastuse [d1], [a2], %3, [e1], %4, t;\n\t"
+      "@q tcgen05.mma.ws.sp.cta_group::1.kind::f16.collector::b3::lastuse [%0], [a3], b3, [e1], %6, t;\n\t"
+      "@q tcgen05.mma.ws.sp.cta_group::1.kind::f16.collector::b2::lastuse [d1], [a3], b2, [e1], %4, t;\n\t"
       "@q tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%7];}" ::"r"(d),
       "r"(a), "r"(e), "l"(br), "r"(idesc), "r"(accum), "r"(idesc | (1u << 13)), "r"(su32(bar))
       : "memory");
-  } else {
-  asm volatile(
-      "{.reg .pred q, p, t;\n\t"
-      ".reg .b32 a1, a2, a3, d1, e1;\n\t"
-      ".reg .b64 b1, b2, b3;\n\t"
-      "elect.sync _|q, 0xffffffff;\n\t"
-      "setp.ne.b32 p, %5, 0;\n\t"
-      "setp.eq.u32 t, %5, %5;\n\t"
-      "add.u32 a1, %1, 8;\n\tadd.u32 a2, %1, 16;\n\tadd.u32 a3, %1, 24;\n\t"
-      "add.u32 d1, %0, 64;\n\tadd.u32 e1, %2, 2;\n\t"
-      "add.u64 b1, %3, 64;\n\tadd.u64 b2, %3, 512;\n\tadd.u64 b3, %3, 576;\n\t"
-      SP_MMA(".sp.cta_group::1.kind::f16 [%0], [%1], %3, [%2], %4, p;\n\t")
-      SP_MMA(".sp.cta_group::1.kind::f16 [d1], [%1], b1, [%2], %4, p;\n\t")
-      SP_MMA(".sp.cta_group::1.kind::f16 [%0], [a1], b2, [%2], %4, t;\n\t")
-      SP_MMA(".sp.cta_group::1.kind::f16 [d1], [a1], b3, [%2], %4, t;\n\t")
-      SP_MMA(".sp.cta_group::1.kind::f16 [%0], [a2], b1, [e1], %6, t;\n\t")
-      SP_MMA(".sp.cta_group::1.kind::f16 [d1], [a2], %3, [e1], %4, t;\n\t")
-      SP_MMA(".sp.cta_group::1.kind::f16 [%0], [a3], b3, [e1], %6, t;\n\t")
-      SP_MMA(".sp.cta_group::1.kind::f16 [d1], [a3], b2, [e1], %4, t;\n\t")
-      "@q tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%7];}" ::"r"(d),
-      "r"(a), "r"(e), "l"(br), "r"(idesc), "r"(accum), "r"(idesc | (1u << 13)), "r"(su32(bar))
-      : "memory");
-  }
-#undef SP_MMA
 }
 // commit to `bar` from one elected lane, branch-free
 __device__ __forceinline__ void tc_commit_elect(uint64_t* bar) {
@@ -402,7 +358,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_sp_score(SpArgs a) {
   unsigned char* cbs = smem;                                             // [R][16 KiB]
   float2* etab = reinterpret_cast<float2*>(cbs + R * kRoundBytes);         // [64 j][32 lanes]
   float* wtab = reinterpret_cast<float*>(etab + 64 * 32);                 // [warp][16 j][2G]
-  float* red = wtab + kEpiWarps * 16 * 2 * G;                             // [2][4 q][4 e][32][G]
+  float* red = wtab + kEpiWarps * kSubsPerEpi * 2 * G;                     // [2][4 q][4 e][32][G]
   uint64_t* bars = reinterpret_cast<uint64_t*>(red + 2 * 16 * 32 * G);
   uint64_t* afull = bars;
   uint64_t* aempty = bars + kAStages;
@@ -435,11 +391,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_sp_score(SpArgs a) {
       mbar_init(aempty + i, 1);
     }
     for (int i = 0; i < 2; ++i) {
-      mbar_init(dfull + i, 1);
+      mbar_init(dfull + i, PAIR ? 1 : kIssuers);
       mbar_init(dempty + i, PAIR ? 2 * kEpiWarps : kEpiWarps);
     }
     mbar_init(cbfull, 1);
-    mbar_init(cbempty, 1);
+    mbar_init(cbempty, PAIR ? 1 : kIssuers);
     mbar_init(cbpeer, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -461,9 +417,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_sp_score(SpArgs a) {
     // warp slot e = subspaces [16 e, 16 e + 16) ==========================
     const int quarter = warp & 3, eslot = warp >> 2;
     const uint32_t lane_base = (uint32_t)(quarter * 32) << 16;
-    // lanes (jj = lane & 15, half = lane >> 4) keep the phase of subspace
-    // 16 e + jj and produce w for heads 2 half, 2 half + 1 (G = 4)
-    const int jl = eslot * 16 + (lane & 15), hh = lane >> 4;
+    // lane keeps the phase of subspace 32 e2 + lane and produces w for all
+    // 4 heads (G = 4) or the one head (G = 1)
+    const int jl = eslot * 32 + lane, hh = 0;
     const double theta = a.thetas[jl];
     float2 step;
     {
@@ -471,18 +427,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_sp_score(SpArgs a) {
       sincos((double)SpIter<PAIR>::kStep * theta, &sn, &cs);  // e^{+i step theta}: one tile later
       step = make_float2((float)cs, (float)sn);
     }
-    float* wt = wtab + warp * (16 * 2 * G);
+    float* wt = wtab + warp * (kSubsPerEpi * 2 * G);
     const float sc = 0.08838834764831845f;  // 1 / sqrt(128)
     float2 ph = make_float2(1.f, 0.f);
-    float2 qv[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
-#ifdef SP_R2_EREG
-    // this lane's phase factors e^{+i lane theta_j} for the warp's 16
-    // subspaces, held in registers for the whole kernel (no smem reads in
-    // the per-tile loop: the MMAs' B operand reads use all the smem bandwidth)
-    float2 ereg[16];
+    constexpr int kQv = G;  // heads per lane
+    float2 qv[kQv];
 #pragma unroll
-    for (int jj = 0; jj < 16; ++jj) ereg[jj] = etab[(eslot * 16 + jj) * 32 + lane];
-#endif
+    for (int u = 0; u < kQv; ++u) qv[u] = make_float2(0.f, 0.f);
     SpIter<PAIR> it;
     int k = 0;
     for (bool ok = it.first(a); ok; ok = it.next(a), ++k) {
@@ -491,15 +442,29 @@ __global__ void __launch_bounds__(kThreads, 1) k_sp_score(SpArgs a) {
         ph = phase_neg(a.t - (a.pos0 + it.base() + 32 * quarter), theta);
         const float* qs = a.q + (size_t)it.s * G * 128;
 #pragma unroll
-        for (int u = 0; u < 2; ++u) {
-          const int h = (G == 4) ? 2 * hh + u : 0;
+        for (int u = 0; u < kQv; ++u) {
+          const int h = u;
           qv[u] = make_float2(__ldg(qs + h * 128 + 2 * jl) * sc, __ldg(qs + h * 128 + 2 * jl + 1) * sc);
         }
       } else {
         ph = make_float2(ph.x * step.x - ph.y * step.y, ph.x * step.y + ph.y * step.x);
       }
       // w = conj(q) ph; stored as (w.x, -w.y) so Re(w z) = w.x z.x + (-w.y) z.y
-      if (G == 4 || hh == 0) {
+      {
+        float o[2 * G];
+#pragma unroll
+        for (int u = 0; u < G; ++u) {
+          o[u] = qv[u].x * ph.x + qv[u].y * ph.y;
+          o[G + u] = -(qv[u].x * ph.y - qv[u].y * ph.x);
+        }
+        if constexpr (G == 4) {  // [j][h pair]: (wx_h0, wx_h1, -wy_h0, -wy_h1), (.. h2, h3)
+          reinterpret_cast<float4*>(wt)[lane * 2] = make_float4(o[0], o[1], o[4], o[5]);
+          reinterpret_cast<float4*>(wt)[lane * 2 + 1] = make_float4(o[2], o[3], o[6], o[7]);
+        } else {
+          reinterpret_cast<float2*>(wt)[lane] = make_float2(o[0], o[1]);
+        }
+      }
+      if (false) {
         float o[4];
 #pragma unroll
         for (int u = 0; u < 2; ++u) {
@@ -520,6 +485,67 @@ __global__ void __launch_bounds__(kThreads, 1) k_sp_score(SpArgs a) {
       mbar_wait_sleep(dfull + db, (k >> 1) & 1);
       if (TRK(k)) SPTR(1024 + warp * 16 + 4 + (k - kTrK0));
       tc_fence_after();
+      {
+      float* rb = red + (size_t)((db * 4 + quarter) * 2) * 32 * G;  // [e2][lane][G]
+      float2 acc01 = make_float2(0.f, 0.f), acc23 = make_float2(0.f, 0.f);
+      float acc1 = 0.f;
+#pragma unroll 1
+      for (int pass = 0; pass < 2; ++pass) {
+        uint32_t re[16], im[16];
+        tmem_ld16(tmem + lane_base + db * 128 + eslot * 32 + pass * 16, re);
+        tmem_ld16(tmem + lane_base + db * 128 + 64 + eslot * 32 + pass * 16, im);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        if (pass == 1) {
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) {  // D[db] is in registers: free it
+            if constexpr (PAIR) mbar_arrive_cluster(dempty + db, 0);
+            else mbar_arrive(dempty + db);
+          }
+        }
+        const float2* E = etab + (eslot * 32 + pass * 16) * 32 + lane;
+        const float* wp = wt + pass * 16 * 2 * G;
+#pragma unroll
+        for (int jj = 0; jj < 16; ++jj) {
+          const float2 ej = E[jj * 32];
+          const float kr = __uint_as_float(re[jj]), ki = __uint_as_float(im[jj]);
+          const float zx = ej.x * kr - ej.y * ki;
+          const float zy = ej.x * ki + ej.y * kr;
+          if constexpr (G == 4) {
+            const float4 w01 = reinterpret_cast<const float4*>(wp)[jj * 2];
+            const float4 w23 = reinterpret_cast<const float4*>(wp)[jj * 2 + 1];
+            acc01 = ffma2(make_float2(w01.x, w01.y), zx, acc01);
+            acc01 = ffma2(make_float2(w01.z, w01.w), zy, acc01);
+            acc23 = ffma2(make_float2(w23.x, w23.y), zx, acc23);
+            acc23 = ffma2(make_float2(w23.z, w23.w), zy, acc23);
+          } else {
+            const float2 w = reinterpret_cast<const float2*>(wp)[jj];
+            acc1 = fmaf(w.x, zx, acc1);
+            acc1 = fmaf(w.y, zy, acc1);
+          }
+        }
+      }
+      if constexpr (G == 4)
+        reinterpret_cast<float4*>(rb)[eslot * 32 + lane] = make_float4(acc01.x, acc01.y, acc23.x, acc23.y);
+      else
+        rb[eslot * 32 + lane] = acc1;
+      asm volatile("bar.sync %0, 64;" ::"r"(1 + quarter) : "memory");
+      // warp e2 writes heads 2 e2, 2 e2 + 1 (G = 4) / e2 = 0 the head (G = 1)
+      {
+        const int tok = 32 * quarter + lane;
+        if (tok < it.valid()) {
+#pragma unroll
+          for (int hq = 0; hq < (G == 4 ? 2 : 1); ++hq) {
+            const int h = (G == 4) ? 2 * eslot + hq : 0;
+            if (G == 1 && eslot != 0) break;
+            const float v = rb[(0 * 32 + lane) * G + h] + rb[(1 * 32 + lane) * G + h];
+            a.ps[(((size_t)it.s * a.js + it.part) * a.n + it.base() + tok) * G + h] = v;
+          }
+        }
+      }
+      if (TRK(k)) SPTR(1024 + warp * 16 + 12 + (k - kTrK0));
+      continue;
+      }
       uint32_t re[16], im[16];
       tmem_ld16(tmem + lane_base + db * 128 + eslot * 16, re);
       tmem_ld16(tmem + lane_base + db * 128 + 64 + eslot * 16, im);
@@ -537,11 +563,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_sp_score(SpArgs a) {
         float2 acc01 = make_float2(0.f, 0.f), acc23 = make_float2(0.f, 0.f);
 #pragma unroll
         for (int jj = 0; jj < 16; ++jj) {
-#ifdef SP_R2_EREG
-          const float2 ej = ereg[jj];
-#else
           const float2 ej = E[jj * 32];
-#endif
           const float kr = __uint_as_float(re[jj]), ki = __uint_as_float(im[jj]);
           const float zx = ej.x * kr - ej.y * ki;
           const float zy = ej.x * ki + ej.y * kr;
@@ -613,16 +635,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_sp_score(SpArgs a) {
       // this warp's rounds r = sub, sub + 2, ...: their 12-bit (a, b) fields
       // packed back to back into (pk0, pk1)
       uint64_t pk0 = 0, pk1 = 0;
-#ifdef SP_R2_GROT
       // rounds by GLOBAL round index: this warp takes g = gbase + r with
-      // g % 2 == sub, so its rounds are exactly 2 apart across tiles too
-      const int rfirst = (int)((uint32_t)(sub + 2 - (int)(gbase & 1u)) & 1u);
-#else
-      const int rfirst = sub;
-#endif
+      // g % kProdPerQ == sub, so its rounds are evenly spaced across tiles
+      const int rfirst = (int)((uint32_t)(sub + kProdPerQ - (int)(gbase % kProdPerQ)) % kProdPerQ);
 #pragma unroll
       for (int r = 0, i = 0; r < R; ++r) {
-        if ((r & 1) != rfirst) continue;
+        if ((r % kProdPerQ) != rfirst) continue;
         const int b0 = 12 * r, wi = b0 >> 6, sh = b0 & 63;
         const uint64_t f = ((w[wi] >> sh) | (sh > 52 ? w[wi + 1] << (64 - sh) : 0ull)) & 0xFFFull;
         if (i < 5) pk0 |= f << (12 * i);
@@ -630,7 +648,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_sp_score(SpArgs a) {
         ++i;
       }
 #pragma unroll 1
-      for (int r = rfirst; r < it.nr; r += 2) {
+      for (int r = rfirst; r < it.nr; r += kProdPerQ) {
         const uint32_t fld = (uint32_t)pk0 & 0xFFFu;
         pk0 = (pk0 >> 12) | (pk1 << 48);
         pk1 >>= 12;
@@ -665,6 +683,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_sp_score(SpArgs a) {
         asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
         tc_fence_before();
         __syncwarp();
+        // hardware named barrier per stage (ids 5..10): one warp per lane
+        // quarter arrives, the MMA warp syncs -- no shared-memory round trip
+        // on the issuer's critical path
+        if constexpr (!PAIR) {
+          asm volatile("bar.arrive %0, 160;" ::"r"(kBarStage0 + (int)st) : "memory");
+        } else
         if (lane == 0) {  // (PAIR: the leader's barrier counts both CTAs' rows)
           if constexpr (PAIR) mbar_arrive_cluster(afull + st, 0);
           else mbar_arrive(afull + st);
@@ -679,7 +703,72 @@ __global__ void __launch_bounds__(kThreads, 1) k_sp_score(SpArgs a) {
       it = nx;
       ok = okn;
     }
-  } else if (warp == kMmaWarp) {
+  }
+  else if (!PAIR && warp >= kMmaWarp) {
+    // ============ two issuer warps: warp kMmaWarp + w issues the rounds
+    // with global round index g = w (mod 2), so one warp's wait for its
+    // next stage overlaps the other's MMAs.  The round-0 issuer of a tile
+    // zeroes D (accumulate = 0) and releases the other warp through named
+    // barrier 11 + db; both commit dfull (count 2) and cbempty (count 2);
+    // warp kMmaWarp reloads the codebook, releasing the other through
+    // barrier 13.
+    constexpr uint32_t idesc = (1u << 2) | (1u << 4) | ((64u >> 3) << 17) | (8u << 24);
+    const int me = warp - kMmaWarp;
+    const uint64_t bdesc0 = sdesc(su32(cbs), 2048, 128);
+    SpIter<PAIR> it;
+    uint32_t nload = 0, gbase = 0;
+    int k = 0, prev_slot = -1;
+    for (bool ok = it.first(a); ok; ok = it.next(a), ++k) {
+      const int db = k & 1;
+      if (it.item_start) {
+        const int slot = (it.s % a.n_slots) * a.js + it.part;
+        if (slot != prev_slot) {
+          if (nload > 0) {
+            tc_commit_elect(cbempty);  // every MMA of this warp reading the old codebook
+            if (me == 0) mbar_wait(cbempty, (nload - 1) & 1);
+          }
+          if (me == 0) {
+            if (elect_one()) {
+              const uint16_t* src = a.cb + (size_t)(it.s % a.n_slots) * a.slot_elems +
+                                    (size_t)it.r0 * (kRoundBytes / 2);
+              mbar_arrive_tx(cbfull, (uint32_t)it.nr * kRoundBytes);
+              for (int r = 0; r < it.nr; ++r)
+                bulk_g2s(cbs + r * kRoundBytes, src + (size_t)r * (kRoundBytes / 2), kRoundBytes,
+                         cbfull);
+            }
+            __syncwarp();
+            mbar_wait(cbfull, nload & 1);
+            asm volatile("bar.arrive %0, 64;" ::"r"(kBarCodebook) : "memory");
+          } else {
+            asm volatile("bar.sync %0, 64;" ::"r"(kBarCodebook) : "memory");
+          }
+          ++nload;
+          prev_slot = slot;
+        }
+      }
+      const int w0 = (int)(gbase & 1u);  // issuer of round 0 of this tile
+      const uint32_t dcol = tmem + (uint32_t)db * 128u;
+      if (me == w0 && k >= 2) {  // D buffer db was read by the epilogue of tile k-2
+        mbar_wait(dempty + db, ((k - 2) >> 1) & 1);
+        tc_fence_after();
+      }
+#pragma unroll 1
+      for (int r = (me == w0) ? 0 : 1; r < it.nr; r += 2) {
+        const uint32_t g = gbase + (uint32_t)r, st = g % kAStages;
+        if (r == 1) asm volatile("bar.sync %0, 64;" ::"r"(kBarZero0 + db) : "memory");  // D zeroed
+        asm volatile("bar.sync %0, 160;" ::"r"(kBarStage0 + (int)st) : "memory");  // stage full
+        tc_fence_after();
+        sp_issue_round(dcol, tmem + kACol0 + 32 * st, tmem + kMetaCol0 + 4 * st,
+                                      bdesc0 + (uint64_t)((r * kRoundBytes) >> 4), idesc,
+                                      r > 0 ? 1u : 0u, aempty + st);
+        if (r == 0) asm volatile("bar.arrive %0, 64;" ::"r"(kBarZero0 + db) : "memory");
+      }
+      tc_commit_elect(dfull + db);
+      gbase += (uint32_t)it.nr;
+    }
+  }
+  else if (PAIR && warp == kMmaWarp) {
+    // ============ CTA-pair issuer (cta_group::2, leader CTA issues) ======
     // ============ tcgen05.mma.sp issuer (warp-uniform walk, elected lane) ==
     // f16 x f16 -> f32, sparse A from TMEM, B K-major in smem; M128 N64
     constexpr uint32_t idesc = (1u << 2) | (1u << 4) | ((64u >> 3) << 17) | (8u << 24);
@@ -786,130 +875,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_sp_score(SpArgs a) {
         if (elect_one()) tc_commit_pair(dfull + db);
         __syncwarp();
         if (TRK(k)) SPTR(144 + (k - kTrK0));
-        continue;
       }
-      if (TRK(k)) SPTR(128 + (k - kTrK0));
-      if (k >= 2) {  // D buffer db was read by the epilogue of tile k-2
-        mbar_wait_iss(dempty + db, ((k - 2) >> 1) & 1);
-        tc_fence_after();
-      }
-      if (TRK(k)) SPTR(136 + (k - kTrK0));
-      const uint32_t dcol = tmem + (uint32_t)db * 128u;
-#ifdef SP_R2_PRED
-#ifndef SP_R2_WS
-#define SP_R2_WS false
-#endif
-      uint64_t br = bdesc0;
-#ifdef SP_R2_PAIRWAIT
-#pragma unroll 1
-      for (int r = 0; r < it.nr; r += 2) {
-        const bool two = r + 1 < it.nr;
-        uint32_t st1 = gst + 1, ph1 = gph;
-        if (st1 == kAStages) {
-          st1 = 0;
-          ph1 ^= 1u;
-        }
-        mbar_wait(afull + gst, gph);
-        if (two) mbar_wait(afull + st1, ph1);
-        tc_fence_after();
-        sp_issue_round<SP_R2_WS>(dcol, tmem + kACol0 + 32 * gst, tmem + kMetaCol0 + 4 * gst, br, idesc,
-                                 r > 0 ? 1u : 0u, aempty + gst);
-        if (two)
-          sp_issue_round<SP_R2_WS>(dcol, tmem + kACol0 + 32 * st1, tmem + kMetaCol0 + 4 * st1,
-                                   br + (uint64_t)(kRoundBytes >> 4), idesc, 1u, aempty + st1);
-        br += (uint64_t)((2 * kRoundBytes) >> 4);
-        gst = two ? st1 + 1 : st1;
-        gph = ph1;
-        if (gst == kAStages) {
-          gst = 0;
-          gph ^= 1u;
-        }
-      }
-#else
-      // one round per issue block: wait its stage, fence, 8 predicated MMAs
-      // and the stage's commit (sp_issue_round)
-#pragma unroll 1
-      for (int r = 0; r < it.nr; ++r) {
-        if (TRK(k)) SPTR(0 + (k - kTrK0) * 16 + r);
-        mbar_wait_iss(afull + gst, gph);
-        if (TRK(k)) SPTR(64 + (k - kTrK0) * 16 + r);
-        tc_fence_after();
-        sp_issue_round<SP_R2_WS>(dcol, tmem + kACol0 + 32 * gst, tmem + kMetaCol0 + 4 * gst, br, idesc,
-                                 r > 0 ? 1u : 0u, aempty + gst);
-        br += (uint64_t)(kRoundBytes >> 4);
-        if (++gst == kAStages) {
-          gst = 0;
-          gph ^= 1u;
-        }
-      }
-#endif
-      tc_commit_elect(dfull + db);
-      if (TRK(k)) SPTR(144 + (k - kTrK0));
     }
   }
   tc_fence_before();
-#else
-      // rounds in pairs: one elected issue region of 16 MMAs (2 rounds x 2
-      // sides x 2 K-halves x Re/Im) per pair, so the per-region overhead
-      // (barrier waits, elect, reconvergence) is paid every 16 MMAs; each
-      // round's stage is released by its own commit
-      uint64_t br = bdesc0;
-#pragma unroll 1
-      for (int r = 0; r < it.nr; r += 2) {
-        const bool two = r + 1 < it.nr;
-        const uint32_t st0 = gst, ph0 = gph;
-        uint32_t st1 = gst + 1, ph1 = gph;
-        if (st1 == kAStages) {
-          st1 = 0;
-          ph1 ^= 1u;
-        }
-        if (TRK(k)) SPTR(0 + (k - kTrK0) * 16 + r);
-        mbar_wait_iss(afull + st0, ph0);
-        if (TRK(k)) SPTR(64 + (k - kTrK0) * 16 + r);
-        if (two) mbar_wait_iss(afull + st1, ph1);
-        if (TRK(k) && two) SPTR(64 + (k - kTrK0) * 16 + r + 1);
-        tc_fence_after();
-        if (elect_one()) {
-#pragma unroll
-          for (int u = 0; u < 2; ++u) {
-            if (u == 1 && !two) break;
-            const uint32_t st = u ? st1 : st0;
-#pragma unroll
-            for (int s = 0; s < 2; ++s) {
-              const uint32_t a_tm = tmem + kACol0 + 32 * st + 16 * s;
-              const uint32_t e_tm = tmem + kMetaCol0 + 4 * st + 2 * s;
-#pragma unroll
-              for (int h = 0; h < 2; ++h) {
-#pragma unroll
-                for (int blk = 0; blk < 2; ++blk) {
-                  // side a: Re += X, Im += Y;  side b: Re -= Y, Im += X
-                  const int rows = s ? (blk ? 0 : 64) : (blk ? 64 : 0);
-                  const uint64_t bd =
-                      br + (uint64_t)((u * kRoundBytes + h * 4 * 2048 + rows * 16) >> 4);
-                  umma_sp_ts(dcol + blk * 64, a_tm + h * 8, bd,
-                             idesc | ((s && !blk) ? kNegA : 0u),
-                             (u > 0 || s > 0 || h > 0 || r > 0) ? 1u : 0u, e_tm);
-                }
-              }
-            }
-            tc_commit(aempty + st);
-          }
-        }
-        __syncwarp();
-        br += (uint64_t)((2 * kRoundBytes) >> 4);
-        gst += two ? 2u : 1u;  // the stages of the rounds just issued
-        if (gst >= kAStages) {
-          gst -= kAStages;
-          gph ^= 1u;
-        }
-      }
-      if (elect_one()) tc_commit(dfull + db);
-      __syncwarp();
-      if (TRK(k)) SPTR(144 + (k - kTrK0));
-    }
-  }
-  tc_fence_before();
-#endif
   if constexpr (PAIR) cluster_sync_all();  // the leader's MMAs into this CTA's TMEM are done
   else __syncthreads();
   tc_fence_after();
@@ -924,7 +893,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_sp_score(SpArgs a) {
 }
 
 size_t sp_smem(int G, int R) {
-  return (size_t)R * kRoundBytes + 64 * 32 * 8 + (size_t)kEpiWarps * 16 * 2 * G * 4 +
+  return (size_t)R * kRoundBytes + 64 * 32 * 8 + (size_t)kEpiWarps * kSubsPerEpi * 2 * G * 4 +
          (size_t)2 * 16 * 32 * G * 4 + (2 * kAStages + 7) * 8 + 16;
 }
 
