@@ -79,6 +79,17 @@ constexpr int kTrK0 = 20;
 #define SPTR(idx) do {} while (0)
 #define TRK(k) false
 #endif
+#ifdef CVQ_DEVICE_CHECKS
+// Debug build (CVQ_NVCC_EXTRA=-DCVQ_DEVICE_CHECKS): the stage / D-buffer
+// protocol is checked with sequence tags in shared memory and every global
+// access is bounds-checked; a violation traps (the launch fails with
+// cudaErrorLaunchFailure).  Stands in for compute-sanitizer racecheck, which
+// this GPU pool does not offer.
+#define SP_CHECK(cond) \
+  do { if (!(cond)) asm volatile("trap;"); } while (0)
+#else
+#define SP_CHECK(cond) do {} while (0)
+#endif
 constexpr int kTok = 128;                 // tokens per tile (MMA M)
 constexpr int kEpiWarps = 8;              // warp (quarter, e2): subspaces [32 e2, +32) in 2 passes
 constexpr int kProdWarps = 16;            // 4 per lane quarter, global rounds g = sub (mod 4)
@@ -297,6 +308,7 @@ struct SpArgs {
   int rtot;              // rounds of the preset (11, 21)
   int js;                // round parts of <= RP rounds (scores are linear in K)
   float* ps;             // [S][js][n][G] partial scores
+  size_t ps_elems;       // its extent (device bounds checks)
 };
 
 // This CTA's tiles in order; each CTA owns a contiguous range of work items
@@ -368,6 +380,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_sp_score(SpArgs a) {
   uint64_t* cbempty = cbfull + 1;
   uint64_t* cbpeer = cbempty + 1;  // PAIR: the second CTA's codebook half is in
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(cbpeer + 1);
+  // protocol tags (CVQ_DEVICE_CHECKS): producers' round per (stage, quarter),
+  // the issued round per stage, the tile per D buffer
+  uint32_t* stag = tmem_slot + 4;       // [kAStages][4]
+  uint32_t* itag = stag + 4 * kAStages;  // [kAStages]
+  uint32_t* dtag = itag + kAStages;      // [2]
   const uint32_t rank = PAIR ? cluster_rank() : 0u;
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -394,6 +411,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_sp_score(SpArgs a) {
       mbar_init(dfull + i, PAIR ? 1 : kIssuers);
       mbar_init(dempty + i, PAIR ? 2 * kEpiWarps : kEpiWarps);
     }
+    for (int i = 0; i < 5 * kAStages + 2; ++i) stag[i] = 0xFFFFFFFFu;
     mbar_init(cbfull, 1);
     mbar_init(cbempty, PAIR ? 1 : kIssuers);
     mbar_init(cbpeer, 1);
@@ -414,12 +432,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_sp_score(SpArgs a) {
 
   if (warp < kEpiWarps) {
     // ============ epilogue: lane = token 32 quarter + lane of the tile,
-    // warp slot e = subspaces [16 e, 16 e + 16) ==========================
+    // warp slot e2 = subspaces [32 e2, 32 e2 + 32) in two passes =========
     const int quarter = warp & 3, eslot = warp >> 2;
     const uint32_t lane_base = (uint32_t)(quarter * 32) << 16;
     // lane keeps the phase of subspace 32 e2 + lane and produces w for all
     // 4 heads (G = 4) or the one head (G = 1)
-    const int jl = eslot * 32 + lane, hh = 0;
+    const int jl = eslot * 32 + lane;
     const double theta = a.thetas[jl];
     float2 step;
     {
@@ -430,10 +448,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_sp_score(SpArgs a) {
     float* wt = wtab + warp * (kSubsPerEpi * 2 * G);
     const float sc = 0.08838834764831845f;  // 1 / sqrt(128)
     float2 ph = make_float2(1.f, 0.f);
-    constexpr int kQv = G;  // heads per lane
-    float2 qv[kQv];
+    float2 qv[G];  // this lane's subspace of every head's query, / sqrt(d)
 #pragma unroll
-    for (int u = 0; u < kQv; ++u) qv[u] = make_float2(0.f, 0.f);
+    for (int u = 0; u < G; ++u) qv[u] = make_float2(0.f, 0.f);
     SpIter<PAIR> it;
     int k = 0;
     for (bool ok = it.first(a); ok; ok = it.next(a), ++k) {
@@ -442,10 +459,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_sp_score(SpArgs a) {
         ph = phase_neg(a.t - (a.pos0 + it.base() + 32 * quarter), theta);
         const float* qs = a.q + (size_t)it.s * G * 128;
 #pragma unroll
-        for (int u = 0; u < kQv; ++u) {
-          const int h = u;
-          qv[u] = make_float2(__ldg(qs + h * 128 + 2 * jl) * sc, __ldg(qs + h * 128 + 2 * jl + 1) * sc);
-        }
+        for (int h = 0; h < G; ++h)
+          qv[h] = make_float2(__ldg(qs + h * 128 + 2 * jl) * sc, __ldg(qs + h * 128 + 2 * jl + 1) * sc);
       } else {
         ph = make_float2(ph.x * step.x - ph.y * step.y, ph.x * step.y + ph.y * step.x);
       }
@@ -464,25 +479,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_sp_score(SpArgs a) {
           reinterpret_cast<float2*>(wt)[lane] = make_float2(o[0], o[1]);
         }
       }
-      if (false) {
-        float o[4];
-#pragma unroll
-        for (int u = 0; u < 2; ++u) {
-          const float wx = qv[u].x * ph.x + qv[u].y * ph.y;
-          const float wy = qv[u].x * ph.y - qv[u].y * ph.x;
-          o[u] = wx;
-          o[2 + u] = -wy;
-        }
-        if constexpr (G == 4) {
-          // [jj][half]: (wx_h0, wx_h1, -wy_h0, -wy_h1)
-          reinterpret_cast<float4*>(wt)[(lane & 15) * 2 + hh] = make_float4(o[0], o[1], o[2], o[3]);
-        } else {
-          reinterpret_cast<float2*>(wt)[lane & 15] = make_float2(o[0], o[2]);
-        }
-      }
       __syncwarp();
       if (TRK(k)) SPTR(1024 + warp * 16 + 0 + (k - kTrK0));
       mbar_wait_sleep(dfull + db, (k >> 1) & 1);
+      if (!PAIR) SP_CHECK(*(volatile uint32_t*)(dtag + db) == (uint32_t)k);
       if (TRK(k)) SPTR(1024 + warp * 16 + 4 + (k - kTrK0));
       tc_fence_after();
       {
@@ -539,69 +539,21 @@ __global__ void __launch_bounds__(kThreads, 1) k_sp_score(SpArgs a) {
             const int h = (G == 4) ? 2 * eslot + hq : 0;
             if (G == 1 && eslot != 0) break;
             const float v = rb[(0 * 32 + lane) * G + h] + rb[(1 * 32 + lane) * G + h];
-            a.ps[(((size_t)it.s * a.js + it.part) * a.n + it.base() + tok) * G + h] = v;
+            const size_t pi = (((size_t)it.s * a.js + it.part) * a.n + it.base() + tok) * G + h;
+            SP_CHECK(pi < a.ps_elems);
+            a.ps[pi] = v;
           }
         }
       }
       if (TRK(k)) SPTR(1024 + warp * 16 + 12 + (k - kTrK0));
-      continue;
       }
-      uint32_t re[16], im[16];
-      tmem_ld16(tmem + lane_base + db * 128 + eslot * 16, re);
-      tmem_ld16(tmem + lane_base + db * 128 + 64 + eslot * 16, im);
-      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) {  // D[db] is in registers: free it
-        if constexpr (PAIR) mbar_arrive_cluster(dempty + db, 0);
-        else mbar_arrive(dempty + db);
-      }
-      if (TRK(k)) SPTR(1024 + warp * 16 + 8 + (k - kTrK0));
-      const float2* E = etab + eslot * 16 * 32 + lane;
-      float* rb = red + (size_t)((db * 4 + quarter) * 4) * 32 * G;  // [e][lane][G]
-      if constexpr (G == 4) {
-        float2 acc01 = make_float2(0.f, 0.f), acc23 = make_float2(0.f, 0.f);
-#pragma unroll
-        for (int jj = 0; jj < 16; ++jj) {
-          const float2 ej = E[jj * 32];
-          const float kr = __uint_as_float(re[jj]), ki = __uint_as_float(im[jj]);
-          const float zx = ej.x * kr - ej.y * ki;
-          const float zy = ej.x * ki + ej.y * kr;
-          const float4 w01 = reinterpret_cast<const float4*>(wt)[jj * 2];
-          const float4 w23 = reinterpret_cast<const float4*>(wt)[jj * 2 + 1];
-          acc01 = ffma2(make_float2(w01.x, w01.y), zx, acc01);
-          acc01 = ffma2(make_float2(w01.z, w01.w), zy, acc01);
-          acc23 = ffma2(make_float2(w23.x, w23.y), zx, acc23);
-          acc23 = ffma2(make_float2(w23.z, w23.w), zy, acc23);
-        }
-        reinterpret_cast<float4*>(rb)[eslot * 32 + lane] = make_float4(acc01.x, acc01.y, acc23.x, acc23.y);
-      } else {
-        float acc = 0.f;
-#pragma unroll
-        for (int jj = 0; jj < 16; ++jj) {
-          const float2 ej = E[jj * 32];
-          const float kr = __uint_as_float(re[jj]), ki = __uint_as_float(im[jj]);
-          const float2 w = reinterpret_cast<const float2*>(wt)[jj];
-          acc = fmaf(w.x, ej.x * kr - ej.y * ki, acc);
-          acc = fmaf(w.y, ej.x * ki + ej.y * kr, acc);
-        }
-        rb[eslot * 32 + lane] = acc;
-      }
-      asm volatile("bar.sync %0, 128;" ::"r"(1 + quarter) : "memory");
-      // warp slot e writes head e (G = 4) / slot 0 writes the head (G = 1)
-      const int tok = 32 * quarter + lane;
-      if (eslot < G && tok < it.valid()) {
-        float v = 0.f;
-#pragma unroll
-        for (int e2 = 0; e2 < 4; ++e2) v += rb[(e2 * 32 + lane) * G + eslot];
-        a.ps[(((size_t)it.s * a.js + it.part) * a.n + it.base() + tok) * G + eslot] = v;
-      }
-      if (TRK(k)) SPTR(1024 + warp * 16 + 12 + (k - kTrK0));
     }
   } else if (warp < kEpiWarps + kProdWarps) {
     // ============ one-hot producers: thread = token 32 quarter + lane; warp
-    // sub = 0 / 1 takes the even / odd rounds (both sides), so two chains of
-    // tcgen05.st -> wait::st per lane quarter run concurrently ===========
+    // sub = 0..3 takes the rounds with global index g = sub (mod 4) (both
+    // sides), so four chains of tcgen05.st -> wait::st per lane quarter run
+    // concurrently; a warp's rounds are 4 apart, fewer than the 6 stages, so
+    // the aempty parity waits stay unambiguous ==========================
     const int p = warp - kEpiWarps, quarter = p & 3, sub = p >> 2;
     const uint32_t lane_base = (uint32_t)(quarter * 32) << 16;
     const int t = quarter * 32 + lane;
@@ -614,6 +566,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_sp_score(SpArgs a) {
       const unsigned long long b0 = (unsigned long long)tok * (12u * a.rtot) + 12u * x.r0;
       off = (uint32_t)(b0 & 63u);
 #pragma unroll
+      SP_CHECK((b0 >> 6) + NW <= a.kstride);
       for (int i = 0; i < NW; ++i) raw[i] = __ldg(kw + (b0 >> 6) + i);
     };
     uint64_t raw[NW], nraw[NW];
@@ -657,6 +610,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_sp_score(SpArgs a) {
         if (use > 0) {
           if (TRK(kk)) SPTR(256 + quarter * 64 + (kk - kTrK0) * 16 + r);
           mbar_wait_sleep(aempty + st, (use - 1) & 1u);  // back off: spinning takes issue slots from the MMA warp
+          if (!PAIR) SP_CHECK(*(volatile uint32_t*)(itag + st) == g - kAStages);
           if (TRK(kk)) SPTR(512 + quarter * 64 + (kk - kTrK0) * 16 + r);
           tc_fence_after();
         }
@@ -687,6 +641,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_sp_score(SpArgs a) {
         // quarter arrives, the MMA warp syncs -- no shared-memory round trip
         // on the issuer's critical path
         if constexpr (!PAIR) {
+#ifdef CVQ_DEVICE_CHECKS
+          if (lane == 0) *(volatile uint32_t*)(stag + st * 4 + quarter) = g;
+#endif
           asm volatile("bar.arrive %0, 160;" ::"r"(kBarStage0 + (int)st) : "memory");
         } else
         if (lane == 0) {  // (PAIR: the leader's barrier counts both CTAs' rows)
@@ -757,6 +714,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_sp_score(SpArgs a) {
         const uint32_t g = gbase + (uint32_t)r, st = g % kAStages;
         if (r == 1) asm volatile("bar.sync %0, 64;" ::"r"(kBarZero0 + db) : "memory");  // D zeroed
         asm volatile("bar.sync %0, 160;" ::"r"(kBarStage0 + (int)st) : "memory");  // stage full
+#ifdef CVQ_DEVICE_CHECKS
+        for (int q2 = 0; q2 < 4; ++q2) SP_CHECK(*(volatile uint32_t*)(stag + st * 4 + q2) == g);
+        if (r == 0 && lane == 0) *(volatile uint32_t*)(dtag + db) = (uint32_t)k;
+        if (lane == 0) *(volatile uint32_t*)(itag + st) = g;
+        __threadfence_block();
+#endif
         tc_fence_after();
         sp_issue_round(dcol, tmem + kACol0 + 32 * st, tmem + kMetaCol0 + 4 * st,
                                       bdesc0 + (uint64_t)((r * kRoundBytes) >> 4), idesc,
@@ -894,7 +857,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_sp_score(SpArgs a) {
 
 size_t sp_smem(int G, int R) {
   return (size_t)R * kRoundBytes + 64 * 32 * 8 + (size_t)kEpiWarps * kSubsPerEpi * 2 * G * 4 +
-         (size_t)2 * 16 * 32 * G * 4 + (2 * kAStages + 7) * 8 + 16;
+         (size_t)2 * 16 * 32 * G * 4 + (2 * kAStages + 7) * 8 + 16 + (5 * kAStages + 2) * 4;
 }
 
 template <int R, int G, bool PAIR>
@@ -1013,6 +976,7 @@ cudaError_t run_sp_score(const AttnJob& job, const uint16_t* cb, size_t slot_ele
   a.js = sp_parts(g.R);
   a.n_items = job.S * a.js * a.cps;
   a.ps = ps;
+  a.ps_elems = (size_t)job.S * sp_parts(g.R) * (size_t)job.n * g.G;
   if (pair) {
     if (g.G == 4) return launch_sp<kRPart, 4, true>(a, st);
     if (g.G == 1) return launch_sp<kRPart, 1, true>(a, st);
