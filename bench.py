@@ -162,6 +162,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"])
     ap.add_argument("--no-prefill", action="store_true")
+    ap.add_argument("--no-naive", action="store_true",
+                    help="skip timing the decode-then-attend baseline on the same cache")
     ap.add_argument("--merge", default="nccl", choices=["nccl", "peer"],
                     help="N>1 shard merge: the C-ABI shard group (one NCCL all-gather of packed "
                          "partials + combine inside libcvq_b200), or peer (experimental): "
@@ -361,6 +363,30 @@ def main():
             "frac_vs_nominal": ach_tf / (TENSOR_NOMINAL_TFLOPS * (2 if sparse else 1)),
             "algorithmic_flops_per_launch": flops}
 
+    # ---- the decode-then-attend baseline on the same cache (Table 4) ----
+    naive = None
+    if world == 1 and not args.no_naive:
+        try:
+            nout = torch.empty_like(q)
+            cache.attention_naive(q, t_q, nout)  # warm (scratch)
+            torch.cuda.synchronize()
+            ne0, ne1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            ne0.record(stream)
+            for _ in range(3):
+                cache.attention_naive(q, t_q, nout)
+            ne1.record(stream)
+            torch.cuda.synchronize()
+            naive_ms = ne0.elapsed_time(ne1) / 3
+            naive = {"ms_per_step": naive_ms, "value": kv_tokens / (naive_ms / 1e3),
+                     "unit": "KV-tokens/s", "naive_over_fused": naive_ms / ms,
+                     "rel_diff_vs_fused": float(((nout - out).norm() / out.norm()).item()),
+                     "path": "cvq_cache_attention_naive: dense fp16 dequantisation of every key "
+                             "(RoPE) and value (tensor-core bits x C_V) + flash-decoding",
+                     "paper_table4": "naive/optimized 6.0x @8K, 8.4x @32K, 9.6x @128K "
+                                     "(PAPER.md:464-466, other hardware)"}
+        except Exception as ex:  # e.g. scratch too large for the device
+            naive = {"unavailable": str(ex)[:200]}
+
     # ---- e2e through the C-ABI with host buffers (decode_step) ----
     e2e = None
     if not args.no_e2e and world > 1 and group is not None:
@@ -428,7 +454,9 @@ def main():
     if not args.no_prefill and world == 1:
         del cache
         torch.cuda.empty_cache()
-        n_pre, S_pre = 1024, layers * H  # one sequence: every (layer, kv head) stream
+        # one sequence, every (layer, kv head) stream; >= 16K tokens so the
+        # projection to C4 (128K x 32 layers x 8 heads) rests on a real run
+        n_pre, S_pre = 16384 + 128, layers * H
         pc = G.QuantizedKVCache(kq, nc, n_seqs=1, n_layers=layers, n_kv_heads=H, q_per_kv=Gq,
                                 capacity=2 * n_pre, hidden=2 * nc, ctx=ctx, keys=args.keys)
         rs2 = np.random.default_rng(77)
@@ -452,7 +480,7 @@ def main():
         th = S_pre * (n_pre - 128) / (p_ms / 1e3)  # token-heads/s
         prefill = {"token_heads_per_s": th, "kv_tokens_per_s": th / H, "unit": "KV-tokens/s",
                    "sample": f"{n_pre - 128} tokens x {S_pre} streams, fp32 K/V on device",
-                   "c4_projected_s": 131072 * layers * H / th,
+                   "c4_projected_s": 131072 * 32 * 8 / th,  # configs[3]: 128K x 32 layers x 8 heads
                    "encoders": "bit-exact fp64 key search + value MLP, device packing"}
         del pc
 
@@ -486,6 +514,7 @@ def main():
                        "l2": "inputs (packed cache) larger than L2"},
             "kv_head_tokens_per_s": value * H, "roofline": roof, "clocks": clk_sum,
             "gpu_launches": launches, "e2e": e2e, "cpu_baseline": cpu, "prefill": prefill,
+            "naive": naive,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -334,6 +334,14 @@ CVQ_API cvq_status cvq_cache_append(cvq_cache* c, const void* k, const void* v,
 CVQ_API cvq_status cvq_cache_attention(cvq_cache* c, const float* q,
                                        uint64_t t, float* out, int where);
 
+/* naive_quantized_attention (attn.cpp:130-162) for every row: decode-then-
+ * attend -- the whole cache dequantised to dense fp16 K (RoPE applied) and V
+ * (512 B per token and stream at d = 128), then dense flash-decoding over
+ * it.  The baseline the fused path is measured against (Table 4);
+ * scratch grows to S x N x d x 4 bytes. */
+CVQ_API cvq_status cvq_cache_attention_naive(cvq_cache* c, const float* q, uint64_t t,
+                                             float* out, int where);
+
 /* Split-K partial for context sharding: per row (seq, layer, q head) the
  * running max m, sum l and normalised o[d] over this cache's tokens
  * (device buffers). */

@@ -630,6 +630,19 @@ class QuantizedKVCache:
             _check(_lib.cvq_cache_attention(self.h, qp, _u64(t), op, _i(where)))
         return out
 
+    def attention_naive(self, q, t=None, out=None):
+        """Decode-then-attend (attn.cpp:130-162) over the same cache: dense
+        fp16 dequantisation of every key / value, then dense attention."""
+        if t is None:
+            t = self.position_offset + self.size() - 1
+        qp, where, qk = _buf(q, np.float32)
+        if out is None:
+            out = np.zeros(qk.shape, np.float32) if where == CVQ_HOST else qk.new_empty(qk.shape)
+        op, _, ok = _buf(out)
+        with _TorchOrder(self.ctx, qk, ok):
+            _check(_lib.cvq_cache_attention_naive(self.h, qp, _u64(t), op, _i(where)))
+        return out
+
     def attention_partial(self, q, m, l, o, t):
         """Device tensors: m, l [rows], o [rows][d] (split-K partial)."""
         with _TorchOrder(self.ctx, q, m, l, o):

@@ -270,84 +270,6 @@ cudaError_t run_lse_combine(const float* m, const float* l, const float* o,
 }
 
 
-// ------------------------------------------------------------------ naive
-// Decode-then-attend (naive_quantized_attention, attn.cpp:130-162): every
-// key is reconstructed densely and rotated to its own position, q to t,
-// then softmax(q K^T / sqrt(d)) V with V reconstructed by the dense
-// code x codebook product (attn.cpp:146-154).  Single stream, G = 1.
-__global__ void k_naive_scores(Geom g, const uint64_t* __restrict__ kw,
-                               const float2* __restrict__ cb, const float* __restrict__ q,
-                               const double* __restrict__ thetas, long long t, long long pos0,
-                               long long n, float* __restrict__ scores) {
-  long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const unsigned long long f0 = (unsigned long long)i * g.fpt;
-  float acc = 0.f;
-  for (int j = 0; j < g.subs; ++j) {
-    const int grp = j / g.g;
-    float kx = 0.f, ky = 0.f;
-    for (int r = 0; r < g.R; ++r) {
-      unsigned long long f = f0 + (unsigned long long)(r * g.groups + grp) * 2;
-      unsigned a = read_field(kw, f * g.lb, g.lb);
-      unsigned b = read_field(kw, (f + 1) * g.lb, g.lb);
-      float2 ua = __ldg(cb + ((size_t)r * g.L + a) * g.subs + j);
-      float2 ub = __ldg(cb + ((size_t)r * g.L + b) * g.subs + j);
-      kx += ua.x - ub.y;
-      ky += ua.y + ub.x;
-    }
-    const float2 pk = phase_neg(-(pos0 + i), thetas[j]);  // e^{+i pos theta}
-    const float2 pq = phase_neg(-t, thetas[j]);
-    const float rkx = kx * pk.x - ky * pk.y, rky = kx * pk.y + ky * pk.x;
-    const float qx = q[2 * j], qy = q[2 * j + 1];
-    const float rqx = qx * pq.x - qy * pq.y, rqy = qx * pq.y + qy * pq.x;
-    acc += rqx * rkx + rqy * rky;
-  }
-  scores[i] = acc * rsqrtf((float)g.d);
-}
-
-__global__ void k_naive_values(Geom g, const uint64_t* __restrict__ vw,
-                               const float* __restrict__ cbv, const float* __restrict__ scores,
-                               long long n, float* __restrict__ out) {
-  __shared__ float red[33];
-  float mx = -FLT_MAX;
-  for (long long i = threadIdx.x; i < n; i += blockDim.x) mx = fmaxf(mx, scores[i]);
-  mx = block_reduce(mx, true, red);
-  float l = 0.f;
-  for (long long i = threadIdx.x; i < n; i += blockDim.x) l += expf(scores[i] - mx);
-  l = block_reduce(l, false, red);
-  for (int j = threadIdx.x; j < g.d; j += blockDim.x) {
-    float acc = 0.f;
-    for (long long i = 0; i < n; ++i) {
-      const float p = expf(scores[i] - mx) / l;
-      float v = 0.f;
-      for (int k = 0; k < g.n_codes; ++k) {
-        const unsigned long long bit = (unsigned long long)i * g.n_codes + k;
-        const float on = (float)((__ldg(vw + (bit >> 6)) >> (bit & 63)) & 1ull);
-        v += on * __ldg(cbv + (size_t)k * g.d + j);
-      }
-      acc += p * v;
-    }
-    out[j] = acc;
-  }
-}
-
-size_t naive_scratch_bytes(const AttnJob& job) { return (size_t)job.n * sizeof(float) + 256; }
-
-cudaError_t run_naive_attention(const AttnJob& job, const float* q, float* out, void* scratch,
-                                size_t scratch_bytes, cudaStream_t st) {
-  if (scratch_bytes < naive_scratch_bytes(job) || job.S != 1 || job.geo.G != 1)
-    return cudaErrorInvalidValue;
-  float* scores = static_cast<float*>(scratch);
-  k_naive_scores<<<(unsigned)((job.n + 127) / 128), 128, 0, st>>>(
-      job.geo, job.kpool, job.cb_key, q, job.thetas, job.t, job.pos0, job.n, scores);
-  count_launch();
-  cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) return e;
-  k_naive_values<<<1, 128, 0, st>>>(job.geo, job.vpool, job.cb_val, scores, job.n, out);
-  count_launch();
-  return cudaGetLastError();
-}
-
 // ------------------------------------------------------------- dispatcher
 bool fast_path_applies(const AttnJob& job);
 size_t fast_scratch_bytes(const AttnJob& job, int* n_chunks);
@@ -356,7 +278,7 @@ cudaError_t run_attention_fast(const AttnJob& job, const float* q, float* pm,
                                cudaStream_t st, cudaEvent_t* prof, float* scores_out);
 cudaError_t run_fast_combine(const AttnJob& job, const float* pm, const float* pl,
                              const float* pz, int n_parts, float* out, float* m_out,
-                             float* l_out, cudaStream_t st);
+                             float* l_out, float* zm, cudaStream_t st);
 
 static int generic_chunk(const AttnJob& job) {
   long long want = (job.n * (long long)job.S + 591) / 592;  // >= ~4 CTAs/SM
@@ -374,7 +296,9 @@ size_t attn_scratch_bytes(const AttnJob& job, int* n_chunks_out) {
     size_t extra = fast_scratch_bytes(job, &nc);
     if (n_chunks_out) *n_chunks_out = nc;
     // partials (m, l, z[n_codes]) per chunk and row
-    return extra + (size_t)nc * rows * (2 + std::max(g.d, g.n_codes)) * sizeof(float) + 256;
+    // + the merged z of every row and its (M, L) for k_combine_project
+    return extra + (size_t)nc * rows * (2 + std::max(g.d, g.n_codes)) * sizeof(float) +
+           (size_t)rows * (g.n_codes + 2) * sizeof(float) + 512;
   }
   const int CH = generic_chunk(job);
   const int nc = (int)((job.n + CH - 1) / CH);
@@ -396,12 +320,14 @@ cudaError_t run_attention(const AttnJob& job, const float* q, float* out,
   float* pm;
   float* pl;
   float* po;
+  float* zm = nullptr;  // merged z rows (fast path)
   cudaError_t e;
   if (fast) {
     size_t extra = fast_scratch_bytes(job, &nc);
     pm = reinterpret_cast<float*>(p + extra);
     pl = pm + (size_t)nc * rows;
     po = pl + (size_t)nc * rows;
+    zm = po + (size_t)nc * rows * std::max(g.d, g.n_codes);
     e = run_attention_fast(job, q, pm, pl, po, &nc, p, st, prof, scores_out);
     if (e != cudaSuccess) return e;
   } else {
@@ -436,12 +362,12 @@ cudaError_t run_attention(const AttnJob& job, const float* q, float* out,
   float* lo = l;
   if (fast) {  // partials hold unnormalised z: merge, then the codebook product
     if (out) {
-      e = run_fast_combine(job, pm, pl, po, nc, out, mo, lo, st);
+      e = run_fast_combine(job, pm, pl, po, nc, out, mo, lo, zm, st);
       if (e != cudaSuccess) return e;
       if (o) e = cudaMemcpyAsync(o, out, (size_t)rows * g.d * sizeof(float), cudaMemcpyDeviceToDevice, st);
       return e;
     }
-    if (o) return run_fast_combine(job, pm, pl, po, nc, o, mo, lo, st);
+    if (o) return run_fast_combine(job, pm, pl, po, nc, o, mo, lo, zm, st);
     return cudaSuccess;
   }
   if (out) {

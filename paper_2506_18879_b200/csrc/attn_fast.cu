@@ -17,7 +17,8 @@
 //     scores, softmax statistics of the chunk, z[k][h] += p_h(i) bit_k(i)
 //     from cp.async-staged value words (attn.cpp:239-247).  Writes the chunk
 //     partial (m, l, z), unnormalised.
-//  k_combine_project  one CTA per (stream, q head) row: LSE merge of the
+//  k_combine_merge / k_combine_project  (row, 32-code slice) CTAs merge the
+//                     chunk partials; then one CTA per row: LSE merge of the
 //     chunk partials, then o = z . C_V / L (attn.cpp:249-255) once per row.
 #include <algorithm>
 #include <cfloat>
@@ -872,37 +873,75 @@ cudaError_t launch_f2_js(const FastArgs& a, int JS, size_t sm, cudaStream_t st) 
 // Merge of the chunk partials (m_p, l_p, z_p) of one row (flash-decoding
 // LSE merge; the reference softmax is global, linalg.cpp:63-75), then the
 // value codebook product o = z . C_V / L once per row (attn.cpp:249-256).
+// LSE merge of the chunk partials of every row, parallel over (row, 32-code
+// slice): grid (rows, NC / 32), 8 warps; warp w takes the parts p = w (mod
+// 8), lane = code -> coalesced 128-B rows of z.  Writes the merged,
+// unnormalised z[row][NC] and (M, L) per row.  (One CTA per row serialised
+// over the parts took 0.5 ms at C5: 32 rows x 128 chunks.)
 template <int NC>
-__global__ void __launch_bounds__(128) k_combine_project(
-    const float* __restrict__ m, const float* __restrict__ l, const float* __restrict__ z,
-    int P, long long rows, int G, const float* __restrict__ cbv, int n_slots,
-    float* __restrict__ out, float* __restrict__ m_out, float* __restrict__ l_out) {
-  extern __shared__ float wsh[];  // [P] part weights e^{m_p - M}
-  __shared__ float zs[NC];
-  __shared__ float red[33];
+__global__ void __launch_bounds__(256) k_combine_merge(const float* __restrict__ m,
+                                                       const float* __restrict__ l,
+                                                       const float* __restrict__ z, int P,
+                                                       long long rows, float* __restrict__ zm) {
+  __shared__ float part[8][32];
+  __shared__ float red[8];
+  __shared__ float Ms, Lsh;
   const long long row = blockIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   float M = -FLT_MAX;
-  for (int p = threadIdx.x; p < P; p += blockDim.x)
+  for (int p = tid; p < P; p += 256)
     if (l[p * rows + row] > 0.f) M = fmaxf(M, m[p * rows + row]);
-  M = block_reduce(M, true, red);
-  float Ls = 0.f;
-  for (int p = threadIdx.x; p < P; p += blockDim.x) {
-    const float lp = l[p * rows + row];
-    const float wgt = lp > 0.f ? expf(m[p * rows + row] - M) : 0.f;
-    wsh[p] = wgt;
-    Ls += lp * wgt;
-  }
-  const float Lsum = block_reduce(Ls, false, red);  // (its barriers publish wsh)
-#pragma unroll
-  for (int k = threadIdx.x; k < NC; k += 128) {
-    float acc = 0.f;
-    for (int p = 0; p < P; ++p) {
-      const float wgt = wsh[p];
-      if (wgt != 0.f) acc += z[(p * rows + row) * NC + k] * wgt;
-    }
-    zs[k] = acc;
+  for (int o = 16; o; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
+  if (lane == 0) red[warp] = M;
+  __syncthreads();
+  if (tid == 0) {
+    float v = red[0];
+    for (int w = 1; w < 8; ++w) v = fmaxf(v, red[w]);
+    Ms = v;
   }
   __syncthreads();
+  M = Ms;
+  const int k = blockIdx.y * 32 + lane;
+  float acc = 0.f, Lp = 0.f;
+#pragma unroll 4
+  for (int p = warp; p < P; p += 8) {
+    const float lp = l[p * rows + row];
+    const float wgt = lp > 0.f ? expf(m[p * rows + row] - M) : 0.f;
+    Lp += lp * wgt;
+    if (wgt != 0.f) acc += z[(p * rows + row) * NC + k] * wgt;
+  }
+  part[warp][lane] = acc;
+  if (lane == 0) red[warp] = Lp;
+  __syncthreads();
+  if (warp == 0) {
+    float v = 0.f;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) v += part[w][lane];
+    zm[row * (NC + 2) + k] = v;
+    if (blockIdx.y == 0 && lane == 0) {
+      float L = 0.f;
+      for (int w = 0; w < 8; ++w) L += red[w];
+      zm[row * (NC + 2) + NC] = M;
+      zm[row * (NC + 2) + NC + 1] = L;
+    }
+  }
+}
+
+// o = z C_V / L per row (attn.cpp:249-256): one CTA of 128 threads per row,
+// thread = output dim, value codebook rows coalesced.
+template <int NC>
+__global__ void __launch_bounds__(128) k_combine_project(const float* __restrict__ zm,
+                                                         long long rows, int G,
+                                                         const float* __restrict__ cbv, int n_slots,
+                                                         float* __restrict__ out,
+                                                         float* __restrict__ m_out,
+                                                         float* __restrict__ l_out) {
+  __shared__ float zs[NC];
+  const long long row = blockIdx.x;
+  const float* zr = zm + row * (NC + 2);
+  for (int k = threadIdx.x; k < NC; k += 128) zs[k] = zr[k];
+  __syncthreads();
+  const float Lsum = zr[NC + 1];
   const float* cb = cbv + (size_t)((row / G) % n_slots) * NC * 128;
   const int jd = threadIdx.x;
   float acc = 0.f;
@@ -910,7 +949,7 @@ __global__ void __launch_bounds__(128) k_combine_project(
   for (int k = 0; k < NC; ++k) acc += zs[k] * __ldg(cb + (size_t)k * 128 + jd);
   out[row * 128 + jd] = acc / Lsum;
   if (jd == 0) {
-    if (m_out) m_out[row] = M;
+    if (m_out) m_out[row] = zr[NC];
     if (l_out) l_out[row] = Lsum;
   }
 }
@@ -919,19 +958,21 @@ __global__ void __launch_bounds__(128) k_combine_project(
 
 cudaError_t run_fast_combine(const AttnJob& job, const float* pm, const float* pl,
                              const float* pz, int n_parts, float* out, float* m_out,
-                             float* l_out, cudaStream_t st) {
+                             float* l_out, float* zm, cudaStream_t st) {
   const long long rows = (long long)job.S * job.geo.G;
   if (rows == 0) return cudaSuccess;
-  const size_t sm = (size_t)n_parts * sizeof(float);
-  if (job.geo.n_codes == 128)
-    k_combine_project<128><<<(unsigned)rows, 128, sm, st>>>(pm, pl, pz, n_parts, rows, job.geo.G,
-                                                            job.cb_val, job.n_slots, out, m_out,
-                                                            l_out);
-  else
-    k_combine_project<256><<<(unsigned)rows, 128, sm, st>>>(pm, pl, pz, n_parts, rows, job.geo.G,
-                                                            job.cb_val, job.n_slots, out, m_out,
-                                                            l_out);
-  count_launch();
+  const int NC = job.geo.n_codes;
+  dim3 gm((unsigned)rows, NC / 32);
+  if (NC == 128) {
+    k_combine_merge<128><<<gm, 256, 0, st>>>(pm, pl, pz, n_parts, rows, zm);
+    k_combine_project<128><<<(unsigned)rows, 128, 0, st>>>(zm, rows, job.geo.G, job.cb_val,
+                                                           job.n_slots, out, m_out, l_out);
+  } else {
+    k_combine_merge<256><<<gm, 256, 0, st>>>(pm, pl, pz, n_parts, rows, zm);
+    k_combine_project<256><<<(unsigned)rows, 128, 0, st>>>(zm, rows, job.geo.G, job.cb_val,
+                                                           job.n_slots, out, m_out, l_out);
+  }
+  count_launch(2);
   return cudaGetLastError();
 }
 

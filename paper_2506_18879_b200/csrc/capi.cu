@@ -37,8 +37,8 @@ cudaError_t ensure_dyn_smem(const void* kernel, size_t bytes) {
 
 std::atomic<unsigned long long> g_launches{0};
 cudaError_t run_naive_attention(const AttnJob& job, const float* q, float* out, void* scratch,
-                                size_t scratch_bytes, cudaStream_t st);
-size_t naive_scratch_bytes(const AttnJob& job);
+                                size_t scratch_bytes, cudaStream_t st, bool exact);
+size_t naive_scratch_bytes(const AttnJob& job, bool exact);
 }  // namespace cvq
 
 using namespace cvq;
@@ -749,7 +749,7 @@ CVQ_API cvq_status cvq_cache_append(cvq_cache* c, const void* k, const void* v, 
 namespace {
 
 cvq_status attention_common(cvq_cache* c, const float* q, uint64_t t, float* out, float* m,
-                            float* l, float* o, int where) {
+                            float* l, float* o, int where, bool naive = false) {
   TRY(ctx_check(c->ctx));
   if (c->length == 0) return fail(CVQ_EINVAL, "attention: empty cache");
   if (t + 1 < c->desc.position_offset + c->length)
@@ -760,8 +760,11 @@ cvq_status attention_common(cvq_cache* c, const float* q, uint64_t t, float* out
   job.t = (long long)t;
   AttnJob cap = job;  // size scratch for the full capacity once, not per step
   cap.n = (long long)c->desc.capacity;
-  CU(c->attn_scratch.ensure(std::max(attn_scratch_bytes(job, nullptr),
-                                     attn_scratch_bytes(cap, nullptr))));
+  if (naive)
+    CU(c->attn_scratch.ensure(naive_scratch_bytes(job, false)));
+  else
+    CU(c->attn_scratch.ensure(std::max(attn_scratch_bytes(job, nullptr),
+                                       attn_scratch_bytes(cap, nullptr))));
   const size_t qbytes = (size_t)c->S * g.G * g.d * sizeof(float);
   const void* qd = nullptr;
   TRY(to_device(c, c->stage_in, q, qbytes, where, &qd));
@@ -770,8 +773,12 @@ cvq_status attention_common(cvq_cache* c, const float* q, uint64_t t, float* out
     CU(c->stage_out.ensure(qbytes));
     od = static_cast<float*>(c->stage_out.p);
   }
-  CU(run_attention(job, static_cast<const float*>(qd), od, m, l, o, nullptr, c->attn_scratch.p,
-                   c->attn_scratch.n, c->ctx->stream, c->ctx->next_prof_pair()));
+  if (naive)
+    CU(run_naive_attention(job, static_cast<const float*>(qd), od, c->attn_scratch.p,
+                           c->attn_scratch.n, c->ctx->stream, false));
+  else
+    CU(run_attention(job, static_cast<const float*>(qd), od, m, l, o, nullptr, c->attn_scratch.p,
+                     c->attn_scratch.n, c->ctx->stream, c->ctx->next_prof_pair()));
   if (out && where == CVQ_HOST) {  // the step's one sync also checks the appends
     CU(cudaMemcpyAsync(out, od, qbytes, cudaMemcpyDeviceToHost, c->ctx->stream));
     TRY(enqueue_error_read(c));
@@ -787,6 +794,12 @@ CVQ_API cvq_status cvq_cache_attention(cvq_cache* c, const float* q, uint64_t t,
                                        int where) {
   if (!c || !q || !out) return fail(CVQ_EINVAL, "null argument");
   return attention_common(c, q, t, out, nullptr, nullptr, nullptr, where);
+}
+
+CVQ_API cvq_status cvq_cache_attention_naive(cvq_cache* c, const float* q, uint64_t t, float* out,
+                                             int where) {
+  if (!c || !q || !out) return fail(CVQ_EINVAL, "null argument");
+  return attention_common(c, q, t, out, nullptr, nullptr, nullptr, where, true);
 }
 
 CVQ_API cvq_status cvq_cache_attention_partial(cvq_cache* c, const float* q, uint64_t t, float* m,
@@ -1148,14 +1161,14 @@ CVQ_API cvq_status cvq_naive_attention(cvq_context* ctx, const cvq_key_config* k
   const Geom& g = c->geo;
   AttnJob job = make_job(c);
   job.t = (long long)t;
-  CU(c->attn_scratch.ensure(naive_scratch_bytes(job)));
+  CU(c->attn_scratch.ensure(naive_scratch_bytes(job, true)));
   CU(c->stage_in.ensure((size_t)g.d * 8 + 64));
   float* qd = static_cast<float*>(c->stage_in.p);
   float* od = qd + g.d;
   std::vector<float> qf(g.d);
   for (int i = 0; i < g.d; ++i) qf[i] = (float)q[i];
   CU(cudaMemcpyAsync(qd, qf.data(), g.d * 4, cudaMemcpyHostToDevice, ctx->stream));
-  CU(run_naive_attention(job, qd, od, c->attn_scratch.p, c->attn_scratch.n, ctx->stream));
+  CU(run_naive_attention(job, qd, od, c->attn_scratch.p, c->attn_scratch.n, ctx->stream, true));
   std::vector<float> of(g.d);
   CU(cudaMemcpyAsync(of.data(), od, g.d * 4, cudaMemcpyDeviceToHost, ctx->stream));
   CU(cudaStreamSynchronize(ctx->stream));

@@ -109,7 +109,16 @@ class PeerMerge:
         return packed_views(self.buf[slot * self.block:(slot + 1) * self.block], self.rows, self.d)
 
     def merge(self, out, G, ctx):
-        """Publish this step's block and merge all ranks' blocks into out."""
+        """Publish this step's block and merge all ranks' blocks into out.
+
+        The symmetric-memory barrier runs on torch's current stream; the
+        combine must run after it and before the next step's writes, so ctx
+        must be bound to that same stream: it is required and
+        checked, not defaulted."""
+        import torch
+        if ctx is None or ctx.stream_ptr != torch.cuda.current_stream().cuda_stream:
+            raise ValueError("PeerMerge.merge: ctx must wrap torch's current stream "
+                             "(Context(device, torch.cuda.current_stream().cuda_stream))")
         slot = self.step & 1
         self.hdl.barrier(channel=0)
         G.lse_combine_ptrs(self.ptrs, slot * self.block, self.world, self.rows, self.d, out, ctx)

@@ -193,3 +193,25 @@ def test_single_stream_mirror_reuses_device_copies(G):
     got, _ = G.fused_attention(kq, atoms, a, b, bits, vrows, q, n_max - 1)
     want, _, _ = P.fused_attention(kq, atoms, a, b, bits, vrows, q, n_max - 1)
     assert fx.rel_err(got, want) <= 1e-5
+
+
+def test_single_level_codebook_cache(G):
+    """n_levels = 1: zero-bit key fields.  Prefill, appends and attention
+    run (round 1 launched a zero-width pack grid) and match the oracle."""
+    kq = KQ(8, 2, 1, 2)
+    f = fx.CacheFixture(kq=kq)
+    c = G.QuantizedKVCache(kq, 8, capacity=4, hidden=16)
+    c.set_key_codebook(0, 0, f.atoms)
+    c.set_value_quantizer(0, 0, f.vrows, f.w1, f.b1, f.w2, f.b2)
+    K, V = P.gen_synth(9, 8, 8, 41), P.gen_synth(9, 8, 8, 42)
+    c.prefill(K[None, None, None, :5], V[None, None, None, :5])
+    for i in range(5, 9):
+        c.append(K[None, None, None, i], V[None, None, None, i])
+    kw, vw = c.export_stream(0, 0, 0)
+    a, b = P.encode_keys(kq, f.atoms, K)
+    bits, _ = P.encoder_forward_infer(f.w1, f.b1, f.w2, f.b2, V)
+    assert kw.size == 0 and (vw == P.pack_value_codes(bits)).all()
+    q = P.rng(3).normal(8)
+    out = c.attention(q.reshape(1, 1, 1, 8).astype(np.float32), 8)
+    want, _, _ = P.fused_attention(kq, f.atoms, a, b, bits, f.vrows, q, 8)
+    assert fx.rel_err(out.reshape(-1), want) <= 1e-5

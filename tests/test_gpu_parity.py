@@ -739,18 +739,25 @@ def test_peer_merge_world_one_roundtrip(G, tmp_path):
     if not dist.is_initialized():
         dist.init_process_group("nccl", init_method=f"file://{tmp_path}/pg", rank=0, world_size=1,
                                 device_id=torch.device("cuda", 0))
+    side = torch.cuda.Stream()  # a real stream shared by torch and the context
+    prev = torch.cuda.current_stream()
+    torch.cuda.set_stream(side)
     try:
         pm = PeerMerge(64, 128)
+        ctx = G.Context(0, side.cuda_stream)
+        with pytest.raises(ValueError):
+            pm.merge(torch.empty(64, 128, device="cuda"), G, None)
         for step in range(2):
             m, l, o = pm.views()
             m.copy_(torch.randn(64, device="cuda"))
             l.copy_(torch.rand(64, device="cuda") + 0.5)
             o.copy_(torch.randn(64, 128, device="cuda"))
             out = torch.empty(64, 128, device="cuda")
-            pm.merge(out, G, None)
+            pm.merge(out, G, ctx)
             torch.cuda.synchronize()
             assert torch.allclose(out, o, rtol=1e-6, atol=1e-6), step
     finally:
+        torch.cuda.set_stream(prev)
         dist.destroy_process_group()
 
 
@@ -789,3 +796,45 @@ def test_mgpu_shard_group_world_one_nccl(G):
         assert fx.rel_err(got, want) <= 1e-6, step
     assert grp.size() == n + 3 and caches[0].size() == n + 3
     grp.close()
+
+
+@pytest.mark.parametrize("preset,n", [("1bit", 3000), ("2bit", 1500)])
+def test_naive_decode_then_attend_multistream(G, preset, n):
+    """cvq_cache_attention_naive (naive.cu): dense fp16 dequantisation of
+    every key (RoPE'd) and value (tensor-core bits x C_V), then flash-decoding
+    -- 2 seqs x 2 layers x 2 KV heads x 4 q heads vs the oracle's
+    naive_quantized_attention and the fused path (1e-3)."""
+    kq = KQ(128, 64, 64, 11 if preset == "1bit" else 21)
+    nc = 128 if preset == "1bit" else 256
+    B, Ly, H, Gq = 2, 2, 2, 4
+    rng = P.rng(n + 5)
+    c = G.QuantizedKVCache(kq, nc, n_seqs=B, n_layers=Ly, n_kv_heads=H, q_per_kv=Gq, capacity=n,
+                           keys="tc")
+    books, codes = {}, {}
+    for layer in range(Ly):
+        for h in range(H):
+            atoms = rng.normal(2 * kq.n_atoms, 0.3)
+            vrows = rng.normal(nc * 128, 1 / 16).reshape(nc, 128)
+            c.set_key_codebook(layer, h, atoms)
+            c.set_value_quantizer(layer, h, vrows)
+            books[layer, h] = (atoms, vrows)
+    for sq in range(B):
+        for layer in range(Ly):
+            for h in range(H):
+                a, b = fx.random_key_codes(kq, n, rng=rng)
+                bits = fx.random_value_codes(nc, n, rng=rng)
+                c.import_stream(sq, layer, h, P.pack_key_codes(kq, a, b), P.pack_value_codes(bits), n)
+                codes[sq, layer, h] = (a, b, bits)
+    q = rng.normal(B * Ly * H * Gq * 128).reshape(B, Ly, H * Gq, 128).astype(np.float32)
+    t = n - 1 + 11
+    naive = c.attention_naive(q, t)
+    fused = c.attention(q, t)
+    assert fx.rel_err(naive, fused) <= 1e-3
+    worst = 0.0
+    for sq, layer, h, j in ((0, 0, 0, 0), (1, 1, 1, 3), (0, 1, 1, 2)):
+        atoms, vrows = books[layer, h]
+        a, b, bits = codes[sq, layer, h]
+        want, _, _ = P.naive_attention(kq, atoms, a, b, bits, vrows,
+                                       q[sq, layer, h * Gq + j].astype(np.float64), t)
+        worst = max(worst, fx.rel_err(naive[sq, layer, h * Gq + j], want))
+    assert worst <= 1e-3, worst

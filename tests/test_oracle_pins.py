@@ -342,3 +342,20 @@ def test_incremental_decode_matches_replay():
         want, _, _ = P.fused_attention(f.kq, f.atoms, a[:(t + 1) * per], b[:(t + 1) * per],
                                        bits[:t + 1], f.vrows, qs[t], t)
         assert fx.rel_err(got, want) <= 1e-6
+
+
+def test_single_level_codebook_packs_nothing(O):
+    """n_levels = 1 passes KeyQuantConfig::validate (is_pow2(1)) and gives
+    zero-bit fields: the packed key stream is empty and unpacks to zeros
+    (cache.cpp:90-135, BitBuffer appends of 0 bits); encode_keys picks the
+    only center."""
+    kq = KQ(8, 2, 1, 2)
+    assert kq.bits_per_token == 0
+    a = np.zeros(5 * kq.rounds * kq.groups, np.uint16)
+    words = O.pack_key_codes(kq, a, a)
+    assert words.size == 0
+    a2, b2 = O.unpack_key_codes(kq, words, 5)
+    assert (a2 == 0).all() and (b2 == 0).all()
+    atoms = O.rng(5).normal(2 * kq.n_atoms)
+    ea, eb = O.encode_keys(kq, atoms, O.rng(6).normal(5 * 8).reshape(5, 8))
+    assert (ea == 0).all() and (eb == 0).all()
