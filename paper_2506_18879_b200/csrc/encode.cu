@@ -157,6 +157,11 @@ __device__ int exact_search(const double* p, const double2* U, int L, int gsz, c
   return bc;
 }
 
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem) : "memory");
+}
+
 constexpr int kEncTok = 32;
 constexpr int kEncWarps = 16;  // measured: 8 -> 4.5e6, 16 -> 6.9e6, 32 -> 3.2e6 token-heads/s (C4 sample)
 
@@ -174,8 +179,18 @@ k_encode_keys_table(Geom g, int n_slots, const double* __restrict__ atoms,
   double* PU = P + (size_t)kEncTok * g.d;               // [warps][L]
   double* PV = PU + (size_t)kEncWarps * g.L;            // [warps][L]
   float* Bf = reinterpret_cast<float*>(PV + (size_t)kEncWarps * g.L);  // [L][L] fp32 screen table
+  // (reassigned below for the tiled layout)
   float* PUf = Bf + (size_t)g.L * g.L;                  // [warps][L]
   float* PVf = PUf + (size_t)kEncWarps * g.L;           // [warps][L]
+  // head presets (L = 64, 64 subspaces per group): projections of the whole
+  // tile per round into [tok][L] tables, which then take the place of the
+  // per-warp PU / PV / PUf / PVf rows (same smem offset)
+  const bool tiled = g.L == 64 && g.g == 64 && kEncTok == 32 && kEncWarps == 16;
+  double* TPU = PU;                                    // [tok][L]
+  double* TPV = TPU + (size_t)kEncTok * g.L;
+  float* TPUf = reinterpret_cast<float*>(TPV + (size_t)kEncTok * g.L);
+  float* TPVf = TPUf + (size_t)kEncTok * g.L;
+  if (tiled) Bf = TPVf + (size_t)kEncTok * g.L;       // the fp32 screen table after them
   const int s = blockIdx.y, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const long long i0 = (long long)blockIdx.x * kEncTok;
   const int nt = (int)min((long long)kEncTok, n - i0);
@@ -188,33 +203,70 @@ k_encode_keys_table(Geom g, int n_slots, const double* __restrict__ atoms,
       __syncthreads();
       const double2* Ug = reinterpret_cast<const double2*>(atoms) +
                           ((size_t)(slot * g.R + r) * g.subs + (size_t)grp * gs) * L;
-      for (int e = tid; e < gs * L; e += blockDim.x) U[e] = Ug[e];
       const double* Bg = base + ((size_t)(slot * g.R + r) * g.groups + grp) * L * L;
-      for (int e = tid; e < L * L; e += blockDim.x) {
-        const double bv = Bg[e];
-        B[e] = bv;
-        Bf[e] = (float)bv;
-      }
+      // the round's slice and base table by cp.async (16 B per request, no
+      // register round trip: the plain load/store loop was latency-bound)
+      for (int e = tid; e < gs * L; e += blockDim.x) cp_async16(U + e, Ug + e);
+      for (int e = 2 * tid; e < L * L; e += 2 * blockDim.x) cp_async16(B + e, Bg + e);
+      asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;\n" ::: "memory");
       const double mn = maxnorm[(size_t)(slot * g.R + r) * g.groups + grp];
       __syncthreads();
-      double* pu = PU + warp * L;
-      double* pv = PV + warp * L;
-      float* puf = PUf + warp * L;
-      float* pvf = PVf + warp * L;
+      for (int e = tid; e < L * L; e += blockDim.x) Bf[e] = (float)B[e];
+      if (!tiled) __syncthreads();  // tiled: the barrier after the projections
+      if (tiled) {
+        // projections of every token of the tile at once, register-tiled:
+        // thread = 2 tokens x 2 levels x (u, v); per subspace 2 + 2 LDS.128
+        // feed 16 FMAs (the per-warp form re-read U per token, 4 FMAs per load)
+        const int lg = tid & 31, t2 = tid >> 5;  // levels 2 lg, 2 lg + 1; tokens 2 t2, 2 t2 + 1
+        double su[2][2] = {{0.0, 0.0}, {0.0, 0.0}}, sv[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+        const double* p0 = P + (size_t)(2 * t2) * g.d + grp * w2;
+        const double* p1 = p0 + g.d;
+#pragma unroll 4
+        for (int si = 0; si < gs; ++si) {
+          const double2 pa = *reinterpret_cast<const double2*>(p0 + 2 * si);
+          const double2 pb = *reinterpret_cast<const double2*>(p1 + 2 * si);
+          const double2 u0 = U[(size_t)si * L + 2 * lg], u1 = U[(size_t)si * L + 2 * lg + 1];
+          su[0][0] = fma(pa.x, u0.x, fma(pa.y, u0.y, su[0][0]));
+          sv[0][0] = fma(pa.y, u0.x, fma(-pa.x, u0.y, sv[0][0]));
+          su[0][1] = fma(pa.x, u1.x, fma(pa.y, u1.y, su[0][1]));
+          sv[0][1] = fma(pa.y, u1.x, fma(-pa.x, u1.y, sv[0][1]));
+          su[1][0] = fma(pb.x, u0.x, fma(pb.y, u0.y, su[1][0]));
+          sv[1][0] = fma(pb.y, u0.x, fma(-pb.x, u0.y, sv[1][0]));
+          su[1][1] = fma(pb.x, u1.x, fma(pb.y, u1.y, su[1][1]));
+          sv[1][1] = fma(pb.y, u1.x, fma(-pb.x, u1.y, sv[1][1]));
+        }
+#pragma unroll
+        for (int a2 = 0; a2 < 2; ++a2)
+#pragma unroll
+          for (int b2 = 0; b2 < 2; ++b2) {
+            const size_t o = (size_t)(2 * t2 + a2) * L + 2 * lg + b2;
+            TPU[o] = su[a2][b2];
+            TPV[o] = sv[a2][b2];
+            TPUf[o] = (float)su[a2][b2];
+            TPVf[o] = (float)sv[a2][b2];
+          }
+        __syncthreads();
+      }
       for (int tk = warp; tk < nt; tk += kEncWarps) {
         double* p = P + (size_t)tk * g.d + grp * w2;
-        for (int l = lane; l < L; l += 32) {
-          double su = 0.0, sv = 0.0;
-          for (int si = 0; si < gs; ++si) {
-            const double2 u = U[(size_t)si * L + l];
-            const double px = p[2 * si], py = p[2 * si + 1];
-            su = fma(px, u.x, fma(py, u.y, su));
-            sv = fma(py, u.x, fma(-px, u.y, sv));
+        double* pu = tiled ? TPU + (size_t)tk * L : PU + warp * L;
+        double* pv = tiled ? TPV + (size_t)tk * L : PV + warp * L;
+        float* puf = tiled ? TPUf + (size_t)tk * L : PUf + warp * L;
+        float* pvf = tiled ? TPVf + (size_t)tk * L : PVf + warp * L;
+        if (!tiled) {
+          for (int l = lane; l < L; l += 32) {
+            double su = 0.0, sv = 0.0;
+            for (int si = 0; si < gs; ++si) {
+              const double2 u = U[(size_t)si * L + l];
+              const double px = p[2 * si], py = p[2 * si + 1];
+              su = fma(px, u.x, fma(py, u.y, su));
+              sv = fma(py, u.x, fma(-px, u.y, sv));
+            }
+            pu[l] = su;
+            pv[l] = sv;
+            puf[l] = (float)su;
+            pvf[l] = (float)sv;
           }
-          pu[l] = su;
-          pv[l] = sv;
-          puf[l] = (float)su;
-          pvf[l] = (float)sv;
         }
         double pn = 0.0;
         for (int e = lane; e < w2; e += 32) pn = fma(p[e], p[e], pn);
@@ -234,17 +286,54 @@ k_encode_keys_table(Geom g, int n_slots, const double* __restrict__ atoms,
           // re-checked exactly whenever the screen is not decisive.
           float b1 = INFINITY, b2 = INFINITY;
           int c1 = 0x7fffffff;
-          for (int b = lane; b < L; b += 32) {
-            const float t2 = 2.f * pvf[b];
-            for (int a = 0; a < L; ++a) {
-              const float sc = fmaf(-2.f, puf[a], Bf[a * L + b]) - t2;
-              const int c = a * L + b;
-              if (sc < b1 || (sc == b1 && c < c1)) {
-                b2 = b1;
-                b1 = sc;
-                c1 = c;
-              } else if (sc < b2) {
-                b2 = sc;
+          if (L == 64) {
+            // lane = columns b = 2 lane, 2 lane + 1 (one LDS.64 per row);
+            // per column the running min / argmin / runner-up of
+            // x = fl(B - 2 pu) over a, the "- 2 pv[b]" applied at the end
+            // (fl(x - t) is monotone in x, so the column's best and
+            // runner-up screen values are those of x; ties only matter
+            // where the margin test sends the token to the exact search)
+            const int b0 = 2 * lane;
+            float m1a = INFINITY, m2a = INFINITY, m1b = INFINITY, m2b = INFINITY;
+            int ia = 0, ib = 0;
+#pragma unroll 4
+            for (int a0 = 0; a0 < 64; a0 += 4) {
+              const float4 pu4 = *reinterpret_cast<const float4*>(puf + a0);
+              const float pus[4] = {pu4.x, pu4.y, pu4.z, pu4.w};
+#pragma unroll
+              for (int u = 0; u < 4; ++u) {
+                const float2 bb = *reinterpret_cast<const float2*>(Bf + (a0 + u) * 64 + b0);
+                const float xa = fmaf(-2.f, pus[u], bb.x), xb = fmaf(-2.f, pus[u], bb.y);
+                if (xa < m1a) ia = a0 + u;
+                m2a = fminf(m2a, fmaxf(m1a, xa));
+                m1a = fminf(m1a, xa);
+                if (xb < m1b) ib = a0 + u;
+                m2b = fminf(m2b, fmaxf(m1b, xb));
+                m1b = fminf(m1b, xb);
+              }
+            }
+            const float2 pv2 = *reinterpret_cast<const float2*>(pvf + b0);
+            const float va = m1a - 2.f * pv2.x, vb = m1b - 2.f * pv2.y;
+            const float ra = m2a - 2.f * pv2.x, rb = m2b - 2.f * pv2.y;
+            const int ca = ia * 64 + b0, cb = ib * 64 + b0 + 1;
+            if (vb < va || (vb == va && cb < ca)) {
+              b1 = vb; c1 = cb; b2 = fminf(rb, va);
+            } else {
+              b1 = va; c1 = ca; b2 = fminf(ra, vb);
+            }
+          } else {
+            for (int b = lane; b < L; b += 32) {
+              const float t2 = 2.f * pvf[b];
+              for (int a = 0; a < L; ++a) {
+                const float sc = fmaf(-2.f, puf[a], Bf[a * L + b]) - t2;
+                const int c = a * L + b;
+                if (sc < b1 || (sc == b1 && c < c1)) {
+                  b2 = b1;
+                  b1 = sc;
+                  c1 = c;
+                } else if (sc < b2) {
+                  b2 = sc;
+                }
               }
             }
           }
@@ -501,9 +590,11 @@ k_encode_keys_small(Geom g, int n_slots, const double* __restrict__ atoms,
 }
 
 static size_t table_smem(const Geom& g) {
+  // per-warp projection rows, or (head presets) per-token projection tables
+  const size_t rows = (g.L == 64 && g.g == 64) ? kEncTok : kEncWarps;
   return sizeof(double) * (2 * (size_t)g.g * g.L + (size_t)g.L * g.L + (size_t)kEncTok * g.d +
-                           2 * (size_t)kEncWarps * g.L) +
-         sizeof(float) * ((size_t)g.L * g.L + 2 * (size_t)kEncWarps * g.L);
+                           2 * rows * g.L) +
+         sizeof(float) * ((size_t)g.L * g.L + 2 * rows * g.L);
 }
 
 cudaError_t run_encode_keys(const Geom& g, int S, int n_slots, const KeyEncTables& tab,
@@ -605,6 +696,89 @@ __global__ void k_encode_values(Geom g, int n_slots, ValEncWeights w,
   }
 }
 
+// Prefill value encoder as two exact-order fp64 GEMMs per 32-token tile:
+// H = relu(T W1 + b1), logits = H W2 + b2 (valquant.cpp:50-70), every output
+// accumulated sequentially over the reduction index in the reference order
+// with its zero-skips (t_i == 0, h_j == 0) and no FMA -- bit-identical to the
+// reference, but register-tiled (thread = 4 tokens x 4 columns, W rows staged
+// in smem 16 at a time) instead of a thread per column re-reading T per
+// product (k_encode_values<16>: fp64 pipe 20%).  grid (ceil(n / 32), S),
+// 256 threads; smem T[32][d], H[32][hidden], W chunk [16][128].
+constexpr int kVgTok = 32, kVgCols = 128, kVgK = 16;
+__global__ void __launch_bounds__(256) k_encode_values_gemm(
+    Geom g, int n_slots, ValEncWeights w, const void* __restrict__ vals, int dtype,
+    long long s_stride, long long n, uint8_t* __restrict__ bits, double* __restrict__ logits,
+    unsigned long long* __restrict__ errpos, unsigned long long tok0) {
+  extern __shared__ double smv[];
+  double* T = smv;                              // [32][d]
+  double* H = T + (size_t)kVgTok * g.d;         // [32][hidden]
+  double* W = H + (size_t)kVgTok * g.hidden;    // [16][128]
+  const int s = blockIdx.y, tid = threadIdx.x;
+  const long long i0 = (long long)blockIdx.x * kVgTok;
+  const int nt = (int)min((long long)kVgTok, n - i0);
+  const int slot = s % n_slots;
+  const int tg = tid >> 5, cg = tid & 31;  // tokens 4 tg .. +3, columns 4 cg .. +3 of a block
+  for (int e = tid; e < kVgTok * g.d; e += 256)
+    T[e] = (e / g.d < nt)
+               ? load_elem(vals, dtype, (long long)s * s_stride + (i0 + e / g.d) * g.d + e % g.d)
+               : 0.0;
+  // one exact-order GEMM: out[32][N] = A[32][K] x B[K][N] (+ bias), per
+  // output sequential over k, skipping A == 0; `post` finishes a column
+  auto gemm = [&](const double* A, int K, const double* B, int N, auto post) {
+    for (int c0 = 0; c0 < N; c0 += kVgCols) {
+      double acc[4][4];
+#pragma unroll
+      for (int m = 0; m < 4; ++m)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) acc[m][c] = 0.0;
+      for (int k0 = 0; k0 < K; k0 += kVgK) {
+        __syncthreads();  // previous chunk consumed (and A complete)
+        for (int e = tid; e < kVgK * kVgCols; e += 256) {
+          const int kk = e / kVgCols, cc = e % kVgCols;
+          W[e] = (k0 + kk < K && c0 + cc < N) ? __ldg(B + (size_t)(k0 + kk) * N + c0 + cc) : 0.0;
+        }
+        __syncthreads();
+        const int kn = min(kVgK, K - k0);
+        for (int kk = 0; kk < kn; ++kk) {
+          double a[4], b[4];
+#pragma unroll
+          for (int m = 0; m < 4; ++m) a[m] = A[(size_t)(4 * tg + m) * K + k0 + kk];
+#pragma unroll
+          for (int c = 0; c < 4; ++c) b[c] = W[kk * kVgCols + 4 * cg + c];
+#pragma unroll
+          for (int m = 0; m < 4; ++m)
+            if (a[m] != 0.0)
+#pragma unroll
+              for (int c = 0; c < 4; ++c) acc[m][c] = __dadd_rn(acc[m][c], __dmul_rn(a[m], b[c]));
+        }
+      }
+#pragma unroll
+      for (int m = 0; m < 4; ++m)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const int col = c0 + 4 * cg + c;
+          if (col < N) post(4 * tg + m, col, acc[m][c]);
+        }
+    }
+  };
+  const double* b1 = w.b1 + (size_t)slot * g.hidden;
+  const double* b2 = w.b2 + (size_t)slot * g.n_codes;
+  gemm(T, g.d, w.w1 + (size_t)slot * g.d * g.hidden, g.hidden, [&](int m, int col, double v) {
+    v = __dadd_rn(v, b1[col]);  // valquant.cpp:58-61
+    H[(size_t)m * g.hidden + col] = v < 0.0 ? 0.0 : v;
+  });
+  __syncthreads();  // H complete before it is read as A
+  gemm(H, g.hidden, w.w2 + (size_t)slot * g.hidden * g.n_codes, g.n_codes,
+       [&](int m, int col, double v) {
+         if (m >= nt) return;
+         v = __dadd_rn(v, b2[col]);  // valquant.cpp:69
+         if (!isfinite(v)) atomicMin(errpos, tok0);
+         const size_t o = ((size_t)s * n + i0 + m) * g.n_codes + col;
+         bits[o] = v > 0.0 ? 1 : 0;
+         if (logits) logits[o] = v;
+       });
+}
+
 template <int TV>
 static cudaError_t launch_values(const Geom& g, int S, int n_slots, const ValEncWeights& w,
                                  const void* vals, int dtype, long long s_stride, long long n,
@@ -634,6 +808,18 @@ cudaError_t run_encode_values(const Geom& g, int S, int n_slots, const ValEncWei
   if (n < 16)  // decode-step appends: one token per CTA, no wasted lanes
     return launch_values<1>(g, S, n_slots, w, vals, dtype, s_stride, n, bits, logits, errpos, tok0,
                             st);
+  if (g.d % 4 == 0 && g.hidden % 4 == 0 && g.n_codes % 4 == 0) {
+    const size_t sm = sizeof(double) * ((size_t)kVgTok * (g.d + g.hidden) + kVgK * kVgCols);
+    if (sm <= 200 * 1024) {
+      cudaError_t e = ensure_dyn_smem(reinterpret_cast<const void*>(k_encode_values_gemm), sm);
+      if (e != cudaSuccess) return e;
+      dim3 grid((unsigned)((n + kVgTok - 1) / kVgTok), S);
+      k_encode_values_gemm<<<grid, 256, sm, st>>>(g, n_slots, w, vals, dtype, s_stride, n, bits,
+                                                   logits, errpos, tok0);
+      count_launch();
+      return cudaGetLastError();
+    }
+  }
   return launch_values<16>(g, S, n_slots, w, vals, dtype, s_stride, n, bits, logits, errpos, tok0,
                            st);
 }
