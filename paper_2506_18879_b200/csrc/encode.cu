@@ -215,36 +215,52 @@ k_encode_keys_table(Geom g, int n_slots, const double* __restrict__ atoms,
       if (!tiled) __syncthreads();  // tiled: the barrier after the projections
       if (tiled) {
         // projections of every token of the tile at once, register-tiled:
-        // thread = 2 tokens x 2 levels x (u, v); per subspace 2 + 2 LDS.128
-        // feed 16 FMAs (the per-warp form re-read U per token, 4 FMAs per load)
-        const int lg = tid & 31, t2 = tid >> 5;  // levels 2 lg, 2 lg + 1; tokens 2 t2, 2 t2 + 1
-        double su[2][2] = {{0.0, 0.0}, {0.0, 0.0}}, sv[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
-        const double* p0 = P + (size_t)(2 * t2) * g.d + grp * w2;
-        const double* p1 = p0 + g.d;
-#pragma unroll 4
-        for (int si = 0; si < gs; ++si) {
-          const double2 pa = *reinterpret_cast<const double2*>(p0 + 2 * si);
-          const double2 pb = *reinterpret_cast<const double2*>(p1 + 2 * si);
+        // thread = 4 tokens x 2 levels x (u, v) over one half of the
+        // subspaces (threads 256..511 the upper half, added through smem).
+        // Per subspace 2 LDS.128 of U (8 wavefronts per warp) + 4 broadcast
+        // P loads feed 32 DFMA: the fp64 pipe, not shared memory, bounds it.
+        // (Summation order is free here: pu / pv only feed the screen.)
+        const int hs = tid >> 8, lg = tid & 31, tq = (tid >> 5) & 7;  // tokens 4 tq .. 4 tq + 3
+        double su[4][2], sv[4][2];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) su[t][0] = su[t][1] = sv[t][0] = sv[t][1] = 0.0;
+        const double* p0 = P + (size_t)(4 * tq) * g.d + grp * w2;
+        const int sh = gs >> 1;
+#pragma unroll 2
+        for (int si = hs * sh; si < (hs + 1) * sh; ++si) {
           const double2 u0 = U[(size_t)si * L + 2 * lg], u1 = U[(size_t)si * L + 2 * lg + 1];
-          su[0][0] = fma(pa.x, u0.x, fma(pa.y, u0.y, su[0][0]));
-          sv[0][0] = fma(pa.y, u0.x, fma(-pa.x, u0.y, sv[0][0]));
-          su[0][1] = fma(pa.x, u1.x, fma(pa.y, u1.y, su[0][1]));
-          sv[0][1] = fma(pa.y, u1.x, fma(-pa.x, u1.y, sv[0][1]));
-          su[1][0] = fma(pb.x, u0.x, fma(pb.y, u0.y, su[1][0]));
-          sv[1][0] = fma(pb.y, u0.x, fma(-pb.x, u0.y, sv[1][0]));
-          su[1][1] = fma(pb.x, u1.x, fma(pb.y, u1.y, su[1][1]));
-          sv[1][1] = fma(pb.y, u1.x, fma(-pb.x, u1.y, sv[1][1]));
-        }
 #pragma unroll
-        for (int a2 = 0; a2 < 2; ++a2)
-#pragma unroll
-          for (int b2 = 0; b2 < 2; ++b2) {
-            const size_t o = (size_t)(2 * t2 + a2) * L + 2 * lg + b2;
-            TPU[o] = su[a2][b2];
-            TPV[o] = sv[a2][b2];
-            TPUf[o] = (float)su[a2][b2];
-            TPVf[o] = (float)sv[a2][b2];
+          for (int t = 0; t < 4; ++t) {
+            const double2 pa = *reinterpret_cast<const double2*>(p0 + (size_t)t * g.d + 2 * si);
+            su[t][0] = fma(pa.x, u0.x, fma(pa.y, u0.y, su[t][0]));
+            sv[t][0] = fma(pa.y, u0.x, fma(-pa.x, u0.y, sv[t][0]));
+            su[t][1] = fma(pa.x, u1.x, fma(pa.y, u1.y, su[t][1]));
+            sv[t][1] = fma(pa.y, u1.x, fma(-pa.x, u1.y, sv[t][1]));
           }
+        }
+        if (hs) {
+#pragma unroll
+          for (int t = 0; t < 4; ++t) {
+            const size_t o = (size_t)(4 * tq + t) * L + 2 * lg;
+            *reinterpret_cast<double2*>(TPU + o) = make_double2(su[t][0], su[t][1]);
+            *reinterpret_cast<double2*>(TPV + o) = make_double2(sv[t][0], sv[t][1]);
+          }
+        }
+        __syncthreads();
+        if (!hs) {
+#pragma unroll
+          for (int t = 0; t < 4; ++t) {
+            const size_t o = (size_t)(4 * tq + t) * L + 2 * lg;
+            const double2 hu = *reinterpret_cast<const double2*>(TPU + o);
+            const double2 hv = *reinterpret_cast<const double2*>(TPV + o);
+            const double u0 = su[t][0] + hu.x, u1 = su[t][1] + hu.y;
+            const double v0 = sv[t][0] + hv.x, v1 = sv[t][1] + hv.y;
+            *reinterpret_cast<double2*>(TPU + o) = make_double2(u0, u1);
+            *reinterpret_cast<double2*>(TPV + o) = make_double2(v0, v1);
+            *reinterpret_cast<float2*>(TPUf + o) = make_float2((float)u0, (float)u1);
+            *reinterpret_cast<float2*>(TPVf + o) = make_float2((float)v0, (float)v1);
+          }
+        }
         __syncthreads();
       }
       for (int tk = warp; tk < nt; tk += kEncWarps) {
