@@ -89,11 +89,13 @@ __device__ __forceinline__ double load_elem(const void* p, int dtype, long long 
 }
 
 // Exact reference distance of residual p (2g values) to center (a, b).
-__device__ __forceinline__ double exact_dist(const double* p, const double2* U, int L, int gsz,
+// U rows are us double2 apart (us = L in global memory, L + 1 in the padded
+// shared-memory copy of k_encode_keys_table).
+__device__ __forceinline__ double exact_dist(const double* p, const double2* U, int us, int gsz,
                                              int a, int b) {
   double s = 0.0;
   for (int si = 0; si < gsz; ++si) {
-    const double2 ua = U[(size_t)si * L + a], ub = U[(size_t)si * L + b];
+    const double2 ua = U[(size_t)si * us + a], ub = U[(size_t)si * us + b];
     const double c0 = __dadd_rn(ua.x, -ub.y);  // u_a + v_b, keyquant.cpp:152-156
     const double c1 = __dadd_rn(ua.y, ub.x);
     const double d0 = __dsub_rn(p[2 * si], c0);
@@ -132,7 +134,7 @@ __device__ __forceinline__ float screen_val(const float* B, const float* PU, con
 }
 
 template <class T>
-__device__ int exact_search(const double* p, const double2* U, int L, int gsz, const T* B,
+__device__ int exact_search(const double* p, const double2* U, int us, int L, int gsz, const T* B,
                             const T* PU, const T* PV, bool use_thr, T thr) {
   const int lane = threadIdx.x & 31;
   double best = INFINITY;
@@ -143,7 +145,7 @@ __device__ int exact_search(const double* p, const double2* U, int L, int gsz, c
       const T sc = screen_val(B, PU, PV, L, a, b);
       if (!(sc <= thr)) continue;
     }
-    const double d = exact_dist(p, U, L, gsz, a, b);
+    const double d = exact_dist(p, U, us, gsz, a, b);
     if (d < best) {  // increasing c per lane: strict '<' keeps the smallest
       best = d;
       bc = c;
@@ -173,8 +175,11 @@ k_encode_keys_table(Geom g, int n_slots, const double* __restrict__ atoms,
                     const void* __restrict__ keys, int dtype, long long s_stride, long long n,
                     uint16_t* __restrict__ a_out, uint16_t* __restrict__ b_out) {
   extern __shared__ double sm[];
-  double2* U = reinterpret_cast<double2*>(sm);          // [g][L]
-  double* B = sm + 2 * (size_t)g.g * g.L;               // [L][L]
+  // U rows padded to L + 1 double2: the residual update reads one column
+  // down all rows (stride L double2 = 1 KiB would be a 32-way bank conflict)
+  const int us = g.L + 1;
+  double2* U = reinterpret_cast<double2*>(sm);          // [g][L + 1]
+  double* B = sm + 2 * (size_t)g.g * us;                // [L][L]
   double* P = B + (size_t)g.L * g.L;                    // [kEncTok][d]
   double* PU = P + (size_t)kEncTok * g.d;               // [warps][L]
   double* PV = PU + (size_t)kEncWarps * g.L;            // [warps][L]
@@ -206,7 +211,7 @@ k_encode_keys_table(Geom g, int n_slots, const double* __restrict__ atoms,
       const double* Bg = base + ((size_t)(slot * g.R + r) * g.groups + grp) * L * L;
       // the round's slice and base table by cp.async (16 B per request, no
       // register round trip: the plain load/store loop was latency-bound)
-      for (int e = tid; e < gs * L; e += blockDim.x) cp_async16(U + e, Ug + e);
+      for (int e = tid; e < gs * L; e += blockDim.x) cp_async16(U + (e / L) * us + e % L, Ug + e);
       for (int e = 2 * tid; e < L * L; e += 2 * blockDim.x) cp_async16(B + e, Bg + e);
       asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;\n" ::: "memory");
       const double mn = maxnorm[(size_t)(slot * g.R + r) * g.groups + grp];
@@ -217,8 +222,8 @@ k_encode_keys_table(Geom g, int n_slots, const double* __restrict__ atoms,
         // projections of every token of the tile at once, register-tiled:
         // thread = 4 tokens x 2 levels x (u, v) over one half of the
         // subspaces (threads 256..511 the upper half, added through smem).
-        // Per subspace 2 LDS.128 of U (8 wavefronts per warp) + 4 broadcast
-        // P loads feed 32 DFMA: the fp64 pipe, not shared memory, bounds it.
+        // Per subspace 2 LDS.128 of U (levels lg and lg + 32: 4 wavefronts
+        // each) + 4 broadcast P loads feed 32 DFMA.
         // (Summation order is free here: pu / pv only feed the screen.)
         const int hs = tid >> 8, lg = tid & 31, tq = (tid >> 5) & 7;  // tokens 4 tq .. 4 tq + 3
         double su[4][2], sv[4][2];
@@ -228,7 +233,7 @@ k_encode_keys_table(Geom g, int n_slots, const double* __restrict__ atoms,
         const int sh = gs >> 1;
 #pragma unroll 2
         for (int si = hs * sh; si < (hs + 1) * sh; ++si) {
-          const double2 u0 = U[(size_t)si * L + 2 * lg], u1 = U[(size_t)si * L + 2 * lg + 1];
+          const double2 u0 = U[(size_t)si * us + lg], u1 = U[(size_t)si * us + lg + 32];
 #pragma unroll
           for (int t = 0; t < 4; ++t) {
             const double2 pa = *reinterpret_cast<const double2*>(p0 + (size_t)t * g.d + 2 * si);
@@ -241,24 +246,28 @@ k_encode_keys_table(Geom g, int n_slots, const double* __restrict__ atoms,
         if (hs) {
 #pragma unroll
           for (int t = 0; t < 4; ++t) {
-            const size_t o = (size_t)(4 * tq + t) * L + 2 * lg;
-            *reinterpret_cast<double2*>(TPU + o) = make_double2(su[t][0], su[t][1]);
-            *reinterpret_cast<double2*>(TPV + o) = make_double2(sv[t][0], sv[t][1]);
+            const size_t o = (size_t)(4 * tq + t) * L + lg;
+            TPU[o] = su[t][0];
+            TPU[o + 32] = su[t][1];
+            TPV[o] = sv[t][0];
+            TPV[o + 32] = sv[t][1];
           }
         }
         __syncthreads();
         if (!hs) {
 #pragma unroll
           for (int t = 0; t < 4; ++t) {
-            const size_t o = (size_t)(4 * tq + t) * L + 2 * lg;
-            const double2 hu = *reinterpret_cast<const double2*>(TPU + o);
-            const double2 hv = *reinterpret_cast<const double2*>(TPV + o);
-            const double u0 = su[t][0] + hu.x, u1 = su[t][1] + hu.y;
-            const double v0 = sv[t][0] + hv.x, v1 = sv[t][1] + hv.y;
-            *reinterpret_cast<double2*>(TPU + o) = make_double2(u0, u1);
-            *reinterpret_cast<double2*>(TPV + o) = make_double2(v0, v1);
-            *reinterpret_cast<float2*>(TPUf + o) = make_float2((float)u0, (float)u1);
-            *reinterpret_cast<float2*>(TPVf + o) = make_float2((float)v0, (float)v1);
+            const size_t o = (size_t)(4 * tq + t) * L + lg;
+            const double u0 = su[t][0] + TPU[o], u1 = su[t][1] + TPU[o + 32];
+            const double v0 = sv[t][0] + TPV[o], v1 = sv[t][1] + TPV[o + 32];
+            TPU[o] = u0;
+            TPU[o + 32] = u1;
+            TPV[o] = v0;
+            TPV[o + 32] = v1;
+            TPUf[o] = (float)u0;
+            TPUf[o + 32] = (float)u1;
+            TPVf[o] = (float)v0;
+            TPVf[o + 32] = (float)v1;
           }
         }
         __syncthreads();
@@ -273,7 +282,7 @@ k_encode_keys_table(Geom g, int n_slots, const double* __restrict__ atoms,
           for (int l = lane; l < L; l += 32) {
             double su = 0.0, sv = 0.0;
             for (int si = 0; si < gs; ++si) {
-              const double2 u = U[(size_t)si * L + l];
+              const double2 u = U[(size_t)si * us + l];
               const double px = p[2 * si], py = p[2 * si + 1];
               su = fma(px, u.x, fma(py, u.y, su));
               sv = fma(py, u.x, fma(-px, u.y, sv));
@@ -292,7 +301,7 @@ k_encode_keys_table(Geom g, int n_slots, const double* __restrict__ atoms,
         const double scale = sqrt(pn) + 2.0 * mn;
         const double scale2 = scale * scale * fmax(1.0, w2 / 128.0);
         if (!(pn < 1e300) || !(mn < 1e150)) {
-          chosen = exact_search(p, U, L, gs, B, pu, pv, false, 0.0);
+          chosen = exact_search(p, U, us, L, gs, B, pu, pv, false, 0.0);
         } else if (scale2 > 1e-30 && scale2 < 1e30) {
           // fp32 screen (twice the pair rate of fp64).  Each screen value is
           // within 3 * 2^-24 * scale^2 of the exact shifted distance (inputs
@@ -369,7 +378,7 @@ k_encode_keys_table(Geom g, int n_slots, const double* __restrict__ atoms,
           if (ru > gb + margin) {
             chosen = gc;
           } else {
-            chosen = exact_search(p, U, L, gs, Bf, puf, pvf, true, gb + margin);
+            chosen = exact_search(p, U, us, L, gs, Bf, puf, pvf, true, gb + margin);
           }
         } else {
           // single pass: lane-local best and runner-up, then warp merge
@@ -399,7 +408,7 @@ k_encode_keys_table(Geom g, int n_slots, const double* __restrict__ atoms,
           if (ru > gb + margin) {
             chosen = gc;
           } else {
-            chosen = exact_search(p, U, L, gs, B, pu, pv, true, gb + margin);
+            chosen = exact_search(p, U, us, L, gs, B, pu, pv, true, gb + margin);
           }
         }
         const int ca = chosen / L, cb = chosen % L;
@@ -409,7 +418,7 @@ k_encode_keys_table(Geom g, int n_slots, const double* __restrict__ atoms,
           b_out[idx] = (uint16_t)cb;
         }
         for (int si = lane; si < gs; si += 32) {
-          const double2 ua = U[(size_t)si * L + ca], ub = U[(size_t)si * L + cb];
+          const double2 ua = U[(size_t)si * us + ca], ub = U[(size_t)si * us + cb];
           p[2 * si] = __dsub_rn(p[2 * si], __dadd_rn(ua.x, -ub.y));
           p[2 * si + 1] = __dsub_rn(p[2 * si + 1], __dadd_rn(ua.y, ub.x));
         }
@@ -439,7 +448,7 @@ k_encode_keys_brute(Geom g, int n_slots, const double* __restrict__ atoms,
       const double2* U = reinterpret_cast<const double2*>(atoms) +
                          ((size_t)(slot * g.R + r) * g.subs + (size_t)grp * g.g) * g.L;
       double* pg = p + grp * 2 * g.g;
-      const int c = exact_search<double>(pg, U, g.L, g.g, nullptr, nullptr, nullptr, false, 0.0);
+      const int c = exact_search<double>(pg, U, g.L, g.L, g.g, nullptr, nullptr, nullptr, false, 0.0);
       const int ca = c / g.L, cb = c % g.L;
       if (lane == 0) {
         const size_t idx = ((size_t)s * n + i) * (g.R * g.groups) + (size_t)r * g.groups + grp;
@@ -608,7 +617,7 @@ k_encode_keys_small(Geom g, int n_slots, const double* __restrict__ atoms,
 static size_t table_smem(const Geom& g) {
   // per-warp projection rows, or (head presets) per-token projection tables
   const size_t rows = (g.L == 64 && g.g == 64) ? kEncTok : kEncWarps;
-  return sizeof(double) * (2 * (size_t)g.g * g.L + (size_t)g.L * g.L + (size_t)kEncTok * g.d +
+  return sizeof(double) * (2 * (size_t)g.g * (g.L + 1) + (size_t)g.L * g.L + (size_t)kEncTok * g.d +
                            2 * rows * g.L) +
          sizeof(float) * ((size_t)g.L * g.L + 2 * rows * g.L);
 }
