@@ -311,16 +311,18 @@ k_encode_keys_table(Geom g, int n_slots, const double* __restrict__ atoms,
           // re-checked exactly whenever the screen is not decisive.
           float b1 = INFINITY, b2 = INFINITY;
           int c1 = 0x7fffffff;
+          float m1a = INFINITY, m1b = INFINITY;
           if (L == 64) {
             // lane = columns b = 2 lane, 2 lane + 1 (one LDS.64 per row);
-            // per column the running min / argmin / runner-up of
-            // x = fl(B - 2 pu) over a, the "- 2 pv[b]" applied at the end
-            // (fl(x - t) is monotone in x, so the column's best and
-            // runner-up screen values are those of x; ties only matter
-            // where the margin test sends the token to the exact search)
+            // per column only the running min and runner-up of
+            // x = fl(B - 2 pu) over a (4 instructions per pair), the
+            // "- 2 pv[b]" applied at the end: fl(x - t) is monotone in x, so
+            // the column's best and runner-up screen values are those of x.
+            // No index is tracked: when the screen is decisive the best is
+            // unique and its row is recovered from the winning column below;
+            // ties leave the runner-up equal to the best, i.e. not decisive.
             const int b0 = 2 * lane;
-            float m1a = INFINITY, m2a = INFINITY, m1b = INFINITY, m2b = INFINITY;
-            int ia = 0, ib = 0;
+            float m2a = INFINITY, m2b = INFINITY;
 #pragma unroll 4
             for (int a0 = 0; a0 < 64; a0 += 4) {
               const float4 pu4 = *reinterpret_cast<const float4*>(puf + a0);
@@ -329,10 +331,8 @@ k_encode_keys_table(Geom g, int n_slots, const double* __restrict__ atoms,
               for (int u = 0; u < 4; ++u) {
                 const float2 bb = *reinterpret_cast<const float2*>(Bf + (a0 + u) * 64 + b0);
                 const float xa = fmaf(-2.f, pus[u], bb.x), xb = fmaf(-2.f, pus[u], bb.y);
-                if (xa < m1a) ia = a0 + u;
                 m2a = fminf(m2a, fmaxf(m1a, xa));
                 m1a = fminf(m1a, xa);
-                if (xb < m1b) ib = a0 + u;
                 m2b = fminf(m2b, fmaxf(m1b, xb));
                 m1b = fminf(m1b, xb);
               }
@@ -340,11 +340,10 @@ k_encode_keys_table(Geom g, int n_slots, const double* __restrict__ atoms,
             const float2 pv2 = *reinterpret_cast<const float2*>(pvf + b0);
             const float va = m1a - 2.f * pv2.x, vb = m1b - 2.f * pv2.y;
             const float ra = m2a - 2.f * pv2.x, rb = m2b - 2.f * pv2.y;
-            const int ca = ia * 64 + b0, cb = ib * 64 + b0 + 1;
-            if (vb < va || (vb == va && cb < ca)) {
-              b1 = vb; c1 = cb; b2 = fminf(rb, va);
+            if (vb < va) {  // c1 = the column (the row comes later)
+              b1 = vb; c1 = b0 + 1; b2 = fminf(rb, va);
             } else {
-              b1 = va; c1 = ca; b2 = fminf(ra, vb);
+              b1 = va; c1 = b0; b2 = fminf(ra, vb);
             }
           } else {
             for (int b = lane; b < L; b += 32) {
@@ -376,7 +375,18 @@ k_encode_keys_table(Geom g, int n_slots, const double* __restrict__ atoms,
           for (int o = 16; o; o >>= 1) ru = fminf(ru, __shfl_xor_sync(0xffffffffu, ru, o));
           const float margin = (float)(kMarginRel32 * scale2);
           if (ru > gb + margin) {
-            chosen = gc;
+            if (L == 64) {
+              // row of the unique best in column gc: the a whose x (same
+              // fmaf, same inputs) equals the column minimum
+              const float mc = __shfl_sync(0xffffffffu, (gc & 1) ? m1b : m1a, gc >> 1);
+              const float x0 = fmaf(-2.f, puf[lane], Bf[lane * 64 + gc]);
+              const float x1 = fmaf(-2.f, puf[lane + 32], Bf[(lane + 32) * 64 + gc]);
+              const unsigned k0 = __ballot_sync(0xffffffffu, x0 == mc);
+              const unsigned k1 = __ballot_sync(0xffffffffu, x1 == mc);
+              chosen = (k0 ? __ffs(k0) - 1 : 31 + __ffs(k1)) * 64 + gc;
+            } else {
+              chosen = gc;
+            }
           } else {
             chosen = exact_search(p, U, us, L, gs, Bf, puf, pvf, true, gb + margin);
           }
