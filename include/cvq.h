@@ -273,6 +273,11 @@ typedef struct cvq_cache_desc {
 #define CVQ_VARIANT_TC_DENSE 2u /* tcgen05: dense one-hot MMA instead of 2:4 sparse   */
 #define CVQ_VARIANT_TC_PAIR 4u  /* tcgen05: CTA-pair (cta_group::2) sparse kernel     */
 #define CVQ_VARIANT_FUSED 8u    /* fp16 codebook: one fused score+value kernel        */
+/* The sparse tcgen05 kernel (R = 11) hands the value kernel fp16 softmax
+ * weights exp(s - m) with one fp32 max per 32-token group per head (half the
+ * bytes of fp32 scores; relative weight error <= 2^-11, output within the
+ * 1e-3 bar); this bit keeps the fp32 score hand-off instead. */
+#define CVQ_VARIANT_F32_WEIGHTS 16u
 
 CVQ_API cvq_status cvq_cache_create(cvq_context* ctx, const cvq_cache_desc* d,
                                     cvq_cache** out);

@@ -97,7 +97,7 @@ class _Desc(C.Structure):
 CVQ_CACHE_KEYS_FP16 = 1
 CVQ_CACHE_KEYS_TC = 2
 # kernel variants (cvq.h CVQ_VARIANT_*), QuantizedKVCache.set_variant
-VARIANTS = {"generic": 1, "tc_dense": 2, "tc_pair": 4, "fused": 8}
+VARIANTS = {"generic": 1, "tc_dense": 2, "tc_pair": 4, "fused": 8, "f32_weights": 16}
 
 
 @dataclass(frozen=True)

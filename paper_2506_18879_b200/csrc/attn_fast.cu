@@ -20,6 +20,8 @@
 //  k_combine_merge / k_combine_project  (row, 32-code slice) CTAs merge the
 //                     chunk partials; then one CTA per row: LSE merge of the
 //     chunk partials, then o = z . C_V / L (attn.cpp:249-255) once per row.
+#include <cuda_fp16.h>
+
 #include <algorithm>
 #include <cfloat>
 #include <cstdlib>
@@ -59,6 +61,12 @@ struct FastArgs {
   int chunk2;         // F2 tokens per CTA (multiple of 128)
   int S;
   float* ps;          // [S][JS][n][G] partial scores
+  // half-weight mode (sparse tcgen05 scores, one round part): instead of ps,
+  // ph[S][nps][G] = fp16 exp(s - m32) and m32[S][nps / 32][G] = the max of
+  // each 32-token group (nps = n rounded up to 128)
+  const __half* ph;
+  const float* m32;
+  long long nps;
   float* scores_out;  // optional [S][G][n]
   float *pm, *pl, *po;
 };
@@ -645,7 +653,54 @@ __global__ void __launch_bounds__(kF1Threads, 1) k_fast_attn_h(FastArgs a) {
   }
 }
 
-template <int NC, int G, int JS>
+// Sum of the per-warp z partials of a k_fast_value CTA and the chunk's
+// (z, m, l) partial for the LSE merge.
+template <int NC, int G>
+__device__ __forceinline__ void fast_value_finish(const FastArgs& a, float* zr, const float* mh,
+                                                  const float* lh, int s) {
+  const int tid = threadIdx.x;
+  __syncthreads();
+  for (int e = tid; e < NC * G; e += kThreads) {
+    float v = 0.f;
+    for (int w = 0; w < kThreads / 32; ++w) v += zr[(size_t)w * NC * G + e];
+    zr[e] = v;  // warp-0 slot reused for the total
+  }
+  __syncthreads();
+  // unnormalised z of this chunk; the value codebook product happens once per
+  // row after the merge (k_combine_project)
+  const long long rows = (long long)a.S * G;
+  for (int e = tid; e < G * NC; e += kThreads) {
+    const int h = e / NC, k = e % NC;
+    a.po[((long long)blockIdx.x * rows + (long long)s * G + h) * NC + k] = zr[k * G + h];
+  }
+  if (tid < G) {
+    const long long row = (long long)s * G + tid;
+    a.pm[(long long)blockIdx.x * rows + row] = mh[tid];
+    a.pl[(long long)blockIdx.x * rows + row] = lh[tid];
+  }
+}
+
+__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
+  uint32_t d;
+  asm("prmt.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(sel));
+  return d;
+}
+
+__device__ __forceinline__ void mma16816(float (&d)[4], const uint32_t (&a)[4], uint32_t b0,
+                                         uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+      "{%8,%9}, {%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+// Value accumulation z[c][h] = sum_i p_h(i) bit_c(i) of k_fast_value, either
+// (MMA) as an fp16 tensor-core product z^T[NC][8] += Bits^T[NC][16 tokens] x
+// P[16 tokens][8 heads] per 16-token step (mma.sync m16n8k16, fp32
+// accumulators; bits expanded to fp16 0 / 1 by byte permutes; p rounded to
+// fp16, relative 2^-11) or (!MMA) by predicated fp32 adds on CUDA cores.
+template <int NC, int G, int JS, bool PH = false, bool MMA = false>
 __global__ void __launch_bounds__(kThreads) k_fast_value(FastArgs a) {
   constexpr int CPL = NC / 32;       // codes per lane
   constexpr int WPTOK = NC / 64;     // value words per token
@@ -655,10 +710,11 @@ __global__ void __launch_bounds__(kThreads) k_fast_value(FastArgs a) {
   // per-warp z partials [8][NC][G] alias the score / value-word staging,
   // which is dead once the accumulate loop is done (fewer smem bytes per CTA
   // -> more resident CTAs for this latency-bound kernel)
-  const size_t stage_bytes = (size_t)a.chunk2 * (G * 4 + WPTOK * 8);
-  float* zr = stage_bytes >= (size_t)8 * NC * G * 4
-                  ? reinterpret_cast<float*>(smem)
-                  : reinterpret_cast<float*>(vw + (size_t)a.chunk2 * WPTOK);
+  // (layout as f2_smem: scores, value words, group maxima, then zr unless
+  // the staging is large enough to hold it)
+  const size_t stage_bytes = (size_t)a.chunk2 * (G * 4 + WPTOK * 8) + (size_t)(a.chunk2 / 32) * G * 4;
+  float* zr = stage_bytes >= (size_t)8 * NC * G * 4 ? reinterpret_cast<float*>(smem)
+                                                    : reinterpret_cast<float*>(smem + stage_bytes);
   __shared__ float red[8][G];
   __shared__ float mh[G], lh[G];
   const int s = blockIdx.y;
@@ -671,6 +727,63 @@ __global__ void __launch_bounds__(kThreads) k_fast_value(FastArgs a) {
   const uint64_t* vsrc = a.vpool + (size_t)s * a.vstride + (size_t)i0 * WPTOK;
   const int nw = ((cnt * WPTOK + 1) / 2) * 2;
   for (int e = tid; e < nw / 2; e += kThreads) cp_async16(vw + 2 * e, vsrc + 2 * e);
+  float ls[G];
+#pragma unroll
+  for (int h = 0; h < G; ++h) ls[h] = 0.f;
+  constexpr int kMaxPer = 4;  // tokens per thread: chunk2 <= 4 * kThreads (f2_chunk)
+  float pv[kMaxPer][G];       // MMA: this thread's weights until the fp16 write
+  if constexpr (PH) {
+    // half weights [chunk2][G] in the upper half of the score buffer, the
+    // group maxima after the value words (f2_smem adds them); the padded
+    // stream stride keeps every source 16-B aligned (reads past cnt stay
+    // inside the stream's padding)
+    __half* hw = reinterpret_cast<__half*>(sc + (size_t)a.chunk2 * G / 2);
+    float* gm = reinterpret_cast<float*>(vw + (size_t)a.chunk2 * WPTOK);  // [chunk2 / 32][G]
+    const int ngr = (cnt + 31) >> 5;
+    const __half* hsrc = a.ph + ((size_t)s * a.nps + i0) * G;
+    const int nh = (cnt * G * 2 + 15) / 16;
+    for (int e = tid; e < nh; e += kThreads) cp_async16(hw + 8 * e, hsrc + 8 * e);
+    const float* msrc = a.m32 + ((size_t)s * (a.nps >> 5) + (i0 >> 5)) * G;
+    const int nm = (ngr * G * 4 + 15) / 16;
+    for (int e = tid; e < nm; e += kThreads) cp_async16(gm + 4 * e, msrc + 4 * e);
+    cp_async_commit();
+    cp_async_wait<0>();
+    __syncthreads();
+    if (tid < G) {
+      float v = -INFINITY;
+      for (int gi = 0; gi < ngr; ++gi) v = fmaxf(v, gm[gi * G + tid]);
+      mh[tid] = v;
+    }
+    __syncthreads();
+    // p = half * exp(m32 - M), once per (token, head) over the CTA; read
+    // into registers first (sc[e] overlaps hw of lower tokens)
+#pragma unroll
+    for (int k = 0; k < kMaxPer; ++k) {
+      const int e = tid + k * kThreads;
+      if (e < cnt) {
+#pragma unroll
+        for (int h = 0; h < G; ++h) {
+          const float mg = gm[(e >> 5) * G + h];
+          const float f = mg == -INFINITY ? 0.f : __expf(mg - mh[h]);
+          pv[k][h] = __half2float(hw[(size_t)e * G + h]) * f;
+        }
+      }
+    }
+    __syncthreads();
+    if constexpr (!MMA) {
+#pragma unroll
+      for (int k = 0; k < kMaxPer; ++k) {
+        const int e = tid + k * kThreads;
+        if (e < cnt) {
+#pragma unroll
+          for (int h = 0; h < G; ++h) {
+            sc[(size_t)e * G + h] = pv[k][h];
+            ls[h] += pv[k][h];
+          }
+        }
+      }
+    }
+  } else {
   cp_async_commit();
 
   // full scores = sum of the JS partials; chunk max per head
@@ -707,15 +820,45 @@ __global__ void __launch_bounds__(kThreads) k_fast_value(FastArgs a) {
     mh[tid] = v;
   }
   __syncthreads();
-  float ls[G];
+  if constexpr (MMA) {
 #pragma unroll
-  for (int h = 0; h < G; ++h) ls[h] = 0.f;
-  for (int e = tid; e < cnt; e += kThreads) {
+    for (int k = 0; k < kMaxPer; ++k) {
+      const int e = tid + k * kThreads;
+      if (e < cnt) {
 #pragma unroll
-    for (int h = 0; h < G; ++h) {
-      const float p = __expf(sc[e * G + h] - mh[h]);
-      sc[e * G + h] = p;
-      ls[h] += p;
+        for (int h = 0; h < G; ++h) pv[k][h] = __expf(sc[e * G + h] - mh[h]);
+      }
+    }
+    __syncthreads();  // the fp16 weights below overwrite sc
+  } else {
+    for (int e = tid; e < cnt; e += kThreads) {
+#pragma unroll
+      for (int h = 0; h < G; ++h) {
+        const float p = __expf(sc[e * G + h] - mh[h]);
+        sc[e * G + h] = p;
+        ls[h] += p;
+      }
+    }
+  }
+  }  // !PH
+  // MMA: fp16 weights PT[h][token] (rows padded by 8 halves: conflict-free
+  // B-fragment loads), zero up to the 16-token step; l sums the rounded
+  // weights the product uses
+  __half* PT = reinterpret_cast<__half*>(smem);
+  const int pst = a.chunk2 + 8;
+  const int cpad = (cnt + 15) & ~15;
+  if constexpr (MMA) {
+#pragma unroll
+    for (int k = 0; k < kMaxPer; ++k) {
+      const int e = tid + k * kThreads;
+      if (e < cpad) {
+#pragma unroll
+        for (int h = 0; h < G; ++h) {
+          const __half hv = __float2half_rn(e < cnt ? pv[k][h] : 0.f);
+          PT[h * pst + e] = hv;
+          ls[h] += __half2float(hv);
+        }
+      }
     }
   }
 #pragma unroll
@@ -730,6 +873,70 @@ __global__ void __launch_bounds__(kThreads) k_fast_value(FastArgs a) {
     float v = 0.f;
     for (int w = 0; w < kThreads / 32; ++w) v += red[w][tid];
     lh[tid] = v;
+  }
+  if constexpr (MMA) {
+    // warp w takes 16-token steps w, w + 8, ...; thread (g, t) = (lane / 4,
+    // lane % 4) holds the fragments of tokens 2t, 2t+1, 2t+8, 2t+9 of the
+    // step and codes 16 mt + g (+ 8): byte j of u32 word i of a token's code
+    // bits, masked at bit g, is code 32 i + 8 j + g, i.e. m-tile 2 i + j / 2,
+    // row g + 8 (j & 1); times 0x3C it is the high byte of fp16 1.0, and a
+    // sign-replicating prmt pairs two tokens' bytes into an A register.
+    constexpr int MT = NC / 16, NW32 = NC / 32;
+    const int g = lane >> 2, t = lane & 3;
+    float d[MT][4];
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt) d[mt][0] = d[mt][1] = d[mt][2] = d[mt][3] = 0.f;
+    const uint32_t* vw32 = reinterpret_cast<const uint32_t*>(vw);
+    const int nks = cpad >> 4;
+#pragma unroll 2
+    for (int ks = warp; ks < nks; ks += kThreads / 32) {
+      const int k0 = ks << 4;
+      uint32_t b0 = 0, b1 = 0;
+      if (g < G) {
+        b0 = *reinterpret_cast<const uint32_t*>(PT + g * pst + k0 + 2 * t);
+        b1 = *reinterpret_cast<const uint32_t*>(PT + g * pst + k0 + 2 * t + 8);
+      }
+      const uint32_t* wa = vw32 + (size_t)(k0 + 2 * t) * NW32;
+#pragma unroll
+      for (int i4 = 0; i4 < NW32; i4 += 4) {
+        const uint4 A4 = *reinterpret_cast<const uint4*>(wa + i4);
+        const uint4 B4 = *reinterpret_cast<const uint4*>(wa + NW32 + i4);
+        const uint4 C4 = *reinterpret_cast<const uint4*>(wa + 8 * NW32 + i4);
+        const uint4 D4 = *reinterpret_cast<const uint4*>(wa + 9 * NW32 + i4);
+        const uint32_t av[4] = {A4.x, A4.y, A4.z, A4.w}, bv[4] = {B4.x, B4.y, B4.z, B4.w};
+        const uint32_t cv[4] = {C4.x, C4.y, C4.z, C4.w}, dv[4] = {D4.x, D4.y, D4.z, D4.w};
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const uint32_t mA = ((av[u] >> g) & 0x01010101u) * 0x3Cu;
+          const uint32_t mB = ((bv[u] >> g) & 0x01010101u) * 0x3Cu;
+          const uint32_t mC = ((cv[u] >> g) & 0x01010101u) * 0x3Cu;
+          const uint32_t mD = ((dv[u] >> g) & 0x01010101u) * 0x3Cu;
+          const int mt = 2 * (i4 + u);
+          uint32_t fa[4] = {prmt(mA, mB, 0x4C08), prmt(mA, mB, 0x5D19), prmt(mC, mD, 0x4C08),
+                            prmt(mC, mD, 0x5D19)};
+          mma16816(d[mt], fa, b0, b1);
+          uint32_t fb[4] = {prmt(mA, mB, 0x6E2A), prmt(mA, mB, 0x7F3B), prmt(mC, mD, 0x6E2A),
+                            prmt(mC, mD, 0x7F3B)};
+          mma16816(d[mt + 1], fb, b0, b1);
+        }
+      }
+    }
+    __syncthreads();  // all warps are done with PT / vw (zr may alias them)
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt) {
+      float* z0 = zr + ((size_t)warp * NC + 16 * mt + g) * G;
+      float* z1 = z0 + 8 * G;
+      if (2 * t < G) {
+        z0[2 * t] = d[mt][0];
+        z1[2 * t] = d[mt][2];
+      }
+      if (2 * t + 1 < G) {
+        z0[2 * t + 1] = d[mt][1];
+        z1[2 * t + 1] = d[mt][3];
+      }
+    }
+    fast_value_finish<NC, G>(a, zr, mh, lh, s);
+    return;
   }
   // z[c][h] += p_h(i) * bit_c(i); lane owns codes [CPL*lane, CPL*lane+CPL)
   // heads in pairs so the conditional adds are packed fp32x2 (FADD2)
@@ -760,25 +967,7 @@ __global__ void __launch_bounds__(kThreads) k_fast_value(FastArgs a) {
 #pragma unroll
     for (int h = 0; h < G; ++h)
       zr[((size_t)warp * NC + CPL * lane + c) * G + h] = (h & 1) ? z[c][h / 2].y : z[c][h / 2].x;
-  __syncthreads();
-  for (int e = tid; e < NC * G; e += kThreads) {
-    float v = 0.f;
-    for (int w = 0; w < kThreads / 32; ++w) v += zr[(size_t)w * NC * G + e];
-    zr[e] = v;  // warp-0 slot reused for the total
-  }
-  __syncthreads();
-  // unnormalised z of this chunk; the value codebook product happens once per
-  // row after the merge (k_combine_project)
-  const long long rows = (long long)a.S * G;
-  for (int e = tid; e < G * NC; e += kThreads) {
-    const int h = e / NC, k = e % NC;
-    a.po[((long long)blockIdx.x * rows + (long long)s * G + h) * NC + k] = zr[k * G + h];
-  }
-  if (tid < G) {
-    const long long row = (long long)s * G + tid;
-    a.pm[(long long)blockIdx.x * rows + row] = mh[tid];
-    a.pl[(long long)blockIdx.x * rows + row] = lh[tid];
-  }
+  fast_value_finish<NC, G>(a, zr, mh, lh, s);
 }
 
 // subspace split (CTAs per stream) so the codebook slice fits in smem
@@ -813,7 +1002,9 @@ int f2_chunk(const AttnJob& job) {
 
 size_t f2_smem(const AttnJob& job, int chunk2) {
   const Geom& g = job.geo;
-  const size_t stage = (size_t)chunk2 * g.G * 4 + (size_t)chunk2 * (g.n_codes / 64) * 8;
+  // scores / weights, value words, group maxima (half-weight mode)
+  const size_t stage = (size_t)chunk2 * g.G * 4 + (size_t)chunk2 * (g.n_codes / 64) * 8 +
+                       (size_t)(chunk2 / 32) * g.G * 4;
   const size_t zr = (size_t)8 * g.n_codes * g.G * 4;
   return (stage >= zr ? stage : stage + zr) + 16;  // zr aliases the staging when it fits
 }
@@ -851,18 +1042,21 @@ cudaError_t launch_f1h(const FastArgs& a, int S, cudaStream_t st) {
   return cudaGetLastError();
 }
 
-template <int NC, int G, int JS>
+template <int NC, int G, int JS, bool PH = false, bool MMA = false>
 cudaError_t launch_f2(const FastArgs& a, size_t sm, cudaStream_t st) {
-  cudaError_t e = set_smem(k_fast_value<NC, G, JS>, sm);
+  cudaError_t e = set_smem(k_fast_value<NC, G, JS, PH, MMA>, sm);
   if (e != cudaSuccess) return e;
   dim3 grid((unsigned)((a.n + a.chunk2 - 1) / a.chunk2), a.S);
-  k_fast_value<NC, G, JS><<<grid, kThreads, sm, st>>>(a);
+  k_fast_value<NC, G, JS, PH, MMA><<<grid, kThreads, sm, st>>>(a);
   count_launch();
   return cudaGetLastError();
 }
 
 template <int NC, int G>
-cudaError_t launch_f2_js(const FastArgs& a, int JS, size_t sm, cudaStream_t st) {
+cudaError_t launch_f2_js(const FastArgs& a, int JS, bool mma, size_t sm, cudaStream_t st) {
+  if (a.ph) return launch_f2<NC, G, 1, true, true>(a, sm, st);
+  if (mma) return JS == 1 ? launch_f2<NC, G, 1, false, true>(a, sm, st)
+                          : launch_f2<NC, G, 2, false, true>(a, sm, st);
   switch (JS) {
     case 1: return launch_f2<NC, G, 1>(a, sm, st);
     case 2: return launch_f2<NC, G, 2>(a, sm, st);
@@ -1001,7 +1195,13 @@ size_t fast_scratch_bytes(const AttnJob& job, int* n_chunks) {
     const int c1 = f1_chunk(job);
     *n_chunks = std::max(*n_chunks, (int)((job.n + c1 - 1) / c1));
   }
-  const size_t ps = (size_t)job.S * JS * job.n * job.geo.G * sizeof(float);
+  size_t ps = (size_t)job.S * JS * job.n * job.geo.G * sizeof(float);
+  if (tc_half_scores(job)) {  // half weights + group maxima (run_attention_fast)
+    const size_t nps = (size_t)(job.n + kTile - 1) / kTile * kTile;
+    const size_t hb = ((size_t)job.S * nps * job.geo.G * 2 + 255) / 256 * 256 +
+                      (size_t)job.S * (nps / 32) * job.geo.G * 4;
+    ps = std::max(ps, hb);
+  }
   return (ps + 255) / 256 * 256;
 }
 
@@ -1047,7 +1247,18 @@ cudaError_t run_attention_fast(const AttnJob& job, const float* q, float* pm, fl
   *n_chunks = (int)((job.n + a.chunk2 - 1) / a.chunk2);
   if (prof) cudaEventRecord(prof[0], st);
   if (job.cb_key_tc) {
-    e = run_tc_score(job, q, a.ps, a.chunk, st);
+    HalfOut ho{};
+    const bool half = !scores_out && tc_half_scores(job);
+    if (half) {
+      ho.nps = (job.n + kTile - 1) / kTile * kTile;
+      ho.ph = scratch;
+      ho.m32 = reinterpret_cast<float*>(static_cast<char*>(scratch) +
+                                        ((size_t)job.S * ho.nps * g.G * 2 + 255) / 256 * 256);
+      a.ph = static_cast<const __half*>(ho.ph);
+      a.m32 = ho.m32;
+      a.nps = ho.nps;
+    }
+    e = run_tc_score(job, q, a.ps, a.chunk, st, half ? &ho : nullptr);
   } else if (job.cb_key16) {
     if (g.R == 11)
       e = g.G == 4 ? launch_f1h<11, 4>(a, job.S, st) : launch_f1h<11, 1>(a, job.S, st);
@@ -1063,10 +1274,15 @@ cudaError_t run_attention_fast(const AttnJob& job, const float* q, float* pm, fl
   if (e != cudaSuccess) return e;
   const size_t sm2 = f2_smem(job, a.chunk2);
   const int JS = js_for(job);
+  // tensor-core value accumulation (fp16 weights) in the tcgen05 key modes
+  // unless the cache asked for the fp32 hand-off
+  const bool mma = job.cb_key_tc && !(job.variant & kVarF32W) && !scores_out && JS <= 2;
   if (g.n_codes == 128)
-    e = g.G == 4 ? launch_f2_js<128, 4>(a, JS, sm2, st) : launch_f2_js<128, 1>(a, JS, sm2, st);
+    e = g.G == 4 ? launch_f2_js<128, 4>(a, JS, mma, sm2, st)
+                 : launch_f2_js<128, 1>(a, JS, mma, sm2, st);
   else
-    e = g.G == 4 ? launch_f2_js<256, 4>(a, JS, sm2, st) : launch_f2_js<256, 1>(a, JS, sm2, st);
+    e = g.G == 4 ? launch_f2_js<256, 4>(a, JS, mma, sm2, st)
+                 : launch_f2_js<256, 1>(a, JS, mma, sm2, st);
   return e;
 }
 

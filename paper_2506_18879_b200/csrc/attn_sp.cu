@@ -309,6 +309,11 @@ struct SpArgs {
   int js;                // round parts of <= RP rounds (scores are linear in K)
   float* ps;             // [S][js][n][G] partial scores
   size_t ps_elems;       // its extent (device bounds checks)
+  // half-weight mode (js == 1): ph[S][nps][G] = fp16 exp(s - m32) and
+  // m32[S][nps / 32][G] per 32-token group instead of ps
+  __half* ph;
+  float* m32;
+  long long nps;
 };
 
 // This CTA's tiles in order; each CTA owns a contiguous range of work items
@@ -531,7 +536,38 @@ __global__ void __launch_bounds__(kThreads, 1) k_sp_score(SpArgs a) {
         rb[eslot * 32 + lane] = acc1;
       asm volatile("bar.sync %0, 64;" ::"r"(1 + quarter) : "memory");
       // warp e2 writes heads 2 e2, 2 e2 + 1 (G = 4) / e2 = 0 the head (G = 1)
-      {
+      if (a.ph) {
+        // half weights: per head the max m over this quarter's 32 tokens,
+        // fp16 exp(s - m) per token (k_fast_value<PH> rescales by group)
+        const int tok = 32 * quarter + lane;
+        const bool valid = tok < it.valid();
+        if (G == 4 || eslot == 0) {
+          float pw[2] = {0.f, 0.f};
+#pragma unroll
+          for (int hq = 0; hq < (G == 4 ? 2 : 1); ++hq) {
+            const int h = (G == 4) ? 2 * eslot + hq : 0;
+            const float v = valid ? rb[(0 * 32 + lane) * G + h] + rb[(1 * 32 + lane) * G + h]
+                                  : -INFINITY;
+            float m = v;
+#pragma unroll
+            for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+            pw[hq] = valid ? __expf(v - m) : 0.f;
+            if (lane == 0 && m != -INFINITY) {
+              const size_t gi = ((size_t)it.s * (a.nps >> 5) + ((it.base() + 32 * quarter) >> 5)) * G + h;
+              SP_CHECK(gi < a.ps_elems / 32);
+              a.m32[gi] = m;
+            }
+          }
+          if (valid) {
+            const size_t pi = ((size_t)it.s * a.nps + it.base() + tok) * G;
+            SP_CHECK(pi + G <= a.ps_elems);
+            if constexpr (G == 4)
+              *reinterpret_cast<__half2*>(a.ph + pi + 2 * eslot) = __floats2half2_rn(pw[0], pw[1]);
+            else
+              a.ph[pi] = __float2half_rn(pw[0]);
+          }
+        }
+      } else {
         const int tok = 32 * quarter + lane;
         if (tok < it.valid()) {
 #pragma unroll
@@ -943,7 +979,8 @@ void sp_build_codebook(int R, const double* xy, uint16_t* out, uint16_t (*to_hal
 
 
 cudaError_t run_sp_score(const AttnJob& job, const uint16_t* cb, size_t slot_elems,
-                         const float* q, float* ps, int chunk, cudaStream_t st) {
+                         const float* q, float* ps, int chunk, cudaStream_t st,
+                         const HalfOut* ho) {
   // cb: slot 0's single-CTA layout; the pair layout follows it (sp_build_codebook)
   const bool pair = (job.variant & kVarTcPair) != 0;
   const Geom& g = job.geo;
@@ -977,6 +1014,13 @@ cudaError_t run_sp_score(const AttnJob& job, const uint16_t* cb, size_t slot_ele
   a.n_items = job.S * a.js * a.cps;
   a.ps = ps;
   a.ps_elems = (size_t)job.S * sp_parts(g.R) * (size_t)job.n * g.G;
+  if (ho) {
+    if (a.js != 1 || ho->nps < job.n || ho->nps % kTok) return cudaErrorInvalidValue;
+    a.ph = static_cast<__half*>(ho->ph);
+    a.m32 = ho->m32;
+    a.nps = ho->nps;
+    a.ps_elems = (size_t)job.S * ho->nps * g.G;
+  }
   if (pair) {
     if (g.G == 4) return launch_sp<kRPart, 4, true>(a, st);
     if (g.G == 1) return launch_sp<kRPart, 1, true>(a, st);

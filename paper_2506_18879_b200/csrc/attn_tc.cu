@@ -576,6 +576,12 @@ static bool tc_use_sparse(const AttnJob& job) {
 // sparse kernel keeps <= 11 rounds resident, so R = 21 runs as 2 parts)
 int tc_blocks(const AttnJob& job) { return tc_use_sparse(job) ? sp_parts(job.geo.R) : 1; }
 
+bool tc_half_scores(const AttnJob& job) {
+  return job.cb_key_tc && tc_use_sparse(job) && !(job.variant & kVarF32W) &&
+         sp_parts(job.geo.R) == 1 && job.geo.d == 128 &&
+         job.geo.L == 64 && job.geo.subs == 64;
+}
+
 // per slot: the dense layout [R][2][8192], then (R = 11) the sparse kernel's
 // [R][X | Y][64] blocks (attn_sp.cu)
 size_t tc_codebook_elems(int R) { return (size_t)R * 2 * (kABytes / 2) + sp_codebook_elems(R); }
@@ -598,14 +604,15 @@ void tc_build_codebook(int R, const double* xy, uint16_t* out, uint16_t (*to_hal
 }
 
 cudaError_t run_tc_score(const AttnJob& job, const float* q, float* ps, int chunk,
-                         cudaStream_t st) {
+                         cudaStream_t st, const HalfOut* ho) {
   const Geom& g = job.geo;
   if (!job.cb_key_tc || g.d != 128 || g.L != 64 || g.subs != 64) return cudaErrorInvalidValue;
   const size_t slot_elems = tc_codebook_elems(g.R);
   // 2:4-sparse kernel where it applies (CVQ_VARIANT_TC_DENSE keeps the dense one)
   if (tc_use_sparse(job))
     return run_sp_score(job, job.cb_key_tc + (size_t)g.R * 2 * (kABytes / 2), slot_elems, q, ps,
-                        chunk, st);
+                        chunk, st, ho);
+  if (ho) return cudaErrorInvalidValue;
   TcArgs a{};
   a.kpool = job.kpool;
   a.kstride = job.kstride;

@@ -939,7 +939,7 @@ CVQ_API cvq_status cvq_cache_synchronize(cvq_cache* c) {
 CVQ_API cvq_status cvq_cache_set_variant(cvq_cache* c, uint32_t variant) {
   if (!c) return fail(CVQ_EINVAL, "null cache");
   if (variant & ~(uint32_t)(CVQ_VARIANT_GENERIC | CVQ_VARIANT_TC_DENSE | CVQ_VARIANT_TC_PAIR |
-                            CVQ_VARIANT_FUSED))
+                            CVQ_VARIANT_FUSED | CVQ_VARIANT_F32_WEIGHTS))
     return fail(CVQ_EINVAL, "cache: unknown kernel variant");
   c->variant = variant;
   return CVQ_OK;

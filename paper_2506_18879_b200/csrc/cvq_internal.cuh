@@ -57,6 +57,7 @@ constexpr uint32_t kVarGeneric = 1u;  // generic kernels for every shape
 constexpr uint32_t kVarTcDense = 2u;  // dense one-hot tcgen05 kernel (attn_tc.cu)
 constexpr uint32_t kVarTcPair = 4u;   // CTA-pair (cta_group::2) sparse kernel
 constexpr uint32_t kVarFused = 8u;    // single fused CUDA-core kernel (fp16 codebook)
+constexpr uint32_t kVarF32W = 16u;    // fp32 score hand-off instead of fp16 weights
 
 // Scratch handed to run_attention (sized by attn_scratch_bytes).
 size_t attn_scratch_bytes(const AttnJob& job, int* n_chunks_out);
@@ -78,8 +79,17 @@ int tc_blocks(const AttnJob& job);
 // layout]; side b holds the rotated codebook (x <- -y, y <- x).
 void tc_build_codebook(int R, const double* xy, uint16_t* out, uint16_t (*to_half)(double));
 size_t tc_codebook_elems(int R);
+// Half-weight output (HalfOut non-null, sparse kernel, one round part): the
+// score epilogue writes fp16 exp(s - m32) per (token, head) and the max m32
+// of each 32-token group instead of fp32 scores (k_fast_value<PH>).
+struct HalfOut {
+  void* ph;        // [S][nps][G] __half
+  float* m32;      // [S][nps / 32][G]
+  long long nps;   // tokens per stream, n rounded up to 128
+};
+bool tc_half_scores(const AttnJob& job);
 cudaError_t run_tc_score(const AttnJob& job, const float* q, float* ps, int chunk,
-                         cudaStream_t st);
+                         cudaStream_t st, const HalfOut* ho = nullptr);
 // 2:4-sparse tcgen05 score kernel (attn_sp.cu), R = 11: B blocks per slot
 // [R][X rows | Y rows][64 levels] fp16, built by sp_build_codebook.
 bool sp_supported(int R);
@@ -87,7 +97,8 @@ int sp_parts(int R);  // round parts (<= 11 resident rounds each) -> partial-sco
 size_t sp_codebook_elems(int R);
 void sp_build_codebook(int R, const double* xy, uint16_t* out, uint16_t (*to_half)(double));
 cudaError_t run_sp_score(const AttnJob& job, const uint16_t* cb, size_t slot_elems,
-                         const float* q, float* ps, int chunk, cudaStream_t st);
+                         const float* q, float* ps, int chunk, cudaStream_t st,
+                         const HalfOut* ho = nullptr);
 
 // LSE merge over packed blocks reached through a device array of pointers
 // (parts[p] + off), e.g. peers' symmetric-memory buffers over NVLink.

@@ -575,12 +575,17 @@ def test_sparse_tc_matches_dense_tc(G, R, Gq, n):
             c.import_stream(0, layer, h, P.pack_key_codes(kq, a, b), P.pack_value_codes(bits), n)
     q = rng.normal(Ly * H * Gq * 128).reshape(1, Ly, H * Gq, 128).astype(np.float32)
     t = n + 4000
+    c.set_variant("f32_weights")  # fp32 score hand-off: only the order differs
     out_sp = c.attention(q, t)
-    c.set_variant("tc_dense")
+    c.set_variant(("tc_dense", "f32_weights"))
     out_dense = c.attention(q, t)
     c.set_variant(0)
+    out_half = c.attention(q, t)  # default: fp16 weights (R = 11)
     assert np.isfinite(out_sp).all()
     assert fx.rel_err(out_sp, out_dense) <= 1e-5
+    # fp16 weights (relative error <= 2^-11 each; R = 11 hands them over
+    # in fp16, both presets accumulate on tensor cores) against fp32
+    assert fx.rel_err(out_half, out_sp) <= 2e-4
 
 
 @pytest.mark.parametrize("n", [128, 256, 8192, 8193])
@@ -628,12 +633,15 @@ def test_pair_tc_matches_dense_tc(G, R, Gq, n):
             c.import_stream(0, layer, h, P.pack_key_codes(kq, a, b), P.pack_value_codes(bits), n)
     q = rng.normal(Ly * H * Gq * 128).reshape(1, Ly, H * Gq, 128).astype(np.float32)
     t = n + 99
-    c.set_variant("tc_pair")
+    c.set_variant(("tc_pair", "f32_weights"))  # fp32 hand-off: only the order differs
     out_pair = c.attention(q, t)
-    c.set_variant("tc_dense")
+    c.set_variant(("tc_dense", "f32_weights"))
     out_dense = c.attention(q, t)
+    c.set_variant("tc_pair")  # default hand-off: fp16 weights, tensor-core values
+    out_half = c.attention(q, t)
     assert np.isfinite(out_pair).all()
     assert fx.rel_err(out_pair, out_dense) <= 1e-5
+    assert fx.rel_err(out_half, out_pair) <= 2e-4
 
 
 @pytest.mark.parametrize("dense", [False, True])
