@@ -701,7 +701,7 @@ __device__ __forceinline__ void mma16816(float (&d)[4], const uint32_t (&a)[4], 
 // accumulators; bits expanded to fp16 0 / 1 by byte permutes; p rounded to
 // fp16, relative 2^-11) or (!MMA) by predicated fp32 adds on CUDA cores.
 template <int NC, int G, int JS, bool PH = false, bool MMA = false>
-__global__ void __launch_bounds__(kThreads) k_fast_value(FastArgs a) {
+__global__ void __launch_bounds__(kThreads, MMA ? 4 : 1) k_fast_value(FastArgs a) {
   constexpr int CPL = NC / 32;       // codes per lane
   constexpr int WPTOK = NC / 64;     // value words per token
   extern __shared__ __align__(16) unsigned char smem[];
@@ -749,24 +749,26 @@ __global__ void __launch_bounds__(kThreads) k_fast_value(FastArgs a) {
     cp_async_commit();
     cp_async_wait<0>();
     __syncthreads();
-    if (tid < G) {
-      float v = -INFINITY;
-      for (int gi = 0; gi < ngr; ++gi) v = fmaxf(v, gm[gi * G + tid]);
-      mh[tid] = v;
+    if (warp < G) {  // chunk max per head: warp h, lane = group (ngr <= 32)
+      float v = lane < ngr ? gm[lane * G + warp] : -INFINITY;
+      for (int o = 16; o; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+      if (lane == 0) mh[warp] = v;
     }
     __syncthreads();
-    // p = half * exp(m32 - M), once per (token, head) over the CTA; read
+    if (tid < ngr * G) {  // group scale exp(m32 - M) in place
+      const float mg = gm[tid];
+      gm[tid] = mg == -INFINITY ? 0.f : __expf(mg - mh[tid % G]);
+    }
+    __syncthreads();
+    // p = half * group scale, once per (token, head) over the CTA; read
     // into registers first (sc[e] overlaps hw of lower tokens)
 #pragma unroll
     for (int k = 0; k < kMaxPer; ++k) {
       const int e = tid + k * kThreads;
       if (e < cnt) {
 #pragma unroll
-        for (int h = 0; h < G; ++h) {
-          const float mg = gm[(e >> 5) * G + h];
-          const float f = mg == -INFINITY ? 0.f : __expf(mg - mh[h]);
-          pv[k][h] = __half2float(hw[(size_t)e * G + h]) * f;
-        }
+        for (int h = 0; h < G; ++h)
+          pv[k][h] = __half2float(hw[(size_t)e * G + h]) * gm[(e >> 5) * G + h];
       }
     }
     __syncthreads();
