@@ -701,7 +701,7 @@ __device__ __forceinline__ void mma16816(float (&d)[4], const uint32_t (&a)[4], 
 // accumulators; bits expanded to fp16 0 / 1 by byte permutes; p rounded to
 // fp16, relative 2^-11) or (!MMA) by predicated fp32 adds on CUDA cores.
 template <int NC, int G, int JS, bool PH = false, bool MMA = false>
-__global__ void __launch_bounds__(kThreads, MMA ? 4 : 1) k_fast_value(FastArgs a) {
+__global__ void __launch_bounds__(kThreads, MMA ? (NC <= 128 ? 4 : 2) : 1) k_fast_value(FastArgs a) {
   constexpr int CPL = NC / 32;       // codes per lane
   constexpr int WPTOK = NC / 64;     // value words per token
   extern __shared__ __align__(16) unsigned char smem[];

@@ -480,7 +480,8 @@ k_encode_keys_brute(Geom g, int n_slots, const double* __restrict__ atoms,
 // round's slice and screen table read straight from L2 (no smem staging --
 // appends encode one token per stream).  Same screen + exact re-check as
 // k_encode_keys_table; requires 2L <= 128 (L <= 64).
-constexpr int kSmallThreads = 128;
+constexpr int kSmallThreads = 512;
+constexpr int kSmallWarps = kSmallThreads / 32;
 
 __device__ __forceinline__ void block_argmin2(double& b1, int& c1, double& b2, double* rv, int* rc) {
   // per-warp: argmin with smallest index, runner-up = min over the rest
@@ -490,33 +491,34 @@ __device__ __forceinline__ void block_argmin2(double& b1, int& c1, double& b2, d
   warp_argmin(v, c);
   double ru = (c1 == c) ? b2 : b1;
   for (int o = 16; o; o >>= 1) ru = fmin(ru, __shfl_xor_sync(0xffffffffu, ru, o));
+  constexpr int W = kSmallWarps;
   if (lane == 0) {
     rv[warp] = v;
     rc[warp] = c;
-    rv[4 + warp] = ru;
+    rv[W + warp] = ru;
   }
   __syncthreads();
   if (threadIdx.x == 0) {
-    double gv = rv[0], gr = rv[4];
+    double gv = rv[0], gr = rv[W];
     int gc = rc[0];
-    for (int w = 1; w < kSmallThreads / 32; ++w) {
-      // merge (gv, gc, gr) with (rv[w], rc[w], rv[4+w])
+    for (int w = 1; w < W; ++w) {
+      // merge (gv, gc, gr) with (rv[w], rc[w], rv[W + w])
       if (rv[w] < gv || (rv[w] == gv && rc[w] < gc)) {
-        gr = fmin(gv, fmin(gr, rv[4 + w]));
+        gr = fmin(gv, fmin(gr, rv[W + w]));
         gv = rv[w];
         gc = rc[w];
       } else {
-        gr = fmin(gr, fmin(rv[w], rv[4 + w]));
+        gr = fmin(gr, fmin(rv[w], rv[W + w]));
       }
     }
-    rv[8] = gv;
-    rv[9] = gr;
-    rc[8] = gc;
+    rv[2 * W] = gv;
+    rv[2 * W + 1] = gr;
+    rc[W] = gc;
   }
   __syncthreads();
-  b1 = rv[8];
-  b2 = rv[9];
-  c1 = rc[8];
+  b1 = rv[2 * W];
+  b2 = rv[2 * W + 1];
+  c1 = rc[W];
   __syncthreads();
 }
 
@@ -526,11 +528,18 @@ k_encode_keys_small(Geom g, int n_slots, const double* __restrict__ atoms,
                     const void* __restrict__ keys, int dtype, long long s_stride, long long n,
                     uint16_t* __restrict__ a_out, uint16_t* __restrict__ b_out) {
   extern __shared__ double sm[];
-  double* P = sm;               // [d]
-  double* PU = P + g.d;         // [L]
-  double* PV = PU + g.L;        // [L]
-  __shared__ double rv[12];
-  __shared__ int rc[12];
+  // the (round, group) slices and base tables double-buffered in smem by
+  // cp.async: the next one streams in while this one is searched
+  const size_t ub = (size_t)g.g * g.L * 2, bb_ = ((size_t)g.L * g.L + 1) & ~(size_t)1;  // doubles per buffer (16-B multiples)
+  double* UB = sm;                    // [2][g][L] double2
+  double* BB = UB + 2 * ub;           // [2][L][L]
+  double* P = BB + 2 * bb_;           // [d]
+  double* PU = P + g.d;               // [L]
+  double* PV = PU + g.L;              // [L]
+  double* PR = PV + g.L;              // [nsplit][2L] projection partials
+  __shared__ double rv[2 * kSmallWarps + 2];
+  __shared__ int rc[kSmallWarps + 1];
+  __shared__ double pns;
   const int s = blockIdx.y, tid = threadIdx.x;
   const long long i = blockIdx.x;
   const int slot = s % n_slots;
@@ -538,41 +547,77 @@ k_encode_keys_small(Geom g, int n_slots, const double* __restrict__ atoms,
     P[e] = load_elem(keys, dtype, (long long)s * s_stride + i * g.d + e);
   __syncthreads();
   const int L = g.L, gs = g.g, w2 = 2 * g.g;
+  const int total = g.R * g.groups;
+  auto stage = [&](int idx, int buf) {
+    const int rr = idx / g.groups, gg = idx % g.groups;
+    const double* Ug = atoms + 2 * (((size_t)(slot * g.R + rr) * g.subs + (size_t)gg * gs) * L);
+    const double* Bg = base + ((size_t)(slot * g.R + rr) * g.groups + gg) * L * L;
+    for (size_t e = 2 * (size_t)tid; e < ub; e += 2 * kSmallThreads) cp_async16(UB + buf * ub + e, Ug + e);
+    if ((L * L) & 1) {  // odd table: 8-B copies (the source is only 8-B aligned)
+      for (size_t e = tid; e < (size_t)L * L; e += kSmallThreads) {
+        const unsigned sa = (unsigned)__cvta_generic_to_shared(BB + buf * bb_ + e);
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(Bg + e) : "memory");
+      }
+    } else {
+      for (size_t e = 2 * (size_t)tid; e < bb_; e += 2 * kSmallThreads) cp_async16(BB + buf * bb_ + e, Bg + e);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  stage(0, 0);
   for (int r = 0; r < g.R; ++r) {
     for (int grp = 0; grp < g.groups; ++grp) {
-      const double2* U = reinterpret_cast<const double2*>(atoms) +
-                         ((size_t)(slot * g.R + r) * g.subs + (size_t)grp * gs) * L;
-      const double* B = base + ((size_t)(slot * g.R + r) * g.groups + grp) * L * L;
+      const int idx = r * g.groups + grp, buf = idx & 1;
+      if (idx + 1 < total) {
+        stage(idx + 1, buf ^ 1);
+        asm volatile("cp.async.wait_group 1;" ::: "memory");
+      } else {
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
+      }
+      __syncthreads();
+      const double2* U = reinterpret_cast<const double2*>(UB + buf * ub);
+      const double* B = BB + buf * bb_;
       const double mn = maxnorm[(size_t)(slot * g.R + r) * g.groups + grp];
       double* p = P + grp * w2;
-      if (tid < 2 * L) {  // threads [0,L): p.u_l, [L,2L): p.v_l
-        const int l = tid % L;
-        const bool isv = tid >= L;
+      // projections: thread (q, o) sums subspaces [q sper, (q + 1) sper) of
+      // output o (o < L: p.u_l, else p.v_l); partials summed below
+      const int nsplit = kSmallThreads / (2 * L), sper = (gs + nsplit - 1) / nsplit;
+      if (tid < nsplit * 2 * L) {
+        const int o = tid % (2 * L), q = tid / (2 * L), l = o % L;
+        const bool isv = o >= L;
+        const int s0 = q * sper, s1 = min(gs, s0 + sper);
         double acc = 0.0;
-        for (int si = 0; si < gs; ++si) {
-          const double2 u = __ldg(U + (size_t)si * L + l);
+#pragma unroll 8
+        for (int si = s0; si < s1; ++si) {
+          const double2 u = U[(size_t)si * L + l];
           const double px = p[2 * si], py = p[2 * si + 1];
           acc = isv ? fma(py, u.x, fma(-px, u.y, acc)) : fma(px, u.x, fma(py, u.y, acc));
         }
-        (isv ? PV : PU)[l] = acc;
+        PR[q * 2 * L + o] = acc;
       }
-      double pn = 0.0;
       if (tid < 32) {
+        double pn = 0.0;
         for (int e = tid; e < w2; e += 32) pn = fma(p[e], p[e], pn);
         for (int o = 16; o; o >>= 1) pn += __shfl_xor_sync(0xffffffffu, pn, o);
-        if (tid == 0) rv[10] = pn;
+        if (tid == 0) pns = pn;
       }
       __syncthreads();
-      pn = rv[10];
+      if (tid < 2 * L) {
+        double acc = 0.0;
+        for (int q = 0; q < nsplit; ++q) acc += PR[q * 2 * L + tid];
+        (tid >= L ? PV : PU)[tid % L] = acc;
+      }
+      __syncthreads();
+      const double pn = pns;
       int chosen;
       bool exact = !(pn < 1e300) || !(mn < 1e150);
       double gb = 0.0, margin = 0.0;
       if (!exact) {
         double b1 = INFINITY, b2 = INFINITY;
         int c1 = 0x7fffffff;
+#pragma unroll 4
         for (int c = tid; c < L * L; c += blockDim.x) {
           const int aa = c / L, bb = c % L;
-          const double sc = __ldg(B + c) - 2.0 * PU[aa] - 2.0 * PV[bb];
+          const double sc = B[c] - 2.0 * PU[aa] - 2.0 * PV[bb];
           if (sc < b1 || (sc == b1 && c < c1)) {
             b2 = b1;
             b1 = sc;
@@ -595,7 +640,7 @@ k_encode_keys_small(Geom g, int n_slots, const double* __restrict__ atoms,
         for (int c = tid; c < L * L; c += blockDim.x) {
           const int aa = c / L, bb = c % L;
           if (!all) {
-            const double sc = __ldg(B + c) - 2.0 * PU[aa] - 2.0 * PV[bb];
+            const double sc = B[c] - 2.0 * PU[aa] - 2.0 * PV[bb];
             if (!(sc <= gb + margin)) continue;
           }
           const double dd = exact_dist(p, U, L, gs, aa, bb);
@@ -610,14 +655,14 @@ k_encode_keys_small(Geom g, int n_slots, const double* __restrict__ atoms,
       }
       const int ca = chosen / L, cb = chosen % L;
       if (tid == 0) {
-        const size_t idx = ((size_t)s * n + i) * (g.R * g.groups) + (size_t)r * g.groups + grp;
-        a_out[idx] = (uint16_t)ca;
-        b_out[idx] = (uint16_t)cb;
+        const size_t o = ((size_t)s * n + i) * (g.R * g.groups) + (size_t)r * g.groups + grp;
+        a_out[o] = (uint16_t)ca;
+        b_out[o] = (uint16_t)cb;
       }
       for (int si = tid; si < gs; si += blockDim.x) {
-        const double2 ua = __ldg(U + (size_t)si * L + ca), ub = __ldg(U + (size_t)si * L + cb);
-        p[2 * si] = __dsub_rn(p[2 * si], __dadd_rn(ua.x, -ub.y));
-        p[2 * si + 1] = __dsub_rn(p[2 * si + 1], __dadd_rn(ua.y, ub.x));
+        const double2 ua = U[(size_t)si * L + ca], vb = U[(size_t)si * L + cb];
+        p[2 * si] = __dsub_rn(p[2 * si], __dadd_rn(ua.x, -vb.y));
+        p[2 * si + 1] = __dsub_rn(p[2 * si + 1], __dadd_rn(ua.y, vb.x));
       }
       __syncthreads();
     }
@@ -638,10 +683,15 @@ cudaError_t run_encode_keys(const Geom& g, int S, int n_slots, const KeyEncTable
   if (n <= 0 || S <= 0) return cudaSuccess;
   const size_t sm = table_smem(g);
   cudaError_t e;
-  if (tab.base != nullptr && n < 8 && 2 * g.L <= kSmallThreads) {
-    // decode-step appends: a CTA per token, no 96-KiB slice staging per round
+  const size_t sm_small =
+      sizeof(double) * (4 * (size_t)g.g * g.L + 2 * (((size_t)g.L * g.L + 1) & ~(size_t)1) + g.d + 2 * g.L +
+                        (size_t)(kSmallThreads / (2 * g.L)) * 2 * g.L);
+  if (tab.base != nullptr && n < 8 && 2 * g.L <= kSmallThreads && sm_small <= 220 * 1024) {
+    // decode-step appends: a CTA per token, the round slices double-buffered
+    e = ensure_dyn_smem(reinterpret_cast<const void*>(k_encode_keys_small), sm_small);
+    if (e != cudaSuccess) return e;
     dim3 grid((unsigned)n, S);
-    k_encode_keys_small<<<grid, kSmallThreads, sizeof(double) * (g.d + 2 * g.L), st>>>(
+    k_encode_keys_small<<<grid, kSmallThreads, sm_small, st>>>(
         g, n_slots, tab.atoms, tab.base, tab.maxnorm, keys, dtype, s_stride, n, a, b);
   } else if (tab.base != nullptr && sm <= 200 * 1024) {
     e = ensure_dyn_smem(reinterpret_cast<const void*>(k_encode_keys_table), sm);
@@ -691,12 +741,23 @@ __global__ void k_encode_values(Geom g, int n_slots, ValEncWeights w,
     double h[TV];
 #pragma unroll
     for (int k = 0; k < TV; ++k) h[k] = 0.0;
-    for (int i = 0; i < g.d; ++i) {
-      const double wv = __ldg(w1 + (size_t)i * g.hidden + j);
+    // weights 16 rows at a time into registers (the loads do not depend on
+    // the sequential, zero-skipping sums: keep 16 in flight)
+    for (int i0 = 0; i0 < g.d; i0 += 16) {
+      double wv[16];
 #pragma unroll
-      for (int k = 0; k < TV; ++k) {
-        const double ti = T[k * g.d + i];
-        if (ti != 0.0) h[k] = __dadd_rn(h[k], __dmul_rn(ti, wv));
+      for (int u = 0; u < 16; ++u)
+        wv[u] = i0 + u < g.d ? __ldg(w1 + (size_t)(i0 + u) * g.hidden + j) : 0.0;
+#pragma unroll
+      for (int u = 0; u < 16; ++u) {
+#pragma unroll
+        for (int k = 0; k < TV; ++k) {
+          // a skipped term (t_i == 0) adds -0.0, which leaves every value
+          // (signed zeros, inf, NaN included) bit-identical: no branch on the
+          // sequential chain
+          const double ti = i0 + u < g.d ? T[k * g.d + i0 + u] : 0.0;
+          h[k] = __dadd_rn(h[k], ti != 0.0 ? __dmul_rn(ti, wv[u]) : -0.0);
+        }
       }
     }
     const double bj = b1[j];
@@ -712,12 +773,18 @@ __global__ void k_encode_values(Geom g, int n_slots, ValEncWeights w,
     double lg[TV];
 #pragma unroll
     for (int k = 0; k < TV; ++k) lg[k] = 0.0;
-    for (int j = 0; j < g.hidden; ++j) {
-      const double wv = __ldg(w2 + (size_t)j * g.n_codes + c);
+    for (int j0 = 0; j0 < g.hidden; j0 += 16) {
+      double wv[16];
 #pragma unroll
-      for (int k = 0; k < TV; ++k) {
-        const double hj = H[k * g.hidden + j];
-        if (hj != 0.0) lg[k] = __dadd_rn(lg[k], __dmul_rn(hj, wv));
+      for (int u = 0; u < 16; ++u)
+        wv[u] = j0 + u < g.hidden ? __ldg(w2 + (size_t)(j0 + u) * g.n_codes + c) : 0.0;
+#pragma unroll
+      for (int u = 0; u < 16; ++u) {
+#pragma unroll
+        for (int k = 0; k < TV; ++k) {
+          const double hj = j0 + u < g.hidden ? H[k * g.hidden + j0 + u] : 0.0;
+          lg[k] = __dadd_rn(lg[k], hj != 0.0 ? __dmul_rn(hj, wv[u]) : -0.0);
+        }
       }
     }
     const double bc = b2[c];
