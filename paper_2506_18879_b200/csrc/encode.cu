@@ -498,22 +498,20 @@ __device__ __forceinline__ void block_argmin2(double& b1, int& c1, double& b2, d
     rv[W + warp] = ru;
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
-    double gv = rv[0], gr = rv[W];
-    int gc = rc[0];
-    for (int w = 1; w < W; ++w) {
-      // merge (gv, gc, gr) with (rv[w], rc[w], rv[W + w])
-      if (rv[w] < gv || (rv[w] == gv && rc[w] < gc)) {
-        gr = fmin(gv, fmin(gr, rv[W + w]));
-        gv = rv[w];
-        gc = rc[w];
-      } else {
-        gr = fmin(gr, fmin(rv[w], rv[W + w]));
-      }
+  if (warp == 0) {  // the same merge over the warps' (best, index, runner-up)
+    const double wv = lane < W ? rv[lane] : INFINITY;
+    const int wc = lane < W ? rc[lane] : 0x7fffffff;
+    const double wr = lane < W ? rv[W + lane] : INFINITY;
+    double gv = wv;
+    int gc = wc;
+    warp_argmin(gv, gc);
+    double gr = (wc == gc) ? wr : wv;
+    for (int o = 16; o; o >>= 1) gr = fmin(gr, __shfl_xor_sync(0xffffffffu, gr, o));
+    if (lane == 0) {
+      rv[2 * W] = gv;
+      rv[2 * W + 1] = gr;
+      rc[W] = gc;
     }
-    rv[2 * W] = gv;
-    rv[2 * W + 1] = gr;
-    rc[W] = gc;
   }
   __syncthreads();
   b1 = rv[2 * W];
@@ -614,10 +612,19 @@ k_encode_keys_small(Geom g, int n_slots, const double* __restrict__ atoms,
       if (!exact) {
         double b1 = INFINITY, b2 = INFINITY;
         int c1 = 0x7fffffff;
+        // candidates c = tid + k * threads in increasing order; (a, b)
+        // stepped without a division per candidate
+        const int da = kSmallThreads / L, db = kSmallThreads % L;
+        int aa = tid / L, bb = tid % L;
 #pragma unroll 4
-        for (int c = tid; c < L * L; c += blockDim.x) {
-          const int aa = c / L, bb = c % L;
+        for (int c = tid; c < L * L; c += kSmallThreads) {
           const double sc = B[c] - 2.0 * PU[aa] - 2.0 * PV[bb];
+          aa += da;
+          bb += db;
+          if (bb >= L) {
+            bb -= L;
+            ++aa;
+          }
           if (sc < b1 || (sc == b1 && c < c1)) {
             b2 = b1;
             b1 = sc;
