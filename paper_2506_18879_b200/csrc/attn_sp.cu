@@ -141,7 +141,22 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   }
 }
 __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+#ifdef CVQ_SP_SUSPEND
+  // try_wait with a suspend-time hint: the warp is parked by the hardware
+  // until the phase completes (or the hint expires) instead of re-issuing a
+  // poll + nanosleep loop that competes for issue slots
+  uint32_t ok;
+  do {
+    asm volatile(
+        "{.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+        "selp.u32 %0, 1, 0, p;}"
+        : "=r"(ok)
+        : "r"(su32(bar)), "r"(parity), "r"((uint32_t)CVQ_SP_SUSPEND)
+        : "memory");
+  } while (!ok);
+#else
   while (!mbar_try(bar, parity)) __nanosleep(64);
+#endif
 }
 __device__ __forceinline__ bool elect_one() {
   uint32_t pred;
@@ -627,14 +642,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_sp_score(SpArgs a) {
       // rounds by GLOBAL round index: this warp takes g = gbase + r with
       // g % kProdPerQ == sub, so its rounds are evenly spaced across tiles
       const int rfirst = (int)((uint32_t)(sub + kProdPerQ - (int)(gbase % kProdPerQ)) % kProdPerQ);
+      static_assert(kProdPerQ == 4 && R <= 12, "at most 3 rounds per producer warp and tile");
 #pragma unroll
-      for (int r = 0, i = 0; r < R; ++r) {
-        if ((r % kProdPerQ) != rfirst) continue;
-        const int b0 = 12 * r, wi = b0 >> 6, sh = b0 & 63;
-        const uint64_t f = ((w[wi] >> sh) | (sh > 52 ? w[wi + 1] << (64 - sh) : 0ull)) & 0xFFFull;
-        if (i < 5) pk0 |= f << (12 * i);
-        else pk1 |= f << (12 * (i - 5));
-        ++i;
+      for (int j = 0; j < 3; ++j) {  // rounds rfirst + 4 j: runtime bit offsets, no skipped rounds
+        const int bit = 12 * (rfirst + 4 * j), wi = bit >> 6, sh = bit & 63;
+        const uint64_t lo = wi == 0 ? w[0] : (wi == 1 ? w[1] : w[2]);
+        const uint64_t hi = wi == 0 ? w[1] : (wi == 1 ? w[2] : w[3]);
+        const uint64_t f = ((lo >> sh) | (sh > 52 ? hi << (64 - sh) : 0ull)) & 0xFFFull;
+        pk0 |= f << (12 * j);
       }
 #pragma unroll 1
       for (int r = rfirst; r < it.nr; r += kProdPerQ) {
@@ -655,9 +670,16 @@ __global__ void __launch_bounds__(kThreads, 1) k_sp_score(SpArgs a) {
           const uint32_t c = (fld >> (6 * s2)) & 63u;
           uint32_t v[16];
           const uint32_t col = ((c >> 5) << 3) | ((c & 31) >> 2);
-          const uint32_t one = (c & 1) ? 0x3C000000u : 0x00003C00u;  // fp16 1.0 in slot c & 1
+          // word col holds fp16 1.0 in slot c & 1; one compare per word pair
+          const uint32_t one = (c & 1) ? 0x3C000000u : 0x00003C00u;
+          const uint32_t onee = (col & 1) ? 0u : one, oneo = (col & 1) ? one : 0u;
+          const uint32_t hp = col >> 1;
 #pragma unroll
-          for (int i = 0; i < 16; ++i) v[i] = (col == (uint32_t)i) ? one : 0u;
+          for (int i = 0; i < 8; ++i) {
+            const bool hit = hp == (uint32_t)i;
+            v[2 * i] = hit ? onee : 0u;
+            v[2 * i + 1] = hit ? oneo : 0u;
+          }
           // metadata word of TMEM lane L = m0 + 8 k1 + 16 m2 (measured,
           // profiles/r01_umma_sparse_lanemap.txt): bits [16 m1, 16 m1 + 16)
           // are the 4 group nibbles of K-half k1 for row m0 + 8 m1 + 16 m2.
