@@ -1151,75 +1151,66 @@ __global__ void __launch_bounds__(128) k_combine_project(const float* __restrict
 }
 
 // Small jobs (few chunk partials): merge + project in ONE kernel, a CTA per
-// stream (its G rows share the value codebook): per row the LSE weights of
-// the P parts, z[h][k] = sum_p w_p z_p[h][k] (thread = (h, k)), then
-// o[h][:] = z[h] . C_V / L_h with the k range split over 4 thread groups so
-// each C_V load feeds G rows.  One launch instead of two, no zm round trip.
+// row (grid streams x G): the LSE weights of the P parts (warp 0), z[k] =
+// sum_p w_p z_p[k] with the parts split over 4 thread groups, then
+// o[:] = z . C_V / L with the k range split over 4 thread groups.  One
+// launch instead of two, no zm round trip, every sequential chain <= P/4 or
+// NC/4 long.
 constexpr int kCfThreads = 512, kCfMaxP = 64;
-template <int NC, int G>
+template <int NC>
 __global__ void __launch_bounds__(kCfThreads) k_combine_fused(
     const float* __restrict__ m, const float* __restrict__ l, const float* __restrict__ z, int P,
-    long long rows, const float* __restrict__ cbv, int n_slots, float* __restrict__ out,
+    long long rows, int G, const float* __restrict__ cbv, int n_slots, float* __restrict__ out,
     float* __restrict__ m_out, float* __restrict__ l_out) {
-  __shared__ float wts[kCfMaxP][G];
-  __shared__ float Mh[G], Lh[G];
-  __shared__ float zs[G][NC];
-  __shared__ float part[4][G][128];
-  const int s = blockIdx.x, tid = threadIdx.x;
-  const long long row0 = (long long)s * G;
-  if (tid < 32 * G) {  // warp h: max and weights of row h over the parts
-    const int h = tid >> 5, lane = tid & 31;
+  __shared__ float wts[kCfMaxP];
+  __shared__ float Ms, Ls;
+  __shared__ float zp[4][NC];
+  __shared__ float zs[NC];
+  __shared__ float part[4][128];
+  const int s = blockIdx.x, tid = threadIdx.x, q = tid >> 7, t = tid & 127;
+  const long long row = (long long)s * G + blockIdx.y;
+  if (tid < 32) {
     float M = -FLT_MAX;
-    for (int p = lane; p < P; p += 32)
-      if (l[p * rows + row0 + h] > 0.f) M = fmaxf(M, m[p * rows + row0 + h]);
+    for (int p = tid; p < P; p += 32)
+      if (l[p * rows + row] > 0.f) M = fmaxf(M, m[p * rows + row]);
     for (int o = 16; o; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
     float L = 0.f;
-    for (int p = lane; p < P; p += 32) {
-      const float lp = l[p * rows + row0 + h];
-      const float w = lp > 0.f ? expf(m[p * rows + row0 + h] - M) : 0.f;
-      wts[p][h] = w;
+    for (int p = tid; p < P; p += 32) {
+      const float lp = l[p * rows + row];
+      const float w = lp > 0.f ? expf(m[p * rows + row] - M) : 0.f;
+      wts[p] = w;
       L += lp * w;
     }
     for (int o = 16; o; o >>= 1) L += __shfl_xor_sync(0xffffffffu, L, o);
-    if (lane == 0) {
-      Mh[h] = M;
-      Lh[h] = L;
+    if (tid == 0) {
+      Ms = M;
+      Ls = L;
     }
   }
   __syncthreads();
-  for (int e = tid; e < G * NC; e += kCfThreads) {
-    const int h = e / NC, k = e % NC;
+#pragma unroll
+  for (int k = t; k < NC; k += 128) {
     float acc = 0.f;
 #pragma unroll 4
-    for (int p = 0; p < P; ++p) {
-      const float w = wts[p][h];
-      if (w != 0.f) acc += z[(p * rows + row0 + h) * NC + k] * w;
+    for (int p = q; p < P; p += 4) {
+      const float w = wts[p];
+      if (w != 0.f) acc += z[(p * rows + row) * NC + k] * w;
     }
-    zs[h][k] = acc;
+    zp[q][k] = acc;
   }
   __syncthreads();
-  const int kq = tid >> 7, jd = tid & 127;
+  for (int k = tid; k < NC; k += kCfThreads) zs[k] = zp[0][k] + zp[1][k] + zp[2][k] + zp[3][k];
+  __syncthreads();
   const float* cb = cbv + (size_t)(s % n_slots) * NC * 128;
-  float acc[G];
-#pragma unroll
-  for (int h = 0; h < G; ++h) acc[h] = 0.f;
+  float acc = 0.f;
 #pragma unroll 8
-  for (int k = kq * (NC / 4); k < (kq + 1) * (NC / 4); ++k) {
-    const float c = __ldg(cb + (size_t)k * 128 + jd);
-#pragma unroll
-    for (int h = 0; h < G; ++h) acc[h] += zs[h][k] * c;
-  }
-#pragma unroll
-  for (int h = 0; h < G; ++h) part[kq][h][jd] = acc[h];
+  for (int k = q * (NC / 4); k < (q + 1) * (NC / 4); ++k) acc += zs[k] * __ldg(cb + (size_t)k * 128 + t);
+  part[q][t] = acc;
   __syncthreads();
-  for (int e = tid; e < G * 128; e += kCfThreads) {
-    const int h = e >> 7, j = e & 127;
-    const float v = part[0][h][j] + part[1][h][j] + part[2][h][j] + part[3][h][j];
-    out[(row0 + h) * 128 + j] = v / Lh[h];
-  }
-  if (tid < G) {
-    if (m_out) m_out[row0 + tid] = Mh[tid];
-    if (l_out) l_out[row0 + tid] = Lh[tid];
+  if (tid < 128) out[row * 128 + tid] = (part[0][tid] + part[1][tid] + part[2][tid] + part[3][tid]) / Ls;
+  if (tid == 0) {
+    if (m_out) m_out[row] = Ms;
+    if (l_out) l_out[row] = Ls;
   }
 }
 
@@ -1232,20 +1223,14 @@ cudaError_t run_fast_combine(const AttnJob& job, const float* pm, const float* p
   if (rows == 0) return cudaSuccess;
   const int NC = job.geo.n_codes;
   dim3 gm((unsigned)rows, NC / 32);
-  if (n_parts <= kCfMaxP && (job.geo.G == 4 || job.geo.G == 1) && job.geo.d == 128) {
-    const unsigned S = (unsigned)job.S;
-    if (NC == 128 && job.geo.G == 4)
-      k_combine_fused<128, 4><<<S, kCfThreads, 0, st>>>(pm, pl, pz, n_parts, rows, job.cb_val,
-                                                         job.n_slots, out, m_out, l_out);
-    else if (NC == 128)
-      k_combine_fused<128, 1><<<S, kCfThreads, 0, st>>>(pm, pl, pz, n_parts, rows, job.cb_val,
-                                                         job.n_slots, out, m_out, l_out);
-    else if (job.geo.G == 4)
-      k_combine_fused<256, 4><<<S, kCfThreads, 0, st>>>(pm, pl, pz, n_parts, rows, job.cb_val,
-                                                         job.n_slots, out, m_out, l_out);
+  if (n_parts <= kCfMaxP && job.geo.d == 128) {
+    const dim3 grid((unsigned)job.S, (unsigned)job.geo.G);
+    if (NC == 128)
+      k_combine_fused<128><<<grid, kCfThreads, 0, st>>>(pm, pl, pz, n_parts, rows, job.geo.G,
+                                                         job.cb_val, job.n_slots, out, m_out, l_out);
     else
-      k_combine_fused<256, 1><<<S, kCfThreads, 0, st>>>(pm, pl, pz, n_parts, rows, job.cb_val,
-                                                         job.n_slots, out, m_out, l_out);
+      k_combine_fused<256><<<grid, kCfThreads, 0, st>>>(pm, pl, pz, n_parts, rows, job.geo.G,
+                                                         job.cb_val, job.n_slots, out, m_out, l_out);
     count_launch(1);
     return cudaGetLastError();
   }
