@@ -154,6 +154,32 @@ inline KeyCodes encode_keys(const Mat& keys, const KeyCodebook& cb,
   return codes;
 }
 
+// keyquant.hpp:137 / keyquant.cpp:741-768: dense keys, bit-identical.
+inline Mat decode_keys(const KeyCodes& codes, const KeyCodebook& cb) {
+  const KeyQuantConfig& cfg = cb.config;
+  if (codes.rounds != cfg.rounds || codes.groups != cfg.groups() ||
+      codes.n_levels != cfg.n_levels)
+    throw std::invalid_argument("decode_keys: codes do not match codebook");
+  Mat out(codes.tokens, cfg.d);
+  if (codes.tokens == 0) return out;
+  const cvq_key_config ck = key_config(cfg);
+  const std::vector<double> xy = atoms_xy(cb);
+  check(cvq_decode_keys(context(), &ck, xy.data(), codes.a.data(), codes.b.data(), codes.tokens,
+                        out.data.data()));
+  return out;
+}
+
+// valquant.hpp:67 / valquant.cpp:115-128: dense values, bit-identical.
+inline Mat decode_values(const ValueCodes& codes, const ValueCodebook& cb) {
+  if (codes.n_codes != cb.n_codes)
+    throw std::invalid_argument("decode_values: codes do not match codebook");
+  Mat out(codes.tokens, cb.d);
+  if (codes.tokens == 0 || cb.d == 0) return out;
+  check(cvq_decode_values(context(), (uint32_t)cb.n_codes, (uint32_t)cb.d, cb.rows.data.data(),
+                          codes.bits.data(), codes.tokens, out.data.data()));
+  return out;
+}
+
 // keyquant.hpp:131-133: the soft-to-hard EM schedule with device E-steps
 // (train.cu); bit-identical to the reference on the golden cases.
 inline KeyTrainResult train_key_codebook(const Mat& calib_keys, const KeyQuantConfig& config,

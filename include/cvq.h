@@ -141,6 +141,20 @@ CVQ_API cvq_status cvq_encode_keys(cvq_context* ctx, const cvq_key_config* kc,
                                    const double* keys, uint64_t n_tokens,
                                    uint16_t* a, uint16_t* b);
 
+/* decode_keys (keyquant.hpp:137, keyquant.cpp:741-768): out[n][d] = the sum
+ * over rounds of each token's cluster centres, in the reference's order
+ * (fp64, no FMA; bit-identical).  a, b as cvq_encode_keys returns them.
+ * CVQ_EINVAL "decode_keys: code out of range" for a code >= n_levels. */
+CVQ_API cvq_status cvq_decode_keys(cvq_context* ctx, const cvq_key_config* kc,
+                                   const double* key_atoms_xy, const uint16_t* a,
+                                   const uint16_t* b, uint64_t n_tokens, double* out);
+/* decode_values (valquant.hpp:67, valquant.cpp:115-128): out[n][d] = the sum
+ * of the codebook rows whose bit is set, ascending code order (fp64;
+ * bit-identical).  bits: [n][n_codes] bytes, 0 / 1; rows: [n_codes][d]. */
+CVQ_API cvq_status cvq_decode_values(cvq_context* ctx, uint32_t n_codes, uint32_t d,
+                                     const double* rows, const uint8_t* bits, uint64_t n_tokens,
+                                     double* out);
+
 /* encode_keys with the AssignSearch argument (keyquant.hpp:135-136):
  * search 0 = brute_force (as cvq_encode_keys), 1 = factorized -- the
  * reference's assign_factorized ranking base - 2 pu - 2 pv (keyquant.cpp:

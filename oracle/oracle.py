@@ -252,6 +252,19 @@ class Oracle:
         return out
 
     # ---- valquant -------------------------------------------------------
+
+    def decode_values(self, rows, bits):
+        """valquant.cpp:115-128."""
+        rows = np.ascontiguousarray(rows, np.float64)
+        bits = np.ascontiguousarray(bits, np.uint8)
+        n_codes, d = rows.shape
+        n = bits.shape[0]
+        out = np.zeros((n, d))
+        name = "cvqo_decode_values" if self.kind == "port" else "cvqr_decode_values"
+        f = getattr(self.lib, name)
+        f.argtypes = [_sz, _sz, _p, _p, _sz, _p]
+        self._check(f(n_codes, d, _ptr(rows), _ptr(bits), n, _ptr(out)))
+        return out
     def encoder_forward_infer(self, w1, b1, w2, b2, values):
         """valquant.cpp:50-101 (infer mode), batched over rows of values."""
         w1 = np.ascontiguousarray(w1, np.float64)

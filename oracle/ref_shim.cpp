@@ -234,6 +234,14 @@ int cvqr_decode_keys(size_t d, size_t g, size_t L, size_t R,
 // obj_out: the hard-objective traces, round-major then group, concatenated
 // (obj_len[r * groups + grp] entries each, at most obj_cap in total);
 // mse_out[R]: reconstruction MSE after each round.
+int cvqr_decode_values(size_t n_codes, size_t d, const double* rows, const uint8_t* bits,
+                       size_t n, double* out) {
+  return guard([&] {
+    Mat m = decode_values(make_vc(n_codes, bits, n), make_vcb(n_codes, d, rows));
+    std::memcpy(out, m.data.data(), n * d * sizeof(double));
+  });
+}
+
 int cvqr_train_key_codebook(size_t d, size_t g, size_t L, size_t R, const double* calib,
                             size_t n, size_t soft_iters, size_t hard_iters_max, double t0,
                             double decay, double tol, double ridge, uint64_t seed,

@@ -11,7 +11,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 SO = os.path.join(HERE, "libcvq_b200.so")
-SOURCES = ["capi.cu", "attn.cu", "attn_fast.cu", "attn_tc.cu", "attn_sp.cu", "encode.cu", "pack.cu", "train.cu", "train_value.cu", "mgpu.cu", "naive.cu"]
+SOURCES = ["capi.cu", "attn.cu", "attn_fast.cu", "attn_tc.cu", "attn_sp.cu", "encode.cu", "pack.cu", "train.cu", "train_value.cu", "mgpu.cu", "naive.cu", "decode.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [
     "-std=c++17", "-O3", "-lineinfo", "-gencode", "arch=compute_100a,code=sm_100a",

@@ -308,6 +308,39 @@ def encode_keys(kq, atoms, keys, ctx=None, search="brute_force"):
     return a[:m], b[:m]
 
 
+def decode_keys(kq, atoms, a, b, ctx=None):
+    """keyquant.cpp:741-768: dense keys [n][d] from codes (bit-identical)."""
+    kq = _kc(kq)
+    ctx = ctx or default_context()
+    atoms = _a(atoms, np.float64)
+    a = _a(a, np.uint16).reshape(-1)
+    b = _a(b, np.uint16).reshape(-1)
+    per = kq.rounds * kq.groups
+    if a.size != b.size or a.size % per:
+        raise ValueError("decode_keys: codes do not match codebook")
+    n = a.size // per
+    out = np.zeros((max(n, 1), kq.d))
+    kc = kq._c()
+    _check(_lib.cvq_decode_keys(ctx.h, C.byref(kc), _ptr(atoms), _ptr(a), _ptr(b), _u64(n),
+                                _ptr(out)))
+    return out[:n]
+
+
+def decode_values(rows, bits, ctx=None):
+    """valquant.cpp:115-128: dense values [n][d] = sum of the codebook rows
+    whose bit is set (bit-identical).  rows [n_codes][d], bits [n][n_codes]."""
+    ctx = ctx or default_context()
+    rows = _a(rows, np.float64)
+    bits = _a(bits, np.uint8)
+    if rows.ndim != 2 or bits.ndim != 2 or bits.shape[1] != rows.shape[0]:
+        raise ValueError("decode_values: codes do not match codebook")
+    n = bits.shape[0]
+    out = np.zeros((max(n, 1), rows.shape[1]))
+    _check(_lib.cvq_decode_values(ctx.h, _u32(rows.shape[0]), _u32(rows.shape[1]), _ptr(rows),
+                                  _ptr(bits), _u64(n), _ptr(out)))
+    return out[:n]
+
+
 class _Em(C.Structure):
     _fields_ = [("soft_iters", _u64), ("hard_iters_max", _u64), ("t0", _d), ("decay", _d),
                 ("tol", _d), ("ridge", _d), ("seed", _u64), ("search", C.c_int32)]

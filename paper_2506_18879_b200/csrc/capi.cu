@@ -1208,6 +1208,53 @@ CVQ_API cvq_status cvq_encode_keys(cvq_context* ctx, const cvq_key_config* kc, c
   return CVQ_OK;
 }
 
+CVQ_API cvq_status cvq_decode_keys(cvq_context* ctx, const cvq_key_config* kc, const double* atoms,
+                                   const uint16_t* a, const uint16_t* b, uint64_t n,
+                                   double* out) {
+  TRY(ctx_check(ctx));
+  TRY(validate_kc(kc));
+  if (!atoms || (n && (!a || !b || !out))) return fail(CVQ_EINVAL, "null argument");
+  if (n == 0) return CVQ_OK;
+  Geom g = make_geom(kc, 1, 0, 1);
+  const size_t na = (size_t)g.R * g.subs * g.L, np = (size_t)n * g.R * g.groups;
+  for (size_t i = 0; i < np; ++i)  // keyquant.cpp:756-757
+    if (a[i] >= g.L || b[i] >= g.L) return fail(CVQ_EINVAL, "decode_keys: code out of range");
+  CU(ctx->scratch.ensure((na * 2 + (size_t)n * g.d) * 8 + np * 4 + 256));
+  double* d_atoms = static_cast<double*>(ctx->scratch.p);
+  double* d_out = d_atoms + na * 2;
+  uint16_t* da = reinterpret_cast<uint16_t*>(d_out + (size_t)n * g.d);
+  uint16_t* db = da + np;
+  cudaStream_t st = ctx->stream;
+  CU(cudaMemcpyAsync(d_atoms, atoms, na * 16, cudaMemcpyHostToDevice, st));
+  CU(cudaMemcpyAsync(da, a, np * 2, cudaMemcpyHostToDevice, st));
+  CU(cudaMemcpyAsync(db, b, np * 2, cudaMemcpyHostToDevice, st));
+  CU(run_decode_keys(g, d_atoms, da, db, (long long)n, d_out, st));
+  CU(cudaMemcpyAsync(out, d_out, (size_t)n * g.d * 8, cudaMemcpyDeviceToHost, st));
+  CU(cudaStreamSynchronize(st));
+  return CVQ_OK;
+}
+
+CVQ_API cvq_status cvq_decode_values(cvq_context* ctx, uint32_t n_codes, uint32_t d,
+                                     const double* rows, const uint8_t* bits, uint64_t n,
+                                     double* out) {
+  TRY(ctx_check(ctx));
+  if (n_codes == 0 || d == 0) return fail(CVQ_EINVAL, "decode_values: empty codebook");
+  if (!rows || (n && (!bits || !out))) return fail(CVQ_EINVAL, "null argument");
+  if (n == 0) return CVQ_OK;
+  const size_t nr = (size_t)n_codes * d, nb = (size_t)n * n_codes;
+  CU(ctx->scratch.ensure((nr + (size_t)n * d) * 8 + nb + 256));
+  double* d_rows = static_cast<double*>(ctx->scratch.p);
+  double* d_out = d_rows + nr;
+  uint8_t* d_bits = reinterpret_cast<uint8_t*>(d_out + (size_t)n * d);
+  cudaStream_t st = ctx->stream;
+  CU(cudaMemcpyAsync(d_rows, rows, nr * 8, cudaMemcpyHostToDevice, st));
+  CU(cudaMemcpyAsync(d_bits, bits, nb, cudaMemcpyHostToDevice, st));
+  CU(run_decode_values((int)n_codes, (int)d, d_rows, d_bits, (long long)n, d_out, st));
+  CU(cudaMemcpyAsync(out, d_out, (size_t)n * d * 8, cudaMemcpyDeviceToHost, st));
+  CU(cudaStreamSynchronize(st));
+  return CVQ_OK;
+}
+
 CVQ_API cvq_status cvq_encode_keys_search(cvq_context* ctx, const cvq_key_config* kc,
                                           const double* atoms, const double* keys, uint64_t n,
                                           int32_t search, uint16_t* a, uint16_t* b) {

@@ -217,6 +217,11 @@ cudaError_t run_pack_values(const Geom& g, int S, const uint8_t* bits,
                             const unsigned long long* errpos = nullptr);
 cudaError_t run_unpack_keys(const Geom& g, const uint64_t* words, long long n,
                             uint16_t* a, uint16_t* b, cudaStream_t st);
+// dense reconstruction, bit-identical to decode_keys / decode_values (decode.cu)
+cudaError_t run_decode_keys(const Geom& g, const double* atoms, const uint16_t* a,
+                            const uint16_t* b, long long n, double* out, cudaStream_t st);
+cudaError_t run_decode_values(int n_codes, int d, const double* rows, const uint8_t* bits,
+                              long long n, double* out, cudaStream_t st);
 cudaError_t run_unpack_values(const Geom& g, const uint64_t* words,
                               long long n, uint8_t* bits, cudaStream_t st);
 

@@ -189,6 +189,14 @@ int main() {
     }
     report(same, "encoder_forward infer bits+logits exact");
     report(commvq::pack_key_codes(ref) == commvq::gpu::pack_key_codes(gpu), "pack_key_codes words");
+    report(commvq::decode_keys(ref, kcb).data == commvq::gpu::decode_keys(gpu, kcb).data,
+           "decode_keys dense rows bit-exact");
+    ValueCodebook vcb = ValueCodebook::zeros(128, 128);
+    for (double& v : vcb.rows.data) v = rng.normal() / 16;
+    ValueCodes vc = ValueCodes::empty(128, 50);
+    for (uint8_t& bt : vc.bits) bt = rng.normal() > 0 ? 1 : 0;
+    report(commvq::decode_values(vc, vcb).data == commvq::gpu::decode_values(vc, vcb).data,
+           "decode_values dense rows bit-exact");
   }
   // 3. cache: prefill / decode_step / CVQC interop both ways
   {

@@ -190,6 +190,27 @@ def test_encode_keys_near_ties_bit_exact(G):
     assert (ga == oa).all() and (gb == ob).all()
 
 
+@pytest.mark.parametrize("shape", [(12, 3, 4, 2, 64), (128, 64, 64, 11, 96),
+                                   (128, 64, 64, 21, 40), (32, 16, 256, 2, 20)])
+def test_decode_keys_values_bit_exact(G, shape):
+    """decode_keys (keyquant.cpp:741-768) and decode_values
+    (valquant.cpp:115-128) on the device: dense rows bit-identical to the
+    oracle; out-of-range codes raise like the reference."""
+    d, g, L, R, n = shape
+    kq = KQ(d, g, L, R)
+    atoms = fx.random_key_codebook(kq, 7 + d, scale=0.3 if d == 128 else 1.0)
+    a, b = fx.random_key_codes(kq, n, rng=P.rng(d + L))
+    assert (G.decode_keys(kq, atoms, a, b) == P.decode_keys(kq, atoms, a, b)).all()
+    nc = 128 if d == 128 else 17
+    rows = P.rng(nc + n).normal(nc * d, 1 / 16).reshape(nc, d)
+    bits = fx.random_value_codes(nc, n, rng=P.rng(n))
+    assert (G.decode_values(rows, bits) == P.decode_values(rows, bits)).all()
+    bad = a.copy()
+    bad[-1] = L
+    with pytest.raises(ValueError):
+        G.decode_keys(kq, atoms, bad, b)
+
+
 def test_value_encoder_bit_exact(G):
     """test_valquant.cpp:108-112 KAT + random weights: bits and logits exact."""
     w1, b1, w2 = np.zeros((4, 4)), np.zeros(4), np.zeros((4, 4))

@@ -301,6 +301,8 @@ def test_port_matches_reference_encoders(shape):
     rb, rl = R.encoder_forward_infer(w1, b1, w2, b2, keys)
     assert (pb == rb).all() and (pl == rl).all()
     assert (P.pack_value_codes(pb) == R.pack_value_codes(rb)).all()
+    rows = rng.normal(nc * d, 1 / 16).reshape(nc, d)
+    assert (P.decode_values(rows, pb) == R.decode_values(rows, rb)).all()
 
 
 def test_prefill_equals_appends_and_oracle_pack():
