@@ -20,8 +20,18 @@ FLAGS = [
 ]
 
 
+def _extra():
+    return os.environ.get("CVQ_NVCC_EXTRA", "").split()  # experiments, e.g. -DNAME=1
+
+
 def _stale():
     if not os.path.exists(SO):
+        return True
+    try:  # a build with other experiment flags is stale too
+        with open(SO + ".flags") as f:
+            if f.read() != " ".join(_extra()):
+                return True
+    except OSError:
         return True
     t = os.path.getmtime(SO)
     deps = [os.path.join(CSRC, f) for f in os.listdir(CSRC)] + [
@@ -32,7 +42,7 @@ def _stale():
 def build(force=False, verbose=False):
     if not force and not _stale():
         return SO
-    extra = os.environ.get("CVQ_NVCC_EXTRA", "").split()  # experiments, e.g. -DNAME=1
+    extra = _extra()
     cmd = [NVCC] + FLAGS + extra + ["-o", SO] + [os.path.join(CSRC, s) for s in SOURCES]
     r = subprocess.run(cmd, capture_output=True, text=True)
     log = os.path.join(HERE, "build.log")
@@ -41,6 +51,8 @@ def build(force=False, verbose=False):
     if r.returncode != 0:
         sys.stderr.write(r.stderr[-8000:])
         raise RuntimeError(f"nvcc failed (see {log})")
+    with open(SO + ".flags", "w") as f:
+        f.write(" ".join(extra))
     if verbose:
         sys.stderr.write(r.stderr)
     return SO

@@ -97,7 +97,14 @@ constexpr int kProdPerQ = 4;
 constexpr int kEpiPerQ = kEpiWarps / 4;    // epilogue warps per lane quarter
 constexpr int kSubsPerEpi = 64 / kEpiPerQ; // subspaces per epilogue warp
 constexpr int kMmaWarp = kEpiWarps + kProdWarps;  // MMA issuer + codebook loader
-constexpr int kIssuers = 2;  // warps kMmaWarp, kMmaWarp + 1 issue alternate rounds
+#ifndef CVQ_SP_ISSUERS
+#define CVQ_SP_ISSUERS 2
+#endif
+constexpr int kIssuers = CVQ_SP_ISSUERS;  // warps kMmaWarp, kMmaWarp + 1 issue alternate rounds
+// 1 issuer: C3 score kernel 11.38 ms vs 10.69 with 2 (same-box A/B).  More
+// than 2 would let an issuer sync a stage / zero named barrier of a later
+// generation while another still owes the current one (measured: hangs).
+static_assert(kIssuers == 1 || kIssuers == 2, "issuer warps");
 constexpr int kThreads = (kMmaWarp + kIssuers) * 32;
 // named barriers (bar.sync ids): 1-4 the epilogue's per-quarter reduction,
 // 5-10 the A stages (producers arrive, the round's issuer syncs), 11-12 the
@@ -448,7 +455,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_sp_score(SpArgs a) {
   if constexpr (PAIR) cluster_sync_all();  // barriers of both CTAs initialised
   else __syncthreads();
   tc_fence_after();
+#ifdef CVQ_SP_TMEM0
+  // the CTA owns all 512 TMEM columns, so the allocation starts at lane 0,
+  // column 0: a compile-time base keeps every TMEM operand address uniform
+  if (*tmem_slot != 0u) __trap();
+  constexpr uint32_t tmem = 0u;
+#else
   const uint32_t tmem = *tmem_slot;
+#endif
 
   if (warp < kEpiWarps) {
     // ============ epilogue: lane = token 32 quarter + lane of the tile,
@@ -753,25 +767,32 @@ __global__ void __launch_bounds__(kThreads, 1) k_sp_score(SpArgs a) {
             }
             __syncwarp();
             mbar_wait(cbfull, nload & 1);
-            asm volatile("bar.arrive %0, 64;" ::"r"(kBarCodebook) : "memory");
+            if (kIssuers > 1)
+              asm volatile("bar.arrive %0, %1;" ::"r"(kBarCodebook), "r"(32 * kIssuers) : "memory");
           } else {
-            asm volatile("bar.sync %0, 64;" ::"r"(kBarCodebook) : "memory");
+            asm volatile("bar.sync %0, %1;" ::"r"(kBarCodebook), "r"(32 * kIssuers) : "memory");
           }
           ++nload;
           prev_slot = slot;
         }
       }
-      const int w0 = (int)(gbase & 1u);  // issuer of round 0 of this tile
+      const int w0 = (int)(gbase % (uint32_t)kIssuers);  // issuer of round 0 of this tile
       const uint32_t dcol = tmem + (uint32_t)db * 128u;
       if (me == w0 && k >= 2) {  // D buffer db was read by the epilogue of tile k-2
+        if (TRK(k)) SPTR(128 + (k - kTrK0));
         mbar_wait(dempty + db, ((k - 2) >> 1) & 1);
+        if (TRK(k)) SPTR(136 + (k - kTrK0));
         tc_fence_after();
       }
 #pragma unroll 1
-      for (int r = (me == w0) ? 0 : 1; r < it.nr; r += 2) {
+      const int rme = (me - w0 + kIssuers) % kIssuers;  // this warp's first round
+      for (int r = rme; r < it.nr; r += kIssuers) {
         const uint32_t g = gbase + (uint32_t)r, st = g % kAStages;
-        if (r == 1) asm volatile("bar.sync %0, 64;" ::"r"(kBarZero0 + db) : "memory");  // D zeroed
+        if (kIssuers > 1 && r == rme && r > 0)  // D zeroed by round 0's issue
+          asm volatile("bar.sync %0, %1;" ::"r"(kBarZero0 + db), "r"(32 * kIssuers) : "memory");
+        if (TRK(k)) SPTR(0 + (k - kTrK0) * 16 + r);
         asm volatile("bar.sync %0, 160;" ::"r"(kBarStage0 + (int)st) : "memory");  // stage full
+        if (TRK(k)) SPTR(64 + (k - kTrK0) * 16 + r);
 #ifdef CVQ_DEVICE_CHECKS
         for (int q2 = 0; q2 < 4; ++q2) SP_CHECK(*(volatile uint32_t*)(stag + st * 4 + q2) == g);
         if (r == 0 && lane == 0) *(volatile uint32_t*)(dtag + db) = (uint32_t)k;
@@ -782,9 +803,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_sp_score(SpArgs a) {
         sp_issue_round(dcol, tmem + kACol0 + 32 * st, tmem + kMetaCol0 + 4 * st,
                                       bdesc0 + (uint64_t)((r * kRoundBytes) >> 4), idesc,
                                       r > 0 ? 1u : 0u, aempty + st);
-        if (r == 0) asm volatile("bar.arrive %0, 64;" ::"r"(kBarZero0 + db) : "memory");
+        if (TRK(k)) SPTR(192 + (k - kTrK0) * 16 + r);
+        if (kIssuers > 1 && r == 0)
+          asm volatile("bar.arrive %0, %1;" ::"r"(kBarZero0 + db), "r"(32 * kIssuers) : "memory");
       }
       tc_commit_elect(dfull + db);
+      if (TRK(k)) SPTR(144 + (k - kTrK0) + 4 * me);
       gbase += (uint32_t)it.nr;
     }
   }

@@ -58,7 +58,7 @@ def main():
             for qq in range(4):
                 b = 256 + qq * 64 + k * 16 + r
                 prod.append(f"{rel(t[b]):6d}>{rel(t[b + 256]):6d}>{rel(t[b + 512]):6d}")
-            mw = f"{rel(t[k * 16 + r]):6d}>{rel(t[64 + k * 16 + r]):6d}"
+            mw = f"{rel(t[k * 16 + r]):6d}>{rel(t[64 + k * 16 + r]):6d}>{rel(t[192 + k * 16 + r]):6d}"
             print(f"  r{r:2d} mma afull {mw} | prod q wait>got>arrive " + " ".join(prod))
         ep = []
         for w in range(16):
