@@ -203,6 +203,8 @@ struct cvq_cache {
   uint16_t* cbtc = nullptr;    // tcgen05 A operand [slot][R][2][8192] (CVQ_CACHE_KEYS_TC)
   float* cbv = nullptr;        // [slot][n_codes][d]
   double *w1 = nullptr, *b1 = nullptr, *w2 = nullptr, *b2 = nullptr;
+  float* w2f = nullptr;   // value-encoder screen tables: fp32 w2 and its fp64
+  double* n2 = nullptr;   // column norms (k_encode_values_screen)
   double* thetas = nullptr;
   std::vector<char> key_set, val_set, enc_set;
   DevBuf attn_scratch, enc_scratch, stage_in, stage_out, stage_kv;
@@ -309,7 +311,7 @@ cvq_status sync_check(cvq_cache* c) {
 void free_cache(cvq_cache* c) {
   for (void* p : {(void*)c->kpool, (void*)c->vpool, (void*)c->atoms64, (void*)c->base,
                   (void*)c->maxnorm, (void*)c->cbk, (void*)c->cbk16, (void*)c->cbtc, (void*)c->cbv, (void*)c->w1, (void*)c->b1,
-                  (void*)c->w2, (void*)c->b2, (void*)c->thetas})
+                  (void*)c->w2, (void*)c->b2, (void*)c->thetas, (void*)c->w2f, (void*)c->n2})
     if (p) cudaFree(p);
   c->attn_scratch.release();
   c->enc_scratch.release();
@@ -528,6 +530,8 @@ CVQ_API cvq_status cvq_cache_create(cvq_context* ctx, const cvq_cache_desc* d, c
     if (e == cudaSuccess) e = alloc((void**)&c->b1, (size_t)c->n_slots * g.hidden * 8);
     if (e == cudaSuccess) e = alloc((void**)&c->w2, (size_t)c->n_slots * g.hidden * g.n_codes * 8);
     if (e == cudaSuccess) e = alloc((void**)&c->b2, (size_t)c->n_slots * g.n_codes * 8);
+    if (e == cudaSuccess) e = alloc((void**)&c->w2f, (size_t)c->n_slots * g.hidden * g.n_codes * 4);
+    if (e == cudaSuccess) e = alloc((void**)&c->n2, (size_t)c->n_slots * g.n_codes * 8);
   }
   if (e == cudaSuccess) {
     std::vector<double> th = make_thetas(g.d, d->rope_base);
@@ -643,6 +647,19 @@ CVQ_API cvq_status cvq_cache_set_value_quantizer(cvq_cache* c, uint32_t layer, u
                        (size_t)g.hidden * g.n_codes * 8, cudaMemcpyHostToDevice, st));
     CU(cudaMemcpyAsync(c->b2 + (size_t)slot * g.n_codes, b2, (size_t)g.n_codes * 8,
                        cudaMemcpyHostToDevice, st));
+    // screen tables: fp32 w2 and its fp64 column norms
+    std::vector<float> f2((size_t)g.hidden * g.n_codes);
+    std::vector<double> m2(g.n_codes, 0.0);
+    for (size_t i = 0; i < f2.size(); ++i) {
+      f2[i] = (float)w2[i];
+      m2[i % g.n_codes] += w2[i] * w2[i];
+    }
+    for (double& v : m2) v = std::sqrt(v);
+    CU(cudaMemcpyAsync(c->w2f + (size_t)slot * f2.size(), f2.data(), f2.size() * 4,
+                       cudaMemcpyHostToDevice, st));
+    CU(cudaMemcpyAsync(c->n2 + (size_t)slot * g.n_codes, m2.data(), g.n_codes * 8,
+                       cudaMemcpyHostToDevice, st));
+    CU(cudaStreamSynchronize(st));  // the host vectors go out of scope
   }
   CU(cudaStreamSynchronize(st));
   c->val_set[slot] = 1;
@@ -666,7 +683,7 @@ cvq_status encode_append(cvq_cache* c, const void* K, const void* V, int dtype,
   uint8_t* bits = reinterpret_cast<uint8_t*>(b + (size_t)c->S * n * g.R * g.groups);
   KeyEncTables tab{c->atoms64, c->base, c->maxnorm};
   CU(run_encode_keys(g, c->S, c->n_slots, tab, K, dtype, s_stride, n, a, b, st));
-  ValEncWeights w{c->w1, c->b1, c->w2, c->b2};
+  ValEncWeights w{c->w1, c->b1, c->w2, c->b2, c->w2f, c->n2};
   CU(run_encode_values(g, c->S, c->n_slots, w, V, dtype, s_stride, n, bits, nullptr, c->d_errpos,
                        err_at, st));
   CU(run_pack_keys(g, c->S, a, b, n, (long long)c->length, c->kpool, c->kstride, st, c->d_errpos));

@@ -157,6 +157,10 @@ struct ValEncWeights {
   const double* b1;  // [slot][hidden]
   const double* w2;  // [slot][hidden][n_codes]
   const double* b2;  // [slot][n_codes]
+  // optional screen tables (prefill encoder, k_encode_values_screen): fp32
+  // copy of w2 and its column 2-norms |w2[:, c]| (fp64)
+  const float* w2f = nullptr;   // [slot][hidden][n_codes]
+  const double* n2 = nullptr;   // [slot][n_codes]
 };
 cudaError_t run_encode_values(const Geom& g, int S, int n_slots,
                               const ValEncWeights& w, const void* vals,

@@ -888,6 +888,172 @@ __global__ void __launch_bounds__(256) k_encode_values_gemm(
        });
 }
 
+// Screened prefill value encoder.  The logits are only needed for their
+// sign (bits = logit > 0).  The hidden layer h = relu(t w1 + b1) runs as the
+// exact-order fp64 GEMM of k_encode_values_gemm (bit-identical to the
+// reference's h); the output layer runs as an fp32 GEMM of fl32(h) with
+// fp32 weights, whose distance to the reference's fp64 logit is bounded by
+//   |l~_c - l_c| <= k2 (|h| |w2[:, c]| + |b2_c|),  k2 = 1.01 (hidden + 4) 2^-24
+// (rounding of h, w2, b2 to fp32 and the FMA dot product of hidden terms,
+// Cauchy-Schwarz; the 1.01 covers the fp64 rounding of the reference sum and
+// of the bound).  A logit farther from 0 than its bound has the reference's
+// sign; a token with any undecided or non-finite logit gets its output layer
+// recomputed exactly (reference order, zero-skips, no FMA) from the exact h,
+// so bits and the TrainingError position are bit-identical.
+constexpr double kU32 = 5.9604644775390625e-08;  // 2^-24
+__global__ void __launch_bounds__(256) k_encode_values_screen(
+    Geom g, int n_slots, ValEncWeights w, const void* __restrict__ vals, int dtype,
+    long long s_stride, long long n, uint8_t* __restrict__ bits,
+    unsigned long long* __restrict__ errpos, unsigned long long tok0) {
+  extern __shared__ double smv[];
+  double* T = smv;                              // [32][d]
+  double* H = T + (size_t)kVgTok * g.d;         // [32][hidden] (exact)
+  double* W = H + (size_t)kVgTok * g.hidden;    // [16][128] fp64 chunk (layer 1)
+  float* Wf = reinterpret_cast<float*>(W);      // [16][128] fp32 chunk (layer 2)
+  __shared__ double hn[kVgTok];
+  __shared__ int flag[kVgTok];
+  const int s = blockIdx.y, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const long long i0 = (long long)blockIdx.x * kVgTok;
+  const int nt = (int)min((long long)kVgTok, n - i0);
+  const int slot = s % n_slots;
+  const int tg = warp, cg = lane;  // tokens 4 tg .. +3, columns 4 cg .. +3 of a block
+  for (int e = tid; e < kVgTok * g.d; e += 256)
+    T[e] = (e / g.d < nt)
+               ? load_elem(vals, dtype, (long long)s * s_stride + (i0 + e / g.d) * g.d + e % g.d)
+               : 0.0;
+  if (tid < kVgTok) flag[tid] = 0;
+  const double* b1 = w.b1 + (size_t)slot * g.hidden;
+  const double* b2 = w.b2 + (size_t)slot * g.n_codes;
+  const double* n2 = w.n2 + (size_t)slot * g.n_codes;
+  // layer 1: exact-order fp64 (as k_encode_values_gemm)
+  {
+    const double* B = w.w1 + (size_t)slot * g.d * g.hidden;
+    const int K = g.d, N = g.hidden;
+    for (int c0 = 0; c0 < N; c0 += kVgCols) {
+      double acc[4][4];
+#pragma unroll
+      for (int m = 0; m < 4; ++m)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) acc[m][c] = 0.0;
+      for (int k0 = 0; k0 < K; k0 += kVgK) {
+        __syncthreads();
+        for (int e = tid; e < kVgK * kVgCols; e += 256) {
+          const int kk = e / kVgCols, cc = e % kVgCols;
+          W[e] = (k0 + kk < K && c0 + cc < N) ? __ldg(B + (size_t)(k0 + kk) * N + c0 + cc) : 0.0;
+        }
+        __syncthreads();
+        const int kn = min(kVgK, K - k0);
+        for (int kk = 0; kk < kn; ++kk) {
+          double a[4], b[4];
+#pragma unroll
+          for (int m = 0; m < 4; ++m) a[m] = T[(size_t)(4 * tg + m) * K + k0 + kk];
+#pragma unroll
+          for (int c = 0; c < 4; ++c) b[c] = W[kk * kVgCols + 4 * cg + c];
+#pragma unroll
+          for (int m = 0; m < 4; ++m)
+            if (a[m] != 0.0)
+#pragma unroll
+              for (int c = 0; c < 4; ++c) acc[m][c] = __dadd_rn(acc[m][c], __dmul_rn(a[m], b[c]));
+        }
+      }
+#pragma unroll
+      for (int m = 0; m < 4; ++m)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const int col = c0 + 4 * cg + c;
+          if (col < N) {
+            double v = __dadd_rn(acc[m][c], b1[col]);  // valquant.cpp:58-61
+            H[(size_t)(4 * tg + m) * N + col] = v < 0.0 ? 0.0 : v;
+          }
+        }
+    }
+  }
+  __syncthreads();
+  if (tid < kVgTok * 8) {  // |h| per token: 8 threads per token
+    const int m = tid >> 3, q = tid & 7;
+    double a = 0.0;
+    for (int j = q; j < g.hidden; j += 8) a = fma(H[(size_t)m * g.hidden + j], H[(size_t)m * g.hidden + j], a);
+    a += __shfl_xor_sync(0xffffffffu, a, 1);
+    a += __shfl_xor_sync(0xffffffffu, a, 2);
+    a += __shfl_xor_sync(0xffffffffu, a, 4);
+    if (q == 0) hn[m] = sqrt(a);
+  }
+  // layer 2: fp32 screen
+  const double k2 = 1.01 * (g.hidden + 4) * kU32;
+  {
+    const float* B = w.w2f + (size_t)slot * g.hidden * g.n_codes;
+    const int K = g.hidden, N = g.n_codes;
+    for (int c0 = 0; c0 < N; c0 += kVgCols) {
+      float acc[4][4];
+#pragma unroll
+      for (int m = 0; m < 4; ++m)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) acc[m][c] = 0.f;
+      for (int k0 = 0; k0 < K; k0 += kVgK) {
+        __syncthreads();
+        for (int e = tid; e < kVgK * kVgCols / 4; e += 256) {
+          const int kk = e / (kVgCols / 4), cc = 4 * (e % (kVgCols / 4));
+          *reinterpret_cast<float4*>(Wf + kk * kVgCols + cc) =
+              __ldg(reinterpret_cast<const float4*>(B + (size_t)(k0 + kk) * N + c0 + cc));
+        }
+        __syncthreads();
+#pragma unroll 4
+        for (int kk = 0; kk < kVgK; ++kk) {
+          float a[4];
+#pragma unroll
+          for (int m = 0; m < 4; ++m) a[m] = (float)H[(size_t)(4 * tg + m) * K + k0 + kk];
+          const float4 b = *reinterpret_cast<const float4*>(Wf + kk * kVgCols + 4 * cg);
+#pragma unroll
+          for (int m = 0; m < 4; ++m) {
+            acc[m][0] = fmaf(a[m], b.x, acc[m][0]);
+            acc[m][1] = fmaf(a[m], b.y, acc[m][1]);
+            acc[m][2] = fmaf(a[m], b.z, acc[m][2]);
+            acc[m][3] = fmaf(a[m], b.w, acc[m][3]);
+          }
+        }
+      }
+#pragma unroll
+      for (int m = 0; m < 4; ++m) {
+        const int tok = 4 * tg + m;
+        if (tok >= nt) continue;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const int col = c0 + 4 * cg + c;
+          const float v = acc[m][c] + (float)b2[col];
+          const double bound = k2 * (hn[tok] * n2[col] + fabs(b2[col]));
+          if (!(fabs((double)v) > bound)) flag[tok] = 1;  // undecided or non-finite
+          else bits[((size_t)s * n + i0 + tok) * N + col] = v > 0.f ? 1 : 0;
+        }
+      }
+    }
+  }
+  __syncthreads();
+  // exact output layer for the flagged tokens (h is exact already)
+  const double* w2 = w.w2 + (size_t)slot * g.hidden * g.n_codes;
+#pragma unroll 1
+  for (int m = 0; m < nt; ++m) {
+    if (!flag[m]) continue;  // uniform (smem)
+    const double* hm = H + (size_t)m * g.hidden;
+    for (int c = tid; c < g.n_codes; c += 256) {
+      double lg = 0.0;
+      for (int j0 = 0; j0 < g.hidden; j0 += 16) {
+        double wv[16];
+#pragma unroll
+        for (int u = 0; u < 16; ++u)
+          wv[u] = j0 + u < g.hidden ? __ldg(w2 + (size_t)(j0 + u) * g.n_codes + c) : 0.0;
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+          const double hj = j0 + u < g.hidden ? hm[j0 + u] : 0.0;
+          lg = __dadd_rn(lg, hj != 0.0 ? __dmul_rn(hj, wv[u]) : -0.0);  // valquant.cpp:63-69
+        }
+      }
+      const double v = __dadd_rn(lg, b2[c]);
+      if (!isfinite(v)) atomicMin(errpos, tok0);  // valquant.cpp:86-87 (TrainingError)
+      bits[((size_t)s * n + i0 + m) * g.n_codes + c] = v > 0.0 ? 1 : 0;
+    }
+  }
+}
+
 template <int TV>
 static cudaError_t launch_values(const Geom& g, int S, int n_slots, const ValEncWeights& w,
                                  const void* vals, int dtype, long long s_stride, long long n,
@@ -917,6 +1083,19 @@ cudaError_t run_encode_values(const Geom& g, int S, int n_slots, const ValEncWei
   if (n < 16)  // decode-step appends: one token per CTA, no wasted lanes
     return launch_values<1>(g, S, n_slots, w, vals, dtype, s_stride, n, bits, logits, errpos, tok0,
                             st);
+  if (w.w2f && !logits && g.d % kVgK == 0 && g.hidden % kVgCols == 0 &&
+      g.hidden % kVgK == 0 && g.n_codes % kVgCols == 0) {
+    const size_t sm = sizeof(double) * ((size_t)kVgTok * (g.d + g.hidden) + kVgK * kVgCols);
+    if (sm <= 200 * 1024) {
+      cudaError_t e = ensure_dyn_smem(reinterpret_cast<const void*>(k_encode_values_screen), sm);
+      if (e != cudaSuccess) return e;
+      dim3 grid((unsigned)((n + kVgTok - 1) / kVgTok), S);
+      k_encode_values_screen<<<grid, 256, sm, st>>>(g, n_slots, w, vals, dtype, s_stride, n, bits,
+                                                     errpos, tok0);
+      count_launch();
+      return cudaGetLastError();
+    }
+  }
   if (g.d % 4 == 0 && g.hidden % 4 == 0 && g.n_codes % 4 == 0) {
     const size_t sm = sizeof(double) * ((size_t)kVgTok * (g.d + g.hidden) + kVgK * kVgCols);
     if (sm <= 200 * 1024) {

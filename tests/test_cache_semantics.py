@@ -215,3 +215,41 @@ def test_single_level_codebook_cache(G):
     out = c.attention(q.reshape(1, 1, 1, 8).astype(np.float32), 8)
     want, _, _ = P.fused_attention(kq, f.atoms, a, b, bits, f.vrows, q, 8)
     assert fx.rel_err(out.reshape(-1), want) <= 1e-5
+
+
+def test_value_screen_presets_bit_exact(G):
+    """The prefill value encoder screens with fp32 GEMMs and a rigorous error
+    bound, re-computing undecided tokens exactly (k_encode_values_screen).
+    Head-preset shapes (hidden 256, 128 codes): bits equal the reference's,
+    including logits forced to exactly 0 (always undecided -> exact path) and
+    a non-finite row (TrainingError, nothing appended)."""
+    kq = KQ(128, 64, 64, 11)
+    nc, hidden, n = 128, 256, 300
+    rng = P.rng(2024)
+    atoms = rng.normal(2 * kq.n_atoms, 0.3)
+    vrows = rng.normal(nc * 128, 1 / 16).reshape(nc, 128)
+    w1 = rng.normal(128 * hidden, 0.1).reshape(128, hidden)
+    b1 = rng.normal(hidden, 0.05)
+    w2 = rng.normal(hidden * nc, 0.1).reshape(hidden, nc)
+    K = P.gen_synth(n, 128, 32, 3)
+    V = P.gen_synth(n, 128, 32, 4)
+    V[7, :5] = 0.0  # zero-skips
+    _, l0 = P.encoder_forward_infer(w1, b1, w2, np.zeros(nc), V)
+    b2 = rng.normal(nc, 0.05)
+    b2[:12] = -l0[5, :12]  # token 5: twelve logits exactly 0 in the reference
+    bits, lg = P.encoder_forward_infer(w1, b1, w2, b2, V)
+    assert (lg[5, :12] == 0.0).all()
+    c = G.QuantizedKVCache(kq, nc, capacity=n, hidden=hidden)
+    c.set_key_codebook(0, 0, atoms)
+    c.set_value_quantizer(0, 0, vrows, w1, b1, w2, b2)
+    c.prefill(K[None, None, None], V[None, None, None])
+    _, vw = c.export_stream(0, 0, 0)
+    assert (vw == P.pack_value_codes(bits)).all()
+    Vb = V.copy()
+    Vb[40, 3] = np.inf
+    c2 = G.QuantizedKVCache(kq, nc, capacity=n, hidden=hidden)
+    c2.set_key_codebook(0, 0, atoms)
+    c2.set_value_quantizer(0, 0, vrows, w1, b1, w2, b2)
+    with pytest.raises(G.TrainingError):
+        c2.prefill(K[None, None, None], Vb[None, None, None])
+    assert c2.size() == 0
