@@ -197,6 +197,7 @@ struct cvq_cache {
   uint64_t* vpool = nullptr;
   double* atoms64 = nullptr;   // [slot][R][subs][L][2]
   double* base = nullptr;      // [slot][R][groups][L][L] (when it fits)
+  float* keyf = nullptr;       // [slot]: fp32 atoms + base (head-preset key encoder)
   double* maxnorm = nullptr;   // [slot][R][groups]
   float2* cbk = nullptr;       // [slot][R][L][subs]
   uint32_t* cbk16 = nullptr;   // same, packed half2 (CVQ_CACHE_KEYS_FP16)
@@ -309,7 +310,7 @@ cvq_status sync_check(cvq_cache* c) {
 }
 
 void free_cache(cvq_cache* c) {
-  for (void* p : {(void*)c->kpool, (void*)c->vpool, (void*)c->atoms64, (void*)c->base,
+  for (void* p : {(void*)c->kpool, (void*)c->vpool, (void*)c->atoms64, (void*)c->base, (void*)c->keyf,
                   (void*)c->maxnorm, (void*)c->cbk, (void*)c->cbk16, (void*)c->cbtc, (void*)c->cbv, (void*)c->w1, (void*)c->b1,
                   (void*)c->w2, (void*)c->b2, (void*)c->thetas, (void*)c->w2f, (void*)c->n2})
     if (p) cudaFree(p);
@@ -525,6 +526,8 @@ CVQ_API cvq_status cvq_cache_create(cvq_context* ctx, const cvq_cache_desc* d, c
     e = alloc((void**)&c->maxnorm, (size_t)c->n_slots * g.R * g.groups * sizeof(double));
   if (e == cudaSuccess && key_tables_fit(g))
     e = alloc((void**)&c->base, (size_t)c->n_slots * g.R * g.groups * g.L * g.L * sizeof(double));
+  if (e == cudaSuccess && key_tables_fit(g) && key_t64_applies(g))
+    e = alloc((void**)&c->keyf, (size_t)c->n_slots * key_t64_table_floats(g) * sizeof(float));
   if (e == cudaSuccess && d->hidden > 0) {
     e = alloc((void**)&c->w1, (size_t)c->n_slots * g.d * g.hidden * 8);
     if (e == cudaSuccess) e = alloc((void**)&c->b1, (size_t)c->n_slots * g.hidden * 8);
@@ -612,9 +615,13 @@ CVQ_API cvq_status cvq_cache_set_key_codebook(cvq_cache* c, uint32_t layer, uint
                        cudaMemcpyHostToDevice, st));
   }
   if (c->base) {
+    float* af = c->keyf ? c->keyf + (size_t)slot * g.R * g.subs * g.L * 2 : nullptr;
+    float* bf = c->keyf ? c->keyf + (size_t)c->n_slots * g.R * g.subs * g.L * 2 +
+                              (size_t)slot * g.R * g.groups * g.L * g.L
+                        : nullptr;
     CU(build_key_enc_tables(g, 1, c->atoms64 + (size_t)slot * na * 2,
                             c->base + (size_t)slot * g.R * g.groups * g.L * g.L,
-                            c->maxnorm + (size_t)slot * g.R * g.groups, st));
+                            c->maxnorm + (size_t)slot * g.R * g.groups, st, af, bf));
   }
   CU(cudaStreamSynchronize(st));  // host vector dl must outlive the copy
   c->key_set[slot] = 1;
@@ -682,6 +689,10 @@ cvq_status encode_append(cvq_cache* c, const void* K, const void* V, int dtype,
   uint16_t* b = a + (size_t)c->S * n * g.R * g.groups;
   uint8_t* bits = reinterpret_cast<uint8_t*>(b + (size_t)c->S * n * g.R * g.groups);
   KeyEncTables tab{c->atoms64, c->base, c->maxnorm};
+  if (c->keyf) {  // fp32 tables: slot-major atoms, then slot-major base
+    tab.atomsf = c->keyf;
+    tab.basef = c->keyf + (size_t)c->n_slots * g.R * g.subs * g.L * 2;
+  }
   CU(run_encode_keys(g, c->S, c->n_slots, tab, K, dtype, s_stride, n, a, b, st));
   ValEncWeights w{c->w1, c->b1, c->w2, c->b2, c->w2f, c->n2};
   CU(run_encode_values(g, c->S, c->n_slots, w, V, dtype, s_stride, n, bits, nullptr, c->d_errpos,
@@ -1205,19 +1216,29 @@ CVQ_API cvq_status cvq_encode_keys(cvq_context* ctx, const cvq_key_config* kc, c
   const bool tables = key_tables_fit(g);
   const size_t nb = tables ? (size_t)g.R * g.groups * g.L * g.L : 0;
   const size_t np = (size_t)n * g.R * g.groups;
-  const size_t bytes = (na * 2 + nb + g.R * g.groups + (size_t)n * g.d) * 8 + np * 4 + 256;
+  const size_t nf = tables && key_t64_applies(g) ? key_t64_table_floats(g) : 0;  // fp32 tables
+  const size_t bytes =
+      (na * 2 + nb + g.R * g.groups + (size_t)n * g.d) * 8 + 16 + nf * 4 + np * 4 + 256;
   CU(ctx->scratch.ensure(bytes));
   double* d_atoms = static_cast<double*>(ctx->scratch.p);
   double* d_base = d_atoms + na * 2;
   double* d_max = d_base + nb;
   double* d_keys = d_max + g.R * g.groups;
-  uint16_t* da = reinterpret_cast<uint16_t*>(d_keys + (size_t)n * g.d);
+  float* d_f = reinterpret_cast<float*>(  // 16-B aligned (cp.async sources)
+      (reinterpret_cast<uintptr_t>(d_keys + (size_t)n * g.d) + 15) & ~(uintptr_t)15);
+  uint16_t* da = reinterpret_cast<uint16_t*>(d_f + nf);
   uint16_t* db = da + np;
   cudaStream_t st = ctx->stream;
   CU(cudaMemcpyAsync(d_atoms, atoms, na * 16, cudaMemcpyHostToDevice, st));
   CU(cudaMemcpyAsync(d_keys, keys, (size_t)n * g.d * 8, cudaMemcpyHostToDevice, st));
-  if (tables) CU(build_key_enc_tables(g, 1, d_atoms, d_base, d_max, st));
+  if (tables)
+    CU(build_key_enc_tables(g, 1, d_atoms, d_base, d_max, st, nf ? d_f : nullptr,
+                            nf ? d_f + na * 2 : nullptr));
   KeyEncTables tab{d_atoms, tables ? d_base : nullptr, d_max};
+  if (nf) {
+    tab.atomsf = d_f;
+    tab.basef = d_f + na * 2;
+  }
   CU(run_encode_keys(g, 1, 1, tab, d_keys, CVQ_F64, 0, (long long)n, da, db, st));
   CU(cudaMemcpyAsync(a, da, np * 2, cudaMemcpyDeviceToHost, st));
   CU(cudaMemcpyAsync(b, db, np * 2, cudaMemcpyDeviceToHost, st));

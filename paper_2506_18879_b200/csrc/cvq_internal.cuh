@@ -141,10 +141,18 @@ struct KeyEncTables {
   const double* atoms;   // [slot][R][subs][L][2] (reference order)
   const double* base;    // [slot][R][groups][L][L]
   const double* maxnorm; // [slot][R][groups]
+  // fp32 copies of atoms / base for the head-preset encoder (k_encode_keys_t64)
+  const float* atomsf = nullptr;
+  const float* basef = nullptr;
 };
+// atomsf / basef (optional): fp32 copies for k_encode_keys_t64
 cudaError_t build_key_enc_tables(const Geom& g, int n_slots,
                                  const double* atoms, double* base,
-                                 double* maxnorm, cudaStream_t st);
+                                 double* maxnorm, cudaStream_t st, float* atomsf = nullptr,
+                                 float* basef = nullptr);
+// whether the head-preset key encoder applies (and wants the fp32 tables)
+bool key_t64_applies(const Geom& g);
+size_t key_t64_table_floats(const Geom& g);  // per slot: atoms + base
 // keys: element (s, i, k) at keys + s*s_stride + i*d + k, dtype 0=f32 1=f64.
 // Codes: a/b [s][n][R*groups] uint16.  err_flag (device int) set on failure.
 cudaError_t run_encode_keys(const Geom& g, int S, int n_slots,

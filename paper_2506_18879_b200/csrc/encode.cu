@@ -41,7 +41,8 @@ constexpr double kMarginRel32 = 4e-6;
 // base[a][b] = |u_a|^2 + |v_b|^2 + 2 u_a.v_b per (slot, round, group) and
 // max_l |u_l| (= max |v_l|, v is u rotated per subspace).
 __global__ void k_key_base(Geom g, const double* __restrict__ atoms,
-                           double* __restrict__ base, double* __restrict__ maxnorm) {
+                           double* __restrict__ base, double* __restrict__ maxnorm,
+                           float* __restrict__ atomsf, float* __restrict__ basef) {
   const int rg = blockIdx.x;  // r * groups + grp
   const int slot = blockIdx.y;
   const int r = rg / g.groups, grp = rg % g.groups;
@@ -66,6 +67,11 @@ __global__ void k_key_base(Geom g, const double* __restrict__ atoms,
       uv += ua.x * (-ub.y) + ua.y * ub.x;  // u_a . v_b, v_b = (-y_b, x_b)
     }
     B[e] = nrm[a] + nrm[b] + 2.0 * uv;
+    if (basef) basef[((size_t)slot * g.R * g.groups + rg) * g.L * g.L + e] = (float)B[e];
+  }
+  if (atomsf) {
+    const size_t o = ((size_t)(slot * g.R + r) * g.subs + (size_t)grp * g.g) * g.L * 2;
+    for (int e = threadIdx.x; e < g.g * g.L * 2; e += blockDim.x) atomsf[o + e] = (float)atoms[o + e];
   }
   if (threadIdx.x == 0) {
     double m = 0.0;
@@ -75,10 +81,11 @@ __global__ void k_key_base(Geom g, const double* __restrict__ atoms,
 }
 
 cudaError_t build_key_enc_tables(const Geom& g, int n_slots, const double* atoms,
-                                 double* base, double* maxnorm, cudaStream_t st) {
+                                 double* base, double* maxnorm, cudaStream_t st, float* atomsf,
+                                 float* basef) {
   if (g.L > 1024) return cudaErrorInvalidValue;
   dim3 grid(g.R * g.groups, n_slots);
-  k_key_base<<<grid, 256, 0, st>>>(g, atoms, base, maxnorm);
+  k_key_base<<<grid, 256, 0, st>>>(g, atoms, base, maxnorm, atomsf, basef);
   count_launch();
   return cudaGetLastError();
 }
@@ -438,6 +445,187 @@ k_encode_keys_table(Geom g, int n_slots, const double* __restrict__ atoms,
   }
 }
 
+// Head-preset key encoder (L = 64 levels, g = 64 subspaces per group):
+// one CTA per (32-token tile, stream), 512 threads.  Per (round, group):
+//  * the fp64 slice U (exact distances, residual update; rows padded to 65)
+//    and the fp32 copies of the slice and of the base table arrive by
+//    cp.async from global fp32 tables built with the codebook;
+//  * projections p.u / p.v of all 32 tokens in fp32 (thread = 4 tokens x
+//    levels lg, lg + 32 over half the subspaces): twice the fp64 rate;
+//  * the index-free column screen of k_encode_keys_table, margin kMarginT64.
+// Screen error with fp32 projections (u = 2^-24, |p.u_a| sums 2g = 128
+// products, computed as two 64-FMA halves + one add, inputs rounded once):
+// |err(pu)| <= 68 u |p| |u_a| <= 68 u |p| mn, the same for pv; with the base
+// rounding and the two screen roundings a screen value is within
+// 3 u scale^2 + 4 * 68 u |p| mn <= 37 u scale^2 (|p| mn <= scale^2 / 8)
+// of the exact shifted distance: 4.4e-6 scale^2 pair to pair, so the margin
+// 8e-6 keeps a 1.8x factor.  Out-of-range scales and non-finite residuals
+// take the exact search over all pairs.
+constexpr double kMarginT64 = 8e-6;
+__global__ void __launch_bounds__(kEncWarps * 32)
+k_encode_keys_t64(Geom g, int n_slots, const double* __restrict__ atoms,
+                  const float* __restrict__ atomsf, const float* __restrict__ basef,
+                  const double* __restrict__ maxnorm, const void* __restrict__ keys, int dtype,
+                  long long s_stride, long long n, uint16_t* __restrict__ a_out,
+                  uint16_t* __restrict__ b_out) {
+  constexpr int L = 64, gs = 64, w2 = 128, us = L + 1;
+  extern __shared__ double sm[];
+  double2* U = reinterpret_cast<double2*>(sm);                     // [64][65]
+  float2* Uf = reinterpret_cast<float2*>(U + gs * us);             // [64][64]
+  float* Bf = reinterpret_cast<float*>(Uf + gs * L);               // [64][64]
+  double* P = reinterpret_cast<double*>(Bf + L * L);               // [32][d]
+  float* Pf = reinterpret_cast<float*>(P + (size_t)kEncTok * g.d); // [32][128] (this group)
+  float* TPUf = Pf + kEncTok * w2;                                 // [32][64]
+  float* TPVf = TPUf + kEncTok * L;                                // [32][64]
+  const int s = blockIdx.y, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const long long i0 = (long long)blockIdx.x * kEncTok;
+  const int nt = (int)min((long long)kEncTok, n - i0);
+  const int slot = s % n_slots;
+  for (int e = tid; e < nt * g.d; e += blockDim.x)
+    P[e] = load_elem(keys, dtype, (long long)s * s_stride + (i0 + e / g.d) * g.d + e % g.d);
+  for (int r = 0; r < g.R; ++r) {
+    for (int grp = 0; grp < g.groups; ++grp) {
+      __syncthreads();
+      const size_t rg = (size_t)(slot * g.R + r) * g.groups + grp;
+      const size_t uo = ((size_t)(slot * g.R + r) * g.subs + (size_t)grp * gs) * L;
+      const double2* Ug = reinterpret_cast<const double2*>(atoms) + uo;
+      for (int e = tid; e < gs * L; e += blockDim.x) cp_async16(U + (e / L) * us + e % L, Ug + e);
+      const float2* Ufg = reinterpret_cast<const float2*>(atomsf) + uo;
+      for (int e = 2 * tid; e < gs * L; e += 2 * blockDim.x) cp_async16(Uf + e, Ufg + e);
+      const float* Bg = basef + rg * L * L;
+      for (int e = 4 * tid; e < L * L; e += 4 * blockDim.x) cp_async16(Bf + e, Bg + e);
+      asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;\n" ::: "memory");
+      for (int e = tid; e < kEncTok * w2; e += blockDim.x)
+        Pf[e] = (float)P[(size_t)(e / w2) * g.d + grp * w2 + e % w2];
+      const double mn = maxnorm[rg];
+      __syncthreads();
+      {  // fp32 projections, halves of the subspaces added through smem
+        const int hs = tid >> 8, lg = tid & 31, tq = (tid >> 5) & 7;
+        float su[4][2], sv[4][2];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) su[t][0] = su[t][1] = sv[t][0] = sv[t][1] = 0.f;
+        const float* p0 = Pf + (size_t)(4 * tq) * w2;
+#pragma unroll 4
+        for (int si = hs * 32; si < hs * 32 + 32; ++si) {
+          const float2 u0 = Uf[si * L + lg], u1 = Uf[si * L + lg + 32];
+#pragma unroll
+          for (int t = 0; t < 4; ++t) {
+            const float2 pa = *reinterpret_cast<const float2*>(p0 + t * w2 + 2 * si);
+            su[t][0] = fmaf(pa.x, u0.x, fmaf(pa.y, u0.y, su[t][0]));
+            sv[t][0] = fmaf(pa.y, u0.x, fmaf(-pa.x, u0.y, sv[t][0]));
+            su[t][1] = fmaf(pa.x, u1.x, fmaf(pa.y, u1.y, su[t][1]));
+            sv[t][1] = fmaf(pa.y, u1.x, fmaf(-pa.x, u1.y, sv[t][1]));
+          }
+        }
+        if (hs) {
+#pragma unroll
+          for (int t = 0; t < 4; ++t) {
+            const int o = (4 * tq + t) * L + lg;
+            TPUf[o] = su[t][0];
+            TPUf[o + 32] = su[t][1];
+            TPVf[o] = sv[t][0];
+            TPVf[o + 32] = sv[t][1];
+          }
+        }
+        __syncthreads();
+        if (!hs) {
+#pragma unroll
+          for (int t = 0; t < 4; ++t) {
+            const int o = (4 * tq + t) * L + lg;
+            TPUf[o] += su[t][0];
+            TPUf[o + 32] += su[t][1];
+            TPVf[o] += sv[t][0];
+            TPVf[o + 32] += sv[t][1];
+          }
+        }
+        __syncthreads();
+      }
+      for (int tk = warp; tk < nt; tk += kEncWarps) {
+        double* p = P + (size_t)tk * g.d + grp * w2;
+        const float* puf = TPUf + tk * L;
+        const float* pvf = TPVf + tk * L;
+        double pn = 0.0;
+        for (int e = lane; e < w2; e += 32) pn = fma(p[e], p[e], pn);
+        for (int o = 16; o; o >>= 1) pn += __shfl_xor_sync(0xffffffffu, pn, o);
+        const double scale = sqrt(pn) + 2.0 * mn;
+        const double scale2 = scale * scale;
+        int chosen;
+        if (!(pn < 1e300) || !(mn < 1e150) || !(scale2 > 1e-30 && scale2 < 1e30)) {
+          chosen = exact_search<float>(p, U, us, L, gs, nullptr, nullptr, nullptr, false, 0.f);
+        } else {
+          // column screen (k_encode_keys_table): lane = columns 2 lane, 2 lane + 1
+          const int b0 = 2 * lane;
+          float m1a = INFINITY, m2a = INFINITY, m1b = INFINITY, m2b = INFINITY;
+#pragma unroll 4
+          for (int a0 = 0; a0 < L; a0 += 4) {
+            const float4 pu4 = *reinterpret_cast<const float4*>(puf + a0);
+            const float pus[4] = {pu4.x, pu4.y, pu4.z, pu4.w};
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const float2 bb = *reinterpret_cast<const float2*>(Bf + (a0 + u) * L + b0);
+              const float xa = fmaf(-2.f, pus[u], bb.x), xb = fmaf(-2.f, pus[u], bb.y);
+              m2a = fminf(m2a, fmaxf(m1a, xa));
+              m1a = fminf(m1a, xa);
+              m2b = fminf(m2b, fmaxf(m1b, xb));
+              m1b = fminf(m1b, xb);
+            }
+          }
+          const float2 pv2 = *reinterpret_cast<const float2*>(pvf + b0);
+          const float va = m1a - 2.f * pv2.x, vb = m1b - 2.f * pv2.y;
+          const float ra = m2a - 2.f * pv2.x, rb = m2b - 2.f * pv2.y;
+          float b1, b2;
+          int c1;
+          if (vb < va) {
+            b1 = vb; c1 = b0 + 1; b2 = fminf(rb, va);
+          } else {
+            b1 = va; c1 = b0; b2 = fminf(ra, vb);
+          }
+          float gb = b1;
+          int gc = c1;
+          for (int o = 16; o; o >>= 1) {
+            const float v2 = __shfl_xor_sync(0xffffffffu, gb, o);
+            const int c2 = __shfl_xor_sync(0xffffffffu, gc, o);
+            if (v2 < gb || (v2 == gb && c2 < gc)) {
+              gb = v2;
+              gc = c2;
+            }
+          }
+          float ru = (c1 == gc) ? b2 : b1;
+          for (int o = 16; o; o >>= 1) ru = fminf(ru, __shfl_xor_sync(0xffffffffu, ru, o));
+          const float margin = (float)(kMarginT64 * scale2);
+          if (ru > gb + margin) {
+            const float mc = __shfl_sync(0xffffffffu, (gc & 1) ? m1b : m1a, gc >> 1);
+            const float x0 = fmaf(-2.f, puf[lane], Bf[lane * L + gc]);
+            const float x1 = fmaf(-2.f, puf[lane + 32], Bf[(lane + 32) * L + gc]);
+            const unsigned k0 = __ballot_sync(0xffffffffu, x0 == mc);
+            const unsigned k1 = __ballot_sync(0xffffffffu, x1 == mc);
+            chosen = (k0 ? __ffs(k0) - 1 : 31 + __ffs(k1)) * L + gc;
+          } else {
+            chosen = exact_search(p, U, us, L, gs, Bf, puf, pvf, true, gb + margin);
+          }
+        }
+        const int ca = chosen / L, cb = chosen % L;
+        if (lane == 0) {
+          const size_t idx = ((size_t)s * n + i0 + tk) * (g.R * g.groups) + (size_t)r * g.groups + grp;
+          a_out[idx] = (uint16_t)ca;
+          b_out[idx] = (uint16_t)cb;
+        }
+        for (int si = lane; si < gs; si += 32) {
+          const double2 ua = U[(size_t)si * us + ca], ub = U[(size_t)si * us + cb];
+          p[2 * si] = __dsub_rn(p[2 * si], __dadd_rn(ua.x, -ub.y));
+          p[2 * si + 1] = __dsub_rn(p[2 * si + 1], __dadd_rn(ua.y, ub.x));
+        }
+        __syncwarp();
+      }
+    }
+  }
+}
+
+static size_t t64_smem(const Geom& g) {
+  return (size_t)64 * 65 * 16 + 64 * 64 * 8 + 64 * 64 * 4 + (size_t)kEncTok * g.d * 8 +
+         kEncTok * 128 * 4 + 2 * kEncTok * 64 * 4;
+}
+
 // Exact brute-force encoder for shapes whose slice does not fit on chip:
 // one warp per token, centers read from global/L1.
 __global__ void __launch_bounds__(128)
@@ -684,10 +872,27 @@ static size_t table_smem(const Geom& g) {
          sizeof(float) * ((size_t)g.L * g.L + 2 * rows * g.L);
 }
 
+bool key_t64_applies(const Geom& g) { return g.L == 64 && g.g == 64 && g.d % 128 == 0; }
+size_t key_t64_table_floats(const Geom& g) {
+  return (size_t)g.R * g.subs * g.L * 2 + (size_t)g.R * g.groups * g.L * g.L;
+}
+
 cudaError_t run_encode_keys(const Geom& g, int S, int n_slots, const KeyEncTables& tab,
                             const void* keys, int dtype, long long s_stride, long long n,
                             uint16_t* a, uint16_t* b, cudaStream_t st) {
   if (n <= 0 || S <= 0) return cudaSuccess;
+  if (tab.atomsf && tab.basef && tab.maxnorm && key_t64_applies(g) && n >= 8 &&
+      t64_smem(g) <= 200 * 1024) {
+    const size_t sm = t64_smem(g);
+    cudaError_t e = ensure_dyn_smem(reinterpret_cast<const void*>(k_encode_keys_t64), sm);
+    if (e != cudaSuccess) return e;
+    dim3 grid((unsigned)((n + kEncTok - 1) / kEncTok), S);
+    k_encode_keys_t64<<<grid, kEncWarps * 32, sm, st>>>(g, n_slots, tab.atoms, tab.atomsf,
+                                                        tab.basef, tab.maxnorm, keys, dtype,
+                                                        s_stride, n, a, b);
+    count_launch();
+    return cudaGetLastError();
+  }
   const size_t sm = table_smem(g);
   cudaError_t e;
   const size_t sm_small =
