@@ -998,7 +998,10 @@ int f2_chunk(const AttnJob& job) {
   if (ch < 256) ch = 256;
   // 32 KiB smem -> 6 CTAs/SM (latency-bound kernel); measured on C3: 1024 and
   // 2048 tie, 512 and 4096 are slower
-  if (ch > 1024) ch = 1024;
+#ifndef CVQ_F2_MAXCHUNK
+#define CVQ_F2_MAXCHUNK 1024
+#endif
+  if (ch > CVQ_F2_MAXCHUNK) ch = CVQ_F2_MAXCHUNK;
   return (int)ch;
 }
 
