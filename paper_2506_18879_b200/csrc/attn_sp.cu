@@ -540,6 +540,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_sp_score(SpArgs a) {
         const float2* E = etab + (eslot * 32 + pass * 16) * 32 + lane;
         const float* wp = wt + pass * 16 * 2 * G;
 #pragma unroll
+#ifdef CVQ_DIAG_NOEPI  // diagnostic only (wrong scores): no epilogue math
+        if (false)
+#endif
         for (int jj = 0; jj < 16; ++jj) {
           const float2 ej = E[jj * 32];
           const float kr = __uint_as_float(re[jj]), ki = __uint_as_float(im[jj]);
@@ -681,7 +684,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_sp_score(SpArgs a) {
         }
 #pragma unroll
         for (int s2 = 0; s2 < 2; ++s2) {
+#ifdef CVQ_DIAG_NOPROD  // diagnostic only (wrong scores): constant codes
+          const uint32_t c = (uint32_t)s2 * 5u + 7u;
+#else
           const uint32_t c = (fld >> (6 * s2)) & 63u;
+#endif
           uint32_t v[16];
           const uint32_t col = ((c >> 5) << 3) | ((c & 31) >> 2);
           // word col holds fp16 1.0 in slot c & 1; one compare per word pair
