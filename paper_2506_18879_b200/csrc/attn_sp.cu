@@ -67,7 +67,10 @@ namespace {
 #ifdef SP_TRACE
 // clock64 trace of CTA 0 over tiles [kTrK0, kTrK0 + 4) (tools/sp_trace.py)
 __device__ long long g_sptr[8192];
-constexpr int kTrK0 = 20;
+#ifndef SP_TRACE_K0
+#define SP_TRACE_K0 20
+#endif
+constexpr int kTrK0 = SP_TRACE_K0;
 #define SPTR(idx) \
   do { if (blockIdx.x == 0 && (threadIdx.x & 31) == 0) g_sptr[(idx)] = clock64(); } while (0)
 #define TRK(k) ((k) >= kTrK0 && (k) < kTrK0 + 4)

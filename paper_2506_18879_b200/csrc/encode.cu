@@ -708,6 +708,184 @@ __device__ __forceinline__ void block_argmin2(double& b1, int& c1, double& b2, d
   __syncthreads();
 }
 
+// Decode-step key encoder for the head presets (L = g = 64) with the fp32
+// tables of k_encode_keys_t64: a CTA of 512 threads per (token, stream).
+// Per (round, group) only the fp32 slice and base table (48 KiB) stream in,
+// double-buffered by cp.async; projections and the screen run in fp32 with
+// the t64 margin (kMarginT64, same error analysis: each projection is four
+// 32-product FMA partials plus three adds).  The fp64 slice is read from
+// global memory only for the residual update and the (rare) exact search.
+__global__ void __launch_bounds__(kSmallThreads)
+k_encode_keys_small32(Geom g, int n_slots, const double* __restrict__ atoms,
+                      const float* __restrict__ atomsf, const float* __restrict__ basef,
+                      const double* __restrict__ maxnorm, const void* __restrict__ keys,
+                      int dtype, long long s_stride, long long n, uint16_t* __restrict__ a_out,
+                      uint16_t* __restrict__ b_out) {
+  constexpr int L = 64, gs = 64, w2 = 128;
+  extern __shared__ double sm[];
+  float2* UB = reinterpret_cast<float2*>(sm);            // [2][64][64]
+  float* BB = reinterpret_cast<float*>(UB + 2 * gs * L); // [2][64][64]
+  double* P = reinterpret_cast<double*>(BB + 2 * L * L); // [d]
+  float* Pf = reinterpret_cast<float*>(P + g.d);         // [128]
+  float* PR = Pf + w2;                                   // [4][128] projection partials
+  float* PUf = PR + 4 * w2;                              // [64]
+  float* PVf = PUf + L;                                  // [64]
+  __shared__ float rv[2 * kSmallWarps + 2];
+  __shared__ int rc[kSmallWarps + 2];
+  __shared__ double pns;
+  const int s = blockIdx.y, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const long long i = blockIdx.x;
+  const int slot = s % n_slots;
+  for (int e = tid; e < g.d; e += blockDim.x)
+    P[e] = load_elem(keys, dtype, (long long)s * s_stride + i * g.d + e);
+  const int total = g.R * g.groups;
+  auto stage = [&](int idx, int buf) {
+    const int rr = idx / g.groups, gg = idx % g.groups;
+    const size_t uo = ((size_t)(slot * g.R + rr) * g.subs + (size_t)gg * gs) * L;
+    const float* Ug = atomsf + 2 * uo;
+    const float* Bg = basef + ((size_t)(slot * g.R + rr) * g.groups + gg) * L * L;
+    float* Ud = reinterpret_cast<float*>(UB + buf * gs * L);
+    for (int e = 4 * tid; e < 2 * gs * L; e += 4 * kSmallThreads) cp_async16(Ud + e, Ug + e);
+    for (int e = 4 * tid; e < L * L; e += 4 * kSmallThreads) cp_async16(BB + buf * L * L + e, Bg + e);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  stage(0, 0);
+  for (int r = 0; r < g.R; ++r) {
+    for (int grp = 0; grp < g.groups; ++grp) {
+      const int idx = r * g.groups + grp, buf = idx & 1;
+      if (idx + 1 < total) {
+        stage(idx + 1, buf ^ 1);
+        asm volatile("cp.async.wait_group 1;" ::: "memory");
+      } else {
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
+      }
+      double* p = P + grp * w2;
+      if (tid < w2) Pf[tid] = (float)p[tid];
+      if (tid < 32) {
+        double pn = 0.0;
+        for (int e = tid; e < w2; e += 32) pn = fma(p[e], p[e], pn);
+        for (int o = 16; o; o >>= 1) pn += __shfl_xor_sync(0xffffffffu, pn, o);
+        if (tid == 0) pns = pn;
+      }
+      __syncthreads();
+      const float2* Uf = UB + buf * gs * L;
+      const float* Bf = BB + buf * L * L;
+      {  // projections: thread (q, o) sums subspaces [16 q, 16 q + 16) of output o
+        const int o = tid & 127, q = tid >> 7, l = o & 63;
+        const bool isv = o >= L;
+        float acc = 0.f;
+#pragma unroll 8
+        for (int si = 16 * q; si < 16 * q + 16; ++si) {
+          const float2 u = Uf[si * L + l];
+          const float px = Pf[2 * si], py = Pf[2 * si + 1];
+          acc = isv ? fmaf(py, u.x, fmaf(-px, u.y, acc)) : fmaf(px, u.x, fmaf(py, u.y, acc));
+        }
+        PR[q * w2 + o] = acc;
+      }
+      __syncthreads();
+      if (tid < w2) {
+        const float v = ((PR[tid] + PR[w2 + tid]) + PR[2 * w2 + tid]) + PR[3 * w2 + tid];
+        (tid >= L ? PVf : PUf)[tid & 63] = v;
+      }
+      __syncthreads();
+      const double pn = pns;
+      const double mn = maxnorm[(size_t)(slot * g.R + r) * g.groups + grp];
+      const double scale = sqrt(pn) + 2.0 * mn, scale2 = scale * scale;
+      const bool screen = pn < 1e300 && mn < 1e150 && scale2 > 1e-30 && scale2 < 1e30;
+      const double2* U = reinterpret_cast<const double2*>(atoms) +
+                         ((size_t)(slot * g.R + r) * g.subs + (size_t)grp * gs) * L;
+      int chosen = 0;
+      bool exact = !screen;
+      float gb = 0.f, margin = 0.f;
+      if (screen) {
+        // thread: column b = tid & 63, rows a = (tid >> 6) + 8 k (increasing c)
+        const int b = tid & 63;
+        float m1 = INFINITY, m2 = INFINITY;
+        int ia = 0;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const int a = (tid >> 6) + 8 * k;
+          const float x = fmaf(-2.f, PUf[a], Bf[a * L + b]);
+          if (x < m1) ia = a;
+          m2 = fminf(m2, fmaxf(m1, x));
+          m1 = fminf(m1, x);
+        }
+        const float t2 = 2.f * PVf[b];
+        float v = m1 - t2, ru = m2 - t2;
+        int c = ia * L + b;
+        // block argmin (value, then smallest index) and runner-up
+        float gv = v;
+        int gc = c;
+        for (int o = 16; o; o >>= 1) {
+          const float v2 = __shfl_xor_sync(0xffffffffu, gv, o);
+          const int c2 = __shfl_xor_sync(0xffffffffu, gc, o);
+          if (v2 < gv || (v2 == gv && c2 < gc)) {
+            gv = v2;
+            gc = c2;
+          }
+        }
+        float wr = (c == gc) ? ru : v;
+        for (int o = 16; o; o >>= 1) wr = fminf(wr, __shfl_xor_sync(0xffffffffu, wr, o));
+        if (lane == 0) {
+          rv[warp] = gv;
+          rc[warp] = gc;
+          rv[kSmallWarps + warp] = wr;
+        }
+        __syncthreads();
+        if (warp == 0) {
+          const float wv = lane < kSmallWarps ? rv[lane] : INFINITY;
+          const int wc = lane < kSmallWarps ? rc[lane] : 0x7fffffff;
+          const float wrr = lane < kSmallWarps ? rv[kSmallWarps + lane] : INFINITY;
+          float bv = wv;
+          int bc = wc;
+          for (int o = 16; o; o >>= 1) {
+            const float v2 = __shfl_xor_sync(0xffffffffu, bv, o);
+            const int c2 = __shfl_xor_sync(0xffffffffu, bc, o);
+            if (v2 < bv || (v2 == bv && c2 < bc)) {
+              bv = v2;
+              bc = c2;
+            }
+          }
+          float br = (wc == bc) ? wrr : wv;
+          for (int o = 16; o; o >>= 1) br = fminf(br, __shfl_xor_sync(0xffffffffu, br, o));
+          if (lane == 0) {
+            rv[2 * kSmallWarps] = bv;
+            rv[2 * kSmallWarps + 1] = br;
+            rc[kSmallWarps] = bc;
+          }
+        }
+        __syncthreads();
+        gb = rv[2 * kSmallWarps];
+        margin = (float)(kMarginT64 * scale2);
+        chosen = rc[kSmallWarps];
+        exact = !(rv[2 * kSmallWarps + 1] > gb + margin);
+      }
+      if (exact) {  // warp 0: exact search (screen-filtered when in range); rare
+        if (warp == 0) {
+          const int c = screen ? exact_search(p, U, L, L, gs, Bf, PUf, PVf, true, gb + margin)
+                               : exact_search<float>(p, U, L, L, gs, nullptr, nullptr, nullptr,
+                                                     false, 0.f);
+          if (lane == 0) rc[kSmallWarps + 1] = c;
+        }
+        __syncthreads();
+        chosen = rc[kSmallWarps + 1];
+      }
+      const int ca = chosen / L, cb = chosen % L;
+      if (tid == 0) {
+        const size_t o = ((size_t)s * n + i) * (g.R * g.groups) + (size_t)r * g.groups + grp;
+        a_out[o] = (uint16_t)ca;
+        b_out[o] = (uint16_t)cb;
+      }
+      if (tid < gs) {
+        const double2 ua = U[(size_t)tid * L + ca], vb = U[(size_t)tid * L + cb];
+        p[2 * tid] = __dsub_rn(p[2 * tid], __dadd_rn(ua.x, -vb.y));
+        p[2 * tid + 1] = __dsub_rn(p[2 * tid + 1], __dadd_rn(ua.y, vb.x));
+      }
+      __syncthreads();
+    }
+  }
+}
+
 __global__ void __launch_bounds__(kSmallThreads)
 k_encode_keys_small(Geom g, int n_slots, const double* __restrict__ atoms,
                     const double* __restrict__ base, const double* __restrict__ maxnorm,
@@ -898,6 +1076,17 @@ cudaError_t run_encode_keys(const Geom& g, int S, int n_slots, const KeyEncTable
   const size_t sm_small =
       sizeof(double) * (4 * (size_t)g.g * g.L + 2 * (((size_t)g.L * g.L + 1) & ~(size_t)1) + g.d + 2 * g.L +
                         (size_t)(kSmallThreads / (2 * g.L)) * 2 * g.L);
+  if (tab.atomsf && tab.basef && key_t64_applies(g) && n < 8) {
+    // decode-step appends, head presets: fp32 screen from the fp32 tables
+    const size_t sm32 = (size_t)2 * 64 * 64 * 8 + 2 * 64 * 64 * 4 + g.d * 8 + (128 + 4 * 128 + 128) * 4;
+    e = ensure_dyn_smem(reinterpret_cast<const void*>(k_encode_keys_small32), sm32);
+    if (e != cudaSuccess) return e;
+    dim3 grid((unsigned)n, S);
+    k_encode_keys_small32<<<grid, kSmallThreads, sm32, st>>>(
+        g, n_slots, tab.atoms, tab.atomsf, tab.basef, tab.maxnorm, keys, dtype, s_stride, n, a, b);
+    count_launch();
+    return cudaGetLastError();
+  }
   if (tab.base != nullptr && n < 8 && 2 * g.L <= kSmallThreads && sm_small <= 220 * 1024) {
     // decode-step appends: a CTA per token, the round slices double-buffered
     e = ensure_dyn_smem(reinterpret_cast<const void*>(k_encode_keys_small), sm_small);

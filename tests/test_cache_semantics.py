@@ -253,3 +253,41 @@ def test_value_screen_presets_bit_exact(G):
     with pytest.raises(G.TrainingError):
         c2.prefill(K[None, None, None], Vb[None, None, None])
     assert c2.size() == 0
+
+
+def test_preset_appends_bit_exact_with_near_ties(G):
+    """Decode-step appends on the head preset run the fp32-screen small
+    encoder (k_encode_keys_small32): codes of single-token appends equal the
+    reference's, including keys constructed exactly midway between two
+    centres (the screen is not decisive there: exact search)."""
+    kq = KQ(128, 64, 64, 11)
+    nc = 128
+    rng = P.rng(77)
+    atoms = rng.normal(2 * kq.n_atoms, 0.3)
+    xy = atoms.reshape(11, 64, 64, 2)
+    n = 24
+    K = P.gen_synth(n, 128, 32, 8)
+    for i in range(0, n, 3):  # every third key: a round-0 midpoint
+        a1, b1, a2, b2 = rng.index(4, 64).tolist()
+        for j in range(64):
+            c1 = (xy[0, j, a1, 0] - xy[0, j, b1, 1], xy[0, j, a1, 1] + xy[0, j, b1, 0])
+            c2 = (xy[0, j, a2, 0] - xy[0, j, b2, 1], xy[0, j, a2, 1] + xy[0, j, b2, 0])
+            K[i, 2 * j] = 0.5 * (c1[0] + c2[0])
+            K[i, 2 * j + 1] = 0.5 * (c1[1] + c2[1])
+    V = P.gen_synth(n, 128, 32, 9)
+    hidden = 256
+    w1 = rng.normal(128 * hidden, 0.1).reshape(128, hidden)
+    w2 = rng.normal(hidden * nc, 0.1).reshape(hidden, nc)
+    b1, b2 = np.zeros(hidden), np.zeros(nc)
+    vrows = rng.normal(nc * 128, 1 / 16).reshape(nc, 128)
+    c = G.QuantizedKVCache(kq, nc, capacity=8, hidden=hidden)
+    c.set_key_codebook(0, 0, atoms)
+    c.set_value_quantizer(0, 0, vrows, w1, b1, w2, b2)
+    for i in range(n):
+        c.append(K[None, None, None, i], V[None, None, None, i])
+    c.synchronize()
+    kw, vw = c.export_stream(0, 0, 0)
+    a, b = P.encode_keys(kq, atoms, K)
+    bits, _ = P.encoder_forward_infer(w1, b1, w2, b2, V)
+    assert (kw == P.pack_key_codes(kq, a, b)).all()
+    assert (vw == P.pack_value_codes(bits)).all()

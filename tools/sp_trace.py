@@ -50,6 +50,8 @@ def main():
     assert rc == 0, rc
     t = np.frombuffer(buf, dtype=np.int64).copy()
     z = t[144 + 0] - 4000  # a reference point before tile 0's end
+    if len(sys.argv) > 2:  # absolute: relative to the kernel's first trace point
+        z = min(v for v in t if v > 0)
     rel = lambda v: int(v - z) if v else -1  # noqa: E731
     for k in range(4):
         print(f"--- tile {k}: MMA dempty wait {rel(t[128 + k])} -> {rel(t[136 + k])}, dfull commit {rel(t[144 + k])}")
