@@ -680,6 +680,27 @@ __device__ __forceinline__ void fast_value_finish(const FastArgs& a, float* zr, 
   }
 }
 
+// one-thread bulk copies (TMA engine) into shared memory, completing on an
+// mbarrier: a CTA's staging costs 3 instructions instead of a cp.async loop
+__device__ __forceinline__ void fv_bulk(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          (uint32_t)__cvta_generic_to_shared(dst)),
+      "l"(src), "r"(bytes), "r"((uint32_t)__cvta_generic_to_shared(bar))
+      : "memory");
+}
+__device__ __forceinline__ void fv_bar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  do {
+    asm volatile(
+        "{.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;}"
+        : "=r"(ok)
+        : "r"((uint32_t)__cvta_generic_to_shared(bar)), "r"(parity)
+        : "memory");
+  } while (!ok);
+}
+
 __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
   uint32_t d;
   asm("prmt.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(sel));
@@ -723,10 +744,30 @@ __global__ void __launch_bounds__(kThreads, MMA ? (NC <= 128 ? 4 : 2) : 1) k_fas
   const int cnt = (int)(i1 - i0);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 
-  // stage the chunk's value words (token-aligned, 16-B aligned)
+  // stage the chunk's value words (token-aligned, 16-B aligned) and, with
+  // half weights, the weights and group maxima: bulk copies by one thread
   const uint64_t* vsrc = a.vpool + (size_t)s * a.vstride + (size_t)i0 * WPTOK;
   const int nw = ((cnt * WPTOK + 1) / 2) * 2;
-  for (int e = tid; e < nw / 2; e += kThreads) cp_async16(vw + 2 * e, vsrc + 2 * e);
+  __shared__ __align__(8) uint64_t tbar;
+  if (tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(
+                     (uint32_t)__cvta_generic_to_shared(&tbar))
+                 : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (tid == 0) {
+    uint32_t bytes = (uint32_t)nw * 8u;
+    if constexpr (PH) {
+      const int ngr0 = (cnt + 31) >> 5;
+      bytes += (uint32_t)((cnt * G * 2 + 15) / 16) * 16u + (uint32_t)((ngr0 * G * 4 + 15) / 16) * 16u;
+    }
+    asm volatile("{.reg .b64 st;\n\tmbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;}" ::"r"(
+                     (uint32_t)__cvta_generic_to_shared(&tbar)),
+                 "r"(bytes)
+                 : "memory");
+    fv_bulk(vw, vsrc, (uint32_t)nw * 8u, &tbar);
+  }
   float ls[G];
 #pragma unroll
   for (int h = 0; h < G; ++h) ls[h] = 0.f;
@@ -742,13 +783,13 @@ __global__ void __launch_bounds__(kThreads, MMA ? (NC <= 128 ? 4 : 2) : 1) k_fas
     const int ngr = (cnt + 31) >> 5;
     const __half* hsrc = a.ph + ((size_t)s * a.nps + i0) * G;
     const int nh = (cnt * G * 2 + 15) / 16;
-    for (int e = tid; e < nh; e += kThreads) cp_async16(hw + 8 * e, hsrc + 8 * e);
     const float* msrc = a.m32 + ((size_t)s * (a.nps >> 5) + (i0 >> 5)) * G;
     const int nm = (ngr * G * 4 + 15) / 16;
-    for (int e = tid; e < nm; e += kThreads) cp_async16(gm + 4 * e, msrc + 4 * e);
-    cp_async_commit();
-    cp_async_wait<0>();
-    __syncthreads();
+    if (tid == 0) {
+      fv_bulk(hw, hsrc, (uint32_t)nh * 16u, &tbar);
+      fv_bulk(gm, msrc, (uint32_t)nm * 16u, &tbar);
+    }
+    fv_bar_wait(&tbar, 0);
     if (warp < G) {  // chunk max per head: warp h, lane = group (ngr <= 32)
       float v = lane < ngr ? gm[lane * G + warp] : -INFINITY;
       for (int o = 16; o; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
@@ -786,8 +827,6 @@ __global__ void __launch_bounds__(kThreads, MMA ? (NC <= 128 ? 4 : 2) : 1) k_fas
       }
     }
   } else {
-  cp_async_commit();
-
   // full scores = sum of the JS partials; chunk max per head
   float mx[G];
 #pragma unroll
@@ -869,7 +908,7 @@ __global__ void __launch_bounds__(kThreads, MMA ? (NC <= 128 ? 4 : 2) : 1) k_fas
     for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
     if (lane == 0) red[warp][h] = v;
   }
-  cp_async_wait<0>();
+  if constexpr (!PH) fv_bar_wait(&tbar, 0);  // value words (PH waited with the weights)
   __syncthreads();
   if (tid < G) {
     float v = 0.f;
