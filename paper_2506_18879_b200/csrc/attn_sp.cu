@@ -39,7 +39,10 @@
 //   E = e^{+i lane theta_j}, score_h += Re(w_hj z) where w_hj = conj(q_hj)
 //   e^{-i(t - p0 - 32 quarter) theta_j} / sqrt(d) is per warp (fp64-based at a
 //   work item's first tile, advanced by e^{+i 128 theta_j} per tile); a
-//   2-warp smem sum per quarter.
+//   2-warp smem sum per quarter.  Output: fp32 partial scores per round part
+//   (R = 21 runs as 2 parts), or -- one part, the default -- fp16 weights
+//   exp(s - m32) with the max m32 of each 32-token group per head
+//   (k_fast_value<PH> rescales them; half the bytes of fp32 scores).
 //   Round-2 measurements of these choices: DESIGN.md section 4 and
 //   profiles/r02_*.
 //
