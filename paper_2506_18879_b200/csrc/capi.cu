@@ -213,6 +213,8 @@ struct cvq_cache {
   bool tc_demoted = false;                // a key codebook failed the fp16 guard
   unsigned long long* d_errpos = nullptr; // first failed append position (~0 = none)
   unsigned long long* h_errpos = nullptr; // pinned mirror, read at sync points
+  void* h_stage = nullptr;                 // pinned [k | v | q] / out staging (small steps)
+  size_t h_stage_n = 0;
   bool pending = false;                   // appends not yet checked for errors
 };
 
@@ -321,6 +323,7 @@ void free_cache(cvq_cache* c) {
   c->stage_kv.release();
   if (c->d_errpos) cudaFree(c->d_errpos);
   if (c->h_errpos) cudaFreeHost(c->h_errpos);
+  if (c->h_stage) cudaFreeHost(c->h_stage);
 }
 
 AttnJob make_job(const cvq_cache* c) {
@@ -869,6 +872,44 @@ CVQ_API cvq_status cvq_lse_combine_ptrs(cvq_context* ctx, const float* const* pa
 CVQ_API cvq_status cvq_cache_decode_step(cvq_cache* c, const void* k, const void* v, int kv_dtype,
                                          const float* q, float* out, int where) {
   if (!c) return fail(CVQ_EINVAL, "null cache");
+  if (where == CVQ_HOST && k && v && q && out && (kv_dtype == CVQ_F32 || kv_dtype == CVQ_F64)) {
+    // small steps: one H2D copy of [k | v | q] through pinned staging and one
+    // D2H of out instead of three + one (copy latency dominates there)
+    const Geom& g = c->geo;
+    const size_t es = kv_dtype == CVQ_F32 ? 4 : 8;
+    const size_t kvb = (size_t)c->S * g.d * es, qb = (size_t)c->S * g.G * g.d * sizeof(float);
+    const size_t qo = (2 * kvb + 15) / 16 * 16, tot = qo + qb;
+    if (tot <= (256u << 10)) {
+      TRY(ctx_check(c->ctx));
+      if (c->h_stage_n < tot) {
+        if (c->h_stage) cudaFreeHost(c->h_stage);
+        c->h_stage = nullptr;
+        c->h_stage_n = 0;
+        CU(cudaMallocHost(&c->h_stage, tot));
+        c->h_stage_n = tot;
+      }
+      char* h = static_cast<char*>(c->h_stage);
+      CU(cudaStreamSynchronize(c->ctx->stream));  // the previous step's D2H has landed
+      std::memcpy(h, k, kvb);
+      std::memcpy(h + kvb, v, kvb);
+      std::memcpy(h + qo, q, qb);
+      CU(c->stage_kv.ensure(tot));
+      char* d = static_cast<char*>(c->stage_kv.p);
+      CU(cudaMemcpyAsync(d, h, tot, cudaMemcpyHostToDevice, c->ctx->stream));
+      TRY(append_tokens(c, d, d + kvb, 1, kv_dtype, CVQ_DEVICE, false));
+      const uint64_t t = c->desc.position_offset + c->length - 1;  // cache.cpp:290
+      CU(c->stage_out.ensure(qb));
+      float* od = static_cast<float*>(c->stage_out.p);
+      TRY(attention_common(c, reinterpret_cast<const float*>(d + qo), t, od, nullptr, nullptr,
+                           nullptr, CVQ_DEVICE));
+      CU(cudaMemcpyAsync(h, od, qb, cudaMemcpyDeviceToHost, c->ctx->stream));
+      TRY(enqueue_error_read(c));
+      CU(cudaStreamSynchronize(c->ctx->stream));
+      TRY(take_errors(c));
+      std::memcpy(out, h, qb);
+      return CVQ_OK;
+    }
+  }
   TRY(cvq_cache_append(c, k, v, kv_dtype, where));
   const uint64_t t = c->desc.position_offset + c->length - 1;  // cache.cpp:290
   return cvq_cache_attention(c, q, t, out, where);
