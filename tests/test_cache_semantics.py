@@ -291,3 +291,32 @@ def test_preset_appends_bit_exact_with_near_ties(G):
     bits, _ = P.encoder_forward_infer(w1, b1, w2, b2, V)
     assert (kw == P.pack_key_codes(kq, a, b)).all()
     assert (vw == P.pack_value_codes(bits)).all()
+
+
+def test_two_group_preset_prefill_and_appends_bit_exact(G):
+    """d = 256 with 64-subspace groups (two key groups per round): the fp32
+    prefill encoder (k_encode_keys_t64) and the fp32 decode-step encoder
+    (k_encode_keys_small32) both handle the second group's residual and
+    slice offsets; words equal the reference packing."""
+    kq = KQ(256, 64, 64, 3)
+    nc, hidden = 128, 0
+    rng = P.rng(555)
+    atoms = rng.normal(2 * kq.n_atoms, 0.3)
+    K = P.gen_synth(70, 256, 32, 12)
+    V = P.gen_synth(70, 256, 32, 13)
+    vrows = rng.normal(nc * 256, 1 / 16).reshape(nc, 256)
+    w1 = rng.normal(256 * 128, 0.1).reshape(256, 128)
+    w2 = rng.normal(128 * nc, 0.1).reshape(128, nc)
+    b1, b2 = np.zeros(128), np.zeros(nc)
+    c = G.QuantizedKVCache(kq, nc, capacity=80, hidden=128)
+    c.set_key_codebook(0, 0, atoms)
+    c.set_value_quantizer(0, 0, vrows, w1, b1, w2, b2)
+    c.prefill(K[None, None, None, :60], V[None, None, None, :60])
+    for i in range(60, 70):
+        c.append(K[None, None, None, i], V[None, None, None, i])
+    c.synchronize()
+    kw, vw = c.export_stream(0, 0, 0)
+    a, b = P.encode_keys(kq, atoms, K)
+    bits, _ = P.encoder_forward_infer(w1, b1, w2, b2, V)
+    assert (kw == P.pack_key_codes(kq, a, b)).all()
+    assert (vw == P.pack_value_codes(bits)).all()

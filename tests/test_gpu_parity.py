@@ -157,7 +157,7 @@ def test_encode_ties_to_smallest_pair(G):
 
 @pytest.mark.parametrize("shape", [
     (12, 3, 4, 2, 64), (8, 2, 4, 2, 100), (16, 4, 16, 3, 77), (128, 64, 64, 11, 96),
-    (128, 64, 64, 21, 40), (128, 16, 16, 4, 33), (32, 16, 256, 2, 20),
+    (128, 64, 64, 21, 40), (128, 16, 16, 4, 33), (32, 16, 256, 2, 20), (256, 64, 64, 3, 50),
 ])
 def test_encode_keys_bit_exact(G, shape):
     d, g, L, R, n = shape
