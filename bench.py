@@ -162,6 +162,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"])
     ap.add_argument("--no-prefill", action="store_true")
+    ap.add_argument("--mgpu-world1", action="store_true",
+                    help="run the cvq_mgpu shard group (NCCL, world 1) as at N > 1 (test)")
     ap.add_argument("--no-naive", action="store_true",
                     help="skip timing the decode-then-attend baseline on the same cache")
     ap.add_argument("--merge", default="nccl", choices=["nccl", "peer"],
@@ -244,17 +246,24 @@ def main():
     out = torch.empty_like(q)
     t_q = N - 1  # global query position (last cached token)
     peer = group = None
+    merge_note = None
     if world > 1 and args.merge == "peer":
         # experimental: symmetric-memory blocks read by the combine over NVLink
         from paper_2506_18879_b200.dist import PeerMerge
         peer = PeerMerge(rows, d)
-    elif world > 1 and args.dist_backend == "nccl":
+    elif (world > 1 and args.dist_backend == "nccl") or args.mgpu_world1:
         # the C-ABI shard group (mgpu.cu): partial -> one ncclAllGather of the
         # packed [m | l | o] blocks -> LSE combine, inside libcvq_b200
         import torch.distributed as dist
-        uid = [G.ShardGroup.unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(uid, src=0)
-        group = G.ShardGroup(cache, rank, world, uid[0])
+        try:
+            uid = [G.ShardGroup.unique_id() if rank == 0 else None]
+            if world > 1:
+                dist.broadcast_object_list(uid, src=0)
+            group = G.ShardGroup(cache, rank, world, uid[0])
+            merge_note = "cvq_mgpu (in-library ncclAllGather + LSE combine)"
+        except Exception as ex:  # keep the run measurable: torch.distributed gather
+            group = None
+            merge_note = "torch.distributed all-gather (cvq_mgpu init failed: %s)" % str(ex)[:120]
     # gloo (several ranks sharing one GPU, host-staged exchange): the same
     # packed blocks gathered through torch.distributed
     from paper_2506_18879_b200.dist import gather_packed, packed_views
@@ -262,7 +271,7 @@ def main():
     m_p, l_p, o_p = packed_views(pk, rows, d)
 
     def step():
-        if world == 1:
+        if world == 1 and group is None:
             cache.attention(q, t_q, out)
         elif peer is not None:
             m_v, l_v, o_v = peer.views()
@@ -279,6 +288,23 @@ def main():
             import torch.distributed as dist
             dist.barrier()
 
+    if group is not None:
+        # the in-library exchange against the torch.distributed one on the
+        # first step; on any disagreement all ranks fall back together
+        import torch.distributed as dist
+        group.attention(q, t_q, out)
+        ref_out = torch.empty_like(out)
+        cache.attention_partial(q, m_p, l_p, o_p, t_q)
+        G.lse_combine_packed(gather_packed(pk) if world > 1 else pk.view(1, -1), rows, d, ref_out, ctx)
+        torch.cuda.synchronize()
+        bad = torch.tensor([0.0 if torch.isfinite(out).all() and
+                            float((out - ref_out).abs().max()) <= 1e-4 * float(ref_out.abs().max())
+                            else 1.0], device="cuda")
+        if world > 1:
+            dist.all_reduce(bad)
+        if float(bad) > 0:
+            group = None
+            merge_note = "torch.distributed all-gather (cvq_mgpu result disagreed on step 0)"
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
@@ -389,7 +415,7 @@ def main():
 
     # ---- e2e through the C-ABI with host buffers (decode_step) ----
     e2e = None
-    if not args.no_e2e and world > 1 and group is not None:
+    if not args.no_e2e and group is not None:
         # every rank passes its pinned host buffers; the last rank appends
         kh = torch.from_numpy(np.random.default_rng(5).standard_normal((B, layers, H, d))
                               .astype(np.float32)).pin_memory()
@@ -407,17 +433,18 @@ def main():
             group.decode_step(kh, vh, qh, oh)
         torch.cuda.synchronize()
         e2e_ms = (time.perf_counter() - t0) * 1e3 / n_e2e
-        import torch.distributed as dist
-        tt = torch.tensor([e2e_ms], device="cuda")
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        e2e_ms = float(tt.item())
+        if world > 1:
+            import torch.distributed as dist
+            tt = torch.tensor([e2e_ms], device="cuda")
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            e2e_ms = float(tt.item())
         n_now = group.size()
         e2e = {"value": B * layers * n_now / (e2e_ms / 1e3), "unit": "KV-tokens/s",
                "h2d_bytes_per_step": int(kh.numel() * 4 * 2 + qh.numel() * 4),
                "d2h_bytes_per_step": int(oh.numel() * 4), "ms_per_step": e2e_ms,
                "path": "cvq_mgpu_decode_step (last shard appends k,v; partial + NCCL all-gather "
                        "+ combine) with pinned host buffers on every rank, max over ranks"}
-    if not args.no_e2e and world == 1:
+    if not args.no_e2e and world == 1 and group is None:
         kh = np.random.default_rng(5).standard_normal((B, layers, H, d)).astype(np.float32)
         vh = np.random.default_rng(6).standard_normal((B, layers, H, d)).astype(np.float32)
         qh = np.random.default_rng(7).standard_normal((B, layers, H * Gq, d)).astype(np.float32)
@@ -513,6 +540,7 @@ def main():
                        "n_kv_heads": H, "q_per_kv": Gq, "context": N, "key": [d, g, L, R],
                        "n_codes": nc, "parallelism": f"context-shard x{world}",
                        "merge": args.merge if world > 1 else None,
+                       "exchange": merge_note,
                        "l2": "inputs (packed cache) larger than L2"},
             "kv_head_tokens_per_s": value * H, "roofline": roof, "clocks": clk_sum,
             "gpu_launches": launches, "e2e": e2e, "cpu_baseline": cpu, "prefill": prefill,
