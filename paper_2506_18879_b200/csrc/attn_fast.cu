@@ -895,9 +895,12 @@ __global__ void __launch_bounds__(kThreads, MMA ? (NC <= 128 ? 4 : 2) : 1) k_fas
       if (e < cpad) {
 #pragma unroll
         for (int h = 0; h < G; ++h) {
-          const __half hv = __float2half_rn(e < cnt ? pv[k][h] : 0.f);
+          // weights carried as p 2^15 against bits of 2^-16 (an fp16
+          // subnormal whose only byte is the bit): the products are p / 2,
+          // exact, and z is doubled at the end
+          const __half hv = __float2half_rn(e < cnt ? pv[k][h] * 32768.f : 0.f);
           PT[h * pst + e] = hv;
-          ls[h] += __half2float(hv);
+          ls[h] += __half2float(hv) * (1.f / 32768.f);
         }
       }
     }
@@ -920,8 +923,9 @@ __global__ void __launch_bounds__(kThreads, MMA ? (NC <= 128 ? 4 : 2) : 1) k_fas
     // lane % 4) holds the fragments of tokens 2t, 2t+1, 2t+8, 2t+9 of the
     // step and codes 16 mt + g (+ 8): byte j of u32 word i of a token's code
     // bits, masked at bit g, is code 32 i + 8 j + g, i.e. m-tile 2 i + j / 2,
-    // row g + 8 (j & 1); times 0x3C it is the high byte of fp16 1.0, and a
-    // sign-replicating prmt pairs two tokens' bytes into an A register.
+    // row g + 8 (j & 1); as the high byte of an fp16 it is 0 or 2^-16 (a
+    // subnormal: exact in the tensor core), and a sign-replicating prmt pairs
+    // two tokens' bytes into an A register.
     constexpr int MT = NC / 16, NW32 = NC / 32;
     const int g = lane >> 2, t = lane & 3;
     float d[MT][4];
@@ -948,10 +952,10 @@ __global__ void __launch_bounds__(kThreads, MMA ? (NC <= 128 ? 4 : 2) : 1) k_fas
         const uint32_t cv[4] = {C4.x, C4.y, C4.z, C4.w}, dv[4] = {D4.x, D4.y, D4.z, D4.w};
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-          const uint32_t mA = ((av[u] >> g) & 0x01010101u) * 0x3Cu;
-          const uint32_t mB = ((bv[u] >> g) & 0x01010101u) * 0x3Cu;
-          const uint32_t mC = ((cv[u] >> g) & 0x01010101u) * 0x3Cu;
-          const uint32_t mD = ((dv[u] >> g) & 0x01010101u) * 0x3Cu;
+          const uint32_t mA = (av[u] >> g) & 0x01010101u;
+          const uint32_t mB = (bv[u] >> g) & 0x01010101u;
+          const uint32_t mC = (cv[u] >> g) & 0x01010101u;
+          const uint32_t mD = (dv[u] >> g) & 0x01010101u;
           const int mt = 2 * (i4 + u);
           uint32_t fa[4] = {prmt(mA, mB, 0x4C08), prmt(mA, mB, 0x5D19), prmt(mC, mD, 0x4C08),
                             prmt(mC, mD, 0x5D19)};
@@ -967,13 +971,14 @@ __global__ void __launch_bounds__(kThreads, MMA ? (NC <= 128 ? 4 : 2) : 1) k_fas
     for (int mt = 0; mt < MT; ++mt) {
       float* z0 = zr + ((size_t)warp * NC + 16 * mt + g) * G;
       float* z1 = z0 + 8 * G;
+      constexpr float zsc = 2.f;  // bits were 2^-16, weights p 2^15
       if (2 * t < G) {
-        z0[2 * t] = d[mt][0];
-        z1[2 * t] = d[mt][2];
+        z0[2 * t] = zsc * d[mt][0];
+        z1[2 * t] = zsc * d[mt][2];
       }
       if (2 * t + 1 < G) {
-        z0[2 * t + 1] = d[mt][1];
-        z1[2 * t + 1] = d[mt][3];
+        z0[2 * t + 1] = zsc * d[mt][1];
+        z1[2 * t + 1] = zsc * d[mt][3];
       }
     }
     fast_value_finish<NC, G>(a, zr, mh, lh, s);
