@@ -174,6 +174,17 @@ struct cvq_context {
   bool prof = false;
   std::vector<cudaEvent_t> prof_ev;  // pairs
   size_t prof_used = 0;
+  // side stream for the value encoder of an append (the key and value
+  // encoders are independent: they overlap, joined before packing)
+  cudaStream_t side = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+  cudaError_t ensure_side() {
+    if (side) return cudaSuccess;
+    cudaError_t e = cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&fork, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&join, cudaEventDisableTiming);
+    return e;
+  }
   cudaEvent_t* next_prof_pair() {
     if (!prof) return nullptr;
     if (2 * (prof_used + 1) > prof_ev.size()) {
@@ -440,6 +451,12 @@ CVQ_API cvq_status cvq_context_destroy(cvq_context* ctx) {
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
   for (cudaEvent_t e : ctx->prof_ev) cudaEventDestroy(e);
+  if (ctx->side) {
+    cudaStreamSynchronize(ctx->side);
+    cudaStreamDestroy(ctx->side);
+    cudaEventDestroy(ctx->fork);
+    cudaEventDestroy(ctx->join);
+  }
   destroy_mirror(ctx->mirror);
   ctx->scratch.release();
   if (ctx->d_err) cudaFree(ctx->d_err);
@@ -696,10 +713,17 @@ cvq_status encode_append(cvq_cache* c, const void* K, const void* V, int dtype,
     tab.atomsf = c->keyf;
     tab.basef = c->keyf + (size_t)c->n_slots * g.R * g.subs * g.L * 2;
   }
+  // the value encoder runs on the context's side stream, overlapping the
+  // key encoder; the packs wait for both
+  CU(c->ctx->ensure_side());
+  CU(cudaEventRecord(c->ctx->fork, st));
+  CU(cudaStreamWaitEvent(c->ctx->side, c->ctx->fork, 0));
   CU(run_encode_keys(g, c->S, c->n_slots, tab, K, dtype, s_stride, n, a, b, st));
   ValEncWeights w{c->w1, c->b1, c->w2, c->b2, c->w2f, c->n2};
   CU(run_encode_values(g, c->S, c->n_slots, w, V, dtype, s_stride, n, bits, nullptr, c->d_errpos,
-                       err_at, st));
+                       err_at, c->ctx->side));
+  CU(cudaEventRecord(c->ctx->join, c->ctx->side));
+  CU(cudaStreamWaitEvent(st, c->ctx->join, 0));
   CU(run_pack_keys(g, c->S, a, b, n, (long long)c->length, c->kpool, c->kstride, st, c->d_errpos));
   CU(run_pack_values(g, c->S, bits, n, (long long)c->length, c->vpool, c->vstride, st,
                      c->d_errpos));
