@@ -722,11 +722,11 @@ cvq_status encode_append(cvq_cache* c, const void* K, const void* V, int dtype,
   ValEncWeights w{c->w1, c->b1, c->w2, c->b2, c->w2f, c->n2};
   CU(run_encode_values(g, c->S, c->n_slots, w, V, dtype, s_stride, n, bits, nullptr, c->d_errpos,
                        err_at, c->ctx->side));
-  CU(cudaEventRecord(c->ctx->join, c->ctx->side));
-  CU(cudaStreamWaitEvent(st, c->ctx->join, 0));
-  CU(run_pack_keys(g, c->S, a, b, n, (long long)c->length, c->kpool, c->kstride, st, c->d_errpos));
-  CU(run_pack_values(g, c->S, bits, n, (long long)c->length, c->vpool, c->vstride, st,
+  CU(run_pack_values(g, c->S, bits, n, (long long)c->length, c->vpool, c->vstride, c->ctx->side,
                      c->d_errpos));
+  CU(cudaEventRecord(c->ctx->join, c->ctx->side));
+  CU(cudaStreamWaitEvent(st, c->ctx->join, 0));  // the key pack reads the error position
+  CU(run_pack_keys(g, c->S, a, b, n, (long long)c->length, c->kpool, c->kstride, st, c->d_errpos));
   c->length += (uint64_t)n;
   c->pending = true;
   return CVQ_OK;
