@@ -713,19 +713,27 @@ cvq_status encode_append(cvq_cache* c, const void* K, const void* V, int dtype,
     tab.atomsf = c->keyf;
     tab.basef = c->keyf + (size_t)c->n_slots * g.R * g.subs * g.L * 2;
   }
-  // the value encoder runs on the context's side stream, overlapping the
-  // key encoder; the packs wait for both
-  CU(c->ctx->ensure_side());
-  CU(cudaEventRecord(c->ctx->fork, st));
-  CU(cudaStreamWaitEvent(c->ctx->side, c->ctx->fork, 0));
+  // decode-step appends (a few tokens per stream): the value encoder and
+  // its pack run on the context's side stream, overlapping the key encoder
+  // (both are latency-bound there); prefill chunks stay on one stream (two
+  // large concurrent encoders measured slower)
+  cudaStream_t vst = st;
+  if (n <= 8) {
+    CU(c->ctx->ensure_side());
+    vst = c->ctx->side;
+    CU(cudaEventRecord(c->ctx->fork, st));
+    CU(cudaStreamWaitEvent(vst, c->ctx->fork, 0));
+  }
   CU(run_encode_keys(g, c->S, c->n_slots, tab, K, dtype, s_stride, n, a, b, st));
   ValEncWeights w{c->w1, c->b1, c->w2, c->b2, c->w2f, c->n2};
   CU(run_encode_values(g, c->S, c->n_slots, w, V, dtype, s_stride, n, bits, nullptr, c->d_errpos,
-                       err_at, c->ctx->side));
-  CU(run_pack_values(g, c->S, bits, n, (long long)c->length, c->vpool, c->vstride, c->ctx->side,
+                       err_at, vst));
+  CU(run_pack_values(g, c->S, bits, n, (long long)c->length, c->vpool, c->vstride, vst,
                      c->d_errpos));
-  CU(cudaEventRecord(c->ctx->join, c->ctx->side));
-  CU(cudaStreamWaitEvent(st, c->ctx->join, 0));  // the key pack reads the error position
+  if (vst != st) {
+    CU(cudaEventRecord(c->ctx->join, vst));
+    CU(cudaStreamWaitEvent(st, c->ctx->join, 0));  // the key pack reads the error position
+  }
   CU(run_pack_keys(g, c->S, a, b, n, (long long)c->length, c->kpool, c->kstride, st, c->d_errpos));
   c->length += (uint64_t)n;
   c->pending = true;
