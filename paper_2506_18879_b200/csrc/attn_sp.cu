@@ -550,13 +550,22 @@ __global__ void __launch_bounds__(kThreads, 1) k_sp_score(SpArgs a) {
         if (false)
 #endif
         for (int jj = 0; jj < 16; ++jj) {
+#ifdef CVQ_DIAG_NOSMEM  // diagnostic only (wrong scores): no E / w table loads
+          const float2 ej = make_float2(__int_as_float(lane + jj), 0.5f);
+#else
           const float2 ej = E[jj * 32];
+#endif
           const float kr = __uint_as_float(re[jj]), ki = __uint_as_float(im[jj]);
           const float zx = ej.x * kr - ej.y * ki;
           const float zy = ej.x * ki + ej.y * kr;
           if constexpr (G == 4) {
+#ifdef CVQ_DIAG_NOSMEM
+            const float4 w01 = make_float4(0.1f * jj, 0.2f, 0.3f, 0.4f);
+            const float4 w23 = make_float4(0.5f, 0.6f * jj, 0.7f, 0.8f);
+#else
             const float4 w01 = reinterpret_cast<const float4*>(wp)[jj * 2];
             const float4 w23 = reinterpret_cast<const float4*>(wp)[jj * 2 + 1];
+#endif
             acc01 = ffma2(make_float2(w01.x, w01.y), zx, acc01);
             acc01 = ffma2(make_float2(w01.z, w01.w), zy, acc01);
             acc23 = ffma2(make_float2(w23.x, w23.y), zx, acc23);
