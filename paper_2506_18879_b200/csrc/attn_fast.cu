@@ -768,6 +768,10 @@ __global__ void __launch_bounds__(kThreads, MMA ? (NC <= 128 ? 4 : 2) : 1) k_fas
                  : "memory");
     fv_bulk(vw, vsrc, (uint32_t)nw * 8u, &tbar);
   }
+  // programmatic dependent launch: the value words above do not depend on the
+  // score kernel; everything below does
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   float ls[G];
 #pragma unroll
   for (int h = 0; h < G; ++h) ls[h] = 0.f;
@@ -1058,6 +1062,24 @@ size_t f2_smem(const AttnJob& job, int chunk2) {
   return (stage >= zr ? stage : stage + zr) + 16;  // zr aliases the staging when it fits
 }
 
+// launch with programmatic stream serialization: the kernel may start while
+// its predecessor drains and waits in griddepcontrol.wait for its results
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                       Args... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...);
+}
+
 template <class K>
 cudaError_t set_smem(K kernel, size_t sm) {
   return ensure_dyn_smem(reinterpret_cast<const void*>(kernel), sm);
@@ -1096,7 +1118,8 @@ cudaError_t launch_f2(const FastArgs& a, size_t sm, cudaStream_t st) {
   cudaError_t e = set_smem(k_fast_value<NC, G, JS, PH, MMA>, sm);
   if (e != cudaSuccess) return e;
   dim3 grid((unsigned)((a.n + a.chunk2 - 1) / a.chunk2), a.S);
-  k_fast_value<NC, G, JS, PH, MMA><<<grid, kThreads, sm, st>>>(a);
+  e = launch_pdl(k_fast_value<NC, G, JS, PH, MMA>, grid, dim3(kThreads), sm, st, a);
+  if (e != cudaSuccess) return e;
   count_launch();
   return cudaGetLastError();
 }
@@ -1129,6 +1152,8 @@ __global__ void __launch_bounds__(256) k_combine_merge(const float* __restrict__
   __shared__ float part[8][32];
   __shared__ float red[8];
   __shared__ float Ms, Lsh;
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // the value kernel's partials
   const long long row = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   float M = -FLT_MAX;
@@ -1180,6 +1205,7 @@ __global__ void __launch_bounds__(128) k_combine_project(const float* __restrict
                                                          float* __restrict__ m_out,
                                                          float* __restrict__ l_out) {
   __shared__ float zs[NC];
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // the merged z rows
   const long long row = blockIdx.x;
   const float* zr = zm + row * (NC + 2);
   for (int k = threadIdx.x; k < NC; k += 128) zs[k] = zr[k];
@@ -1214,6 +1240,7 @@ __global__ void __launch_bounds__(kCfThreads) k_combine_fused(
   __shared__ float zp[4][NC];
   __shared__ float zs[NC];
   __shared__ float part[4][128];
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // the value kernel's partials
   const int s = blockIdx.x, tid = threadIdx.x, q = tid >> 7, t = tid & 127;
   const long long row = (long long)s * G + blockIdx.y;
   if (tid < 32) {
@@ -1273,22 +1300,22 @@ cudaError_t run_fast_combine(const AttnJob& job, const float* pm, const float* p
   if (n_parts <= kCfMaxP && job.geo.d == 128) {
     const dim3 grid((unsigned)job.S, (unsigned)job.geo.G);
     if (NC == 128)
-      k_combine_fused<128><<<grid, kCfThreads, 0, st>>>(pm, pl, pz, n_parts, rows, job.geo.G,
-                                                         job.cb_val, job.n_slots, out, m_out, l_out);
+      launch_pdl(k_combine_fused<128>, grid, dim3(kCfThreads), 0, st, pm, pl, pz, n_parts, rows,
+                 job.geo.G, job.cb_val, job.n_slots, out, m_out, l_out);
     else
-      k_combine_fused<256><<<grid, kCfThreads, 0, st>>>(pm, pl, pz, n_parts, rows, job.geo.G,
-                                                         job.cb_val, job.n_slots, out, m_out, l_out);
+      launch_pdl(k_combine_fused<256>, grid, dim3(kCfThreads), 0, st, pm, pl, pz, n_parts, rows,
+                 job.geo.G, job.cb_val, job.n_slots, out, m_out, l_out);
     count_launch(1);
     return cudaGetLastError();
   }
   if (NC == 128) {
-    k_combine_merge<128><<<gm, 256, 0, st>>>(pm, pl, pz, n_parts, rows, zm);
-    k_combine_project<128><<<(unsigned)rows, 128, 0, st>>>(zm, rows, job.geo.G, job.cb_val,
-                                                           job.n_slots, out, m_out, l_out);
+    launch_pdl(k_combine_merge<128>, gm, dim3(256), 0, st, pm, pl, pz, n_parts, rows, zm);
+    launch_pdl(k_combine_project<128>, dim3((unsigned)rows), dim3(128), 0, st, zm, rows,
+               job.geo.G, job.cb_val, job.n_slots, out, m_out, l_out);
   } else {
-    k_combine_merge<256><<<gm, 256, 0, st>>>(pm, pl, pz, n_parts, rows, zm);
-    k_combine_project<256><<<(unsigned)rows, 128, 0, st>>>(zm, rows, job.geo.G, job.cb_val,
-                                                           job.n_slots, out, m_out, l_out);
+    launch_pdl(k_combine_merge<256>, gm, dim3(256), 0, st, pm, pl, pz, n_parts, rows, zm);
+    launch_pdl(k_combine_project<256>, dim3((unsigned)rows), dim3(128), 0, st, zm, rows,
+               job.geo.G, job.cb_val, job.n_slots, out, m_out, l_out);
   }
   count_launch(2);
   return cudaGetLastError();

@@ -399,6 +399,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_sp_score(SpArgs a) {
   static_assert(kMetaCol0 + 4 * kAStages <= kTmemCols, "TMEM columns");
   constexpr int NSTEP = 2 * R;
   constexpr int NW = (NSTEP * 6 + 63 + 63) / 64;  // raw words covering a token's record
+  // the value kernel (launched with programmatic stream serialization) may
+  // be scheduled onto SMs this persistent grid frees; it waits for our writes
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   extern __shared__ __align__(1024) unsigned char smem[];
   unsigned char* cbs = smem;                                             // [R][16 KiB]
   float2* etab = reinterpret_cast<float2*>(cbs + R * kRoundBytes);         // [64 j][32 lanes]
