@@ -464,6 +464,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_sp_score(SpArgs a) {
   if constexpr (PAIR) cluster_sync_all();  // barriers of both CTAs initialised
   else __syncthreads();
   tc_fence_after();
+  // launched with programmatic stream serialization: the prologue above (TMEM,
+  // barriers, the fp64 phase table) overlapped the previous kernel; the codes,
+  // queries and codebooks it may have written are read only from here on
+  asm volatile("griddepcontrol.wait;" ::: "memory");
 #ifdef CVQ_SP_TMEM0
   // the CTA owns all 512 TMEM columns, so the allocation starts at lane 0,
   // column 0: a compile-time base keeps every TMEM operand address uniform
@@ -994,8 +998,17 @@ cudaError_t launch_sp(const SpArgs& a, cudaStream_t st) {
     e = cudaLaunchKernelEx(&cfg, k_sp_score<R, G, PAIR>, a);
   } else {
     const int grid = a.n_items < sms ? a.n_items : sms;
-    k_sp_score<R, G, PAIR><<<grid, kThreads, sm, st>>>(a);
-    e = cudaGetLastError();
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = sm;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    e = cudaLaunchKernelEx(&cfg, k_sp_score<R, G, PAIR>, a);
   }
   count_launch();
   return e;
