@@ -462,7 +462,7 @@ k_encode_keys_table(Geom g, int n_slots, const double* __restrict__ atoms,
 // 8e-6 keeps a 1.8x factor.  Out-of-range scales and non-finite residuals
 // take the exact search over all pairs.
 constexpr double kMarginT64 = 8e-6;
-__global__ void __launch_bounds__(kEncWarps * 32)
+__global__ void __launch_bounds__(kEncWarps * 32, 1)
 k_encode_keys_t64(Geom g, int n_slots, const double* __restrict__ atoms,
                   const float* __restrict__ atomsf, const float* __restrict__ basef,
                   const double* __restrict__ maxnorm, const void* __restrict__ keys, int dtype,
@@ -506,15 +506,20 @@ k_encode_keys_t64(Geom g, int n_slots, const double* __restrict__ atoms,
         for (int t = 0; t < 4; ++t) su[t][0] = su[t][1] = sv[t][0] = sv[t][1] = 0.f;
         const float* p0 = Pf + (size_t)(4 * tq) * w2;
 #pragma unroll 4
-        for (int si = hs * 32; si < hs * 32 + 32; ++si) {
+        for (int si = hs * 32; si < hs * 32 + 32; si += 2) {  // two subspaces per P load
           const float2 u0 = Uf[si * L + lg], u1 = Uf[si * L + lg + 32];
+          const float2 v0 = Uf[(si + 1) * L + lg], v1 = Uf[(si + 1) * L + lg + 32];
 #pragma unroll
           for (int t = 0; t < 4; ++t) {
-            const float2 pa = *reinterpret_cast<const float2*>(p0 + t * w2 + 2 * si);
-            su[t][0] = fmaf(pa.x, u0.x, fmaf(pa.y, u0.y, su[t][0]));
-            sv[t][0] = fmaf(pa.y, u0.x, fmaf(-pa.x, u0.y, sv[t][0]));
-            su[t][1] = fmaf(pa.x, u1.x, fmaf(pa.y, u1.y, su[t][1]));
-            sv[t][1] = fmaf(pa.y, u1.x, fmaf(-pa.x, u1.y, sv[t][1]));
+            const float4 pq = *reinterpret_cast<const float4*>(p0 + t * w2 + 2 * si);
+            su[t][0] = fmaf(pq.x, u0.x, fmaf(pq.y, u0.y, su[t][0]));
+            sv[t][0] = fmaf(pq.y, u0.x, fmaf(-pq.x, u0.y, sv[t][0]));
+            su[t][1] = fmaf(pq.x, u1.x, fmaf(pq.y, u1.y, su[t][1]));
+            sv[t][1] = fmaf(pq.y, u1.x, fmaf(-pq.x, u1.y, sv[t][1]));
+            su[t][0] = fmaf(pq.z, v0.x, fmaf(pq.w, v0.y, su[t][0]));
+            sv[t][0] = fmaf(pq.w, v0.x, fmaf(-pq.z, v0.y, sv[t][0]));
+            su[t][1] = fmaf(pq.z, v1.x, fmaf(pq.w, v1.y, su[t][1]));
+            sv[t][1] = fmaf(pq.w, v1.x, fmaf(-pq.z, v1.y, sv[t][1]));
           }
         }
         if (hs) {
