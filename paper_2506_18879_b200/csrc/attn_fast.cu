@@ -927,11 +927,15 @@ __global__ void __launch_bounds__(kThreads, MMA ? (NC <= 128 ? 4 : 2) : 1) k_fas
     // lane % 4) holds the fragments of tokens 2t, 2t+1, 2t+8, 2t+9 of the
     // step and codes 16 mt + g (+ 8): byte j of u32 word i of a token's code
     // bits, masked at bit g, is code 32 i + 8 j + g, i.e. m-tile 2 i + j / 2,
-    // row g + 8 (j & 1); as the high byte of an fp16 it is 0 or 2^-16 (a
-    // subnormal: exact in the tensor core), and a sign-replicating prmt pairs
-    // two tokens' bytes into an A register.
+    // row g + 8 (j & 1). The mask stays in place (one LOP3 per word): a byte
+    // m in {0, 2^g} doubled into both bytes of an fp16 (m << 8 | m, one prmt
+    // pairs two tokens' bytes into an A register) is 0 or c_g = fp16(0x0101
+    // << g), the same constant for every row this thread supplies (c_7 =
+    // -2^-17 has the sign bit; subnormals are exact in the tensor core), so
+    // z = D / (2^15 c_g) at the end.
     constexpr int MT = NC / 16, NW32 = NC / 32;
     const int g = lane >> 2, t = lane & 3;
+    const uint32_t gmask = 0x01010101u << g;
     float d[MT][4];
 #pragma unroll
     for (int mt = 0; mt < MT; ++mt) d[mt][0] = d[mt][1] = d[mt][2] = d[mt][3] = 0.f;
@@ -956,26 +960,27 @@ __global__ void __launch_bounds__(kThreads, MMA ? (NC <= 128 ? 4 : 2) : 1) k_fas
         const uint32_t cv[4] = {C4.x, C4.y, C4.z, C4.w}, dv[4] = {D4.x, D4.y, D4.z, D4.w};
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-          const uint32_t mA = (av[u] >> g) & 0x01010101u;
-          const uint32_t mB = (bv[u] >> g) & 0x01010101u;
-          const uint32_t mC = (cv[u] >> g) & 0x01010101u;
-          const uint32_t mD = (dv[u] >> g) & 0x01010101u;
           const int mt = 2 * (i4 + u);
-          uint32_t fa[4] = {prmt(mA, mB, 0x4C08), prmt(mA, mB, 0x5D19), prmt(mC, mD, 0x4C08),
-                            prmt(mC, mD, 0x5D19)};
+          const uint32_t mA = av[u] & gmask, mB = bv[u] & gmask;
+          const uint32_t mC = cv[u] & gmask, mD = dv[u] & gmask;
+          uint32_t fa[4] = {prmt(mA, mB, 0x4400), prmt(mA, mB, 0x5511), prmt(mC, mD, 0x4400),
+                            prmt(mC, mD, 0x5511)};
           mma16816(d[mt], fa, b0, b1);
-          uint32_t fb[4] = {prmt(mA, mB, 0x6E2A), prmt(mA, mB, 0x7F3B), prmt(mC, mD, 0x6E2A),
-                            prmt(mC, mD, 0x7F3B)};
+          uint32_t fb[4] = {prmt(mA, mB, 0x6622), prmt(mA, mB, 0x7733), prmt(mC, mD, 0x6622),
+                            prmt(mC, mD, 0x7733)};
           mma16816(d[mt + 1], fb, b0, b1);
         }
       }
     }
     __syncthreads();  // all warps are done with PT / vw (zr may alias them)
+    // bits were c_g, weights p 2^15 (fast division: a couple of ulp on z,
+    // far inside the fp16 weights' 2^-11)
+    const float zsc =
+        __fdividef(1.f, 32768.f * __half2float(__ushort_as_half((unsigned short)(0x0101u << g))));
 #pragma unroll
     for (int mt = 0; mt < MT; ++mt) {
       float* z0 = zr + ((size_t)warp * NC + 16 * mt + g) * G;
       float* z1 = z0 + 8 * G;
-      constexpr float zsc = 2.f;  // bits were 2^-16, weights p 2^15
       if (2 * t < G) {
         z0[2 * t] = zsc * d[mt][0];
         z1[2 * t] = zsc * d[mt][2];
