@@ -806,14 +806,37 @@ __global__ void __launch_bounds__(kThreads, MMA ? (NC <= 128 ? 4 : 2) : 1) k_fas
     }
     __syncthreads();
     // p = half * group scale, once per (token, head) over the CTA; read
-    // into registers first (sc[e] overlaps hw of lower tokens)
+    // into registers first (sc[e] overlaps hw of lower tokens). MMA: the
+    // thread takes token pairs (e, e + 1), e = 2 tid + 2 kThreads kp (one
+    // 16-B load of both tokens' halves, one half2 store per head below)
+    if constexpr (MMA) {
 #pragma unroll
-    for (int k = 0; k < kMaxPer; ++k) {
-      const int e = tid + k * kThreads;
-      if (e < cnt) {
+      for (int kp = 0; kp < kMaxPer / 2; ++kp) {
+        const int e = 2 * tid + kp * 2 * kThreads;
+        if (e < cnt) {
+          __half hv[2 * G];
+          if constexpr (G == 4) {
+            *reinterpret_cast<uint4*>(hv) = *reinterpret_cast<const uint4*>(hw + (size_t)e * G);
+          } else {
+            *reinterpret_cast<__half2*>(hv) = *reinterpret_cast<const __half2*>(hw + (size_t)e * G);
+          }
 #pragma unroll
-        for (int h = 0; h < G; ++h)
-          pv[k][h] = __half2float(hw[(size_t)e * G + h]) * gm[(e >> 5) * G + h];
+          for (int h = 0; h < G; ++h) {
+            const float gs = gm[(e >> 5) * G + h];  // e even: e, e + 1 share a group
+            pv[2 * kp][h] = __half2float(hv[h]) * gs;
+            pv[2 * kp + 1][h] = __half2float(hv[G + h]) * gs;
+          }
+        }
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < kMaxPer; ++k) {
+        const int e = tid + k * kThreads;
+        if (e < cnt) {
+#pragma unroll
+          for (int h = 0; h < G; ++h)
+            pv[k][h] = __half2float(hw[(size_t)e * G + h]) * gm[(e >> 5) * G + h];
+        }
       }
     }
     __syncthreads();
@@ -892,16 +915,32 @@ __global__ void __launch_bounds__(kThreads, MMA ? (NC <= 128 ? 4 : 2) : 1) k_fas
   __half* PT = reinterpret_cast<__half*>(smem);
   const int pst = a.chunk2 + 8;
   const int cpad = (cnt + 15) & ~15;
-  if constexpr (MMA) {
+  if constexpr (MMA && PH) {
+    // token pairs (e, e + 1) as above; cpad is a multiple of 16 and e even,
+    // so e < cpad covers e + 1; weights carried as p 2^15 (see the
+    // accumulation below)
+#pragma unroll
+    for (int kp = 0; kp < kMaxPer / 2; ++kp) {
+      const int e = 2 * tid + kp * 2 * kThreads;
+      if (e < cpad) {
+#pragma unroll
+        for (int h = 0; h < G; ++h) {
+          const __half2 hv = __floats2half2_rn(e < cnt ? pv[2 * kp][h] * 32768.f : 0.f,
+                                               e + 1 < cnt ? pv[2 * kp + 1][h] * 32768.f : 0.f);
+          *reinterpret_cast<__half2*>(PT + h * pst + e) = hv;
+          const float2 hf = __half22float2(hv);
+          ls[h] += (hf.x + hf.y) * (1.f / 32768.f);
+        }
+      }
+    }
+  } else if constexpr (MMA) {
 #pragma unroll
     for (int k = 0; k < kMaxPer; ++k) {
       const int e = tid + k * kThreads;
       if (e < cpad) {
 #pragma unroll
         for (int h = 0; h < G; ++h) {
-          // weights carried as p 2^15 against bits of 2^-16 (an fp16
-          // subnormal whose only byte is the bit): the products are p / 2,
-          // exact, and z is doubled at the end
+          // weights carried as p 2^15 (see the accumulation below)
           const __half hv = __float2half_rn(e < cnt ? pv[k][h] * 32768.f : 0.f);
           PT[h * pst + e] = hv;
           ls[h] += __half2float(hv) * (1.f / 32768.f);
